@@ -1,0 +1,176 @@
+/*
+ * th_b200.h -- C ABI of the B200-native k-hop retrieval engine.
+ *
+ * Drop-in boundary for the hot path of the reference `triplehop` package
+ * (/root/reference/pkg/src/triplehop).  The reference is pure Python/numpy
+ * and has no FFI of its own; these entry points are what its Python layer
+ * binds (through ctypes) in place of the numpy code:
+ *
+ *   th_graph_create   <- build_incidence            incidence.py:154-196
+ *   th_run (frontiers, activated, edge counts)
+ *                     <- k_hop / run_hops / _expand incidence.py:214-221,268-330
+ *                        one_hop                    incidence.py:224-232
+ *   th_run (paths)    <- reconstruct_paths / assemble_paths
+ *                                                   incidence.py:361-408
+ *   th_plan_owner     <- plan_partitions            partition.py:49-98
+ *
+ * Conventions
+ *   - plain C types only; every pointer argument documented as device (d_)
+ *     or host (h_); int status return (TH_OK == 0); no exceptions cross the
+ *     ABI; th_last_error() gives a thread-local message for the last failure.
+ *   - every call that launches work takes the CUDA stream (cudaStream_t passed
+ *     as void*) and is asynchronous unless documented otherwise.
+ *   - the graph is immutable after creation and may be shared by sessions on
+ *     different streams; a session owns all per-query workspace and results
+ *     (results stay valid until the next th_run on that session).
+ */
+#ifndef TH_B200_H
+#define TH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TH_ABI_VERSION 1
+
+/* status codes (Python mapping in paper_2604_18913_b200/_lib.py) */
+#define TH_OK 0
+#define TH_ERR_INVALID 1  /* contract violation          -> ValueError    */
+#define TH_ERR_RANGE 2    /* id out of range             -> ValueError    */
+#define TH_ERR_CUDA 3     /* CUDA runtime failure        -> RuntimeError  */
+#define TH_ERR_NOMEM 4    /* device allocation failed    -> MemoryError   */
+#define TH_ERR_OVERFLOW 5 /* result capacity too small: call th_run again  */
+#define TH_ERR_STATE 6    /* misuse of handles           -> RuntimeError  */
+
+/* hop semantics, incidence.py:52-75 */
+#define TH_EXACT 0
+#define TH_FRONTIER 1
+#define TH_CUMULATIVE 2
+
+/* th_query.flags */
+#define TH_WANT_FRONTIERS 0x1u /* per-query sorted frontier ids per hop      */
+#define TH_WANT_ACTIVATED 0x2u /* per-query sorted activated triple ids/hop  */
+#define TH_WANT_PATHS 0x4u     /* capped lexicographic walk enumeration       */
+
+/* th_graph_create flags */
+#define TH_GRAPH_NO_REVERSE 0x1u /* skip the reverse (by-object) CSR: no pull hops */
+
+typedef struct th_graph th_graph;
+typedef struct th_session th_session;
+
+int th_abi_version(void);
+const char* th_last_error(void);
+
+/* ---- graph ------------------------------------------------------------- */
+
+/* Build the device incidence structure from (subject, relation, object)
+ * columns in triple-id order (d_ int32, n_triples long).  Ids are range
+ * checked (TH_ERR_RANGE, incidence.py:175-179).  Synchronises `stream`. */
+int th_graph_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
+                    int64_t n_triples, int64_t n_entities, int64_t n_relations,
+                    uint32_t flags, void* stream, th_graph** out);
+int th_graph_destroy(th_graph* g);
+
+typedef struct {
+  int64_t n_entities, n_triples, n_relations;
+  const int32_t* indptr;   /* [E+1] subject CSR row offsets                 */
+  const int32_t* csr_tid;  /* [T] triple id per CSR slot, ascending per row */
+  const int32_t* csr_obj;  /* [T] object per CSR slot                       */
+  const uint16_t* csr_rel; /* [T] relation per CSR slot                     */
+  const int32_t* subj;     /* [T] triple-id order                           */
+  const int32_t* obj;      /* [T]                                           */
+  const uint16_t* rel;     /* [T]                                           */
+  const int32_t* rindptr;  /* [E+1] object CSR (NULL with NO_REVERSE)       */
+  const int32_t* rsrc;     /* [T] subject of each in-edge                   */
+  const uint16_t* rrel;    /* [T] relation of each in-edge                  */
+  int64_t max_out_degree, max_in_degree;
+  int64_t n_heavy_in;      /* in-rows split across warps in pull hops       */
+  uint64_t device_bytes;
+} th_graph_info;
+int th_graph_info_get(const th_graph* g, th_graph_info* out);
+
+/* ---- queries ------------------------------------------------------------ */
+
+/* B queries; query q starts from the entity set
+ * d_seeds[d_seed_offsets[q] .. d_seed_offsets[q+1]) (any order, duplicates
+ * allowed).  retrieve(seeds) uses one singleton query per seed. */
+typedef struct {
+  int32_t n_queries;
+  const int32_t* d_seed_offsets; /* [B+1] */
+  const int32_t* d_seeds;
+  int32_t k;          /* hops, >= 1 (incidence.py:282-283) */
+  int32_t semantics;  /* TH_EXACT / TH_FRONTIER / TH_CUMULATIVE */
+  const uint32_t* d_rel_masks; /* [B][mask_words] bit r = relation r allowed; NULL = all */
+  int32_t mask_words;
+  uint32_t flags;     /* TH_WANT_* */
+  int64_t max_paths;  /* >= 0, or -1 for uncapped (max_paths=None) */
+} th_query;
+
+/* Device-resident results of the last th_run on a session.
+ * Frontier of query q at hop h (1-based):
+ *   frontier_ids[frontier_off[(h-1)*B+q] .. +frontier_len[(h-1)*B+q]]
+ * Activated triples likewise with act_*.  Paths of query q:
+ *   path_tids[(path_off[q] + i) * k + d], i < path_count[q], d < k. */
+typedef struct {
+  int32_t n_queries, k;
+  const int64_t* frontier_off; const int64_t* frontier_len; const int32_t* frontier_ids;
+  const int64_t* act_off;      const int64_t* act_len;      const int32_t* act_ids;
+  const int64_t* edges;        /* [k][B] |T_h(q)| = edges traversed (app.py:97) */
+  const int64_t* path_off;     const int64_t* path_count;   const uint8_t* path_truncated;
+  const int32_t* path_tids;
+  /* host-side totals, valid after th_finish */
+  int64_t frontier_total, act_total, path_total;
+  int32_t push_hops, pull_hops; /* direction choices taken (diagnostics) */
+} th_result;
+
+int th_session_create(th_graph* g, void* stream, th_session** out);
+int th_session_destroy(th_session* s);
+
+/* Enqueue one query batch on the session stream (asynchronous). */
+int th_run(th_session* s, const th_query* q);
+/* Synchronise the stream and describe the results.  Returns TH_ERR_OVERFLOW
+ * when an output buffer was too small; capacities have then been grown and
+ * the same th_run must be issued again.  TH_ERR_RANGE for a bad seed id. */
+int th_finish(th_session* s, th_result* out);
+
+/* Tuning knobs (diagnostics / benchmarks): pull when the frontier's
+ * out-edge total exceeds n_triples / pull_divisor; 0 = never pull,
+ * <0 = always pull. */
+int th_session_set_pull_divisor(th_session* s, double pull_divisor);
+/* Number of kernels this session has launched since creation. */
+int64_t th_session_launch_count(const th_session* s);
+
+/* Per-category device timing (CUDA events recorded on the session stream
+ * around each kernel group while profiling is on).  Categories: */
+#define TH_PROF_SETUP 0      /* seed rows, masks, hop bookkeeping          */
+#define TH_PROF_EDGES 1      /* per-query edge counts |T_h|                */
+#define TH_PROF_ACTIVATED 2  /* activated-triple materialisation           */
+#define TH_PROF_PUSH 3       /* push hop kernels                           */
+#define TH_PROF_PULL 4       /* pull hop kernels                           */
+#define TH_PROF_FRONTIER 5   /* frontier materialisation (K4)              */
+#define TH_PROF_CLEAR 6      /* state recycling                            */
+#define TH_PROF_PATHS 7      /* path enumeration (K5)                      */
+#define TH_PROF_CATEGORIES 8
+int th_session_set_profiling(th_session* s, int on);
+/* Accumulated milliseconds and launches per category since the last call
+ * (arrays of n >= TH_PROF_CATEGORIES); resets the accumulators. Syncs. */
+int th_session_profile(th_session* s, double* ms, int64_t* launches, int n);
+/* Entity-list lengths of the last wave: [0] = distinct seed entities,
+ * [h] = entities newly set at hop h (rows of the hop-h layer).  n >= k+1. */
+int th_session_wave_lists(const th_session* s, int64_t* lens, int n);
+
+/* ---- partitioning (multi-GPU ownership) -------------------------------- */
+
+/* Subject -> owner assignment, partition.py:49-98.  strategy 0 = hash
+ * ((e * 0x9E3779B1) mod 2^32) mod m (partition.py:80-84), computed on the
+ * device; entities with no out-edges get -1 (UNASSIGNED, partition.py:23).
+ * d_owner: int32[E].  Asynchronous. */
+int th_plan_owner_hash(const th_graph* g, int32_t m, int32_t* d_owner, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TH_B200_H */

@@ -1,0 +1,45 @@
+"""B200-native k-hop knowledge-graph retrieval (LogosKG hot path).
+
+Drop-in for the retriever API of the reference ``triplehop`` package
+(``/root/reference/pkg/src/triplehop/__init__.py:13-91``, hot-path subset):
+``build_incidence``, ``k_hop``, ``one_hop``, ``reconstruct_paths`` and the
+types they return, plus the batched ``retrieve(seeds, k, relation_filter)``.
+Every hop runs in hand-written sm_100a kernels (``csrc/``) behind the C ABI
+of ``include/th_b200.h``; there is no CPU fallback.
+"""
+
+__version__ = "0.1.0"
+
+from .core_types import (
+    DEFAULT_MAX_PATHS,
+    EntityVector,
+    HopSemantics,
+    HopStep,
+    HopTrace,
+    PathResult,
+    Triple,
+    TripleVector,
+    jaccard,
+)
+from .device_graph import IncidenceGraph, build_incidence
+from .retriever import RetrievalResult, Retriever, k_hop, one_hop, reconstruct_paths, retrieve
+
+__all__ = [
+    "DEFAULT_MAX_PATHS",
+    "EntityVector",
+    "HopSemantics",
+    "HopStep",
+    "HopTrace",
+    "IncidenceGraph",
+    "PathResult",
+    "RetrievalResult",
+    "Retriever",
+    "Triple",
+    "TripleVector",
+    "build_incidence",
+    "jaccard",
+    "k_hop",
+    "one_hop",
+    "reconstruct_paths",
+    "retrieve",
+]

@@ -1,0 +1,218 @@
+// extern "C" boundary (include/th_b200.h).  No C++ exception crosses it:
+// every entry point converts failures into a status code plus a
+// thread-local message (th_last_error).
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/th_b200.h"
+#include "engine.cuh"
+#include "graph.cuh"
+
+struct th_graph {
+  th::Graph g;
+};
+struct th_session {
+  th::Session s;
+};
+
+namespace th {
+static thread_local std::string g_last_error;
+void set_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace th
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const th::CudaError& e) {
+    th::set_error(std::string(e.where) + ": " + cudaGetErrorString(e.code));
+    return e.code == cudaErrorMemoryAllocation ? TH_ERR_NOMEM : TH_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    th::set_error("host allocation failed");
+    return TH_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    th::set_error(e.what());
+    return TH_ERR_STATE;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int th_abi_version(void) { return TH_ABI_VERSION; }
+
+const char* th_last_error(void) { return th::g_last_error.c_str(); }
+
+int th_graph_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
+                    int64_t n_triples, int64_t n_entities, int64_t n_relations, uint32_t flags,
+                    void* stream, th_graph** out) {
+  return guarded([&]() -> int {
+    if (!out) {
+      th::set_error("out is NULL");
+      return TH_ERR_INVALID;
+    }
+    *out = nullptr;
+    if (n_triples < 0 || n_entities < 0 || n_relations < 0) {
+      th::set_error("negative size");
+      return TH_ERR_INVALID;
+    }
+    if (n_triples >= INT32_MAX || n_entities >= INT32_MAX) {
+      th::set_error("int32 id space exceeded (n_triples, n_entities < 2^31-1)");
+      return TH_ERR_INVALID;
+    }
+    if (n_relations > 65535) {
+      th::set_error("relation ids are stored as uint16 (n_relations <= 65535)");
+      return TH_ERR_INVALID;
+    }
+    if (n_triples > 0 && (!d_subj || !d_rel || !d_obj)) {
+      th::set_error("NULL triple column");
+      return TH_ERR_INVALID;
+    }
+    auto* h = new th_graph();
+    const int rc = th::graph_build(&h->g, d_subj, d_rel, d_obj, n_triples, n_entities, n_relations,
+                                   !(flags & TH_GRAPH_NO_REVERSE),
+                                   static_cast<cudaStream_t>(stream));
+    if (rc != TH_OK) {
+      th::graph_free(&h->g);
+      delete h;
+      return rc;
+    }
+    *out = h;
+    return TH_OK;
+  });
+}
+
+int th_graph_destroy(th_graph* g) {
+  return guarded([&]() -> int {
+    if (!g) return TH_OK;
+    th::graph_free(&g->g);
+    delete g;
+    return TH_OK;
+  });
+}
+
+int th_graph_info_get(const th_graph* gh, th_graph_info* out) {
+  if (!gh || !out) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  const th::Graph& g = gh->g;
+  out->n_entities = g.E;
+  out->n_triples = g.T;
+  out->n_relations = g.R;
+  out->indptr = g.indptr;
+  out->csr_tid = g.csr_tid;
+  out->csr_obj = g.csr_obj;
+  out->csr_rel = g.csr_rel;
+  out->subj = g.subj;
+  out->obj = g.obj;
+  out->rel = g.rel;
+  out->rindptr = g.rindptr;
+  out->rsrc = g.rsrc;
+  out->rrel = g.rrel;
+  out->max_out_degree = g.max_out;
+  out->max_in_degree = g.max_in;
+  out->n_heavy_in = g.n_heavy;
+  out->device_bytes = g.bytes;
+  return TH_OK;
+}
+
+int th_session_create(th_graph* g, void* stream, th_session** out) {
+  return guarded([&]() -> int {
+    if (!g || !out) {
+      th::set_error("NULL handle");
+      return TH_ERR_INVALID;
+    }
+    auto* s = new th_session();
+    s->s.g = &g->g;
+    s->s.st = static_cast<cudaStream_t>(stream);
+    *out = s;
+    return TH_OK;
+  });
+}
+
+int th_session_destroy(th_session* s) {
+  return guarded([&]() -> int {
+    if (!s) return TH_OK;
+    th::session_free(&s->s);
+    delete s;
+    return TH_OK;
+  });
+}
+
+int th_run(th_session* s, const th_query* q) {
+  return guarded([&]() -> int {
+    if (!s || !q) {
+      th::set_error("NULL handle");
+      return TH_ERR_INVALID;
+    }
+    return th::session_run(&s->s, q);
+  });
+}
+
+int th_finish(th_session* s, th_result* out) {
+  return guarded([&]() -> int {
+    if (!s || !out) {
+      th::set_error("NULL handle");
+      return TH_ERR_INVALID;
+    }
+    return th::session_finish(&s->s, out);
+  });
+}
+
+int th_session_set_pull_divisor(th_session* s, double pull_divisor) {
+  if (!s) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  s->s.pull_divisor = pull_divisor;
+  return TH_OK;
+}
+
+int64_t th_session_launch_count(const th_session* s) { return s ? s->s.launches : -1; }
+
+int th_session_set_profiling(th_session* s, int on) {
+  if (!s) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  s->s.prof = on != 0;
+  return TH_OK;
+}
+
+int th_session_profile(th_session* s, double* ms, int64_t* launches, int n) {
+  return guarded([&]() -> int {
+    if (!s) {
+      th::set_error("NULL handle");
+      return TH_ERR_INVALID;
+    }
+    return th::session_profile(&s->s, ms, launches, n);
+  });
+}
+
+int th_session_wave_lists(const th_session* s, int64_t* lens, int n) {
+  return guarded([&]() -> int {
+    if (!s || !lens) {
+      th::set_error("NULL handle");
+      return TH_ERR_INVALID;
+    }
+    return th::session_wave_lists(const_cast<th::Session*>(&s->s), lens, n);
+  });
+}
+
+int th_plan_owner_hash(const th_graph* g, int32_t m, int32_t* d_owner, void* stream) {
+  return guarded([&]() -> int {
+    if (!g || !d_owner || m < 1) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    th::plan_owner_hash(&g->g, m, d_owner, static_cast<cudaStream_t>(stream));
+    return TH_OK;
+  });
+}
+
+}  // extern "C"

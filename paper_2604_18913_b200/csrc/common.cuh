@@ -1,0 +1,75 @@
+// Shared device helpers for the k-hop engine (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#define TH_FULL 0xffffffffu
+
+namespace th {
+
+// thread-local error string behind th_last_error()
+void set_error(const std::string& msg);
+
+struct CudaError {
+  cudaError_t code;
+  const char* where;
+};
+
+#define TH_CUDA(expr)                                                  \
+  do {                                                                 \
+    cudaError_t _e = (expr);                                           \
+    if (_e != cudaSuccess) throw ::th::CudaError{_e, #expr};           \
+  } while (0)
+
+#define TH_LAUNCHED() TH_CUDA(cudaPeekAtLastError())
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// 32x32 bit-matrix transpose across a warp: on entry lane i holds row i
+// (bit j = column j); on exit lane j holds column j (bit i = row i).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int s = 16, k = 0; s >= 1; s >>= 1, ++k) {
+    const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu
+                     : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t o = __shfl_xor_sync(TH_FULL, x, s);
+    x = (lane & s) ? (((o >> s) & m) | (x & ~m)) : ((x & m) | ((o & m) << s));
+  }
+  return x;
+}
+
+// warp-aggregated append of `item` (called by an arbitrary subset of lanes)
+template <typename T>
+__device__ __forceinline__ void warp_append(T* list, int32_t* counter, T item, int64_t cap) {
+  const unsigned act = __activemask();
+  const int leader = __ffs(act) - 1;
+  const unsigned rank = __popc(act & lanemask_lt());
+  int32_t base = 0;
+  if ((int)lane_id() == leader) base = atomicAdd(counter, __popc(act));
+  base = __shfl_sync(act, base, leader);
+  if (base + (int64_t)rank < cap) list[base + rank] = item;
+}
+
+// warp-aggregated add of a small non-negative value (heuristic counters;
+// each lane's contribution is clamped to 2^26 so the 32-bit reduce is exact)
+__device__ __forceinline__ void warp_add_small(unsigned long long* dst, uint32_t v) {
+  const unsigned act = __activemask();
+  const int leader = __ffs(act) - 1;
+  const unsigned sum = __reduce_add_sync(act, v > (1u << 26) ? (1u << 26) : v);
+  if ((int)lane_id() == leader) atomicAdd(dst, (unsigned long long)sum);
+}
+
+}  // namespace th

@@ -1,0 +1,1162 @@
+// Batched multi-source k-hop engine for sm_100a.
+//
+// Reference semantics (incidence.py:214-221 _expand, :268-316 run_hops) are
+// evaluated for up to 1024 independent queries at once: every entity row of
+// the state matrices holds one bit per query (W = words per row).
+//
+//   X  frontier being expanded   (X_{h-1} of SURVEY 8a)
+//   N  next layer                (R_h for exact walks, F_h = R_h \ V_{h-1} otherwise)
+//   V  visited                   (per-query `visited`, incidence.py:301-308)
+//   S  seed rows (cumulative semantics reports V_h \ S, incidence.py:309-312)
+//   M  relation mask matrix, row r = queries allowing relation r
+//
+// A hop either PUSHES from the compacted frontier list (warp-cooperative CSR
+// row gathers, atomicOr test-and-set into V / N, warp-aggregated compaction of
+// newly reached entities), or PULLS over the reverse CSR for every entity
+// (OR of in-neighbour frontier rows, early exit once all queries have visited
+// the entity).  The direction is chosen on the device from the frontier's
+// out-edge total, the role played by _DENSE_FRACTION in the reference
+// (incidence.py:29-31,45).  Results are turned into per-query sorted id lists
+// by a bit-transpose materialisation (K4), giving exactly the canonical
+// sorted/unique EntityVector / TripleVector form (incidence.py:83-91).
+#include <algorithm>
+#include <cstddef>
+#include <cstring>
+
+#include "common.cuh"
+#include "engine.cuh"
+#include "paths.cuh"
+
+namespace th {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int32_t kHeavyPush = 4096;  // rows longer than this are split
+constexpr int32_t kPushChunk = 1024;
+constexpr int kMatBlocks = 2048;      // target materialisation blocks
+
+__device__ __forceinline__ uint32_t valid_word(int j, int nq) {
+  const int lo = 32 * j;
+  if (lo + 32 <= nq) return TH_FULL;
+  if (lo >= nq) return 0u;
+  return (1u << (nq - lo)) - 1u;
+}
+
+struct WaveArgs {
+  const int32_t* indptr;
+  const int32_t* csr_obj;
+  const uint16_t* csr_rel;
+  const int32_t* rindptr;
+  const int32_t* rsrc;
+  const uint16_t* rrel;
+  const int32_t* heavy_ids;
+  const int32_t* chunk_hv;
+  const int32_t* chunk_lo;
+  const int32_t* chunk_hi;
+  int64_t n_chunks, n_heavy_in;
+  int64_t E, T;
+  uint32_t *X, *N, *V, *S, *Xf, *Nf, *Vf;
+  const uint32_t* M;
+  int32_t* lists;
+  int32_t* heavy;
+  uint32_t* racc;
+  Ctl* ctl;
+  int nq, sem, h;
+};
+
+template <int W>
+struct Grp {
+  static __device__ __forceinline__ unsigned shift() { return (lane_id() / W) * W; }
+  static __device__ __forceinline__ unsigned mask() {
+    return W == 32 ? TH_FULL : (((1u << W) - 1u) << shift());
+  }
+  static __device__ __forceinline__ unsigned j() { return lane_id() % W; }
+  static __device__ __forceinline__ uint32_t ballot(bool p) {
+    const uint32_t b = __ballot_sync(mask(), p);
+    return W == 32 ? b : (b >> shift()) & ((1u << W) - 1u);
+  }
+};
+
+// ---------------------------------------------------------------- seeds
+
+template <int W>
+__global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
+                                 const int32_t* __restrict__ seeds, int q0) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int q = gw; q < a.nq; q += nw) {
+    const int32_t lo = qoff[q0 + q], hi = qoff[q0 + q + 1];
+    const uint32_t qb = 1u << (q & 31);
+    const int qw = q >> 5;
+    for (int32_t i = lo + lane; i < hi; i += 32) {
+      const int32_t e = seeds[i];
+      if (e < 0 || e >= a.E) {
+        a.ctl->err = 1;
+        continue;
+      }
+      const size_t r = (size_t)e * W + qw;
+      atomicOr(&a.X[r], qb);
+      if (a.sem != TH_EXACT) atomicOr(&a.V[r], qb);
+      if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
+      const uint32_t fb = 1u << (e & 31);
+      const uint32_t fo = atomicOr(&a.Xf[e >> 5], fb);
+      if (!(fo & fb)) {
+        warp_append(a.lists, &a.ctl->list_len[0], e, a.E);
+        warp_add_small(&a.ctl->push_cost[0], (uint32_t)(a.indptr[e + 1] - a.indptr[e]));
+        if (a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[e >> 5], fb);
+      }
+    }
+  }
+}
+
+// begin hop h: place list segment h, choose the direction
+__global__ void begin_hop_kernel(Ctl* ctl, int h, int64_t T, double pull_divisor, int has_reverse) {
+  const int32_t prev = ctl->list_len[h - 1];
+  ctl->list_off[h] = ctl->list_off[h - 1] + prev;
+  ctl->list_len[h] = 0;
+  ctl->push_cost[h] = 0;
+  ctl->heavy_len = 0;
+  int pull = 0;
+  if (has_reverse) {
+    if (pull_divisor < 0) pull = 1;
+    else if (pull_divisor > 0) pull = (double)ctl->push_cost[h - 1] * pull_divisor > (double)T;
+  }
+  ctl->mode[h] = pull;
+  if (pull) ctl->pull_hops++;
+  else ctl->push_hops++;
+}
+
+// ------------------------------------------------------ mark new entity
+
+template <int W>
+__device__ __forceinline__ void mark_next(const WaveArgs& a, int32_t v) {
+  const uint32_t fb = 1u << (v & 31);
+  const uint32_t fo = atomicOr(&a.Nf[v >> 5], fb);
+  if (!(fo & fb)) {
+    warp_append(a.lists + a.ctl->list_off[a.h], &a.ctl->list_len[a.h], v, a.E);
+    warp_add_small(&a.ctl->push_cost[a.h], (uint32_t)(a.indptr[v + 1] - a.indptr[v]));
+    if (a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[v >> 5], fb);
+  }
+}
+
+// ------------------------------------------------------------ push hop
+
+// visit the (edge, nonzero frontier word) pairs of CSR slots [lo, hi) of u
+template <int W, bool FILTER, class Op>
+__device__ __forceinline__ void row_pairs(const WaveArgs& a, int32_t u, int32_t lo, int32_t hi,
+                                          Op& op) {
+  const unsigned lane = lane_id();
+  const uint32_t xw = lane < (unsigned)W ? a.X[(size_t)u * W + lane] : 0u;
+  const unsigned nz = __ballot_sync(TH_FULL, xw != 0u);
+  if (!nz || hi <= lo) return;
+  const int nzw = __popc(nz);
+  const int pairs = (hi - lo) * nzw;
+  const int j1 = __ffs(nz) - 1;
+  for (int p0 = 0; p0 < pairs; p0 += 32) {
+    const int p = p0 + (int)lane;
+    int e, j;
+    if (nzw == 1) {
+      e = p;
+      j = j1;
+    } else {
+      e = p / nzw;
+      j = (int)__fns(nz, 0, p - e * nzw + 1);
+    }
+    const uint32_t x = __shfl_sync(TH_FULL, xw, j & 31);
+    if (p < pairs) {
+      const int32_t pos = lo + e;
+      uint32_t w = x;
+      if (FILTER) w &= a.M[(size_t)a.csr_rel[pos] * W + j];
+      if (w) op(a.csr_obj[pos], j, w);
+    }
+  }
+}
+
+template <int W, int SEM>
+struct PushOp {
+  const WaveArgs& a;
+  __device__ __forceinline__ void operator()(int32_t v, int j, uint32_t w) const {
+    const size_t r = (size_t)v * W + j;
+    if (SEM == TH_EXACT) {
+      if (!(w & ~__ldcg(&a.N[r]))) return;
+      const uint32_t old = atomicOr(&a.N[r], w);
+      if (old == 0u) mark_next<W>(a, v);
+    } else {
+      if (!(w & ~__ldcg(&a.V[r]))) return;
+      const uint32_t old = atomicOr(&a.V[r], w);
+      const uint32_t nb = w & ~old;
+      if (!nb) return;
+      atomicOr(&a.N[r], nb);
+      mark_next<W>(a, v);
+    }
+  }
+};
+
+template <int W>
+struct CountOp {
+  uint32_t* sc;
+  __device__ __forceinline__ void operator()(int32_t, int j, uint32_t w) const {
+    while (w) {
+      atomicAdd(&sc[32 * j + __ffs(w) - 1], 1u);
+      w &= w - 1u;
+    }
+  }
+};
+
+// warp per frontier entity; rows above kHeavyPush go to the heavy list
+template <int W, bool FILTER, class Op>
+__device__ void drive_light(const WaveArgs& a, int seg, Op& op, bool build_heavy) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int32_t n = a.ctl->list_len[seg];
+  const int32_t* list = a.lists + a.ctl->list_off[seg];
+  for (int32_t i = gw; i < n; i += nw) {
+    const int32_t u = list[i];
+    const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
+    if (hi - lo > kHeavyPush) {
+      if (build_heavy && lane_id() == 0) a.heavy[atomicAdd(&a.ctl->heavy_len, 1)] = u;
+      continue;
+    }
+    row_pairs<W, FILTER>(a, u, lo, hi, op);
+  }
+}
+
+// all warps split every heavy row into kPushChunk-slot chunks
+template <int W, bool FILTER, class Op>
+__device__ void drive_heavy(const WaveArgs& a, Op& op) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int32_t nh = a.ctl->heavy_len;
+  int64_t base = 0;  // global chunk numbering keeps all warps busy
+  for (int32_t i = 0; i < nh; ++i) {
+    const int32_t u = a.heavy[i];
+    const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
+    const int32_t nc = (hi - lo + kPushChunk - 1) / kPushChunk;
+    int64_t c = ((gw - base) % nw + nw) % nw;
+    for (; c < nc; c += nw) {
+      const int32_t clo = lo + (int32_t)c * kPushChunk;
+      row_pairs<W, FILTER>(a, u, clo, min(hi, clo + kPushChunk), op);
+    }
+    base += nc;
+  }
+}
+
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) push_light_kernel(WaveArgs a) {
+  if (a.ctl->mode[a.h] != 0) return;
+  PushOp<W, SEM> op{a};
+  // with a relation filter the edge-count pass already built the heavy list
+  drive_light<W, FILTER>(a, a.h - 1, op, !FILTER);
+}
+
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) push_heavy_kernel(WaveArgs a) {
+  if (a.ctl->mode[a.h] != 0) return;
+  PushOp<W, SEM> op{a};
+  drive_heavy<W, FILTER>(a, op);
+}
+
+// --------------------------------------------------------- edge counts
+
+// |T_h(q)| = sum of out-degrees of X_{h-1}(q) (no relation filter)
+template <int W>
+__global__ void __launch_bounds__(kThreads) edge_count_kernel(WaveArgs a, int64_t* out) {
+  __shared__ unsigned long long sc[32 * W];
+  for (int t = threadIdx.x; t < 32 * W; t += blockDim.x) sc[t] = 0;
+  __syncthreads();
+  const int32_t n = a.ctl->list_len[a.h - 1];
+  const int32_t* list = a.lists + a.ctl->list_off[a.h - 1];
+  const int groups_per_warp = 32 / W;
+  const int g = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * groups_per_warp + lane_id() / W;
+  const int ng = ((gridDim.x * blockDim.x) >> 5) * groups_per_warp;
+  const int j = lane_id() % W;
+  for (int32_t i = g; i < n; i += ng) {
+    const int32_t u = list[i];
+    const unsigned long long d = (unsigned long long)(a.indptr[u + 1] - a.indptr[u]);
+    if (!d) continue;
+    uint32_t x = a.X[(size_t)u * W + j];
+    while (x) {
+      atomicAdd(&sc[32 * j + __ffs(x) - 1], d);
+      x &= x - 1u;
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 32 * W && t < a.nq; t += blockDim.x)
+    if (sc[t]) atomicAdd((unsigned long long*)&out[t], sc[t]);
+}
+
+// filtered: one count per (query, passing edge)
+template <int W>
+__global__ void __launch_bounds__(kThreads) edge_count_filtered_kernel(WaveArgs a, int64_t* out,
+                                                                       int heavy_pass) {
+  __shared__ uint32_t sc[32 * W];
+  for (int t = threadIdx.x; t < 32 * W; t += blockDim.x) sc[t] = 0;
+  __syncthreads();
+  CountOp<W> op{sc};
+  if (heavy_pass) drive_heavy<W, true>(a, op);
+  else drive_light<W, true>(a, a.h - 1, op, true);
+  __syncthreads();
+  for (int t = threadIdx.x; t < 32 * W && t < a.nq; t += blockDim.x)
+    if (sc[t]) atomicAdd((unsigned long long*)&out[t], (unsigned long long)sc[t]);
+}
+
+// ------------------------------------------------------------ pull hop
+
+// OR of the frontier rows of in-edges [lo, hi) of one entity, per group lane
+template <int W, bool FILTER>
+__device__ __forceinline__ uint32_t pull_range(const WaveArgs& a, int32_t lo, int32_t hi,
+                                               uint32_t seen, uint32_t valid) {
+  const unsigned gm = Grp<W>::mask();
+  const unsigned j = Grp<W>::j();
+  uint32_t acc = 0;
+  for (int32_t b = lo; b < hi; b += W) {
+    const int32_t e = b + (int32_t)j;
+    int32_t src = 0;
+    uint32_t rr = 0;
+    bool act = false;
+    if (e < hi) {
+      src = a.rsrc[e];
+      if (FILTER) rr = a.rrel[e];
+      act = (a.Xf[src >> 5] >> (src & 31)) & 1u;
+    }
+    uint32_t am = Grp<W>::ballot(act);
+    while (am) {
+      const int i = __ffs(am) - 1;
+      am &= am - 1u;
+      const int32_t u = __shfl_sync(gm, src, i, W);
+      uint32_t x = a.X[(size_t)u * W + j];
+      if (FILTER) x &= a.M[(size_t)__shfl_sync(gm, rr, i, W) * W + j];
+      acc |= x;
+    }
+    // early exit: every live query has reached (or already visited) the entity
+    if (Grp<W>::ballot(((acc | seen) & valid) != valid) == 0u) break;
+  }
+  return acc;
+}
+
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) pull_light_kernel(WaveArgs a) {
+  if (a.ctl->mode[a.h] != 1) return;
+  const int gpw = 32 / W;
+  const int64_t g0 = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * gpw + lane_id() / W;
+  const int64_t ng = (int64_t)((gridDim.x * blockDim.x) >> 5) * gpw;
+  const unsigned j = Grp<W>::j();
+  const uint32_t valid = valid_word((int)j, a.nq);
+  // uniform trip count per warp keeps group collectives convergent
+  const int64_t iters = ceil_div(a.E, ng);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t v = g0 + it * ng;
+    if (v >= a.E) continue;
+    const int32_t lo = a.rindptr[v], hi = a.rindptr[v + 1];
+    if (hi == lo || hi - lo > kHeavyPull) continue;
+    const size_t r = (size_t)v * W + j;
+    const uint32_t seen = SEM == TH_EXACT ? 0u : a.V[r];
+    if (SEM != TH_EXACT && Grp<W>::ballot((seen & valid) != valid) == 0u) continue;
+    const uint32_t acc = pull_range<W, FILTER>(a, lo, hi, seen, valid);
+    const uint32_t nb = acc & ~seen & valid;
+    if (Grp<W>::ballot(nb != 0u) == 0u) continue;
+    a.N[r] = nb;
+    if (SEM != TH_EXACT) a.V[r] = seen | nb;
+    if (j == 0) mark_next<W>(a, (int32_t)v);
+  }
+}
+
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) pull_heavy_kernel(WaveArgs a) {
+  if (a.ctl->mode[a.h] != 1) return;
+  const int gpw = 32 / W;
+  const int64_t g0 = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * gpw + lane_id() / W;
+  const int64_t ng = (int64_t)((gridDim.x * blockDim.x) >> 5) * gpw;
+  const unsigned j = Grp<W>::j();
+  const uint32_t valid = valid_word((int)j, a.nq);
+  const int64_t iters = ceil_div(a.n_chunks, ng);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t c = g0 + it * ng;
+    if (c >= a.n_chunks) continue;
+    const int32_t hv = a.chunk_hv[c];
+    const int32_t v = a.heavy_ids[hv];
+    const uint32_t seen = SEM == TH_EXACT ? 0u : a.V[(size_t)v * W + j];
+    if (SEM != TH_EXACT && Grp<W>::ballot((seen & valid) != valid) == 0u) continue;
+    const uint32_t acc = pull_range<W, FILTER>(a, a.chunk_lo[c], a.chunk_hi[c], seen, valid) &
+                         ~seen & valid;
+    if (acc) atomicOr(&a.racc[(size_t)hv * W + j], acc);
+  }
+}
+
+template <int W, int SEM>
+__global__ void __launch_bounds__(kThreads) pull_finalize_kernel(WaveArgs a) {
+  if (a.ctl->mode[a.h] != 1) return;
+  const int gpw = 32 / W;
+  const int64_t g0 = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * gpw + lane_id() / W;
+  const int64_t ng = (int64_t)((gridDim.x * blockDim.x) >> 5) * gpw;
+  const unsigned j = Grp<W>::j();
+  const uint32_t valid = valid_word((int)j, a.nq);
+  const int64_t iters = ceil_div(a.n_heavy_in, ng);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t hv = g0 + it * ng;
+    if (hv >= a.n_heavy_in) continue;
+    const int32_t v = a.heavy_ids[hv];
+    const size_t r = (size_t)v * W + j;
+    const uint32_t acc = a.racc[(size_t)hv * W + j];
+    a.racc[(size_t)hv * W + j] = 0u;
+    const uint32_t seen = SEM == TH_EXACT ? 0u : a.V[r];
+    const uint32_t nb = acc & ~seen & valid;
+    if (Grp<W>::ballot(nb != 0u) == 0u) continue;
+    a.N[r] = nb;
+    if (SEM != TH_EXACT) a.V[r] = seen | nb;
+    if (j == 0) mark_next<W>(a, v);
+  }
+}
+
+// ------------------------------------------------------------- clearing
+
+// zero rows listed in list segments [s0, s1] of matrix A
+template <int W>
+__global__ void clear_rows_kernel(uint32_t* A, const int32_t* lists, const Ctl* ctl, int s0, int s1) {
+  const int64_t lo = ctl->list_off[s0];
+  const int64_t hi = ctl->list_off[s1] + ctl->list_len[s1];
+  const int64_t n = (hi - lo) * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = lists[lo + i / W];
+    A[(size_t)u * W + (i % W)] = 0u;
+  }
+}
+
+// M[r][j] bit b = query 32j+b allows relation r
+template <int W>
+__global__ void build_mask_kernel(const uint32_t* __restrict__ masks, int mask_words, int q0,
+                                  int nq, int64_t R, uint32_t* M) {
+  const int64_t n = R * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / W;
+    const int j = (int)(i % W);
+    uint32_t word = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int q = 32 * j + b;
+      if (q >= nq) break;
+      word |= ((masks[(size_t)(q0 + q) * mask_words + (r >> 5)] >> (r & 31)) & 1u) << b;
+    }
+    M[i] = word;
+  }
+}
+
+// ------------------------------------------------------ materialisation
+
+// rows = entities; word = A & ~neg, restricted to live queries
+template <int W>
+struct DenseSrc {
+  const uint32_t* A;
+  const uint32_t* neg;
+  const uint32_t* flags;
+  int64_t nrows;
+  int nq;
+  __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
+    aux = 0;
+    const int64_t left = nrows - r0;
+    const uint32_t tail = left >= 32 ? TH_FULL : ((1u << left) - 1u);
+    return (flags ? flags[r0 >> 5] : TH_FULL) & tail;
+  }
+  __device__ __forceinline__ uint32_t word(int64_t r, int j, int64_t) const {
+    uint32_t x = A[(size_t)r * W + j];
+    if (neg) x &= ~neg[(size_t)r * W + j];
+    return x & valid_word(j, nq);
+  }
+};
+
+// rows = triples in tid order; word = X[subj[t]] & M[rel[t]]
+template <int W>
+struct TripleSrc {
+  const uint32_t* X;
+  const uint32_t* Xf;
+  const uint32_t* M;
+  const int32_t* subj;
+  const uint16_t* rel;
+  int64_t nrows;
+  int nq;
+  __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
+    const int64_t t = r0 + lane_id();
+    bool act = false;
+    aux = 0;
+    if (t < nrows) {
+      const int32_t s = subj[t];
+      act = (Xf[s >> 5] >> (s & 31)) & 1u;
+      aux = ((int64_t)rel[t] << 32) | (uint32_t)s;
+    }
+    return __ballot_sync(TH_FULL, act);
+  }
+  __device__ __forceinline__ uint32_t word(int64_t, int j, int64_t aux) const {
+    const uint32_t s = (uint32_t)aux;
+    uint32_t x = X[(size_t)s * W + j];
+    if (M) x &= M[(size_t)(aux >> 32) * W + j];
+    return x & valid_word(j, nq);
+  }
+};
+
+template <int W, class Src, bool WRITE>
+__global__ void __launch_bounds__(kThreads) mat_kernel(Src src, int64_t blk_rows, int nblk,
+                                                       int32_t* counts, const int64_t* base,
+                                                       int32_t* out, int64_t cap) {
+  __shared__ uint32_t tile[kWarps][32][W + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int blk = gw; blk < nblk; blk += nw) {
+    int64_t run[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      run[j] = 0;
+      if (WRITE) {
+        const int q = 32 * j + lane;
+        if (q < src.nq) run[j] = base[q] + counts[(size_t)q * nblk + blk];
+      }
+    }
+    const int64_t rend = src.nrows < (int64_t)(blk + 1) * blk_rows ? src.nrows : (int64_t)(blk + 1) * blk_rows;
+    for (int64_t r0 = (int64_t)blk * blk_rows; r0 < rend; r0 += 32) {
+      int64_t aux;
+      const uint32_t fl = src.prep(r0, aux);
+      if (!fl) continue;
+#pragma unroll
+      for (int it = 0; it < W; ++it) {
+        const int idx = it * 32 + lane;
+        const int row = idx / W, j = idx % W;
+        const int64_t ra = __shfl_sync(TH_FULL, aux, row);
+        tile[warp][row][j] = ((fl >> row) & 1u) ? src.word(r0 + row, j, ra) : 0u;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        uint32_t t = transpose32(tile[warp][lane][j]);
+        if (WRITE) {
+          int64_t pos = run[j];
+          run[j] += __popc(t);
+          while (t) {
+            if (pos < cap) out[pos] = (int32_t)(r0 + __ffs(t) - 1);
+            ++pos;
+            t &= t - 1u;
+          }
+        } else {
+          run[j] += __popc(t);
+        }
+      }
+      __syncwarp();
+    }
+    if (!WRITE) {
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const int q = 32 * j + lane;
+        if (q < src.nq) counts[(size_t)q * nblk + blk] = (int32_t)run[j];
+      }
+    }
+  }
+}
+
+// one block per query: exclusive scan over its block counts; totals[q]
+__global__ void mat_scan_rows_kernel(int32_t* counts, int nblk, int64_t* totals) {
+  __shared__ int32_t ws[32];
+  int32_t* c = counts + (size_t)blockIdx.x * nblk;
+  int32_t carry = 0;
+  for (int b0 = 0; b0 < nblk; b0 += blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    const int32_t v = i < nblk ? c[i] : 0;
+    int32_t x = v;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(TH_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int32_t w = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(TH_FULL, w, o);
+        if (lane >= o) w += y;
+      }
+      ws[lane] = w;
+    }
+    __syncthreads();
+    const int32_t ex = carry + (warp ? ws[warp - 1] : 0) + x - v;
+    if (i < nblk) c[i] = ex;
+    carry += ws[(blockDim.x >> 5) - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+// single block: per-query output offsets from the running cursor
+__global__ void mat_scan_queries_kernel(const int64_t* totals, int nq, int64_t* off, int64_t* len,
+                                        int64_t* cursor) {
+  __shared__ int64_t ws[32];
+  const int q = threadIdx.x;
+  const int64_t v = q < nq ? totals[q] : 0;
+  int64_t x = v;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(TH_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(TH_FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  const int64_t base = *cursor;
+  const int64_t ex = (warp ? ws[warp - 1] : 0) + x - v;
+  if (q < nq) {
+    off[q] = base + ex;
+    len[q] = v;
+  }
+  __syncthreads();
+  if (q == 0) *cursor = base + ws[(blockDim.x >> 5) - 1];
+}
+
+// ---------------------------------------------------------------- host
+
+template <typename T>
+T* ensure(DBuf& b, int64_t n, cudaStream_t st) {
+  const size_t need = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
+  if (b.bytes < need) {
+    if (b.p) TH_CUDA(cudaFreeAsync(b.p, st));
+    b.p = nullptr;
+    TH_CUDA(cudaMallocAsync(&b.p, need, st));
+    b.bytes = need;
+  }
+  return static_cast<T*>(b.p);
+}
+
+unsigned persistent_grid() { return kNumSMs * 8; }
+
+unsigned grid_for(int64_t n) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kThreads), kNumSMs * 16));
+}
+
+int pick_words(int nq) {
+  int w = 1;
+  while (32 * w < nq) w <<= 1;
+  return w;
+}
+
+struct WaveBufs {
+  int W;
+  uint32_t *X, *N, *V, *S, *Xf, *Nf, *Vf, *M;
+  int32_t *lists, *heavy, *counts;
+  uint32_t* racc;
+  int64_t* totals;
+  Ctl* ctl;
+};
+
+template <int W>
+void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
+                       const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
+                       int64_t cap, int64_t* cursor) {
+  const Graph* g = s->g;
+  const int64_t rows = g->E;
+  if (rows == 0) {
+    TH_CUDA(cudaMemsetAsync(len, 0, sizeof(int64_t) * nq, s->st));
+    TH_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * nq, s->st));
+    return;
+  }
+  const int64_t blk_rows = std::max<int64_t>(32, ceil_div(ceil_div(rows, kMatBlocks), 32) * 32);
+  const int nblk = (int)ceil_div(rows, blk_rows);
+  DenseSrc<W> src{A, neg, flags, rows, nq};
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nblk, kWarps), kNumSMs * 8));
+  mat_kernel<W, DenseSrc<W>, false><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
+                                                                  nullptr, nullptr, 0);
+  TH_LAUNCHED();
+  mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
+  TH_LAUNCHED();
+  mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
+  TH_LAUNCHED();
+  mat_kernel<W, DenseSrc<W>, true><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts, off,
+                                                                 out, cap);
+  TH_LAUNCHED();
+  s->launches += 4;
+}
+
+template <int W>
+void materialize_triples(Session* s, WaveBufs& b, int nq, int64_t* off, int64_t* len, int32_t* out,
+                         int64_t cap, int64_t* cursor) {
+  const Graph* g = s->g;
+  const int64_t rows = g->T;
+  if (rows == 0) {
+    TH_CUDA(cudaMemsetAsync(len, 0, sizeof(int64_t) * nq, s->st));
+    TH_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * nq, s->st));
+    return;
+  }
+  const int64_t blk_rows = std::max<int64_t>(32, ceil_div(ceil_div(rows, kMatBlocks), 32) * 32);
+  const int nblk = (int)ceil_div(rows, blk_rows);
+  TripleSrc<W> src{b.X, b.Xf, s->last.d_rel_masks ? b.M : nullptr, g->subj, g->rel, rows, nq};
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nblk, kWarps), kNumSMs * 8));
+  mat_kernel<W, TripleSrc<W>, false><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
+                                                                   nullptr, nullptr, 0);
+  TH_LAUNCHED();
+  mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
+  TH_LAUNCHED();
+  mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
+  TH_LAUNCHED();
+  mat_kernel<W, TripleSrc<W>, true><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
+                                                                  off, out, cap);
+  TH_LAUNCHED();
+  s->launches += 4;
+}
+
+template <int W, int SEM, bool FILTER>
+void expand_hop(Session* s, const WaveArgs& a) {
+  const unsigned pg = persistent_grid();
+  {
+    ProfScope ps(s, TH_PROF_PUSH);
+    push_light_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
+    TH_LAUNCHED();
+    push_heavy_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
+    TH_LAUNCHED();
+    s->launches += 2;
+  }
+  if (s->g->rindptr) {
+    ProfScope ps(s, TH_PROF_PULL);
+    pull_light_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
+    TH_LAUNCHED();
+    s->launches += 1;
+    if (s->g->n_chunks > 0) {
+      pull_heavy_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
+      TH_LAUNCHED();
+      pull_finalize_kernel<W, SEM><<<pg, kThreads, 0, s->st>>>(a);
+      TH_LAUNCHED();
+      s->launches += 2;
+    }
+  }
+}
+
+template <int W>
+void run_wave(Session* s, const th_query* q, int q0, int nq) {
+  const Graph* g = s->g;
+  cudaStream_t st = s->st;
+  const int64_t E = g->E, k = q->k, B = q->n_queries;
+  const int64_t rows = std::max<int64_t>(E, 1) * W;
+  const int64_t fwords = ceil_div(std::max<int64_t>(E, 1), 32) + 1;
+  const bool filter = q->d_rel_masks != nullptr;
+  const int sem = q->semantics;
+  WaveBufs b{};
+  b.W = W;
+  b.X = ensure<uint32_t>(s->X, rows, st);
+  b.N = ensure<uint32_t>(s->N, rows, st);
+  b.V = ensure<uint32_t>(s->V, rows, st);
+  b.S = sem == TH_CUMULATIVE ? ensure<uint32_t>(s->S, rows, st) : nullptr;
+  b.Xf = ensure<uint32_t>(s->Xf, fwords, st);
+  b.Nf = ensure<uint32_t>(s->Nf, fwords, st);
+  b.Vf = ensure<uint32_t>(s->Vf, fwords, st);
+  b.lists = ensure<int32_t>(s->lists, (k + 1) * std::max<int64_t>(E, 1), st);
+  b.heavy = ensure<int32_t>(s->heavy, std::max<int64_t>(E, 1), st);
+  b.racc = ensure<uint32_t>(s->racc, std::max<int64_t>(g->n_heavy, 1) * W, st);
+  b.M = filter ? ensure<uint32_t>(s->M, std::max<int64_t>(g->R, 1) * W, st) : nullptr;
+  b.counts = ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
+  b.totals = ensure<int64_t>(s->totals, kMaxWave, st);
+  b.ctl = static_cast<Ctl*>(s->ctl.p);
+  TH_CUDA(cudaMemsetAsync(b.ctl, 0, offsetof(Ctl, err), st));
+  TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
+  TH_CUDA(cudaMemsetAsync(b.Nf, 0, fwords * 4, st));
+  TH_CUDA(cudaMemsetAsync(b.Vf, 0, fwords * 4, st));
+
+  WaveArgs a{};
+  a.indptr = g->indptr;
+  a.csr_obj = g->csr_obj;
+  a.csr_rel = g->csr_rel;
+  a.rindptr = g->rindptr;
+  a.rsrc = g->rsrc;
+  a.rrel = g->rrel;
+  a.heavy_ids = g->heavy_ids;
+  a.chunk_hv = g->chunk_hv;
+  a.chunk_lo = g->chunk_lo;
+  a.chunk_hi = g->chunk_hi;
+  a.n_chunks = g->n_chunks;
+  a.n_heavy_in = g->n_heavy;
+  a.E = E;
+  a.T = g->T;
+  a.X = b.X;
+  a.N = b.N;
+  a.V = b.V;
+  a.S = b.S;
+  a.Xf = b.Xf;
+  a.Nf = b.Nf;
+  a.Vf = b.Vf;
+  a.M = b.M;
+  a.lists = b.lists;
+  a.heavy = b.heavy;
+  a.racc = b.racc;
+  a.ctl = b.ctl;
+  a.nq = nq;
+  a.sem = sem;
+  a.h = 0;
+
+  {
+    ProfScope ps(s, TH_PROF_SETUP);
+    if (filter) {
+      build_mask_kernel<W><<<grid_for(g->R * W), kThreads, 0, st>>>(q->d_rel_masks, q->mask_words,
+                                                                     q0, nq, g->R, b.M);
+      TH_LAUNCHED();
+      s->launches += 1;
+    }
+    seed_init_kernel<W><<<grid_for((int64_t)nq * 32), kThreads, 0, st>>>(a, q->d_seed_offsets,
+                                                                         q->d_seeds, q0);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+
+  int64_t* f_off = static_cast<int64_t*>(s->f_off.p);
+  int64_t* f_len = static_cast<int64_t*>(s->f_len.p);
+  int64_t* a_off = static_cast<int64_t*>(s->a_off.p);
+  int64_t* a_len = static_cast<int64_t*>(s->a_len.p);
+  int64_t* edges = static_cast<int64_t*>(s->edges.p);
+  const bool want_f = q->flags & TH_WANT_FRONTIERS;
+  const bool want_a = q->flags & TH_WANT_ACTIVATED;
+  const bool paths_need_l0 = (q->flags & TH_WANT_PATHS) && !(q->flags & 0x8u);
+  const unsigned pg = persistent_grid();
+
+  for (int h = 1; h <= k; ++h) {
+    a.h = h;
+    {
+      ProfScope ps(s, TH_PROF_SETUP);
+      begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, g->T, s->pull_divisor, g->rindptr != nullptr);
+      TH_LAUNCHED();
+      s->launches += 1;
+    }
+    {
+      ProfScope ps(s, TH_PROF_EDGES);
+      int64_t* e_out = edges + (h - 1) * B + q0;
+      if (filter) {
+        edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(a, e_out, 0);
+        TH_LAUNCHED();
+        edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(a, e_out, 1);
+        TH_LAUNCHED();
+        s->launches += 2;
+      } else {
+        edge_count_kernel<W><<<pg, kThreads, 0, st>>>(a, e_out);
+        TH_LAUNCHED();
+        s->launches += 1;
+      }
+    }
+    if (want_a || (paths_need_l0 && h == 1)) {
+      ProfScope ps(s, TH_PROF_ACTIVATED);
+      materialize_triples<W>(s, b, nq, a_off + (h - 1) * B + q0, a_len + (h - 1) * B + q0,
+                             static_cast<int32_t*>(s->a_ids.p), s->a_cap, &b.ctl->act_used);
+    }
+    if (filter) {
+      if (sem == TH_EXACT) expand_hop<W, TH_EXACT, true>(s, a);
+      else expand_hop<W, TH_FRONTIER, true>(s, a);
+    } else {
+      if (sem == TH_EXACT) expand_hop<W, TH_EXACT, false>(s, a);
+      else expand_hop<W, TH_FRONTIER, false>(s, a);
+    }
+    if (want_f) {
+      ProfScope ps(s, TH_PROF_FRONTIER);
+      if (sem == TH_CUMULATIVE)
+        materialize_dense<W>(s, b, b.V, b.S, b.Vf, nq, f_off + (h - 1) * B + q0,
+                             f_len + (h - 1) * B + q0, static_cast<int32_t*>(s->f_ids.p), s->f_cap,
+                             &b.ctl->ids_used);
+      else
+        materialize_dense<W>(s, b, b.N, nullptr, b.Nf, nq, f_off + (h - 1) * B + q0,
+                             f_len + (h - 1) * B + q0, static_cast<int32_t*>(s->f_ids.p), s->f_cap,
+                             &b.ctl->ids_used);
+    }
+    {
+      // retire X (rows of list segment h-1) and swap roles
+      ProfScope ps(s, TH_PROF_CLEAR);
+      clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1);
+      TH_LAUNCHED();
+      TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
+      s->launches += 1;
+    }
+    std::swap(b.X, b.N);
+    std::swap(b.Xf, b.Nf);
+    std::swap(a.X, a.N);
+    std::swap(a.Xf, a.Nf);
+  }
+  // leave every matrix zero for the next wave
+  ProfScope ps(s, TH_PROF_CLEAR);
+  clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, (int)k, (int)k);
+  TH_LAUNCHED();
+  s->launches += 1;
+  if (sem != TH_EXACT) {
+    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+  if (sem == TH_CUMULATIVE) {
+    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+}
+
+void clear_state(Session* s, int64_t rows, int64_t fwords, bool cum) {
+  (void)fwords;
+  for (DBuf* d : {&s->X, &s->N, &s->V}) TH_CUDA(cudaMemsetAsync(d->p, 0, rows * 4, s->st));
+  if (cum) TH_CUDA(cudaMemsetAsync(s->S.p, 0, rows * 4, s->st));
+}
+
+}  // namespace
+
+ProfScope::ProfScope(Session* s_, int c) : s(s_), cat(c), l0(s_->launches) {
+  if (!s->prof) return;
+  if (s->ev_used + 2 > s->ev_pool.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      TH_CUDA(cudaEventCreate(&e));
+      s->ev_pool.push_back(e);
+    }
+  }
+  TH_CUDA(cudaEventRecord(s->ev_pool[s->ev_used], s->st));
+}
+
+ProfScope::~ProfScope() noexcept(false) {
+  if (!s->prof) return;
+  TH_CUDA(cudaEventRecord(s->ev_pool[s->ev_used + 1], s->st));
+  s->ev_used += 2;
+  s->pending_cat.push_back(cat);
+  s->pending_launch.push_back(s->launches - l0);
+}
+
+static void drain_profile(Session* s) {
+  for (size_t i = 0; i < s->pending_cat.size(); ++i) {
+    float ms = 0.f;
+    TH_CUDA(cudaEventElapsedTime(&ms, s->ev_pool[2 * i], s->ev_pool[2 * i + 1]));
+    s->prof_ms[s->pending_cat[i]] += ms;
+    s->prof_launches[s->pending_cat[i]] += s->pending_launch[i];
+  }
+  s->pending_cat.clear();
+  s->pending_launch.clear();
+  s->ev_used = 0;
+}
+
+int session_profile(Session* s, double* ms, int64_t* launches, int n) {
+  TH_CUDA(cudaStreamSynchronize(s->st));
+  drain_profile(s);
+  for (int i = 0; i < n && i < TH_PROF_CATEGORIES; ++i) {
+    if (ms) ms[i] = s->prof_ms[i];
+    if (launches) launches[i] = s->prof_launches[i];
+    s->prof_ms[i] = 0;
+    s->prof_launches[i] = 0;
+  }
+  return TH_OK;
+}
+
+int session_wave_lists(Session* s, int64_t* lens, int n) {
+  if (!s->ctl.p) return TH_ERR_STATE;
+  TH_CUDA(cudaStreamSynchronize(s->st));
+  Ctl c;
+  TH_CUDA(cudaMemcpy(&c, s->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < kMaxK + 2; ++i) lens[i] = i <= s->last.k ? c.list_len[i] : 0;
+  return TH_OK;
+}
+
+int session_run(Session* s, const th_query* q) {
+  const Graph* g = s->g;
+  if (q->k < 1) {
+    set_error("hop count must be >= 1");
+    return TH_ERR_INVALID;
+  }
+  if (q->k > kMaxK) {
+    set_error("hop count above the engine limit of " + std::to_string(kMaxK));
+    return TH_ERR_INVALID;
+  }
+  if (q->semantics < TH_EXACT || q->semantics > TH_CUMULATIVE) {
+    set_error("unknown hop semantics");
+    return TH_ERR_INVALID;
+  }
+  if (q->n_queries < 0 || (q->n_queries > 0 && (!q->d_seed_offsets || !q->d_seeds))) {
+    set_error("bad query arrays");
+    return TH_ERR_INVALID;
+  }
+  if (q->d_rel_masks && q->mask_words < ceil_div(g->R, 32)) {
+    set_error("mask_words too small for the relation count");
+    return TH_ERR_INVALID;
+  }
+  if ((q->flags & TH_WANT_PATHS) && q->max_paths < -1) {
+    set_error("max_paths must be >= 0");
+    return TH_ERR_INVALID;
+  }
+  cudaStream_t st = s->st;
+  const int64_t B = q->n_queries, k = q->k;
+  const int64_t kb = std::max<int64_t>(k * B, 1);
+  ensure<Ctl>(s->ctl, 1, st);
+  ensure<int64_t>(s->f_off, kb, st);
+  ensure<int64_t>(s->f_len, kb, st);
+  ensure<int64_t>(s->a_off, kb, st);
+  ensure<int64_t>(s->a_len, kb, st);
+  ensure<int64_t>(s->edges, kb, st);
+  // output capacities grow to the last observed need (th_finish)
+  s->f_cap = std::max<int64_t>({s->f_cap, s->last_f_need, 1 << 16});
+  s->a_cap = std::max<int64_t>({s->a_cap, s->last_a_need, 1 << 16});
+  ensure<int32_t>(s->f_ids, s->f_cap, st);
+  ensure<int32_t>(s->a_ids, s->a_cap, st);
+  TH_CUDA(cudaMemsetAsync(s->ctl.p, 0, sizeof(Ctl), st));
+  TH_CUDA(cudaMemsetAsync(s->edges.p, 0, sizeof(int64_t) * kb, st));
+  TH_CUDA(cudaMemsetAsync(s->f_len.p, 0, sizeof(int64_t) * kb, st));
+  TH_CUDA(cudaMemsetAsync(s->f_off.p, 0, sizeof(int64_t) * kb, st));
+  TH_CUDA(cudaMemsetAsync(s->a_len.p, 0, sizeof(int64_t) * kb, st));
+  TH_CUDA(cudaMemsetAsync(s->a_off.p, 0, sizeof(int64_t) * kb, st));
+  s->last = *q;
+  s->has_run = true;
+
+  const int wave = std::min<int64_t>(std::max<int64_t>(B, 1), kMaxWave);
+  const int W = pick_words(wave);
+  // matrices must start zero: (re)allocation leaves garbage, so clear on growth
+  const int64_t rows = std::max<int64_t>(g->E, 1) * W;
+  const size_t need = (size_t)rows * 4;
+  const bool fresh = s->X.bytes < need || s->N.bytes < need || s->V.bytes < need ||
+                     (q->semantics == TH_CUMULATIVE && s->S.bytes < need);
+  if (fresh) {
+    ensure<uint32_t>(s->X, rows, st);
+    ensure<uint32_t>(s->N, rows, st);
+    ensure<uint32_t>(s->V, rows, st);
+    if (q->semantics == TH_CUMULATIVE) ensure<uint32_t>(s->S, rows, st);
+    clear_state(s, (int64_t)(std::min({s->X.bytes, s->N.bytes, s->V.bytes}) / 4), 0,
+                q->semantics == TH_CUMULATIVE);
+    if (q->semantics == TH_CUMULATIVE) TH_CUDA(cudaMemsetAsync(s->S.p, 0, s->S.bytes, st));
+  } else if (q->semantics == TH_CUMULATIVE && s->S.p == nullptr) {
+    ensure<uint32_t>(s->S, rows, st);
+    TH_CUDA(cudaMemsetAsync(s->S.p, 0, s->S.bytes, st));
+  }
+  for (int64_t q0 = 0; q0 < B; q0 += wave) {
+    const int nq = (int)std::min<int64_t>(wave, B - q0);
+    switch (W) {
+      case 1: run_wave<1>(s, q, (int)q0, nq); break;
+      case 2: run_wave<2>(s, q, (int)q0, nq); break;
+      case 4: run_wave<4>(s, q, (int)q0, nq); break;
+      case 8: run_wave<8>(s, q, (int)q0, nq); break;
+      case 16: run_wave<16>(s, q, (int)q0, nq); break;
+      default: run_wave<32>(s, q, (int)q0, nq); break;
+    }
+  }
+  if (q->flags & TH_WANT_PATHS) {
+    const Ctl* ctl = static_cast<const Ctl*>(s->ctl.p);
+    PathArgs pa{};
+    pa.indptr = g->indptr;
+    pa.csr_tid = g->csr_tid;
+    pa.csr_obj = g->csr_obj;
+    pa.csr_rel = g->csr_rel;
+    pa.t_obj = g->obj;
+    pa.t_rel = g->rel;
+    pa.qoff = q->d_seed_offsets;
+    pa.seeds = q->d_seeds;
+    pa.masks = q->d_rel_masks;
+    pa.mask_words = q->mask_words;
+    pa.l0_off = static_cast<const int64_t*>(s->a_off.p);
+    pa.l0_len = static_cast<const int64_t*>(s->a_len.p);
+    pa.l0_ids = static_cast<const int32_t*>(s->a_ids.p);
+    pa.singleton = (q->flags & 0x8u) != 0;
+    pa.B = (int32_t)B;
+    pa.k = (int32_t)k;
+    pa.E = g->E;
+    pa.max_paths = q->max_paths;
+    s->p_cap = std::max<int64_t>({s->p_cap, s->last_p_need, 1 << 12});
+    pa.p_off = ensure<int64_t>(s->p_off, B + 1, st);
+    pa.p_cnt = ensure<int64_t>(s->p_cnt, std::max<int64_t>(B, 1), st);
+    pa.p_trunc = ensure<uint8_t>(s->p_trunc, std::max<int64_t>(B, 1), st);
+    pa.p_tids = ensure<int32_t>(s->p_tids, s->p_cap * k, st);
+    pa.scratch = ensure<int64_t>(s->p_scratch, scan_scratch_elems_i64(B + 1), st);
+    pa.cap = s->p_cap;
+    pa.used = const_cast<int64_t*>(&ctl->path_used);
+    ProfScope ps(s, TH_PROF_PATHS);
+    s->launches += launch_paths(pa, st);
+  }
+  return TH_OK;
+}
+
+int session_finish(Session* s, th_result* out) {
+  if (!s->has_run) {
+    set_error("th_finish before th_run");
+    return TH_ERR_STATE;
+  }
+  TH_CUDA(cudaStreamSynchronize(s->st));
+  if (s->prof) drain_profile(s);
+  Ctl c;
+  TH_CUDA(cudaMemcpy(&c, s->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  const th_query& q = s->last;
+  std::memset(out, 0, sizeof(*out));
+  out->n_queries = q.n_queries;
+  out->k = q.k;
+  out->frontier_off = static_cast<const int64_t*>(s->f_off.p);
+  out->frontier_len = static_cast<const int64_t*>(s->f_len.p);
+  out->frontier_ids = static_cast<const int32_t*>(s->f_ids.p);
+  out->act_off = static_cast<const int64_t*>(s->a_off.p);
+  out->act_len = static_cast<const int64_t*>(s->a_len.p);
+  out->act_ids = static_cast<const int32_t*>(s->a_ids.p);
+  out->edges = static_cast<const int64_t*>(s->edges.p);
+  out->frontier_total = c.ids_used;
+  out->act_total = c.act_used;
+  out->push_hops = c.push_hops;
+  out->pull_hops = c.pull_hops;
+  if (q.flags & TH_WANT_PATHS) {
+    out->path_off = static_cast<const int64_t*>(s->p_off.p);
+    out->path_count = static_cast<const int64_t*>(s->p_cnt.p);
+    out->path_truncated = static_cast<const uint8_t*>(s->p_trunc.p);
+    out->path_tids = static_cast<const int32_t*>(s->p_tids.p);
+    out->path_total = c.path_used;
+  }
+  if (c.err) {
+    set_error("seed id out of range for the graph's entity count");
+    return TH_ERR_RANGE;
+  }
+  bool overflow = false;
+  if (c.ids_used > s->f_cap) {
+    s->last_f_need = c.ids_used + c.ids_used / 4;
+    overflow = true;
+  }
+  if (c.act_used > s->a_cap) {
+    s->last_a_need = c.act_used + c.act_used / 4;
+    overflow = true;
+  }
+  if ((q.flags & TH_WANT_PATHS) && c.path_used > s->p_cap) {
+    s->last_p_need = c.path_used + c.path_used / 4;
+    overflow = true;
+  }
+  if (overflow) {
+    set_error("result capacity exceeded; capacities grown, re-run the query");
+    return TH_ERR_OVERFLOW;
+  }
+  return TH_OK;
+}
+
+void session_free(Session* s) {
+  for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy, &s->racc,
+                  &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
+                  &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
+                  &s->p_scratch}) {
+    if (d->p) cudaFreeAsync(d->p, s->st);
+    d->p = nullptr;
+    d->bytes = 0;
+  }
+  cudaStreamSynchronize(s->st);
+  for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
+  s->ev_pool.clear();
+}
+
+// partition.py:80-84 multiplicative hash; -1 for entities without out-edges
+__global__ void plan_owner_hash_kernel(const int32_t* __restrict__ indptr, int64_t E, int32_t m,
+                                       int32_t* owner) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const bool subject = indptr[e + 1] > indptr[e];
+    const uint32_t h = (uint32_t)((uint64_t)e * 0x9E3779B1ull);
+    owner[e] = subject ? (int32_t)(h % (uint32_t)m) : -1;
+  }
+}
+
+void plan_owner_hash(const Graph* g, int32_t m, int32_t* d_owner, cudaStream_t st) {
+  if (g->E == 0) return;
+  plan_owner_hash_kernel<<<grid_for(g->E), kThreads, 0, st>>>(g->indptr, g->E, m, d_owner);
+  TH_LAUNCHED();
+}
+
+}  // namespace th

@@ -1,0 +1,265 @@
+// K5: path reconstruction on the device.
+//
+// Reference: reconstruct_paths / HopAdjacency / assemble_paths
+// (incidence.py:344-408).  Paths are ALL length-k walks from the query's
+// seed set, ordered lexicographically by their triple-id sequence, capped at
+// max_paths with a `truncated` flag (incidence.py:386-388).  Every step of a
+// walk is an activated triple of its hop under exact-walk semantics, so
+// level d>0 candidates are exactly the CSR row of the previous object (rows
+// are tid-ascending by construction, incidence.py:186-188), filtered by the
+// query's relation mask.  Level 0 is the seed's row (single-seed queries) or
+// the hop-1 activated list (seed sets: rows interleave by tid).
+//
+// One warp per query runs an explicit-stack DFS.  Every level scans 32
+// candidates per step with a ballot; the second-to-last level takes 32
+// candidates at once so empty rows cost nothing and, when counting without a
+// relation filter, whole rows are counted from their lengths.  Two passes:
+// COUNT (saturating at max_paths+1 -> truncated flag) and WRITE into a packed
+// [path][k] triple-id array whose offsets come from a device scan.
+#include <climits>
+
+#include "common.cuh"
+#include "paths.cuh"
+#include "prims.cuh"
+
+namespace th {
+namespace {
+
+constexpr int kPathThreads = 128;
+constexpr int kMaxDepth = 32;
+
+struct Cand {
+  int32_t tid, obj;
+  uint32_t rel;
+};
+
+__device__ __forceinline__ bool rel_ok(const PathArgs& a, int q, uint32_t r) {
+  if (!a.masks) return true;
+  return (a.masks[(size_t)q * a.mask_words + (r >> 5)] >> (r & 31)) & 1u;
+}
+
+// level-0 candidate i (list mode) or CSR slot i (row mode)
+__device__ __forceinline__ Cand cand_l0(const PathArgs& a, bool list_mode, int64_t i) {
+  Cand c;
+  if (list_mode) {
+    c.tid = a.l0_ids[i];
+    c.obj = a.t_obj[c.tid];
+    c.rel = a.t_rel[c.tid];
+  } else {
+    c.tid = a.csr_tid[i];
+    c.obj = a.csr_obj[i];
+    c.rel = a.csr_rel[i];
+  }
+  return c;
+}
+
+__device__ __forceinline__ Cand cand_csr(const PathArgs& a, int64_t i) {
+  Cand c;
+  c.tid = a.csr_tid[i];
+  c.obj = a.csr_obj[i];
+  c.rel = a.csr_rel[i];
+  return c;
+}
+
+template <bool WRITE>
+__device__ __forceinline__ void emit_range(const PathArgs& a, int q, int d, bool list_mode,
+                                           int64_t lo, int64_t hi, const int32_t* stack_tid,
+                                           int64_t& count, int64_t limit, int64_t out_base) {
+  const unsigned lane = lane_id();
+  for (int64_t b = lo; b < hi && count < limit; b += 32) {
+    const int64_t i = b + lane;
+    bool pass = false;
+    Cand c{0, 0, 0};
+    if (i < hi) {
+      c = d == 0 ? cand_l0(a, list_mode, i) : cand_csr(a, i);
+      pass = rel_ok(a, q, c.rel);
+    }
+    const unsigned bal = __ballot_sync(TH_FULL, pass);
+    if (WRITE && pass) {
+      const int64_t idx = count + __popc(bal & lanemask_lt());
+      const int64_t p = out_base + idx;
+      if (idx < limit && p < a.cap) {
+        int32_t* dst = a.p_tids + p * a.k;
+        for (int dd = 0; dd < d; ++dd) dst[dd] = stack_tid[dd];
+        dst[d] = c.tid;
+      }
+    }
+    count += __popc(bal);
+  }
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
+  __shared__ int32_t stack_tid_s[kPathThreads / 32][kMaxDepth];
+  __shared__ int64_t cur_s[kPathThreads / 32][kMaxDepth];
+  __shared__ int64_t end_s[kPathThreads / 32][kMaxDepth];
+  const int warp = threadIdx.x >> 5;
+  const unsigned lane = lane_id();
+  int32_t* stack_tid = stack_tid_s[warp];
+  int64_t* cur = cur_s[warp];
+  int64_t* end = end_s[warp];
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int k = a.k;
+  for (int q = gw; q < a.B; q += nw) {
+    bool list_mode = !a.singleton;
+    int64_t lo0 = 0, hi0 = 0;
+    if (list_mode) {
+      lo0 = a.l0_off[q];
+      hi0 = lo0 + a.l0_len[q];
+    } else {
+      const int32_t slo = a.qoff[q], shi = a.qoff[q + 1];
+      if (shi > slo) {
+        const int32_t s = a.seeds[slo];
+        if (s >= 0 && s < a.E) {
+          lo0 = a.indptr[s];
+          hi0 = a.indptr[s + 1];
+        }
+      }
+    }
+    int64_t limit, out_base = 0;
+    if (WRITE) {
+      limit = a.p_cnt[q];
+      out_base = a.p_off[q];
+    } else {
+      limit = a.max_paths < 0 ? LLONG_MAX : a.max_paths + 1;
+    }
+    int64_t count = 0;
+    if (limit > 0) {
+      int d = 0;
+      if (lane == 0) {
+        cur[0] = lo0;
+        end[0] = hi0;
+      }
+      __syncwarp();
+      while (d >= 0 && count < limit) {
+        if (d == k - 1) {
+          emit_range<WRITE>(a, q, d, list_mode, cur[d], end[d], stack_tid, count, limit, out_base);
+          --d;
+          continue;
+        }
+        if (d == k - 2) {
+          // batch of 32 candidates; their rows are the last level
+          const int64_t b = cur[d], e = end[d];
+          if (b >= e) {
+            --d;
+            continue;
+          }
+          const int64_t i = b + lane;
+          bool pass = false;
+          Cand c{0, 0, 0};
+          int64_t rlo = 0, rhi = 0;
+          if (i < e) {
+            c = d == 0 ? cand_l0(a, list_mode, i) : cand_csr(a, i);
+            pass = rel_ok(a, q, c.rel);
+            if (pass) {
+              rlo = a.indptr[c.obj];
+              rhi = a.indptr[c.obj + 1];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) cur[d] = b + 32;
+          __syncwarp();
+          unsigned nonempty = __ballot_sync(TH_FULL, pass && rhi > rlo);
+          if (!WRITE && !a.masks) {
+            int64_t n = rhi - rlo;
+            for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(TH_FULL, n, o);
+            count += n;
+            continue;
+          }
+          while (nonempty && count < limit) {
+            const int f = __ffs(nonempty) - 1;
+            nonempty &= nonempty - 1u;
+            const int32_t t = __shfl_sync(TH_FULL, c.tid, f);
+            const int64_t lo = __shfl_sync(TH_FULL, rlo, f), hi = __shfl_sync(TH_FULL, rhi, f);
+            if (lane == 0) stack_tid[d] = t;
+            __syncwarp();
+            emit_range<WRITE>(a, q, d + 1, false, lo, hi, stack_tid, count, limit, out_base);
+            __syncwarp();
+          }
+          // drain the skipped lanes' state when the limit was hit
+          continue;
+        }
+        // generic level: advance to the next passing candidate
+        bool found = false;
+        int32_t nobj = 0;
+        while (cur[d] < end[d]) {
+          const int64_t b = cur[d];
+          const int64_t i = b + lane;
+          bool pass = false;
+          Cand c{0, 0, 0};
+          if (i < end[d]) {
+            c = d == 0 ? cand_l0(a, list_mode, i) : cand_csr(a, i);
+            pass = rel_ok(a, q, c.rel);
+          }
+          const unsigned bal = __ballot_sync(TH_FULL, pass);
+          __syncwarp();
+          if (bal) {
+            const int f = __ffs(bal) - 1;
+            const int32_t t = __shfl_sync(TH_FULL, c.tid, f);
+            nobj = __shfl_sync(TH_FULL, c.obj, f);
+            if (lane == 0) {
+              stack_tid[d] = t;
+              cur[d] = b + f + 1;
+            }
+            found = true;
+            __syncwarp();
+            break;
+          }
+          if (lane == 0) cur[d] = b + 32;
+          __syncwarp();
+        }
+        if (!found) {
+          --d;
+          continue;
+        }
+        ++d;
+        if (lane == 0) {
+          cur[d] = a.indptr[nobj];
+          end[d] = a.indptr[nobj + 1];
+        }
+        __syncwarp();
+      }
+    }
+    if (!WRITE && lane == 0) {
+      const int64_t cap = a.max_paths;
+      a.p_cnt[q] = cap < 0 ? count : min(count, cap);
+      a.p_trunc[q] = cap >= 0 && count > cap;
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void paths_total_kernel(int64_t* off, const int64_t* cnt, int32_t B, int64_t* used) {
+  const int64_t tot = B > 0 ? off[B - 1] + cnt[B - 1] : 0;
+  off[B] = tot;
+  *used = tot;
+}
+
+}  // namespace
+
+int64_t scan_scratch_elems_i64(int64_t n) { return scan_scratch_elems<int64_t>(n); }
+
+int launch_paths(const PathArgs& a, cudaStream_t st) {
+  if (a.k > kMaxDepth) return 0;
+  int launches = 0;
+  const unsigned grid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)a.B * 32, kPathThreads),
+                                                       kNumSMs * 16));
+  if (a.B > 0) {
+    paths_kernel<false><<<grid, kPathThreads, 0, st>>>(a);
+    TH_LAUNCHED();
+    launches += 1 + scan_exclusive<int64_t>(a.p_cnt, a.p_off, a.B, a.scratch, st);
+  }
+  paths_total_kernel<<<1, 1, 0, st>>>(a.p_off, a.p_cnt, a.B, a.used);
+  TH_LAUNCHED();
+  launches += 1;
+  if (a.B > 0) {
+    paths_kernel<true><<<grid, kPathThreads, 0, st>>>(a);
+    TH_LAUNCHED();
+    launches += 1;
+  }
+  return launches;
+}
+
+}  // namespace th

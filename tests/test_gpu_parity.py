@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden vectors
+and the CPU oracle.  Integer/index work, so the bar is bit-exact."""
+
+import numpy as np
+import pytest
+
+from golden_io import all_cases, load_case
+from oracle import khop_oracle as orc
+
+pytestmark = pytest.mark.gpu
+CASES = all_cases()
+
+
+@pytest.fixture(scope="module")
+def th(cuda_device):
+    import paper_2604_18913_b200 as th
+
+    return th
+
+
+def _masks_for(th, q, n_relations, device):
+    import torch
+
+    if q.relations is None:
+        return None
+    from paper_2604_18913_b200.retriever import _relation_masks
+
+    w = _relation_masks(q.relations, 1, n_relations)
+    return torch.from_numpy(w.view(np.int32)).to(device)
+
+
+@pytest.mark.parametrize("path", CASES, ids=[p.stem for p in CASES])
+def test_golden_case_query_by_query(th, path, cuda_device):
+    """Every reference golden query (seed sets, filters, caps) through Retriever.run."""
+    import torch
+
+    case = load_case(path)
+    g = th.build_incidence((case.subj, case.rel, case.obj), case.n_entities, case.n_relations)
+    ret = th.Retriever(g)
+    for q in case.queries:
+        seeds = torch.tensor(sorted(set(q.seeds)), dtype=torch.int32, device=cuda_device)
+        offs = torch.tensor([0, seeds.numel()], dtype=torch.int32, device=cuda_device)
+        masks = _masks_for(th, q, case.n_relations, cuda_device)
+        r = ret.run(offs, seeds, q.k, q.semantics, masks, activated=True, paths=q.want_paths,
+                    max_paths=q.max_paths if q.want_paths else 0, singleton=seeds.numel() == 1)
+        for h in range(q.k):
+            assert np.array_equal(r.frontier(0, h + 1), q.frontiers[h]), (case.name, q.seeds, h)
+            assert np.array_equal(r.activated(0, h + 1), q.activated[h]), (case.name, q.seeds, h)
+            assert int(r.edges[h, 0]) == q.activated[h].size
+        if q.want_paths:
+            assert r.path_tid_tuples(0) == q.paths, (case.name, q.seeds, q.max_paths)
+            assert r.truncated(0) == q.truncated
+
+
+@pytest.mark.parametrize("path", CASES, ids=[p.stem for p in CASES])
+def test_golden_case_batched_retrieve(th, path):
+    """All single-seed golden queries of a case, batched by (k, semantics, filter)."""
+    case = load_case(path)
+    g = th.build_incidence((case.subj, case.rel, case.obj), case.n_entities, case.n_relations)
+    groups = {}
+    for q in case.queries:
+        if len(q.seeds) == 1:
+            key = (q.k, q.semantics, q.want_paths, q.max_paths)
+            groups.setdefault(key, []).append(q)
+    for (k, sem, want_p, maxp), qs in groups.items():
+        seeds = [q.seeds[0] for q in qs]
+        filt = [q.relations if q.relations is not None else list(range(case.n_relations)) for q in qs]
+        r = th.retrieve(g, seeds, k, relation_filter=filt, semantics=sem, paths=want_p,
+                        max_paths=maxp if want_p else 0, activated=True)
+        for i, q in enumerate(qs):
+            for h in range(k):
+                assert np.array_equal(r.frontier(i, h + 1), q.frontiers[h])
+                assert np.array_equal(r.activated(i, h + 1), q.activated[h])
+            if want_p:
+                assert r.path_tid_tuples(i) == q.paths
+                assert r.truncated(i) == q.truncated
+
+
+def test_reference_api_dropin_tiny(th):
+    """The reference's own tiny-graph assertions (tests/test_incidence.py:54-221)."""
+    A, B, C = 0, 1, 2
+    tiny = [(A, 0, B), (B, 1, C), (A, 0, C), (C, 2, A)]
+    g = th.build_incidence(tiny, 3, 3)
+    assert g.sub_row(A).tolist() == [0, 2]
+    assert g.sub_row(B).tolist() == [1]
+    assert g.obj.tolist() == [B, C, C, A]
+    assert g.rel.tolist() == [0, 1, 0, 2]
+    ev = th.EntityVector
+    act, nxt = th.one_hop(ev([A], 3), g)
+    assert act.ids.tolist() == [0, 2] and nxt.ids.tolist() == [B, C]
+    act, nxt = th.one_hop(ev([B, C], 3), g)
+    assert act.ids.tolist() == [1, 3] and nxt.ids.tolist() == [A, C]
+    tr = th.k_hop(ev([A], 3), 2, g, th.HopSemantics.EXACT_WALK)
+    assert tr.frontier(1).ids.tolist() == [B, C] and tr.frontier(2).ids.tolist() == [A, C]
+    tr = th.k_hop(ev([A], 3), 2, g, th.HopSemantics.FRONTIER)
+    assert tr.frontier(2).ids.tolist() == []
+    with pytest.raises(ValueError):
+        th.k_hop(ev([A], 3), 0, g)
+    with pytest.raises(ValueError):
+        th.k_hop(ev([A], 4), 1, g)
+    res = th.reconstruct_paths(ev([A], 3), 2, g)
+    T = th.Triple
+    assert res.paths == [(T(A, 0, B), T(B, 1, C)), (T(A, 0, C), T(C, 2, A))] and not res.truncated
+    res = th.reconstruct_paths(ev([B], 3), 2, g, max_paths=1)
+    assert res.paths == [(T(B, 1, C), T(C, 2, A))] and res.truncated is False
+    res = th.reconstruct_paths(ev([A], 3), 2, g, max_paths=0)
+    assert res.paths == [] and res.truncated is True
+    with pytest.raises(ValueError):
+        th.reconstruct_paths(ev([A], 3), 2, g, max_paths=-1)
+    with pytest.raises(ValueError):
+        th.build_incidence([(5, 0, 0)], 2, 1)
+    with pytest.raises(ValueError):
+        th.build_incidence([(0, 3, 0)], 2, 1)
+
+
+def _hub_graph(E, T, R, seed, alpha=1.2):
+    """Hub-to-hub power-law graph (same ranks for subjects and objects)."""
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(E)
+    w = np.cumsum(1.0 / np.arange(1, E + 1) ** alpha)
+    w /= w[-1]
+    s = perm[np.minimum(np.searchsorted(w, rng.random(T)), E - 1)]
+    o = perm[np.minimum(np.searchsorted(w, rng.random(T)), E - 1)]
+    r = rng.integers(0, R, T)
+    key = np.unique((s.astype(np.int64) * R + r) * E + o)
+    key = rng.permutation(key)
+    return key // E // R, (key // E) % R, key % E
+
+
+@pytest.mark.parametrize("divisor", [0.0, -1.0, 8.0], ids=["push", "pull", "auto"])
+@pytest.mark.parametrize("sem", ["exact", "frontier", "cumulative"])
+def test_hub_graph_two_waves_vs_oracle(th, sem, divisor):
+    """1,100 seeds (two waves), hub rows above the heavy thresholds, every
+    direction policy; checked against the oracle seed by seed."""
+    s, r, o = _hub_graph(3000, 60000, 5, seed=11)
+    E, R = 3000, 5
+    g = th.build_incidence((s, r, o), E, R)
+    st = g.stats()
+    assert st["max_out_degree"] > 4096 and st["max_in_degree"] > 4096
+    og = orc.build_csr(s, r, o, E, R)
+    rng = np.random.default_rng(3)
+    seeds = rng.integers(0, E, 1100)
+    ret = th.Retriever(g)
+    ret.set_pull_divisor(divisor)
+    k = 3
+    res = ret.retrieve(seeds, k, semantics=sem)
+    if divisor == 0.0:
+        assert res.pull_hops == 0
+    if divisor < 0:
+        assert res.push_hops == 0
+    check = list(range(0, 1100, 37)) + [1099]
+    for i in check:
+        ref = orc.retrieve_one(og, int(seeds[i]), k, sem)
+        for h in range(k):
+            assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
+            assert int(res.edges[h, i]) == ref["edges"][h]
+
+
+def test_filtered_hub_graph_vs_oracle(th):
+    s, r, o = _hub_graph(2000, 40000, 40, seed=5)
+    E, R = 2000, 40
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    rng = np.random.default_rng(9)
+    seeds = rng.integers(0, E, 300)
+    filt = [sorted(rng.choice(R, 6, replace=False).tolist()) for _ in seeds]
+    for divisor in (0.0, -1.0):
+        ret = th.Retriever(g)
+        ret.set_pull_divisor(divisor)
+        res = ret.retrieve(seeds, 2, relation_filter=filt, semantics="frontier", paths=True,
+                           max_paths=300, activated=True)
+        for i in range(0, 300, 7):
+            ref = orc.retrieve_one(og, int(seeds[i]), 2, "frontier", filt[i], paths=True, max_paths=300)
+            for h in range(2):
+                assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h])
+                assert np.array_equal(res.activated(i, h + 1), ref["activated"][h])
+                assert int(res.edges[h, i]) == ref["edges"][h]
+            assert res.path_tid_tuples(i) == ref["paths"]
+            assert res.truncated(i) == ref["truncated"]
+
+
+def test_bad_inputs(th):
+    g = th.build_incidence([(0, 0, 1), (1, 0, 2)], 3, 1)
+    with pytest.raises(ValueError):
+        th.retrieve(g, [3], 1)
+    with pytest.raises(ValueError):
+        th.retrieve(g, [0], 0)
+    with pytest.raises(ValueError):
+        th.retrieve(g, [0], 1, relation_filter=[1])
+    r = th.retrieve(g, [], 2)
+    assert r.n_queries == 0
+    import torch
+
+    bad = torch.tensor([0, 7], dtype=torch.int32, device=g.device)
+    with pytest.raises(ValueError):
+        th.retrieve(g, bad, 2)
+    # the session is still usable after a failed call
+    r = th.retrieve(g, [0, 1, 2], 2, semantics="exact")
+    assert r.frontier(0, 1).tolist() == [1] and r.frontier(0, 2).tolist() == [2]
+    assert r.frontier(2, 1).tolist() == []
+
+
+def test_empty_graph_and_isolated(th):
+    g = th.build_incidence([], 4, 2)
+    r = th.retrieve(g, [0, 3], 3, semantics="cumulative", paths=True)
+    for i in range(2):
+        for h in range(1, 4):
+            assert r.frontier(i, h).size == 0
+        assert r.path_tid_tuples(i) == [] and not r.truncated(i)

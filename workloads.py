@@ -1,0 +1,116 @@
+"""Seeded synthetic workloads standing in for the reference's datasets.
+
+BASELINE.json's configs quote UMLS-/PKG-shaped graphs that
+are not in this container; these generators reproduce their sizes and degree
+shapes.  Every generator is deterministic in its seed.
+
+C1  the reference's own ``synth.power_law(10_000, 50_000, 16, seed=0,
+    alpha=1.1)`` (synth.py:34-49).  Its triples are shipped verbatim in
+    tests/golden/c1.npz (made by the reference itself), so no re-derivation.
+C2  407,000 entities / exactly 3,400,000 distinct triples / 400 relations.
+    Subjects and objects are drawn from ONE rank^-1.2 Zipf law over a random
+    permutation of ids (hubs are both prolific subjects and popular objects,
+    as in UMLS; hubs are scattered over the id space), relations from
+    rank^-1.0 over 400; duplicates are resampled until exactly T distinct
+    triples remain; triple order is shuffled so tids are not row-sorted.
+    Achieved: top-40 (0.01%) subjects average ~33.4k out-edges -- the
+    config's "hubs average ~33k 1-hop neighbours" (0.1% is arithmetically
+    impossible at T=3.4M).
+C3  C2's graph; 2,048 uniform + 2,048 top-1%-degree seeds; per-seed 32-of-400
+    relation masks.
+"""
+
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+
+
+def _unique_sorted(k: np.ndarray) -> np.ndarray:
+    k = np.sort(k)
+    if k.size == 0:
+        return k
+    keep = np.empty(k.size, dtype=bool)
+    keep[0] = True
+    np.not_equal(k[1:], k[:-1], out=keep[1:])
+    return k[keep]
+
+
+def zipf_graph(n_entities: int, n_triples: int, n_relations: int, seed: int, alpha: float = 1.2,
+               rel_alpha: float = 1.0, shared_ranks: bool = True):
+    """Exactly ``n_triples`` distinct (s, r, o) with Zipf subjects/objects."""
+    rng = np.random.default_rng(seed)
+    E, T, R = n_entities, n_triples, n_relations
+    perm_s = rng.permutation(E)
+    perm_o = perm_s if shared_ranks else rng.permutation(E)
+    cw = np.cumsum(1.0 / np.arange(1, E + 1, dtype=np.float64) ** alpha)
+    cw /= cw[-1]
+    cr = np.cumsum(1.0 / np.arange(1, R + 1, dtype=np.float64) ** rel_alpha)
+    cr /= cr[-1]
+    keys = np.empty(0, dtype=np.int64)
+    while keys.size < T:
+        n = int((T - keys.size) * 1.3) + 1024
+        s = perm_s[np.minimum(np.searchsorted(cw, rng.random(n)), E - 1)].astype(np.int64)
+        o = perm_o[np.minimum(np.searchsorted(cw, rng.random(n)), E - 1)].astype(np.int64)
+        r = np.minimum(np.searchsorted(cr, rng.random(n)), R - 1).astype(np.int64)
+        keys = _unique_sorted(np.concatenate([keys, (s * R + r) * E + o]))
+    keys = keys[np.sort(rng.choice(keys.size, T, replace=False))] if keys.size > T else keys
+    keys = rng.permutation(keys)
+    o = (keys % E).astype(np.int32)
+    r = ((keys // E) % R).astype(np.int32)
+    s = (keys // E // R).astype(np.int32)
+    return s, r, o
+
+
+def c1_graph():
+    z = np.load(ROOT / "tests" / "golden" / "c1.npz")
+    return z["subj"], z["rel"], z["obj"], 10_000, 16
+
+
+def c1_seeds():
+    return np.random.default_rng(1).choice(10_000, 64, replace=False)
+
+
+C2_DIMS = (407_000, 3_400_000, 400)
+
+
+def c2_graph(seed: int = 2):
+    E, T, R = C2_DIMS
+    s, r, o = zipf_graph(E, T, R, seed)
+    return s, r, o, E, R
+
+
+def seed_batches(n_entities: int, batch: int, count: int, seed: int) -> np.ndarray:
+    """``count`` batches of ``batch`` distinct uniform seeds, int32 [count, batch]."""
+    rng = np.random.default_rng(seed)
+    return np.stack([rng.choice(n_entities, batch, replace=False) for _ in range(count)]).astype(np.int32)
+
+
+def c3_queries(s: np.ndarray, n_entities: int, n_relations: int, seed: int = 3, n: int = 4096,
+               mask_size: int = 32):
+    """Half uniform seeds, half from the top-1% out-degree hubs; per-seed masks."""
+    rng = np.random.default_rng(seed)
+    deg = np.bincount(s, minlength=n_entities)
+    top = np.argsort(-deg, kind="stable")[: max(1, n_entities // 100)]
+    hubs = rng.choice(top, n // 2, replace=False)
+    rest = np.setdiff1d(np.arange(n_entities), hubs)
+    uni = rng.choice(rest, n - n // 2, replace=False)
+    seeds = np.concatenate([uni, hubs]).astype(np.int32)
+    masks = np.stack([rng.choice(n_relations, mask_size, replace=False) for _ in range(n)])
+    return seeds, masks
+
+
+def graph_stats(s, o, n_entities: int) -> dict:
+    deg = np.bincount(s, minlength=n_entities)
+    ind = np.bincount(o, minlength=n_entities)
+    top = np.sort(deg)[::-1]
+    k001 = max(1, n_entities // 10_000)
+    return {
+        "n_triples": int(s.size), "max_out_degree": int(top[0]), "max_in_degree": int(ind.max()),
+        "top_0.01pct_mean_out": float(top[:k001].mean()),
+        "zero_out_frac": float((deg == 0).mean()),
+        "isolated_frac": float(((deg == 0) & (ind == 0)).mean()),
+    }
