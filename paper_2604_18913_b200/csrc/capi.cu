@@ -116,7 +116,7 @@ int th_graph_info_get(const th_graph* gh, th_graph_info* out) {
   out->rrel = g.rrel;
   out->max_out_degree = g.max_out;
   out->max_in_degree = g.max_in;
-  out->n_heavy_in = g.n_heavy;
+  out->n_heavy_in = g.n_split;
   out->device_bytes = g.bytes;
   return TH_OK;
 }

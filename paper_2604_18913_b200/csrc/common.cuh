@@ -51,25 +51,27 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
   return x;
 }
 
-// warp-aggregated append of `item` (called by an arbitrary subset of lanes)
+// Warp-aggregated append of `item` from the lanes with `take` set.  Must be
+// called by all 32 lanes in converged code (full-mask collectives only; no
+// __activemask-based aggregation, which can deadlock under independent
+// thread scheduling when lanes diverge inside the aggregated region).
+// Also adds `cost` of the appending lanes (clamped to 2^26 each) to *sum.
 template <typename T>
-__device__ __forceinline__ void warp_append(T* list, int32_t* counter, T item, int64_t cap) {
-  const unsigned act = __activemask();
-  const int leader = __ffs(act) - 1;
-  const unsigned rank = __popc(act & lanemask_lt());
+__device__ __forceinline__ void warp_append_all(bool take, T item, uint32_t cost, T* list,
+                                                int32_t* counter, int64_t cap,
+                                                unsigned long long* sum) {
+  const unsigned m = __ballot_sync(TH_FULL, take);
+  if (!m) return;
+  const int leader = __ffs(m) - 1;
   int32_t base = 0;
-  if ((int)lane_id() == leader) base = atomicAdd(counter, __popc(act));
-  base = __shfl_sync(act, base, leader);
-  if (base + (int64_t)rank < cap) list[base + rank] = item;
-}
-
-// warp-aggregated add of a small non-negative value (heuristic counters;
-// each lane's contribution is clamped to 2^26 so the 32-bit reduce is exact)
-__device__ __forceinline__ void warp_add_small(unsigned long long* dst, uint32_t v) {
-  const unsigned act = __activemask();
-  const int leader = __ffs(act) - 1;
-  const unsigned sum = __reduce_add_sync(act, v > (1u << 26) ? (1u << 26) : v);
-  if ((int)lane_id() == leader) atomicAdd(dst, (unsigned long long)sum);
+  if ((int)lane_id() == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(TH_FULL, base, leader);
+  const unsigned rank = __popc(m & lanemask_lt());
+  if (take && base + (int64_t)rank < cap) list[base + rank] = item;
+  if (sum) {
+    const unsigned c = __reduce_add_sync(TH_FULL, take ? (cost > (1u << 26) ? (1u << 26) : cost) : 0u);
+    if ((int)lane_id() == leader) atomicAdd(sum, (unsigned long long)c);
+  }
 }
 
 }  // namespace th

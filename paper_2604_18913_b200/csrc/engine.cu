@@ -21,6 +21,8 @@
 // sorted/unique EntityVector / TripleVector form (incidence.py:83-91).
 #include <algorithm>
 #include <cstddef>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -51,17 +53,15 @@ struct WaveArgs {
   const int32_t* rindptr;
   const int32_t* rsrc;
   const uint16_t* rrel;
-  const int32_t* heavy_ids;
-  const int32_t* chunk_hv;
-  const int32_t* chunk_lo;
-  const int32_t* chunk_hi;
-  int64_t n_chunks, n_heavy_in;
+  const int32_t* item_v;
+  const int32_t* item_lo;
+  const int32_t* item_hi;
+  int64_t n_items;
   int64_t E, T;
   uint32_t *X, *N, *V, *S, *Xf, *Nf, *Vf;
   const uint32_t* M;
   int32_t* lists;
   int32_t* heavy;
-  uint32_t* racc;
   Ctl* ctl;
   int nq, sem, h;
 };
@@ -91,23 +91,28 @@ __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
     const int32_t lo = qoff[q0 + q], hi = qoff[q0 + q + 1];
     const uint32_t qb = 1u << (q & 31);
     const int qw = q >> 5;
-    for (int32_t i = lo + lane; i < hi; i += 32) {
-      const int32_t e = seeds[i];
-      if (e < 0 || e >= a.E) {
-        a.ctl->err = 1;
-        continue;
+    for (int32_t i0 = lo; i0 < hi; i0 += 32) {
+      const int32_t i = i0 + lane;
+      int32_t e = -1;
+      bool fresh = false;
+      if (i < hi) {
+        e = seeds[i];
+        if (e < 0 || e >= a.E) {
+          a.ctl->err = 1;
+          e = -1;
+        }
       }
-      const size_t r = (size_t)e * W + qw;
-      atomicOr(&a.X[r], qb);
-      if (a.sem != TH_EXACT) atomicOr(&a.V[r], qb);
-      if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
-      const uint32_t fb = 1u << (e & 31);
-      const uint32_t fo = atomicOr(&a.Xf[e >> 5], fb);
-      if (!(fo & fb)) {
-        warp_append(a.lists, &a.ctl->list_len[0], e, a.E);
-        warp_add_small(&a.ctl->push_cost[0], (uint32_t)(a.indptr[e + 1] - a.indptr[e]));
-        if (a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[e >> 5], fb);
+      if (e >= 0) {
+        const size_t r = (size_t)e * W + qw;
+        atomicOr(&a.X[r], qb);
+        if (a.sem != TH_EXACT) atomicOr(&a.V[r], qb);
+        if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
+        const uint32_t fb = 1u << (e & 31);
+        fresh = !(atomicOr(&a.Xf[e >> 5], fb) & fb);
+        if (fresh && a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[e >> 5], fb);
       }
+      const uint32_t d = fresh ? (uint32_t)(a.indptr[e + 1] - a.indptr[e]) : 0u;
+      warp_append_all(fresh, e, d, a.lists, &a.ctl->list_len[0], a.E, &a.ctl->push_cost[0]);
     }
   }
 }
@@ -131,15 +136,20 @@ __global__ void begin_hop_kernel(Ctl* ctl, int h, int64_t T, double pull_divisor
 
 // ------------------------------------------------------ mark new entity
 
-template <int W>
-__device__ __forceinline__ void mark_next(const WaveArgs& a, int32_t v) {
+// test-and-set the next-layer flag of v; true when this lane set it first
+__device__ __forceinline__ bool flag_next(const WaveArgs& a, int32_t v) {
   const uint32_t fb = 1u << (v & 31);
-  const uint32_t fo = atomicOr(&a.Nf[v >> 5], fb);
-  if (!(fo & fb)) {
-    warp_append(a.lists + a.ctl->list_off[a.h], &a.ctl->list_len[a.h], v, a.E);
-    warp_add_small(&a.ctl->push_cost[a.h], (uint32_t)(a.indptr[v + 1] - a.indptr[v]));
-    if (a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[v >> 5], fb);
-  }
+  const bool fresh = !(atomicOr(&a.Nf[v >> 5], fb) & fb);
+  if (fresh && a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[v >> 5], fb);
+  return fresh;
+}
+
+// converged (all 32 lanes): append the lanes' freshly flagged entities to
+// the hop's list segment and add their out-degrees to the push cost
+__device__ __forceinline__ void append_next(const WaveArgs& a, bool fresh, int32_t v) {
+  const uint32_t d = fresh ? (uint32_t)(a.indptr[v + 1] - a.indptr[v]) : 0u;
+  warp_append_all(fresh, v, d, a.lists + a.ctl->list_off[a.h], &a.ctl->list_len[a.h], a.E,
+                  &a.ctl->push_cost[a.h]);
 }
 
 // ------------------------------------------------------------ push hop
@@ -166,43 +176,52 @@ __device__ __forceinline__ void row_pairs(const WaveArgs& a, int32_t u, int32_t 
       j = (int)__fns(nz, 0, p - e * nzw + 1);
     }
     const uint32_t x = __shfl_sync(TH_FULL, xw, j & 31);
+    bool fresh = false;
+    int32_t v = 0;
     if (p < pairs) {
       const int32_t pos = lo + e;
       uint32_t w = x;
       if (FILTER) w &= a.M[(size_t)a.csr_rel[pos] * W + j];
-      if (w) op(a.csr_obj[pos], j, w);
+      if (w) {
+        v = a.csr_obj[pos];
+        fresh = op(v, j, w);
+      }
     }
+    if (Op::kAppends) append_next(a, fresh, v);
   }
 }
 
 template <int W, int SEM>
 struct PushOp {
+  static constexpr bool kAppends = true;
   const WaveArgs& a;
-  __device__ __forceinline__ void operator()(int32_t v, int j, uint32_t w) const {
+  // returns true when v entered the next layer's list through this lane
+  __device__ __forceinline__ bool operator()(int32_t v, int j, uint32_t w) const {
     const size_t r = (size_t)v * W + j;
     if (SEM == TH_EXACT) {
-      if (!(w & ~__ldcg(&a.N[r]))) return;
+      if (!(w & ~__ldcg(&a.N[r]))) return false;
       const uint32_t old = atomicOr(&a.N[r], w);
-      if (old == 0u) mark_next<W>(a, v);
-    } else {
-      if (!(w & ~__ldcg(&a.V[r]))) return;
-      const uint32_t old = atomicOr(&a.V[r], w);
-      const uint32_t nb = w & ~old;
-      if (!nb) return;
-      atomicOr(&a.N[r], nb);
-      mark_next<W>(a, v);
+      return old == 0u && flag_next(a, v);
     }
+    if (!(w & ~__ldcg(&a.V[r]))) return false;
+    const uint32_t old = atomicOr(&a.V[r], w);
+    const uint32_t nb = w & ~old;
+    if (!nb) return false;
+    atomicOr(&a.N[r], nb);
+    return flag_next(a, v);
   }
 };
 
 template <int W>
 struct CountOp {
+  static constexpr bool kAppends = false;
   uint32_t* sc;
-  __device__ __forceinline__ void operator()(int32_t, int j, uint32_t w) const {
+  __device__ __forceinline__ bool operator()(int32_t, int j, uint32_t w) const {
     while (w) {
       atomicAdd(&sc[32 * j + __ffs(w) - 1], 1u);
       w &= w - 1u;
     }
+    return false;
   }
 };
 
@@ -305,109 +324,166 @@ __global__ void __launch_bounds__(kThreads) edge_count_filtered_kernel(WaveArgs 
 
 // ------------------------------------------------------------ pull hop
 
-// OR of the frontier rows of in-edges [lo, hi) of one entity, per group lane
-template <int W, bool FILTER>
-__device__ __forceinline__ uint32_t pull_range(const WaveArgs& a, int32_t lo, int32_t hi,
-                                               uint32_t seen, uint32_t valid) {
-  const unsigned gm = Grp<W>::mask();
-  const unsigned j = Grp<W>::j();
-  uint32_t acc = 0;
-  for (int32_t b = lo; b < hi; b += W) {
-    const int32_t e = b + (int32_t)j;
-    int32_t src = 0;
-    uint32_t rr = 0;
-    bool act = false;
-    if (e < hi) {
-      src = a.rsrc[e];
-      if (FILTER) rr = a.rrel[e];
-      act = (a.Xf[src >> 5] >> (src & 31)) & 1u;
-    }
-    uint32_t am = Grp<W>::ballot(act);
-    while (am) {
-      const int i = __ffs(am) - 1;
-      am &= am - 1u;
-      const int32_t u = __shfl_sync(gm, src, i, W);
-      uint32_t x = a.X[(size_t)u * W + j];
-      if (FILTER) x &= a.M[(size_t)__shfl_sync(gm, rr, i, W) * W + j];
-      acc |= x;
-    }
-    // early exit: every live query has reached (or already visited) the entity
-    if (Grp<W>::ballot(((acc | seen) & valid) != valid) == 0u) break;
+// VEC words per lane, LPR lanes per entity row, GPW rows (groups) per warp
+template <int W>
+struct RowShape {
+  static constexpr int VEC = W >= 4 ? 4 : W;
+  static constexpr int LPR = W / VEC;
+  static constexpr int GPW = 32 / LPR;
+};
+
+template <int VEC>
+__device__ __forceinline__ void ld_words(const uint32_t* p, uint32_t (&o)[VEC]) {
+  if constexpr (VEC == 4) {
+    const uint4 t = *reinterpret_cast<const uint4*>(p);
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  } else if constexpr (VEC == 2) {
+    const uint2 t = *reinterpret_cast<const uint2*>(p);
+    o[0] = t.x; o[1] = t.y;
+  } else {
+    o[0] = *p;
   }
-  return acc;
 }
 
+// read-only path for data the kernel never writes (frontier rows, masks)
+template <int VEC>
+__device__ __forceinline__ void ldg_words(const uint32_t* p, uint32_t (&o)[VEC]) {
+  if constexpr (VEC == 4) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  } else if constexpr (VEC == 2) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+    o[0] = t.x; o[1] = t.y;
+  } else {
+    o[0] = __ldg(p);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_words(uint32_t* p, const uint32_t (&v)[VEC]) {
+  if constexpr (VEC == 4) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (VEC == 2) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[1]);
+  } else {
+    *p = v[0];
+  }
+}
+
+// Pull hop over the static in-edge items of the reverse CSR.  Each lane
+// group (LPR lanes, 16 B per lane) owns one item and ORs the frontier rows of
+// its active in-neighbours (4 rows in flight per group, GPW groups per warp,
+// all in lockstep so the warp stays convergent).  A group stops early once
+// every live query has visited or reached the entity.  Whole in-rows are
+// finished with plain stores; rows split over several items merge with
+// atomicOr (the union of the pieces is exactly R_h & ~V_{h-1}).
 template <int W, int SEM, bool FILTER>
-__global__ void __launch_bounds__(kThreads) pull_light_kernel(WaveArgs a) {
+__global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   if (a.ctl->mode[a.h] != 1) return;
-  const int gpw = 32 / W;
-  const int64_t g0 = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * gpw + lane_id() / W;
-  const int64_t ng = (int64_t)((gridDim.x * blockDim.x) >> 5) * gpw;
-  const unsigned j = Grp<W>::j();
-  const uint32_t valid = valid_word((int)j, a.nq);
-  // uniform trip count per warp keeps group collectives convergent
-  const int64_t iters = ceil_div(a.E, ng);
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t v = g0 + it * ng;
-    if (v >= a.E) continue;
-    const int32_t lo = a.rindptr[v], hi = a.rindptr[v + 1];
-    if (hi == lo || hi - lo > kHeavyPull) continue;
-    const size_t r = (size_t)v * W + j;
-    const uint32_t seen = SEM == TH_EXACT ? 0u : a.V[r];
-    if (SEM != TH_EXACT && Grp<W>::ballot((seen & valid) != valid) == 0u) continue;
-    const uint32_t acc = pull_range<W, FILTER>(a, lo, hi, seen, valid);
-    const uint32_t nb = acc & ~seen & valid;
-    if (Grp<W>::ballot(nb != 0u) == 0u) continue;
-    a.N[r] = nb;
-    if (SEM != TH_EXACT) a.V[r] = seen | nb;
-    if (j == 0) mark_next<W>(a, (int32_t)v);
-  }
-}
-
-template <int W, int SEM, bool FILTER>
-__global__ void __launch_bounds__(kThreads) pull_heavy_kernel(WaveArgs a) {
-  if (a.ctl->mode[a.h] != 1) return;
-  const int gpw = 32 / W;
-  const int64_t g0 = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * gpw + lane_id() / W;
-  const int64_t ng = (int64_t)((gridDim.x * blockDim.x) >> 5) * gpw;
-  const unsigned j = Grp<W>::j();
-  const uint32_t valid = valid_word((int)j, a.nq);
-  const int64_t iters = ceil_div(a.n_chunks, ng);
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t c = g0 + it * ng;
-    if (c >= a.n_chunks) continue;
-    const int32_t hv = a.chunk_hv[c];
-    const int32_t v = a.heavy_ids[hv];
-    const uint32_t seen = SEM == TH_EXACT ? 0u : a.V[(size_t)v * W + j];
-    if (SEM != TH_EXACT && Grp<W>::ballot((seen & valid) != valid) == 0u) continue;
-    const uint32_t acc = pull_range<W, FILTER>(a, a.chunk_lo[c], a.chunk_hi[c], seen, valid) &
-                         ~seen & valid;
-    if (acc) atomicOr(&a.racc[(size_t)hv * W + j], acc);
-  }
-}
-
-template <int W, int SEM>
-__global__ void __launch_bounds__(kThreads) pull_finalize_kernel(WaveArgs a) {
-  if (a.ctl->mode[a.h] != 1) return;
-  const int gpw = 32 / W;
-  const int64_t g0 = (int64_t)((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * gpw + lane_id() / W;
-  const int64_t ng = (int64_t)((gridDim.x * blockDim.x) >> 5) * gpw;
-  const unsigned j = Grp<W>::j();
-  const uint32_t valid = valid_word((int)j, a.nq);
-  const int64_t iters = ceil_div(a.n_heavy_in, ng);
-  for (int64_t it = 0; it < iters; ++it) {
-    const int64_t hv = g0 + it * ng;
-    if (hv >= a.n_heavy_in) continue;
-    const int32_t v = a.heavy_ids[hv];
-    const size_t r = (size_t)v * W + j;
-    const uint32_t acc = a.racc[(size_t)hv * W + j];
-    a.racc[(size_t)hv * W + j] = 0u;
-    const uint32_t seen = SEM == TH_EXACT ? 0u : a.V[r];
-    const uint32_t nb = acc & ~seen & valid;
-    if (Grp<W>::ballot(nb != 0u) == 0u) continue;
-    a.N[r] = nb;
-    if (SEM != TH_EXACT) a.V[r] = seen | nb;
-    if (j == 0) mark_next<W>(a, v);
+  using RS = RowShape<W>;
+  constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
+  const unsigned lane = lane_id();
+  const int part = (int)lane % LPR, grp = (int)lane / LPR;
+  const unsigned gbits = (LPR == 32 ? TH_FULL : ((1u << LPR) - 1u)) << (grp * LPR);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t valid[VEC];
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) valid[c] = valid_word(part * VEC + c, a.nq);
+  const int64_t n = a.n_items;
+  for (int64_t base = warp * GPW; base < n; base += nwarps * GPW) {
+    const int64_t it = base + grp;
+    const bool live = it < n;
+    int32_t vv = 0, lo = 0, hi = 0;
+    if (live) {
+      vv = a.item_v[it];
+      lo = a.item_lo[it];
+      hi = a.item_hi[it];
+    }
+    const bool split = vv < 0;
+    const int32_t v = split ? ~vv : vv;
+    const size_t row = (size_t)v * W + part * VEC;
+    uint32_t seen[VEC], acc[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) {
+      seen[c] = 0u;
+      acc[c] = 0u;
+    }
+    if (SEM != TH_EXACT && live) ld_words<VEC>(a.V + row, seen);
+    bool sat = true;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) sat &= (seen[c] & valid[c]) == valid[c];
+    // the full-mask ballot must run on every lane (no short-circuit around it)
+    const bool group_sat = (__ballot_sync(TH_FULL, sat) & gbits) == gbits;
+    bool done = !live || (SEM != TH_EXACT && group_sat);
+    const int len = done ? 0 : hi - lo;
+    int maxlen = len;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(TH_FULL, maxlen, o));
+    for (int e0 = 0; e0 < maxlen; e0 += 4) {
+      int32_t u[4];
+      uint32_t rr[4];
+      bool act[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        act[k] = !done && e0 + k < len;
+        u[k] = act[k] ? __ldg(a.rsrc + lo + e0 + k) : 0;
+        rr[k] = (FILTER && act[k]) ? (uint32_t)__ldg(a.rrel + lo + e0 + k) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (act[k]) act[k] = (__ldg(a.Xf + (u[k] >> 5)) >> (u[k] & 31)) & 1u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (act[k]) {
+          uint32_t x[VEC];
+          ldg_words<VEC>(a.X + (size_t)u[k] * W + part * VEC, x);
+          if (FILTER) {
+            uint32_t m[VEC];
+            ldg_words<VEC>(a.M + (size_t)rr[k] * W + part * VEC, m);
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) x[c] &= m[c];
+          }
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
+        }
+      }
+      bool full = true;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) full &= ((acc[c] | seen[c]) & valid[c]) == valid[c];
+      if ((__ballot_sync(TH_FULL, full) & gbits) == gbits) done = true;
+      if (__all_sync(TH_FULL, done)) break;
+    }
+    uint32_t nb[VEC];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) {
+      nb[c] = acc[c] & ~seen[c] & valid[c];
+      any |= nb[c] != 0u;
+    }
+    any = (__ballot_sync(TH_FULL, any) & gbits) != 0u;
+    bool fresh = false;
+    if (live && any) {
+      if (!split) {
+        st_words<VEC>(a.N + row, nb);
+        if (SEM != TH_EXACT) {
+          uint32_t nv[VEC];
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) nv[c] = seen[c] | nb[c];
+          st_words<VEC>(a.V + row, nv);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          if (nb[c]) {
+            atomicOr(a.N + row + c, nb[c]);
+            if (SEM != TH_EXACT) atomicOr(a.V + row + c, nb[c]);
+          }
+        }
+      }
+      if (part == 0) fresh = flag_next(a, v);
+    }
+    append_next(a, fresh, v);
   }
 }
 
@@ -497,61 +573,127 @@ struct TripleSrc {
   }
 };
 
+constexpr int kMatThreads = 128;
+constexpr int kMatWarps = kMatThreads / 32;
+constexpr int kSB = 4;                 // 32-row sub-blocks per batch
+constexpr int kBatch = 32 * kSB;       // rows per batch
+constexpr int kStageStride = kBatch + 1;
+
+template <int W>
+struct MatShape {
+  static constexpr int JC = W < 8 ? W : 8;  // words staged per pass (one 32 B sector per row)
+};
+
+template <int W, bool WRITE>
+constexpr size_t mat_smem_bytes() {
+  return (size_t)kMatWarps *
+         ((size_t)kBatch * (MatShape<W>::JC + 1) + (size_t)32 * W +
+          (WRITE ? (size_t)32 * kStageStride : 0)) *
+         sizeof(uint32_t);
+}
+
+// K4 materialisation: bit-transpose entity-major rows into per-query sorted
+// id lists.  A warp walks its block of rows in 128-row batches; for every
+// 8-word column chunk it stages the batch's 32 B row sectors in shared
+// memory, transposes 32x32 bit tiles (lane b then holds query 32j+b's row
+// masks), and COUNT accumulates popcounts while WRITE first gathers each
+// query's ids into a per-query shared-memory run and then stores the runs
+// with all 32 lanes (coalesced, query by query).
 template <int W, class Src, bool WRITE>
-__global__ void __launch_bounds__(kThreads) mat_kernel(Src src, int64_t blk_rows, int nblk,
-                                                       int32_t* counts, const int64_t* base,
-                                                       int32_t* out, int64_t cap) {
-  __shared__ uint32_t tile[kWarps][32][W + 1];
+__global__ void __launch_bounds__(kMatThreads) mat_kernel(Src src, int64_t blk_rows, int nblk,
+                                                          int32_t* counts, const int64_t* base,
+                                                          int32_t* out, int64_t cap) {
+  constexpr int JC = MatShape<W>::JC;
+  extern __shared__ uint32_t mat_smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* tile = mat_smem + (size_t)warp * kBatch * (JC + 1);
+  int32_t* runs = reinterpret_cast<int32_t*>(mat_smem + (size_t)kMatWarps * kBatch * (JC + 1)) +
+                  (size_t)warp * 32 * W;
+  int32_t* stage = reinterpret_cast<int32_t*>(mat_smem + (size_t)kMatWarps * (kBatch * (JC + 1) + 32 * W)) +
+                   (size_t)warp * 32 * kStageStride;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int blk = gw; blk < nblk; blk += nw) {
-    int64_t run[W];
+    // runs[j*32+lane]: ids so far in this block for query 32j+lane
+    for (int j = 0; j < W; ++j) runs[j * 32 + lane] = 0;
+    const int64_t r_begin = (int64_t)blk * blk_rows;
+    const int64_t rend = src.nrows < r_begin + blk_rows ? src.nrows : r_begin + blk_rows;
+    for (int64_t r0 = r_begin; r0 < rend; r0 += kBatch) {
+      uint32_t fl[kSB];
+      int64_t aux[kSB];
+      uint32_t anyfl = 0;
 #pragma unroll
-    for (int j = 0; j < W; ++j) {
-      run[j] = 0;
-      if (WRITE) {
-        const int q = 32 * j + lane;
-        if (q < src.nq) run[j] = base[q] + counts[(size_t)q * nblk + blk];
+      for (int sb = 0; sb < kSB; ++sb) {
+        fl[sb] = r0 + 32 * sb < rend ? src.prep(r0 + 32 * sb, aux[sb]) : 0u;
+        anyfl |= fl[sb];
       }
-    }
-    const int64_t rend = src.nrows < (int64_t)(blk + 1) * blk_rows ? src.nrows : (int64_t)(blk + 1) * blk_rows;
-    for (int64_t r0 = (int64_t)blk * blk_rows; r0 < rend; r0 += 32) {
-      int64_t aux;
-      const uint32_t fl = src.prep(r0, aux);
-      if (!fl) continue;
+      if (!anyfl) continue;
+#pragma unroll 1
+      for (int jc = 0; jc < W; jc += JC) {
+        // stage words [jc, jc+JC) of the batch's flagged rows
 #pragma unroll
-      for (int it = 0; it < W; ++it) {
-        const int idx = it * 32 + lane;
-        const int row = idx / W, j = idx % W;
-        const int64_t ra = __shfl_sync(TH_FULL, aux, row);
-        tile[warp][row][j] = ((fl >> row) & 1u) ? src.word(r0 + row, j, ra) : 0u;
-      }
-      __syncwarp();
+        for (int sb = 0; sb < kSB; ++sb) {
+          if (!fl[sb]) continue;
 #pragma unroll
-      for (int j = 0; j < W; ++j) {
-        uint32_t t = transpose32(tile[warp][lane][j]);
-        if (WRITE) {
-          int64_t pos = run[j];
-          run[j] += __popc(t);
-          while (t) {
-            if (pos < cap) out[pos] = (int32_t)(r0 + __ffs(t) - 1);
-            ++pos;
-            t &= t - 1u;
+          for (int it = 0; it < JC; ++it) {
+            const int idx = it * 32 + lane;
+            const int row = idx / JC, jj = idx % JC;
+            const int64_t ra = __shfl_sync(TH_FULL, aux[sb], row);
+            tile[(sb * 32 + row) * (JC + 1) + jj] =
+                ((fl[sb] >> row) & 1u) ? src.word(r0 + 32 * sb + row, jc + jj, ra) : 0u;
           }
-        } else {
-          run[j] += __popc(t);
         }
+        __syncwarp();
+#pragma unroll 1
+        for (int jj = 0; jj < JC; ++jj) {
+          const int j = jc + jj;
+          uint32_t t[kSB];
+          int c = 0;
+#pragma unroll
+          for (int sb = 0; sb < kSB; ++sb) {
+            t[sb] = fl[sb] ? transpose32(tile[(sb * 32 + lane) * (JC + 1) + jj]) : 0u;
+            c += __popc(t[sb]);
+          }
+          const int prev = runs[j * 32 + lane];
+          if (WRITE) {
+            int32_t* my = stage + lane * kStageStride;
+            int k = 0;
+#pragma unroll
+            for (int sb = 0; sb < kSB; ++sb) {
+              uint32_t m = t[sb];
+              while (m) {
+                my[k++] = (int32_t)(r0 + 32 * sb + __ffs(m) - 1);
+                m &= m - 1u;
+              }
+            }
+            __syncwarp();
+            const int q = 32 * j + lane;
+            int64_t mypos = 0;
+            if (c > 0) mypos = base[q] + counts[(size_t)q * nblk + blk] + prev;
+            unsigned nzq = __ballot_sync(TH_FULL, c > 0);
+            while (nzq) {
+              const int b = __ffs(nzq) - 1;
+              nzq &= nzq - 1u;
+              const int cb = __shfl_sync(TH_FULL, c, b);
+              const int64_t pb = __shfl_sync(TH_FULL, mypos, b);
+              const int32_t* src_run = stage + b * kStageStride;
+              for (int kk = lane; kk < cb; kk += 32)
+                if (pb + kk < cap) out[pb + kk] = src_run[kk];
+            }
+            __syncwarp();
+          }
+          runs[j * 32 + lane] = prev + c;
+        }
+        __syncwarp();
       }
-      __syncwarp();
     }
     if (!WRITE) {
-#pragma unroll
       for (int j = 0; j < W; ++j) {
         const int q = 32 * j + lane;
-        if (q < src.nq) counts[(size_t)q * nblk + blk] = (int32_t)run[j];
+        if (q < src.nq) counts[(size_t)q * nblk + blk] = runs[j * 32 + lane];
       }
     }
+    __syncwarp();
   }
 }
 
@@ -651,64 +793,62 @@ struct WaveBufs {
   int W;
   uint32_t *X, *N, *V, *S, *Xf, *Nf, *Vf, *M;
   int32_t *lists, *heavy, *counts;
-  uint32_t* racc;
   int64_t* totals;
   Ctl* ctl;
 };
 
-template <int W>
-void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
-                       const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
-                       int64_t cap, int64_t* cursor) {
-  const Graph* g = s->g;
-  const int64_t rows = g->E;
+// count -> per-query scan -> offsets -> write, for any row source
+template <int W, class Src>
+void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, int64_t* len,
+                 int32_t* out, int64_t cap, int64_t* cursor) {
+  const int64_t rows = src.nrows;
   if (rows == 0) {
     TH_CUDA(cudaMemsetAsync(len, 0, sizeof(int64_t) * nq, s->st));
     TH_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * nq, s->st));
     return;
   }
-  const int64_t blk_rows = std::max<int64_t>(32, ceil_div(ceil_div(rows, kMatBlocks), 32) * 32);
+  constexpr size_t smem_c = mat_smem_bytes<W, false>();
+  constexpr size_t smem_w = mat_smem_bytes<W, true>();
+  static bool attr_done = false;  // one per template instantiation
+  if (!attr_done) {
+    TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
+    TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
+    attr_done = true;
+  }
+  constexpr int64_t batch = kBatch;
+  const int64_t blk_rows = std::max<int64_t>(batch, ceil_div(ceil_div(rows, kMatBlocks), batch) * batch);
   const int nblk = (int)ceil_div(rows, blk_rows);
-  DenseSrc<W> src{A, neg, flags, rows, nq};
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nblk, kWarps), kNumSMs * 8));
-  mat_kernel<W, DenseSrc<W>, false><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
-                                                                  nullptr, nullptr, 0);
+  const unsigned grid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nblk, kMatWarps), kNumSMs * 16));
+  mat_kernel<W, Src, false><<<grid, kMatThreads, smem_c, s->st>>>(src, blk_rows, nblk, b.counts,
+                                                               nullptr, nullptr, 0);
   TH_LAUNCHED();
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
   TH_LAUNCHED();
   mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
   TH_LAUNCHED();
-  mat_kernel<W, DenseSrc<W>, true><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts, off,
-                                                                 out, cap);
+  mat_kernel<W, Src, true><<<grid, kMatThreads, smem_w, s->st>>>(src, blk_rows, nblk, b.counts, off,
+                                                              out, cap);
   TH_LAUNCHED();
   s->launches += 4;
+}
+
+template <int W>
+void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
+                       const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
+                       int64_t cap, int64_t* cursor) {
+  DenseSrc<W> src{A, neg, flags, s->g->E, nq};
+  materialize<W>(s, b, src, nq, off, len, out, cap, cursor);
 }
 
 template <int W>
 void materialize_triples(Session* s, WaveBufs& b, int nq, int64_t* off, int64_t* len, int32_t* out,
                          int64_t cap, int64_t* cursor) {
   const Graph* g = s->g;
-  const int64_t rows = g->T;
-  if (rows == 0) {
-    TH_CUDA(cudaMemsetAsync(len, 0, sizeof(int64_t) * nq, s->st));
-    TH_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * nq, s->st));
-    return;
-  }
-  const int64_t blk_rows = std::max<int64_t>(32, ceil_div(ceil_div(rows, kMatBlocks), 32) * 32);
-  const int nblk = (int)ceil_div(rows, blk_rows);
-  TripleSrc<W> src{b.X, b.Xf, s->last.d_rel_masks ? b.M : nullptr, g->subj, g->rel, rows, nq};
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nblk, kWarps), kNumSMs * 8));
-  mat_kernel<W, TripleSrc<W>, false><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
-                                                                   nullptr, nullptr, 0);
-  TH_LAUNCHED();
-  mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
-  TH_LAUNCHED();
-  mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
-  TH_LAUNCHED();
-  mat_kernel<W, TripleSrc<W>, true><<<grid, kThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
-                                                                  off, out, cap);
-  TH_LAUNCHED();
-  s->launches += 4;
+  TripleSrc<W> src{b.X, b.Xf, s->last.d_rel_masks ? b.M : nullptr, g->subj, g->rel, g->T, nq};
+  materialize<W>(s, b, src, nq, off, len, out, cap, cursor);
 }
 
 template <int W, int SEM, bool FILTER>
@@ -724,16 +864,9 @@ void expand_hop(Session* s, const WaveArgs& a) {
   }
   if (s->g->rindptr) {
     ProfScope ps(s, TH_PROF_PULL);
-    pull_light_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
+    pull_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
     TH_LAUNCHED();
     s->launches += 1;
-    if (s->g->n_chunks > 0) {
-      pull_heavy_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
-      TH_LAUNCHED();
-      pull_finalize_kernel<W, SEM><<<pg, kThreads, 0, s->st>>>(a);
-      TH_LAUNCHED();
-      s->launches += 2;
-    }
   }
 }
 
@@ -757,7 +890,6 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   b.Vf = ensure<uint32_t>(s->Vf, fwords, st);
   b.lists = ensure<int32_t>(s->lists, (k + 1) * std::max<int64_t>(E, 1), st);
   b.heavy = ensure<int32_t>(s->heavy, std::max<int64_t>(E, 1), st);
-  b.racc = ensure<uint32_t>(s->racc, std::max<int64_t>(g->n_heavy, 1) * W, st);
   b.M = filter ? ensure<uint32_t>(s->M, std::max<int64_t>(g->R, 1) * W, st) : nullptr;
   b.counts = ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
   b.totals = ensure<int64_t>(s->totals, kMaxWave, st);
@@ -774,12 +906,10 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   a.rindptr = g->rindptr;
   a.rsrc = g->rsrc;
   a.rrel = g->rrel;
-  a.heavy_ids = g->heavy_ids;
-  a.chunk_hv = g->chunk_hv;
-  a.chunk_lo = g->chunk_lo;
-  a.chunk_hi = g->chunk_hi;
-  a.n_chunks = g->n_chunks;
-  a.n_heavy_in = g->n_heavy;
+  a.item_v = g->item_v;
+  a.item_lo = g->item_lo;
+  a.item_hi = g->item_hi;
+  a.n_items = g->n_items;
   a.E = E;
   a.T = g->T;
   a.X = b.X;
@@ -792,7 +922,6 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   a.M = b.M;
   a.lists = b.lists;
   a.heavy = b.heavy;
-  a.racc = b.racc;
   a.ctl = b.ctl;
   a.nq = nq;
   a.sem = sem;
@@ -898,11 +1027,6 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   }
 }
 
-void clear_state(Session* s, int64_t rows, int64_t fwords, bool cum) {
-  (void)fwords;
-  for (DBuf* d : {&s->X, &s->N, &s->V}) TH_CUDA(cudaMemsetAsync(d->p, 0, rows * 4, s->st));
-  if (cum) TH_CUDA(cudaMemsetAsync(s->S.p, 0, rows * 4, s->st));
-}
 
 }  // namespace
 
@@ -919,6 +1043,15 @@ ProfScope::ProfScope(Session* s_, int c) : s(s_), cat(c), l0(s_->launches) {
 }
 
 ProfScope::~ProfScope() noexcept(false) {
+  static const bool debug_sync = std::getenv("TH_DEBUG_SYNC") != nullptr;
+  if (debug_sync) {
+    // diagnostics: serialise and name every kernel group as it completes
+    static const char* names[] = {"setup", "edges", "activated", "push", "pull", "frontier",
+                                  "clear", "paths"};
+    std::fprintf(stderr, "[th] wait %s\n", names[cat]);
+    TH_CUDA(cudaStreamSynchronize(s->st));
+    std::fprintf(stderr, "[th] done %s\n", names[cat]);
+  }
   if (!s->prof) return;
   TH_CUDA(cudaEventRecord(s->ev_pool[s->ev_used + 1], s->st));
   s->ev_used += 2;
@@ -1013,19 +1146,12 @@ int session_run(Session* s, const th_query* q) {
   // matrices must start zero: (re)allocation leaves garbage, so clear on growth
   const int64_t rows = std::max<int64_t>(g->E, 1) * W;
   const size_t need = (size_t)rows * 4;
-  const bool fresh = s->X.bytes < need || s->N.bytes < need || s->V.bytes < need ||
-                     (q->semantics == TH_CUMULATIVE && s->S.bytes < need);
-  if (fresh) {
-    ensure<uint32_t>(s->X, rows, st);
-    ensure<uint32_t>(s->N, rows, st);
-    ensure<uint32_t>(s->V, rows, st);
-    if (q->semantics == TH_CUMULATIVE) ensure<uint32_t>(s->S, rows, st);
-    clear_state(s, (int64_t)(std::min({s->X.bytes, s->N.bytes, s->V.bytes}) / 4), 0,
-                q->semantics == TH_CUMULATIVE);
-    if (q->semantics == TH_CUMULATIVE) TH_CUDA(cudaMemsetAsync(s->S.p, 0, s->S.bytes, st));
-  } else if (q->semantics == TH_CUMULATIVE && s->S.p == nullptr) {
-    ensure<uint32_t>(s->S, rows, st);
-    TH_CUDA(cudaMemsetAsync(s->S.p, 0, s->S.bytes, st));
+  for (DBuf* d : {&s->X, &s->N, &s->V, &s->S}) {
+    if (d == &s->S && q->semantics != TH_CUMULATIVE) continue;
+    if (d->bytes < need) {
+      ensure<uint32_t>(*d, rows, st);
+      TH_CUDA(cudaMemsetAsync(d->p, 0, d->bytes, st));
+    }
   }
   for (int64_t q0 = 0; q0 < B; q0 += wave) {
     const int nq = (int)std::min<int64_t>(wave, B - q0);
@@ -1129,7 +1255,7 @@ int session_finish(Session* s, th_result* out) {
 }
 
 void session_free(Session* s) {
-  for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy, &s->racc,
+  for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
                   &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
                   &s->p_scratch}) {

@@ -37,7 +37,7 @@ struct Session {
   double pull_divisor = 8.0;
   int64_t launches = 0;
   // wave state
-  DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, racc, M, counts, totals;
+  DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals;
   DBuf ctl;
   // outputs
   DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch;

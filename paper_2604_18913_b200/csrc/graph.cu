@@ -86,33 +86,32 @@ __global__ void max_degree_kernel(const int32_t* __restrict__ ptr, int64_t E, in
   if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
-// counts heavy in-rows and their chunks: ctr[0] += rows, ctr[1] += chunks
-__global__ void heavy_count_kernel(const int32_t* __restrict__ rptr, int64_t E, int32_t* ctr) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < E;
+// items per in-row (cnt[v], cnt[E] = 0) and the number of split rows
+__global__ void item_count_kernel(const int32_t* __restrict__ rptr, int64_t E, int32_t* cnt,
+                                  int32_t* n_split) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= E;
        v += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t d = rptr[v + 1] - rptr[v];
-    if (d > kHeavyPull) {
-      atomicAdd(&ctr[0], 1);
-      atomicAdd(&ctr[1], (d + kPullChunk - 1) / kPullChunk);
+    if (v == E) {
+      cnt[v] = 0;
+      continue;
     }
+    const int32_t d = rptr[v + 1] - rptr[v];
+    const int32_t c = (d + kPullChunk - 1) / kPullChunk;
+    cnt[v] = c;
+    if (c > 1) atomicAdd(n_split, 1);
   }
 }
 
-__global__ void heavy_fill_kernel(const int32_t* __restrict__ rptr, int64_t E, int32_t* ctr,
-                                  int32_t* heavy_ids, int32_t* chv, int32_t* clo, int32_t* chi) {
+__global__ void item_fill_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ off,
+                                 int64_t E, int32_t* iv, int32_t* ilo, int32_t* ihi) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < E;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int32_t lo = rptr[v], hi = rptr[v + 1];
-    if (hi - lo > kHeavyPull) {
-      const int32_t nc = (hi - lo + kPullChunk - 1) / kPullChunk;
-      const int32_t h = atomicAdd(&ctr[0], 1);
-      const int32_t c0 = atomicAdd(&ctr[1], nc);
-      heavy_ids[h] = (int32_t)v;
-      for (int32_t c = 0; c < nc; ++c) {
-        chv[c0 + c] = h;
-        clo[c0 + c] = lo + c * kPullChunk;
-        chi[c0 + c] = min(hi, lo + (c + 1) * kPullChunk);
-      }
+    const int32_t o = off[v], c = off[v + 1] - o;
+    for (int32_t i = 0; i < c; ++i) {
+      iv[o + i] = c > 1 ? ~(int32_t)v : (int32_t)v;
+      ilo[o + i] = lo + i * kPullChunk;
+      ihi[o + i] = min(hi, lo + (i + 1) * kPullChunk);
     }
   }
 }
@@ -243,32 +242,32 @@ int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int
       TH_LAUNCHED();
       g->launches += 1;
     }
-    int32_t* ctr = nullptr;
-    TH_CUDA(cudaMalloc(&ctr, 2 * sizeof(int32_t)));
-    TH_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(int32_t), st));
-    if (E > 0) {
-      heavy_count_kernel<<<grid_for(E), 256, 0, st>>>(g->rindptr, E, ctr);
-      TH_LAUNCHED();
-      g->launches += 1;
-    }
+    // static pull items: scan of per-row item counts, then fill
+    int32_t* cnt = talloc<int32_t>(E + 2);
+    int32_t* off = talloc<int32_t>(E + 1);
+    int32_t* nsplit = cnt + E + 1;
+    TH_CUDA(cudaMemsetAsync(nsplit, 0, sizeof(int32_t), st));
+    item_count_kernel<<<grid_for(E + 1), 256, 0, st>>>(g->rindptr, E, cnt, nsplit);
+    TH_LAUNCHED();
+    int32_t* scratch = talloc<int32_t>(scan_scratch_elems<int32_t>(E + 1));
+    g->launches += 1 + scan_exclusive<int32_t>(cnt, off, E + 1, scratch, st);
     int32_t hc[2];
-    TH_CUDA(cudaMemcpyAsync(hc, ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    TH_CUDA(cudaMemcpyAsync(&hc[0], off + E, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    TH_CUDA(cudaMemcpyAsync(&hc[1], nsplit, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     TH_CUDA(cudaStreamSynchronize(st));
-    g->n_heavy = hc[0];
-    g->n_chunks = hc[1];
-    g->heavy_ids = dalloc<int32_t>(g, g->n_heavy);
-    g->chunk_hv = dalloc<int32_t>(g, g->n_chunks);
-    g->chunk_lo = dalloc<int32_t>(g, g->n_chunks);
-    g->chunk_hi = dalloc<int32_t>(g, g->n_chunks);
-    if (g->n_heavy > 0) {
-      TH_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(int32_t), st));
-      heavy_fill_kernel<<<grid_for(E), 256, 0, st>>>(g->rindptr, E, ctr, g->heavy_ids, g->chunk_hv,
-                                                     g->chunk_lo, g->chunk_hi);
+    g->n_items = hc[0];
+    g->n_split = hc[1];
+    g->item_v = dalloc<int32_t>(g, g->n_items);
+    g->item_lo = dalloc<int32_t>(g, g->n_items);
+    g->item_hi = dalloc<int32_t>(g, g->n_items);
+    if (E > 0) {
+      item_fill_kernel<<<grid_for(E), 256, 0, st>>>(g->rindptr, off, E, g->item_v, g->item_lo,
+                                                    g->item_hi);
       TH_LAUNCHED();
       g->launches += 1;
     }
     TH_CUDA(cudaStreamSynchronize(st));
-    cudaFree(ctr);
+    for (void* p : {(void*)cnt, (void*)off, (void*)scratch}) cudaFree(p);
   }
   int32_t hm[2];
   TH_CUDA(cudaMemcpyAsync(hm, dmax, sizeof(hm), cudaMemcpyDeviceToHost, st));
@@ -282,8 +281,7 @@ int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int
 void graph_free(Graph* g) {
   for (void* p : {(void*)g->indptr, (void*)g->csr_tid, (void*)g->csr_obj, (void*)g->csr_rel,
                   (void*)g->subj, (void*)g->obj, (void*)g->rel, (void*)g->rindptr, (void*)g->rsrc,
-                  (void*)g->rrel, (void*)g->heavy_ids, (void*)g->chunk_hv, (void*)g->chunk_lo,
-                  (void*)g->chunk_hi}) {
+                  (void*)g->rrel, (void*)g->item_v, (void*)g->item_lo, (void*)g->item_hi}) {
     if (p) cudaFree(p);
   }
   *g = Graph{};

@@ -6,10 +6,9 @@
 
 namespace th {
 
-// in-rows longer than this are split into chunks of kPullChunk edges and
-// processed by many warps (pull hops); see engine.cu
-constexpr int32_t kHeavyPull = 4096;
-constexpr int32_t kPullChunk = 2048;
+// pull hops walk in-rows in items of at most kPullChunk in-edges; a lane
+// group owns one item (see engine.cu pull_kernel)
+constexpr int32_t kPullChunk = 64;
 
 struct Graph {
   int64_t E = 0, T = 0, R = 0;
@@ -26,14 +25,14 @@ struct Graph {
   int32_t* rindptr = nullptr;  // [E+1]
   int32_t* rsrc = nullptr;     // [T]
   uint16_t* rrel = nullptr;    // [T]
-  // pull schedule for heavy in-rows: chunk c covers in-edges
-  // [chunk_lo[c], chunk_hi[c]) of entity heavy_ids[chunk_hv[c]]
-  int32_t* heavy_ids = nullptr;
-  int64_t n_heavy = 0;
-  int32_t* chunk_hv = nullptr;
-  int32_t* chunk_lo = nullptr;
-  int32_t* chunk_hi = nullptr;
-  int64_t n_chunks = 0;
+  // static pull schedule: item i covers in-edges [item_lo[i], item_hi[i]) of
+  // entity item_v[i] (stored as ~v when the in-row is split over several
+  // items, which then merge with atomics); items ascend by entity
+  int32_t* item_v = nullptr;
+  int32_t* item_lo = nullptr;
+  int32_t* item_hi = nullptr;
+  int64_t n_items = 0;
+  int64_t n_split = 0;  // entities whose in-row spans several items
   int64_t max_out = 0, max_in = 0;
   uint64_t bytes = 0;
   int64_t launches = 0;

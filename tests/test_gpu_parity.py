@@ -132,8 +132,8 @@ def _hub_graph(E, T, R, seed, alpha=1.2):
 def test_hub_graph_two_waves_vs_oracle(th, sem, divisor):
     """1,100 seeds (two waves), hub rows above the heavy thresholds, every
     direction policy; checked against the oracle seed by seed."""
-    s, r, o = _hub_graph(3000, 60000, 5, seed=11)
-    E, R = 3000, 5
+    s, r, o = _hub_graph(3000, 100000, 64, seed=11)
+    E, R = 3000, 64
     g = th.build_incidence((s, r, o), E, R)
     st = g.stats()
     assert st["max_out_degree"] > 4096 and st["max_in_degree"] > 4096
