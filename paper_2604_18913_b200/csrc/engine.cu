@@ -37,7 +37,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int32_t kHeavyPush = 4096;  // rows longer than this are split
 constexpr int32_t kPushChunk = 1024;
-constexpr int kMatBlocks = 2048;      // target materialisation blocks
+constexpr int kMatBlocks = 4096;      // target materialisation blocks
 
 __device__ __forceinline__ uint32_t valid_word(int j, int nq) {
   const int lo = 32 * j;
@@ -322,170 +322,7 @@ __global__ void __launch_bounds__(kThreads) edge_count_filtered_kernel(WaveArgs 
     if (sc[t]) atomicAdd((unsigned long long*)&out[t], (unsigned long long)sc[t]);
 }
 
-// ------------------------------------------------------------ pull hop
-
-// VEC words per lane, LPR lanes per entity row, GPW rows (groups) per warp
-template <int W>
-struct RowShape {
-  static constexpr int VEC = W >= 4 ? 4 : W;
-  static constexpr int LPR = W / VEC;
-  static constexpr int GPW = 32 / LPR;
-};
-
-template <int VEC>
-__device__ __forceinline__ void ld_words(const uint32_t* p, uint32_t (&o)[VEC]) {
-  if constexpr (VEC == 4) {
-    const uint4 t = *reinterpret_cast<const uint4*>(p);
-    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
-  } else if constexpr (VEC == 2) {
-    const uint2 t = *reinterpret_cast<const uint2*>(p);
-    o[0] = t.x; o[1] = t.y;
-  } else {
-    o[0] = *p;
-  }
-}
-
-// read-only path for data the kernel never writes (frontier rows, masks)
-template <int VEC>
-__device__ __forceinline__ void ldg_words(const uint32_t* p, uint32_t (&o)[VEC]) {
-  if constexpr (VEC == 4) {
-    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
-    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
-  } else if constexpr (VEC == 2) {
-    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
-    o[0] = t.x; o[1] = t.y;
-  } else {
-    o[0] = __ldg(p);
-  }
-}
-
-template <int VEC>
-__device__ __forceinline__ void st_words(uint32_t* p, const uint32_t (&v)[VEC]) {
-  if constexpr (VEC == 4) {
-    *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
-  } else if constexpr (VEC == 2) {
-    *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[1]);
-  } else {
-    *p = v[0];
-  }
-}
-
-// Pull hop over the static in-edge items of the reverse CSR.  Each lane
-// group (LPR lanes, 16 B per lane) owns one item and ORs the frontier rows of
-// its active in-neighbours (4 rows in flight per group, GPW groups per warp,
-// all in lockstep so the warp stays convergent).  A group stops early once
-// every live query has visited or reached the entity.  Whole in-rows are
-// finished with plain stores; rows split over several items merge with
-// atomicOr (the union of the pieces is exactly R_h & ~V_{h-1}).
-template <int W, int SEM, bool FILTER>
-__global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
-  if (a.ctl->mode[a.h] != 1) return;
-  using RS = RowShape<W>;
-  constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
-  const unsigned lane = lane_id();
-  const int part = (int)lane % LPR, grp = (int)lane / LPR;
-  const unsigned gbits = (LPR == 32 ? TH_FULL : ((1u << LPR) - 1u)) << (grp * LPR);
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint32_t valid[VEC];
-#pragma unroll
-  for (int c = 0; c < VEC; ++c) valid[c] = valid_word(part * VEC + c, a.nq);
-  const int64_t n = a.n_items;
-  for (int64_t base = warp * GPW; base < n; base += nwarps * GPW) {
-    const int64_t it = base + grp;
-    const bool live = it < n;
-    int32_t vv = 0, lo = 0, hi = 0;
-    if (live) {
-      vv = a.item_v[it];
-      lo = a.item_lo[it];
-      hi = a.item_hi[it];
-    }
-    const bool split = vv < 0;
-    const int32_t v = split ? ~vv : vv;
-    const size_t row = (size_t)v * W + part * VEC;
-    uint32_t seen[VEC], acc[VEC];
-#pragma unroll
-    for (int c = 0; c < VEC; ++c) {
-      seen[c] = 0u;
-      acc[c] = 0u;
-    }
-    if (SEM != TH_EXACT && live) ld_words<VEC>(a.V + row, seen);
-    bool sat = true;
-#pragma unroll
-    for (int c = 0; c < VEC; ++c) sat &= (seen[c] & valid[c]) == valid[c];
-    // the full-mask ballot must run on every lane (no short-circuit around it)
-    const bool group_sat = (__ballot_sync(TH_FULL, sat) & gbits) == gbits;
-    bool done = !live || (SEM != TH_EXACT && group_sat);
-    const int len = done ? 0 : hi - lo;
-    int maxlen = len;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(TH_FULL, maxlen, o));
-    for (int e0 = 0; e0 < maxlen; e0 += 4) {
-      int32_t u[4];
-      uint32_t rr[4];
-      bool act[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        act[k] = !done && e0 + k < len;
-        u[k] = act[k] ? __ldg(a.rsrc + lo + e0 + k) : 0;
-        rr[k] = (FILTER && act[k]) ? (uint32_t)__ldg(a.rrel + lo + e0 + k) : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (act[k]) act[k] = (__ldg(a.Xf + (u[k] >> 5)) >> (u[k] & 31)) & 1u;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (act[k]) {
-          uint32_t x[VEC];
-          ldg_words<VEC>(a.X + (size_t)u[k] * W + part * VEC, x);
-          if (FILTER) {
-            uint32_t m[VEC];
-            ldg_words<VEC>(a.M + (size_t)rr[k] * W + part * VEC, m);
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) x[c] &= m[c];
-          }
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
-        }
-      }
-      bool full = true;
-#pragma unroll
-      for (int c = 0; c < VEC; ++c) full &= ((acc[c] | seen[c]) & valid[c]) == valid[c];
-      if ((__ballot_sync(TH_FULL, full) & gbits) == gbits) done = true;
-      if (__all_sync(TH_FULL, done)) break;
-    }
-    uint32_t nb[VEC];
-    bool any = false;
-#pragma unroll
-    for (int c = 0; c < VEC; ++c) {
-      nb[c] = acc[c] & ~seen[c] & valid[c];
-      any |= nb[c] != 0u;
-    }
-    any = (__ballot_sync(TH_FULL, any) & gbits) != 0u;
-    bool fresh = false;
-    if (live && any) {
-      if (!split) {
-        st_words<VEC>(a.N + row, nb);
-        if (SEM != TH_EXACT) {
-          uint32_t nv[VEC];
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) nv[c] = seen[c] | nb[c];
-          st_words<VEC>(a.V + row, nv);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < VEC; ++c) {
-          if (nb[c]) {
-            atomicOr(a.N + row + c, nb[c]);
-            if (SEM != TH_EXACT) atomicOr(a.V + row + c, nb[c]);
-          }
-        }
-      }
-      if (part == 0) fresh = flag_next(a, v);
-    }
-    append_next(a, fresh, v);
-  }
-}
+#include "k3_pull.cuh"
 
 // ------------------------------------------------------------- clearing
 
@@ -523,179 +360,7 @@ __global__ void build_mask_kernel(const uint32_t* __restrict__ masks, int mask_w
 
 // ------------------------------------------------------ materialisation
 
-// rows = entities; word = A & ~neg, restricted to live queries
-template <int W>
-struct DenseSrc {
-  const uint32_t* A;
-  const uint32_t* neg;
-  const uint32_t* flags;
-  int64_t nrows;
-  int nq;
-  __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
-    aux = 0;
-    const int64_t left = nrows - r0;
-    const uint32_t tail = left >= 32 ? TH_FULL : ((1u << left) - 1u);
-    return (flags ? flags[r0 >> 5] : TH_FULL) & tail;
-  }
-  __device__ __forceinline__ uint32_t word(int64_t r, int j, int64_t) const {
-    uint32_t x = A[(size_t)r * W + j];
-    if (neg) x &= ~neg[(size_t)r * W + j];
-    return x & valid_word(j, nq);
-  }
-};
-
-// rows = triples in tid order; word = X[subj[t]] & M[rel[t]]
-template <int W>
-struct TripleSrc {
-  const uint32_t* X;
-  const uint32_t* Xf;
-  const uint32_t* M;
-  const int32_t* subj;
-  const uint16_t* rel;
-  int64_t nrows;
-  int nq;
-  __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
-    const int64_t t = r0 + lane_id();
-    bool act = false;
-    aux = 0;
-    if (t < nrows) {
-      const int32_t s = subj[t];
-      act = (Xf[s >> 5] >> (s & 31)) & 1u;
-      aux = ((int64_t)rel[t] << 32) | (uint32_t)s;
-    }
-    return __ballot_sync(TH_FULL, act);
-  }
-  __device__ __forceinline__ uint32_t word(int64_t, int j, int64_t aux) const {
-    const uint32_t s = (uint32_t)aux;
-    uint32_t x = X[(size_t)s * W + j];
-    if (M) x &= M[(size_t)(aux >> 32) * W + j];
-    return x & valid_word(j, nq);
-  }
-};
-
-constexpr int kMatThreads = 128;
-constexpr int kMatWarps = kMatThreads / 32;
-constexpr int kSB = 4;                 // 32-row sub-blocks per batch
-constexpr int kBatch = 32 * kSB;       // rows per batch
-constexpr int kStageStride = kBatch + 1;
-
-template <int W>
-struct MatShape {
-  static constexpr int JC = W < 8 ? W : 8;  // words staged per pass (one 32 B sector per row)
-};
-
-template <int W, bool WRITE>
-constexpr size_t mat_smem_bytes() {
-  return (size_t)kMatWarps *
-         ((size_t)kBatch * (MatShape<W>::JC + 1) + (size_t)32 * W +
-          (WRITE ? (size_t)32 * kStageStride : 0)) *
-         sizeof(uint32_t);
-}
-
-// K4 materialisation: bit-transpose entity-major rows into per-query sorted
-// id lists.  A warp walks its block of rows in 128-row batches; for every
-// 8-word column chunk it stages the batch's 32 B row sectors in shared
-// memory, transposes 32x32 bit tiles (lane b then holds query 32j+b's row
-// masks), and COUNT accumulates popcounts while WRITE first gathers each
-// query's ids into a per-query shared-memory run and then stores the runs
-// with all 32 lanes (coalesced, query by query).
-template <int W, class Src, bool WRITE>
-__global__ void __launch_bounds__(kMatThreads) mat_kernel(Src src, int64_t blk_rows, int nblk,
-                                                          int32_t* counts, const int64_t* base,
-                                                          int32_t* out, int64_t cap) {
-  constexpr int JC = MatShape<W>::JC;
-  extern __shared__ uint32_t mat_smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* tile = mat_smem + (size_t)warp * kBatch * (JC + 1);
-  int32_t* runs = reinterpret_cast<int32_t*>(mat_smem + (size_t)kMatWarps * kBatch * (JC + 1)) +
-                  (size_t)warp * 32 * W;
-  int32_t* stage = reinterpret_cast<int32_t*>(mat_smem + (size_t)kMatWarps * (kBatch * (JC + 1) + 32 * W)) +
-                   (size_t)warp * 32 * kStageStride;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int blk = gw; blk < nblk; blk += nw) {
-    // runs[j*32+lane]: ids so far in this block for query 32j+lane
-    for (int j = 0; j < W; ++j) runs[j * 32 + lane] = 0;
-    const int64_t r_begin = (int64_t)blk * blk_rows;
-    const int64_t rend = src.nrows < r_begin + blk_rows ? src.nrows : r_begin + blk_rows;
-    for (int64_t r0 = r_begin; r0 < rend; r0 += kBatch) {
-      uint32_t fl[kSB];
-      int64_t aux[kSB];
-      uint32_t anyfl = 0;
-#pragma unroll
-      for (int sb = 0; sb < kSB; ++sb) {
-        fl[sb] = r0 + 32 * sb < rend ? src.prep(r0 + 32 * sb, aux[sb]) : 0u;
-        anyfl |= fl[sb];
-      }
-      if (!anyfl) continue;
-#pragma unroll 1
-      for (int jc = 0; jc < W; jc += JC) {
-        // stage words [jc, jc+JC) of the batch's flagged rows
-#pragma unroll
-        for (int sb = 0; sb < kSB; ++sb) {
-          if (!fl[sb]) continue;
-#pragma unroll
-          for (int it = 0; it < JC; ++it) {
-            const int idx = it * 32 + lane;
-            const int row = idx / JC, jj = idx % JC;
-            const int64_t ra = __shfl_sync(TH_FULL, aux[sb], row);
-            tile[(sb * 32 + row) * (JC + 1) + jj] =
-                ((fl[sb] >> row) & 1u) ? src.word(r0 + 32 * sb + row, jc + jj, ra) : 0u;
-          }
-        }
-        __syncwarp();
-#pragma unroll 1
-        for (int jj = 0; jj < JC; ++jj) {
-          const int j = jc + jj;
-          uint32_t t[kSB];
-          int c = 0;
-#pragma unroll
-          for (int sb = 0; sb < kSB; ++sb) {
-            t[sb] = fl[sb] ? transpose32(tile[(sb * 32 + lane) * (JC + 1) + jj]) : 0u;
-            c += __popc(t[sb]);
-          }
-          const int prev = runs[j * 32 + lane];
-          if (WRITE) {
-            int32_t* my = stage + lane * kStageStride;
-            int k = 0;
-#pragma unroll
-            for (int sb = 0; sb < kSB; ++sb) {
-              uint32_t m = t[sb];
-              while (m) {
-                my[k++] = (int32_t)(r0 + 32 * sb + __ffs(m) - 1);
-                m &= m - 1u;
-              }
-            }
-            __syncwarp();
-            const int q = 32 * j + lane;
-            int64_t mypos = 0;
-            if (c > 0) mypos = base[q] + counts[(size_t)q * nblk + blk] + prev;
-            unsigned nzq = __ballot_sync(TH_FULL, c > 0);
-            while (nzq) {
-              const int b = __ffs(nzq) - 1;
-              nzq &= nzq - 1u;
-              const int cb = __shfl_sync(TH_FULL, c, b);
-              const int64_t pb = __shfl_sync(TH_FULL, mypos, b);
-              const int32_t* src_run = stage + b * kStageStride;
-              for (int kk = lane; kk < cb; kk += 32)
-                if (pb + kk < cap) out[pb + kk] = src_run[kk];
-            }
-            __syncwarp();
-          }
-          runs[j * 32 + lane] = prev + c;
-        }
-        __syncwarp();
-      }
-    }
-    if (!WRITE) {
-      for (int j = 0; j < W; ++j) {
-        const int q = 32 * j + lane;
-        if (q < src.nq) counts[(size_t)q * nblk + blk] = runs[j * 32 + lane];
-      }
-    }
-    __syncwarp();
-  }
-}
+#include "k4_materialize.cuh"
 
 // one block per query: exclusive scan over its block counts; totals[q]
 __global__ void mat_scan_rows_kernel(int32_t* counts, int nblk, int64_t* totals) {
@@ -807,29 +472,19 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
     TH_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * nq, s->st));
     return;
   }
-  constexpr size_t smem_c = mat_smem_bytes<W, false>();
-  constexpr size_t smem_w = mat_smem_bytes<W, true>();
-  static bool attr_done = false;  // one per template instantiation
-  if (!attr_done) {
-    TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_c));
-    TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, true>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
-    attr_done = true;
-  }
-  constexpr int64_t batch = kBatch;
+  constexpr int64_t batch = 32;
   const int64_t blk_rows = std::max<int64_t>(batch, ceil_div(ceil_div(rows, kMatBlocks), batch) * batch);
   const int nblk = (int)ceil_div(rows, blk_rows);
   const unsigned grid =
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nblk, kMatWarps), kNumSMs * 16));
-  mat_kernel<W, Src, false><<<grid, kMatThreads, smem_c, s->st>>>(src, blk_rows, nblk, b.counts,
+  mat_kernel<W, Src, false><<<grid, kMatThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
                                                                nullptr, nullptr, 0);
   TH_LAUNCHED();
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
   TH_LAUNCHED();
   mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
   TH_LAUNCHED();
-  mat_kernel<W, Src, true><<<grid, kMatThreads, smem_w, s->st>>>(src, blk_rows, nblk, b.counts, off,
+  mat_kernel<W, Src, true><<<grid, kMatThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts, off,
                                                               out, cap);
   TH_LAUNCHED();
   s->launches += 4;

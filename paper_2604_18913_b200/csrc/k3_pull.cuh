@@ -1,0 +1,169 @@
+// Part of engine.cu (included inside namespace th::{anonymous}); kept in its
+// own file so the kernel can be revised in isolation.
+#pragma once
+
+// ------------------------------------------------------------ pull hop
+
+// VEC words per lane, LPR lanes per entity row, GPW rows (groups) per warp
+template <int W>
+struct RowShape {
+  static constexpr int VEC = W >= 4 ? 4 : W;
+  static constexpr int LPR = W / VEC;
+  static constexpr int GPW = 32 / LPR;
+};
+
+template <int VEC>
+__device__ __forceinline__ void ld_words(const uint32_t* p, uint32_t (&o)[VEC]) {
+  if constexpr (VEC == 4) {
+    const uint4 t = *reinterpret_cast<const uint4*>(p);
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  } else if constexpr (VEC == 2) {
+    const uint2 t = *reinterpret_cast<const uint2*>(p);
+    o[0] = t.x; o[1] = t.y;
+  } else {
+    o[0] = *p;
+  }
+}
+
+// read-only path for data the kernel never writes (frontier rows, masks)
+template <int VEC>
+__device__ __forceinline__ void ldg_words(const uint32_t* p, uint32_t (&o)[VEC]) {
+  if constexpr (VEC == 4) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+    o[0] = t.x; o[1] = t.y; o[2] = t.z; o[3] = t.w;
+  } else if constexpr (VEC == 2) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+    o[0] = t.x; o[1] = t.y;
+  } else {
+    o[0] = __ldg(p);
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void st_words(uint32_t* p, const uint32_t (&v)[VEC]) {
+  if constexpr (VEC == 4) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (VEC == 2) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(v[0], v[1]);
+  } else {
+    *p = v[0];
+  }
+}
+
+// Pull hop over the static in-edge items of the reverse CSR.  Each lane
+// group (LPR lanes, 16 B per lane) owns one item and ORs the frontier rows of
+// its active in-neighbours (4 rows in flight per group, GPW groups per warp,
+// all in lockstep so the warp stays convergent).  A group stops early once
+// every live query has visited or reached the entity.  Whole in-rows are
+// finished with plain stores; rows split over several items merge with
+// atomicOr (the union of the pieces is exactly R_h & ~V_{h-1}).
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
+  if (a.ctl->mode[a.h] != 1) return;
+  using RS = RowShape<W>;
+  constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
+  const unsigned lane = lane_id();
+  const int part = (int)lane % LPR, grp = (int)lane / LPR;
+  const unsigned gbits = (LPR == 32 ? TH_FULL : ((1u << LPR) - 1u)) << (grp * LPR);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t valid[VEC];
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) valid[c] = valid_word(part * VEC + c, a.nq);
+  const int64_t n = a.n_items;
+  for (int64_t base = warp * GPW; base < n; base += nwarps * GPW) {
+    const int64_t it = base + grp;
+    const bool live = it < n;
+    int32_t vv = 0, lo = 0, hi = 0;
+    if (live) {
+      vv = a.item_v[it];
+      lo = a.item_lo[it];
+      hi = a.item_hi[it];
+    }
+    const bool split = vv < 0;
+    const int32_t v = split ? ~vv : vv;
+    const size_t row = (size_t)v * W + part * VEC;
+    uint32_t seen[VEC], acc[VEC];
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) {
+      seen[c] = 0u;
+      acc[c] = 0u;
+    }
+    if (SEM != TH_EXACT && live) ld_words<VEC>(a.V + row, seen);
+    bool sat = true;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) sat &= (seen[c] & valid[c]) == valid[c];
+    // the full-mask ballot must run on every lane (no short-circuit around it)
+    const bool group_sat = (__ballot_sync(TH_FULL, sat) & gbits) == gbits;
+    bool done = !live || (SEM != TH_EXACT && group_sat);
+    const int len = done ? 0 : hi - lo;
+    int maxlen = len;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(TH_FULL, maxlen, o));
+    for (int e0 = 0; e0 < maxlen; e0 += 4) {
+      int32_t u[4];
+      uint32_t rr[4];
+      bool act[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        act[k] = !done && e0 + k < len;
+        u[k] = act[k] ? __ldg(a.rsrc + lo + e0 + k) : 0;
+        rr[k] = (FILTER && act[k]) ? (uint32_t)__ldg(a.rrel + lo + e0 + k) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (act[k]) act[k] = (__ldg(a.Xf + (u[k] >> 5)) >> (u[k] & 31)) & 1u;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (act[k]) {
+          uint32_t x[VEC];
+          ldg_words<VEC>(a.X + (size_t)u[k] * W + part * VEC, x);
+          if (FILTER) {
+            uint32_t m[VEC];
+            ldg_words<VEC>(a.M + (size_t)rr[k] * W + part * VEC, m);
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) x[c] &= m[c];
+          }
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
+        }
+      }
+      bool full = true;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) full &= ((acc[c] | seen[c]) & valid[c]) == valid[c];
+      if ((__ballot_sync(TH_FULL, full) & gbits) == gbits) done = true;
+      if (__all_sync(TH_FULL, done)) break;
+    }
+    uint32_t nb[VEC];
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < VEC; ++c) {
+      nb[c] = acc[c] & ~seen[c] & valid[c];
+      any |= nb[c] != 0u;
+    }
+    any = (__ballot_sync(TH_FULL, any) & gbits) != 0u;
+    bool fresh = false;
+    if (live && any) {
+      if (!split) {
+        st_words<VEC>(a.N + row, nb);
+        if (SEM != TH_EXACT) {
+          uint32_t nv[VEC];
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) nv[c] = seen[c] | nb[c];
+          st_words<VEC>(a.V + row, nv);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          if (nb[c]) {
+            atomicOr(a.N + row + c, nb[c]);
+            if (SEM != TH_EXACT) atomicOr(a.V + row + c, nb[c]);
+          }
+        }
+      }
+      if (part == 0) fresh = flag_next(a, v);
+    }
+    append_next(a, fresh, v);
+  }
+}
+
