@@ -35,8 +35,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int32_t kHeavyPush = 4096;  // rows longer than this are split
-constexpr int32_t kPushChunk = 1024;
+constexpr int32_t kHeavyPush = 256;  // rows longer than this are split across warps
+constexpr int32_t kPushChunk = 256;
 constexpr int kMatBlocks = 4096;      // target materialisation blocks
 
 __device__ __forceinline__ uint32_t valid_word(int j, int nq) {
@@ -472,20 +472,29 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
     TH_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * nq, s->st));
     return;
   }
-  constexpr int64_t batch = 32;
-  const int64_t blk_rows = std::max<int64_t>(batch, ceil_div(ceil_div(rows, kMatBlocks), batch) * batch);
+  constexpr int NW = mat_warps<W>();
+  constexpr int NG = W / NW;
+  constexpr size_t smem_w = mat_smem_bytes<W, true>();
+  static bool attr_done = false;  // one per template instantiation
+  if (!attr_done) {
+    TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
+    attr_done = true;
+  }
+  // about six CTAs per SM in total; blocks are whole 32-row tiles
+  const int64_t target = std::max<int64_t>(1, (int64_t)kNumSMs * 6 / NG);
+  const int64_t blk_rows = std::max<int64_t>(32, ceil_div(ceil_div(rows, target), 32) * 32);
   const int nblk = (int)ceil_div(rows, blk_rows);
-  const unsigned grid =
-      (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(nblk, kMatWarps), kNumSMs * 16));
-  mat_kernel<W, Src, false><<<grid, kMatThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts,
-                                                               nullptr, nullptr, 0);
+  const unsigned grid = (unsigned)(nblk * NG);
+  mat_kernel<W, Src, false><<<grid, 32 * NW, 0, s->st>>>(src, blk_rows, nblk, b.counts, nullptr,
+                                                         nullptr, 0);
   TH_LAUNCHED();
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
   TH_LAUNCHED();
   mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
   TH_LAUNCHED();
-  mat_kernel<W, Src, true><<<grid, kMatThreads, 0, s->st>>>(src, blk_rows, nblk, b.counts, off,
-                                                              out, cap);
+  mat_kernel<W, Src, true><<<grid, 32 * NW, smem_w, s->st>>>(src, blk_rows, nblk, b.counts, off,
+                                                             out, cap);
   TH_LAUNCHED();
   s->launches += 4;
 }

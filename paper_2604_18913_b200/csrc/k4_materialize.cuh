@@ -1,28 +1,26 @@
 // Part of engine.cu (included inside namespace th::{anonymous}); kept in its
 // own file so the kernel can be revised in isolation.
+//
+// K4 materialisation: per-query sorted id lists (the canonical EntityVector /
+// TripleVector form, incidence.py:83-91) from entity-major bit rows.
+//
+// Grid = (row block) x (group of up to 8 row words).  Warp w of a CTA owns
+// word j = 8g + w, i.e. queries 32j..32j+31, over the block's rows; the 8
+// warps read the 8 words of one 32-byte sector per row, so every row sector
+// is fetched from L2 once.  Per 32-row tile a lane loads its row's word, a
+// 32x32 bit transpose hands lane b the row mask of query 32j+b.
+//   COUNT: per-lane popcounts -> counts[q][blk].
+//   WRITE: lane b appends its query's row ids to a 64-entry shared-memory
+//          ring; whenever a ring holds 32 ids the whole warp stores them as
+//          one coalesced 128-byte run.  Ascending row order is preserved, so
+//          every query's output is sorted and duplicate-free.
 #pragma once
 
-// one lane loads the W words of row r of an entity-major matrix
-template <int W>
-__device__ __forceinline__ void load_row(const uint32_t* A, int64_t r, bool live, uint32_t (&w)[W]) {
-  const uint32_t* p = A + (size_t)r * W;
-  if constexpr (W >= 4) {
-#pragma unroll
-    for (int k = 0; k < W / 4; ++k) {
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      if (live) v = *reinterpret_cast<const uint4*>(p + 4 * k);
-      w[4 * k] = v.x;
-      w[4 * k + 1] = v.y;
-      w[4 * k + 2] = v.z;
-      w[4 * k + 3] = v.w;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < W; ++k) w[k] = live ? p[k] : 0u;
-  }
-}
+constexpr int kMatWordsPerCta = 8;
+constexpr int kRing = 64;
+constexpr int kRingStride = kRing + 1;
 
-// rows = entities; row word j = A & ~neg, restricted to live queries
+// rows = entities; word j of row r = A & ~neg, restricted to live queries
 template <int W>
 struct DenseSrc {
   const uint32_t* A;
@@ -37,21 +35,14 @@ struct DenseSrc {
     const uint32_t tail = left >= 32 ? TH_FULL : ((1u << left) - 1u);
     return (flags ? flags[r0 >> 5] : TH_FULL) & tail;
   }
-  // the W words of row r into w (zero when !live)
-  __device__ __forceinline__ void row(int64_t r, int64_t, bool live, uint32_t (&w)[W]) const {
-    load_row<W>(A, r, live, w);
-    if (neg && live) {
-      uint32_t n[W];
-      load_row<W>(neg, r, true, n);
-#pragma unroll
-      for (int j = 0; j < W; ++j) w[j] &= ~n[j];
-    }
-#pragma unroll
-    for (int j = 0; j < W; ++j) w[j] &= valid_word(j, nq);
+  __device__ __forceinline__ uint32_t word(int64_t r, int64_t, int j) const {
+    uint32_t x = A[(size_t)r * W + j];
+    if (neg) x &= ~neg[(size_t)r * W + j];
+    return x & valid_word(j, nq);
   }
 };
 
-// rows = triples in tid order; row word j = X[subj[t]] & M[rel[t]]
+// rows = triples in tid order; word j of row t = X[subj[t]] & M[rel[t]]
 template <int W>
 struct TripleSrc {
   const uint32_t* X;
@@ -72,85 +63,87 @@ struct TripleSrc {
     }
     return __ballot_sync(TH_FULL, act);
   }
-  __device__ __forceinline__ void row(int64_t, int64_t aux, bool live, uint32_t (&w)[W]) const {
-    load_row<W>(X, (int64_t)(uint32_t)aux, live, w);
-    if (M && live) {
-      uint32_t m[W];
-      load_row<W>(M, aux >> 32, true, m);
-#pragma unroll
-      for (int j = 0; j < W; ++j) w[j] &= m[j];
-    }
-#pragma unroll
-    for (int j = 0; j < W; ++j) w[j] &= valid_word(j, nq);
+  __device__ __forceinline__ uint32_t word(int64_t, int64_t aux, int j) const {
+    uint32_t x = X[(size_t)(uint32_t)aux * W + j];
+    if (M) x &= M[(size_t)(aux >> 32) * W + j];
+    return x & valid_word(j, nq);
   }
 };
 
-constexpr int kMatThreads = 128;
-constexpr int kMatWarps = kMatThreads / 32;
+template <int W>
+constexpr int mat_warps() {
+  return W < kMatWordsPerCta ? W : kMatWordsPerCta;
+}
 
-// K4 materialisation: per-query sorted id lists from entity-major bit rows.
-// A warp owns a block of rows and walks it 32 rows at a time: lane i loads
-// row r0+i (W words, 16-byte loads), one 32x32 bit transpose per word j
-// gives lane b the 32-row mask of query 32j+b.  COUNT adds popcounts;
-// WRITE visits each query with ids in the tile and lets the lanes holding
-// them store their row ids into consecutive slots (one coalesced store per
-// query and tile, ascending row order = the canonical sorted form).
+template <int W, bool WRITE>
+constexpr size_t mat_smem_bytes() {
+  return WRITE ? (size_t)mat_warps<W>() * 32 * kRingStride * sizeof(int32_t) : 0;
+}
+
 template <int W, class Src, bool WRITE>
-__global__ void __launch_bounds__(kMatThreads) mat_kernel(Src src, int64_t blk_rows, int nblk,
-                                                          int32_t* counts, const int64_t* base,
-                                                          int32_t* out, int64_t cap) {
-  __shared__ int64_t gbase_s[kMatWarps][WRITE ? 32 * W : 1];
+__global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int64_t blk_rows,
+                                                                   int nblk, int32_t* counts,
+                                                                   const int64_t* base, int32_t* out,
+                                                                   int64_t cap) {
+  extern __shared__ int32_t ring_smem[];
+  constexpr int NW = mat_warps<W>();
+  constexpr int NG = W / NW;  // word groups
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned lt = lanemask_lt();
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int blk = gw; blk < nblk; blk += nw) {
-    int32_t run[W];
-#pragma unroll
-    for (int j = 0; j < W; ++j) run[j] = 0;
-    if (WRITE) {
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        const int q = 32 * j + lane;
-        gbase_s[warp][32 * j + lane] = q < src.nq ? base[q] + counts[(size_t)q * nblk + blk] : 0;
-      }
-      __syncwarp();
+  const int blk = blockIdx.x / NG;
+  const int j = (blockIdx.x % NG) * NW + warp;
+  const int q = 32 * j + lane;
+  if (blk >= nblk) return;
+  int32_t* ring = ring_smem + (size_t)warp * 32 * kRingStride;
+  int32_t* mine = ring + lane * kRingStride;
+  int64_t pos = 0;
+  int head = 0, fill = 0;
+  int32_t total = 0;
+  if (WRITE && q < src.nq) pos = base[q] + counts[(size_t)q * nblk + blk];
+  const int64_t r_begin = (int64_t)blk * blk_rows;
+  const int64_t rend = src.nrows < r_begin + blk_rows ? src.nrows : r_begin + blk_rows;
+  for (int64_t r0 = r_begin; r0 < rend; r0 += 32) {
+    int64_t aux;
+    const uint32_t fl = src.prep(r0, aux);
+    if (!fl) continue;
+    const uint32_t x = ((fl >> lane) & 1u) ? src.word(r0 + lane, aux, j) : 0u;
+    if (!__any_sync(TH_FULL, x != 0u)) continue;
+    uint32_t m = transpose32(x);
+    total += __popc(m);
+    if (!WRITE) continue;
+    while (m) {
+      mine[(head + fill) & (kRing - 1)] = (int32_t)(r0 + __ffs(m) - 1);
+      ++fill;
+      m &= m - 1u;
     }
-    const int64_t r_begin = (int64_t)blk * blk_rows;
-    const int64_t rend = src.nrows < r_begin + blk_rows ? src.nrows : r_begin + blk_rows;
-    for (int64_t r0 = r_begin; r0 < rend; r0 += 32) {
-      int64_t aux;
-      const uint32_t fl = src.prep(r0, aux);
-      if (!fl) continue;
-      uint32_t w[W];
-      src.row(r0 + lane, aux, (fl >> lane) & 1u, w);
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        const uint32_t t = transpose32(w[j]);
-        if (WRITE) {
-          unsigned act = __ballot_sync(TH_FULL, t != 0u);
-          while (act) {
-            const int b = __ffs(act) - 1;
-            act &= act - 1u;
-            const uint32_t m = __shfl_sync(TH_FULL, t, b);
-            const int32_t rb = __shfl_sync(TH_FULL, run[j], b);
-            if ((m >> lane) & 1u) {
-              const int64_t pos = gbase_s[warp][32 * j + b] + rb + __popc(m & lt);
-              if (pos < cap) out[pos] = (int32_t)(r0 + lane);
-            }
-          }
-        }
-        run[j] += __popc(t);
-      }
-    }
-    if (!WRITE) {
-#pragma unroll
-      for (int j = 0; j < W; ++j) {
-        const int q = 32 * j + lane;
-        if (q < src.nq) counts[(size_t)q * nblk + blk] = run[j];
+    __syncwarp();
+    unsigned full = __ballot_sync(TH_FULL, fill >= 32);
+    while (full) {
+      const int b = __ffs(full) - 1;
+      full &= full - 1u;
+      const int hb = __shfl_sync(TH_FULL, head, b);
+      const int64_t pb = __shfl_sync(TH_FULL, pos, b);
+      const int32_t id = ring[b * kRingStride + ((hb + lane) & (kRing - 1))];
+      if (pb + lane < cap) out[pb + lane] = id;
+      if (lane == b) {
+        head = (head + 32) & (kRing - 1);
+        fill -= 32;
+        pos += 32;
       }
     }
     __syncwarp();
+  }
+  if (WRITE) {
+    unsigned rest = __ballot_sync(TH_FULL, fill > 0);
+    while (rest) {
+      const int b = __ffs(rest) - 1;
+      rest &= rest - 1u;
+      const int hb = __shfl_sync(TH_FULL, head, b);
+      const int fb = __shfl_sync(TH_FULL, fill, b);
+      const int64_t pb = __shfl_sync(TH_FULL, pos, b);
+      if (lane < fb && pb + lane < cap) out[pb + lane] = ring[b * kRingStride + ((hb + lane) & (kRing - 1))];
+    }
+  } else if (q < src.nq) {
+    counts[(size_t)q * nblk + blk] = total;
   }
 }
 
