@@ -465,7 +465,7 @@ struct WaveBufs {
 // count -> per-query scan -> offsets -> write, for any row source
 template <int W, class Src>
 void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, int64_t* len,
-                 int32_t* out, int64_t cap, int64_t* cursor) {
+                 int32_t* out, int64_t cap, int64_t* cursor, EdgeSum es = {}) {
   const int64_t rows = src.nrows;
   if (rows == 0) {
     TH_CUDA(cudaMemsetAsync(len, 0, sizeof(int64_t) * nq, s->st));
@@ -486,8 +486,12 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   const int64_t blk_rows = std::max<int64_t>(32, ceil_div(ceil_div(rows, target), 32) * 32);
   const int nblk = (int)ceil_div(rows, blk_rows);
   const unsigned grid = (unsigned)(nblk * NG);
-  mat_kernel<W, Src, false><<<grid, 32 * NW, 0, s->st>>>(src, blk_rows, nblk, b.counts, nullptr,
-                                                         nullptr, 0);
+  if (es.out)
+    mat_kernel<W, Src, false, true><<<grid, 32 * NW, 0, s->st>>>(src, blk_rows, nblk, b.counts,
+                                                                 nullptr, nullptr, 0, es);
+  else
+    mat_kernel<W, Src, false><<<grid, 32 * NW, 0, s->st>>>(src, blk_rows, nblk, b.counts, nullptr,
+                                                           nullptr, 0);
   TH_LAUNCHED();
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
   TH_LAUNCHED();
@@ -502,9 +506,9 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
 template <int W>
 void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
                        const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
-                       int64_t cap, int64_t* cursor) {
+                       int64_t cap, int64_t* cursor, EdgeSum es = {}) {
   DenseSrc<W> src{A, neg, flags, s->g->E, nq};
-  materialize<W>(s, b, src, nq, off, len, out, cap, cursor);
+  materialize<W>(s, b, src, nq, off, len, out, cap, cursor, es);
 }
 
 template <int W>
@@ -615,15 +619,20 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   const bool paths_need_l0 = (q->flags & TH_WANT_PATHS) && !(q->flags & 0x8u);
   const unsigned pg = persistent_grid();
 
+  int nplanes = 0;
+  while (nplanes < 31 && (int64_t(1) << nplanes) <= g->max_out) ++nplanes;
+  bool next_edges_done = false;
   for (int h = 1; h <= k; ++h) {
     a.h = h;
+    const bool edges_done = next_edges_done;
+    next_edges_done = false;
     {
       ProfScope ps(s, TH_PROF_SETUP);
       begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, g->T, s->pull_divisor, g->rindptr != nullptr);
       TH_LAUNCHED();
       s->launches += 1;
     }
-    {
+    if (!edges_done) {
       ProfScope ps(s, TH_PROF_EDGES);
       int64_t* e_out = edges + (h - 1) * B + q0;
       if (filter) {
@@ -656,10 +665,20 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
         materialize_dense<W>(s, b, b.V, b.S, b.Vf, nq, f_off + (h - 1) * B + q0,
                              f_len + (h - 1) * B + q0, static_cast<int32_t*>(s->f_ids.p), s->f_cap,
                              &b.ctl->ids_used);
-      else
+      else {
+        // the layer just materialised is X_h, so its count pass also yields
+        // |T_{h+1}| = sum of its out-degrees (unfiltered exact/frontier)
+        EdgeSum es{};
+        if (!filter && h < k) {
+          es.indptr = g->indptr;
+          es.nplanes = nplanes;
+          es.out = edges + h * B + q0;
+        }
         materialize_dense<W>(s, b, b.N, nullptr, b.Nf, nq, f_off + (h - 1) * B + q0,
                              f_len + (h - 1) * B + q0, static_cast<int32_t*>(s->f_ids.p), s->f_cap,
-                             &b.ctl->ids_used);
+                             &b.ctl->ids_used, es);
+        next_edges_done = es.out != nullptr;
+      }
     }
     {
       // retire X (rows of list segment h-1) and swap roles

@@ -80,11 +80,22 @@ constexpr size_t mat_smem_bytes() {
   return WRITE ? (size_t)mat_warps<W>() * 32 * kRingStride * sizeof(int32_t) : 0;
 }
 
-template <int W, class Src, bool WRITE>
+// EDGES (COUNT pass over an entity layer): also sum the out-degrees of each
+// query's rows -- |T_{h+1}(q)| when the layer is the next hop's frontier
+// (incidence.py:214-221: one activated triple per out-edge).  Degrees are
+// split into bit planes, one ballot per plane, so a query's sum is
+// sum_k popc(mask & plane_k) << k with no per-id work.
+struct EdgeSum {
+  const int32_t* indptr = nullptr;
+  int nplanes = 0;
+  int64_t* out = nullptr;  // [nq], accumulated with atomics
+};
+
+template <int W, class Src, bool WRITE, bool EDGES = false>
 __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int64_t blk_rows,
                                                                    int nblk, int32_t* counts,
                                                                    const int64_t* base, int32_t* out,
-                                                                   int64_t cap) {
+                                                                   int64_t cap, EdgeSum es = {}) {
   extern __shared__ int32_t ring_smem[];
   constexpr int NW = mat_warps<W>();
   constexpr int NG = W / NW;  // word groups
@@ -98,6 +109,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
   int64_t pos = 0;
   int head = 0, fill = 0;
   int32_t total = 0;
+  unsigned long long esum = 0;
   if (WRITE && q < src.nq) pos = base[q] + counts[(size_t)q * nblk + blk];
   const int64_t r_begin = (int64_t)blk * blk_rows;
   const int64_t rend = src.nrows < r_begin + blk_rows ? src.nrows : r_begin + blk_rows;
@@ -109,6 +121,13 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
     if (!__any_sync(TH_FULL, x != 0u)) continue;
     uint32_t m = transpose32(x);
     total += __popc(m);
+    if (EDGES) {
+      const int64_t r = r0 + lane;
+      const uint32_t d = ((fl >> lane) & 1u) ? (uint32_t)(es.indptr[r + 1] - es.indptr[r]) : 0u;
+      const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d));  // planes this tile needs
+      for (int k = 0; k < np; ++k)
+        esum += (unsigned long long)__popc(m & __ballot_sync(TH_FULL, (d >> k) & 1u)) << k;
+    }
     if (!WRITE) continue;
     while (m) {
       mine[(head + fill) & (kRing - 1)] = (int32_t)(r0 + __ffs(m) - 1);
@@ -144,6 +163,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
     }
   } else if (q < src.nq) {
     counts[(size_t)q * nblk + blk] = total;
+    if (EDGES && esum) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), esum);
   }
 }
 
