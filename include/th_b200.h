@@ -54,6 +54,8 @@ extern "C" {
 #define TH_WANT_FRONTIERS 0x1u /* per-query sorted frontier ids per hop      */
 #define TH_WANT_ACTIVATED 0x2u /* per-query sorted activated triple ids/hop  */
 #define TH_WANT_PATHS 0x4u     /* capped lexicographic walk enumeration       */
+#define TH_SINGLETON_SEEDS 0x8u /* every query is one seed (retrieve(seeds)):
+                                   paths start from the seed's CSR row       */
 
 /* th_graph_create flags */
 #define TH_GRAPH_NO_REVERSE 0x1u /* skip the reverse (by-object) CSR: no pull hops */

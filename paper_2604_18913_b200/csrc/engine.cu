@@ -616,7 +616,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   int64_t* edges = static_cast<int64_t*>(s->edges.p);
   const bool want_f = q->flags & TH_WANT_FRONTIERS;
   const bool want_a = q->flags & TH_WANT_ACTIVATED;
-  const bool paths_need_l0 = (q->flags & TH_WANT_PATHS) && !(q->flags & 0x8u);
+  const bool paths_need_l0 = (q->flags & TH_WANT_PATHS) && !(q->flags & TH_SINGLETON_SEEDS);
   const unsigned pg = persistent_grid();
 
   int nplanes = 0;
@@ -863,7 +863,7 @@ int session_run(Session* s, const th_query* q) {
     pa.l0_off = static_cast<const int64_t*>(s->a_off.p);
     pa.l0_len = static_cast<const int64_t*>(s->a_len.p);
     pa.l0_ids = static_cast<const int32_t*>(s->a_ids.p);
-    pa.singleton = (q->flags & 0x8u) != 0;
+    pa.singleton = (q->flags & TH_SINGLETON_SEEDS) != 0;
     pa.B = (int32_t)B;
     pa.k = (int32_t)k;
     pa.E = g->E;
