@@ -481,9 +481,11 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
     attr_done = true;
   }
-  // about six CTAs per SM in total; blocks are whole 32-row tiles
-  const int64_t target = std::max<int64_t>(1, (int64_t)kNumSMs * 6 / NG);
-  const int64_t blk_rows = std::max<int64_t>(32, ceil_div(ceil_div(rows, target), 32) * 32);
+  // about twelve CTAs per SM in total (two waves of the write pass, six
+  // resident CTAs per SM); blocks are whole 1024-row chunks
+  const int64_t target = std::max<int64_t>(1, (int64_t)kNumSMs * 12 / NG);
+  const int64_t blk_rows =
+      std::max<int64_t>(kChunkRows, ceil_div(ceil_div(rows, target), kChunkRows) * kChunkRows);
   const int nblk = (int)ceil_div(rows, blk_rows);
   const unsigned grid = (unsigned)(nblk * NG);
   if (es.out)

@@ -4,21 +4,26 @@
 // K4 materialisation: per-query sorted id lists (the canonical EntityVector /
 // TripleVector form, incidence.py:83-91) from entity-major bit rows.
 //
-// Grid = (row block) x (group of up to 8 row words).  Warp w of a CTA owns
-// word j = 8g + w, i.e. queries 32j..32j+31, over the block's rows; the 8
-// warps read the 8 words of one 32-byte sector per row, so every row sector
-// is fetched from L2 once.  Per 32-row tile a lane loads its row's word, a
-// 32x32 bit transpose hands lane b the row mask of query 32j+b.
-//   COUNT: per-lane popcounts -> counts[q][blk].
-//   WRITE: lane b appends its query's row ids to a 64-entry shared-memory
-//          ring; whenever a ring holds 32 ids the whole warp stores them as
-//          one coalesced 128-byte run.  Ascending row order is preserved, so
-//          every query's output is sorted and duplicate-free.
+// Grid = (row block) x (group of NW row words).  Warp w of a CTA owns word
+// j = NW*g + w, i.e. queries 32j..32j+31, and walks its block's rows in
+// chunks of 32 tiles x 32 rows:
+//   A. per tile, lane i loads row (r0+i)'s word j and a 32x32 bit transpose
+//      hands lane b the tile mask of query 32j+b; the 32 masks of the chunk
+//      go to shared memory as S[b][t] (lane b: its query's tile masks).
+//   COUNT: per-lane popcounts -> counts[q][blk]  (+ optional degree sums).
+//   WRITE: query by query, the warp takes S[b][0..31] (lane t = tile t),
+//          scans the popcounts for offsets, extracts the row ids of its tile
+//          into a shared staging run (ascending by construction), then
+//          stores the whole run coalesced at the query's cursor.
+// Ascending row order is preserved, so every query's output is sorted and
+// duplicate-free.  Per output id this costs about one extraction step on
+// one lane plus 1/32 of a coalesced store, instead of a per-lane serial
+// append with ring flushes.
 #pragma once
 
-constexpr int kMatWordsPerCta = 8;
-constexpr int kRing = 64;
-constexpr int kRingStride = kRing + 1;
+constexpr int kMatWordsPerCta = 4;          // warps per CTA (one row word each)
+constexpr int kChunkRows = 1024;            // 32 tiles of 32 rows
+constexpr int kSStride = 33;                // S[b][t] row stride (bank-conflict free)
 
 // rows = entities; word j of row r = A & ~neg, restricted to live queries
 template <int W>
@@ -28,6 +33,18 @@ struct DenseSrc {
   const uint32_t* flags;
   int64_t nrows;
   int nq;
+  static constexpr bool kDense = true;
+  // lane t: flags of rows [r0+32t, r0+32t+32) below `rend` (r0 % 32 == 0)
+  __device__ __forceinline__ uint32_t chunk_flags(int64_t r0, int64_t rend) const {
+    const int64_t t0 = r0 + 32 * (int64_t)lane_id();
+    if (t0 >= rend) return 0u;
+    const int64_t left = rend - t0;
+    const uint32_t tail = left >= 32 ? TH_FULL : ((1u << left) - 1u);
+    return (flags ? flags[t0 >> 5] : TH_FULL) & tail;
+  }
+  __device__ __forceinline__ bool chunk_any(int64_t r0, int64_t rend) const {
+    return __any_sync(TH_FULL, chunk_flags(r0, rend) != 0u);
+  }
   // flags of rows r0..r0+31 (warp-uniform); aux unused
   __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
     aux = 0;
@@ -52,6 +69,8 @@ struct TripleSrc {
   const uint16_t* rel;
   int64_t nrows;
   int nq;
+  static constexpr bool kDense = false;
+  __device__ __forceinline__ bool chunk_any(int64_t, int64_t) const { return true; }
   __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
     const int64_t t = r0 + lane_id();
     bool act = false;
@@ -75,9 +94,12 @@ constexpr int mat_warps() {
   return W < kMatWordsPerCta ? W : kMatWordsPerCta;
 }
 
+// S (33 x 32 words) + staging run (kChunkRows ids) per warp
+constexpr size_t kMatWarpSmem = (size_t)(32 * kSStride + kChunkRows) * sizeof(uint32_t);
+
 template <int W, bool WRITE>
 constexpr size_t mat_smem_bytes() {
-  return WRITE ? (size_t)mat_warps<W>() * 32 * kRingStride * sizeof(int32_t) : 0;
+  return (size_t)mat_warps<W>() * kMatWarpSmem;
 }
 
 // EDGES (COUNT pass over an entity layer): also sum the out-degrees of each
@@ -91,12 +113,22 @@ struct EdgeSum {
   int64_t* out = nullptr;  // [nq], accumulated with atomics
 };
 
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const unsigned lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(TH_FULL, v, o);
+    if (lane >= (unsigned)o) v += y;
+  }
+  return v;
+}
+
 template <int W, class Src, bool WRITE, bool EDGES = false>
 __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int64_t blk_rows,
                                                                    int nblk, int32_t* counts,
                                                                    const int64_t* base, int32_t* out,
                                                                    int64_t cap, EdgeSum es = {}) {
-  extern __shared__ int32_t ring_smem[];
+  extern __shared__ uint32_t mat_smem[];
   constexpr int NW = mat_warps<W>();
   constexpr int NG = W / NW;  // word groups
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -104,66 +136,92 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
   const int j = (blockIdx.x % NG) * NW + warp;
   const int q = 32 * j + lane;
   if (blk >= nblk) return;
-  int32_t* ring = ring_smem + (size_t)warp * 32 * kRingStride;
-  int32_t* mine = ring + lane * kRingStride;
+  uint32_t* S = mat_smem + (size_t)warp * (kMatWarpSmem / sizeof(uint32_t));
+  int32_t* stg = reinterpret_cast<int32_t*>(S + 32 * kSStride);
   int64_t pos = 0;
-  int head = 0, fill = 0;
   int32_t total = 0;
   unsigned long long esum = 0;
   if (WRITE && q < src.nq) pos = base[q] + counts[(size_t)q * nblk + blk];
   const int64_t r_begin = (int64_t)blk * blk_rows;
   const int64_t rend = src.nrows < r_begin + blk_rows ? src.nrows : r_begin + blk_rows;
-  for (int64_t r0 = r_begin; r0 < rend; r0 += 32) {
-    int64_t aux;
-    const uint32_t fl = src.prep(r0, aux);
-    if (!fl) continue;
-    const uint32_t x = ((fl >> lane) & 1u) ? src.word(r0 + lane, aux, j) : 0u;
-    if (!__any_sync(TH_FULL, x != 0u)) continue;
-    uint32_t m = transpose32(x);
-    total += __popc(m);
-    if (EDGES) {
-      const int64_t r = r0 + lane;
-      const uint32_t d = ((fl >> lane) & 1u) ? (uint32_t)(es.indptr[r + 1] - es.indptr[r]) : 0u;
-      const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d));  // planes this tile needs
-      for (int k = 0; k < np; ++k)
-        esum += (unsigned long long)__popc(m & __ballot_sync(TH_FULL, (d >> k) & 1u)) << k;
-    }
-    if (!WRITE) continue;
-    while (m) {
-      mine[(head + fill) & (kRing - 1)] = (int32_t)(r0 + __ffs(m) - 1);
-      ++fill;
-      m &= m - 1u;
-    }
-    __syncwarp();
-    unsigned full = __ballot_sync(TH_FULL, fill >= 32);
-    while (full) {
-      const int b = __ffs(full) - 1;
-      full &= full - 1u;
-      const int hb = __shfl_sync(TH_FULL, head, b);
-      const int64_t pb = __shfl_sync(TH_FULL, pos, b);
-      const int32_t id = ring[b * kRingStride + ((hb + lane) & (kRing - 1))];
-      if (pb + lane < cap) out[pb + lane] = id;
-      if (lane == b) {
-        head = (head + 32) & (kRing - 1);
-        fill -= 32;
-        pos += 32;
+  for (int64_t c0 = r_begin; c0 < rend; c0 += kChunkRows) {
+    if (!src.chunk_any(c0, rend)) continue;
+    // ---- A: tile masks of this chunk, S[b][t] = rows of tile t in query b.
+    // Loads of 8 tiles are issued before their transposes (memory-level
+    // parallelism); dense sources get all 32 tile flags from one load.
+    int32_t ccount = 0;
+    uint32_t cflags = 0u;  // lane t: flags of tile t (dense sources)
+    if constexpr (Src::kDense) cflags = src.chunk_flags(c0, rend);
+#pragma unroll 1
+    for (int t0 = 0; t0 < 32; t0 += 8) {
+      uint32_t x[8], fl[8];
+      int64_t aux[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t r0 = c0 + 32 * (t0 + u);
+        if constexpr (Src::kDense) {
+          fl[u] = __shfl_sync(TH_FULL, cflags, t0 + u);
+          aux[u] = 0;
+        } else {
+          fl[u] = r0 < rend ? src.prep(r0, aux[u]) : 0u;
+        }
+        x[u] = ((fl[u] >> lane) & 1u) ? src.word(r0 + lane, aux[u], j) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t r0 = c0 + 32 * (t0 + u);
+        uint32_t m = 0u;
+        if (__any_sync(TH_FULL, x[u] != 0u)) {
+          m = transpose32(x[u]);
+          if (EDGES) {
+            const int64_t r = r0 + lane;
+            const uint32_t d =
+                ((fl[u] >> lane) & 1u) ? (uint32_t)(es.indptr[r + 1] - es.indptr[r]) : 0u;
+            const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d));
+            for (int k = 0; k < np; ++k)
+              esum += (unsigned long long)__popc(m & __ballot_sync(TH_FULL, (d >> k) & 1u)) << k;
+          }
+        }
+        ccount += __popc(m);
+        if (WRITE) S[lane * kSStride + t0 + u] = m;
       }
     }
+    total += ccount;
+    if (!WRITE) continue;
     __syncwarp();
-  }
-  if (WRITE) {
-    unsigned rest = __ballot_sync(TH_FULL, fill > 0);
-    while (rest) {
-      const int b = __ffs(rest) - 1;
-      rest &= rest - 1u;
-      const int hb = __shfl_sync(TH_FULL, head, b);
-      const int fb = __shfl_sync(TH_FULL, fill, b);
+    // ---- WRITE: query by query, lane t extracts tile t's rows
+    unsigned todo = __ballot_sync(TH_FULL, ccount != 0);
+    while (todo) {
+      const int b = __ffs(todo) - 1;
+      todo &= todo - 1u;
+      uint32_t m = S[b * kSStride + lane];
+      const int c = __popc(m);
+      const int incl = warp_incl_scan(c);
+      const int n = __shfl_sync(TH_FULL, incl, 31);
+      // highest set bit first, filling the lane's run from its end (FLO
+      // gives the top bit directly; no bit reversal per id)
+      const int32_t rbase = (int32_t)(c0 + 32 * lane);
+      int32_t* dst = stg + incl - 1;
+      while (m) {
+        const int bit = 31 - __clz((int)m);
+        *dst-- = rbase + bit;
+        m ^= 1u << bit;
+      }
+      __syncwarp();
       const int64_t pb = __shfl_sync(TH_FULL, pos, b);
-      if (lane < fb && pb + lane < cap) out[pb + lane] = ring[b * kRingStride + ((hb + lane) & (kRing - 1))];
+      if (pb + n <= cap) {
+        int32_t* o = out + pb;
+        for (int i = lane; i < n; i += 32) o[i] = stg[i];
+      } else {
+        for (int i = lane; i < n; i += 32)
+          if (pb + i < cap) out[pb + i] = stg[i];
+      }
+      if (lane == b) pos += n;
+      __syncwarp();
     }
-  } else if (q < src.nq) {
+  }
+  if (!WRITE && q < src.nq) {
     counts[(size_t)q * nblk + blk] = total;
     if (EDGES && esum) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), esum);
   }
 }
-

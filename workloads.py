@@ -18,7 +18,17 @@ C2  407,000 entities / exactly 3,400,000 distinct triples / 400 relations.
     impossible at T=3.4M).
 C3  C2's graph; 2,048 uniform + 2,048 top-1%-degree seeds; per-seed 32-of-400
     relation masks.
+C4  54.4M entities / exactly 86.5M distinct triples / 1,000 uniform
+    relations, PKG-shaped.  Chung-Lu style power law:
+    exactly 1% of entities are isolated; every other entity gets one
+    incident "base" edge (as subject or object, coin flip) so nothing else
+    is isolated; the remaining endpoints are drawn with weights whose tail
+    is P(w >= x) ~ x^-1.3 (the config's "Zipf 1.3"), sampled in closed form
+    by inverse CDF over rank (rank = N * U^(1/(1-1/1.3))), with independent
+    random rank->id permutations for the subject and object sides.
+    Duplicates are topped up to exactly T; triple order is shuffled.
 """
+
 
 from __future__ import annotations
 
@@ -114,3 +124,58 @@ def graph_stats(s, o, n_entities: int) -> dict:
         "zero_out_frac": float((deg == 0).mean()),
         "isolated_frac": float(((deg == 0) & (ind == 0)).mean()),
     }
+
+
+C4_DIMS = (54_400_000, 86_500_000, 1_000)
+
+
+def _sorted_unique(keys: np.ndarray) -> np.ndarray:
+    # np.sort + neighbour mask (numpy 2.3's np.unique is ~80x slower here)
+    return _unique_sorted(keys)
+
+
+def powerlaw_graph(n_entities: int, n_triples: int, n_relations: int, seed: int,
+                   alpha: float = 1.3, isolated: float = 0.01):
+    """Exactly ``n_triples`` distinct (s, r, o); ``isolated`` of entities untouched."""
+    rng = np.random.default_rng(seed)
+    E, T, R = n_entities, n_triples, n_relations
+    perm = rng.permutation(E).astype(np.int64)
+    act = perm[int(round(E * isolated)):]
+    N = act.size
+    by_rank_out = act
+    by_rank_in = act[rng.permutation(N)]
+    ex = 1.0 / (1.0 - 1.0 / alpha)
+
+    def draw(by_rank, n):
+        k = (N * rng.random(n) ** ex).astype(np.int64)
+        return by_rank[np.minimum(k, N - 1)]
+
+    side = rng.random(N) < 0.5
+    s = np.where(side, act, draw(by_rank_out, N))
+    o = np.where(side, draw(by_rank_in, N), act)
+    extra = max(0, T - N)
+    s = np.concatenate([s, draw(by_rank_out, extra)])
+    o = np.concatenate([o, draw(by_rank_in, extra)])
+    r = rng.integers(0, R, s.size)
+    keys = _sorted_unique((s * R + r) * E + o)
+    del s, o, r
+    while keys.size < T:
+        n = 2 * (T - keys.size) + 1024
+        add = _sorted_unique((draw(by_rank_out, n) * R + rng.integers(0, R, n)) * E
+                             + draw(by_rank_in, n))
+        pos = np.minimum(np.searchsorted(keys, add), keys.size - 1)
+        add = add[keys[pos] != add][: T - keys.size]
+        keys = np.sort(np.concatenate([keys, add]))
+    if keys.size > T:
+        keys = keys[np.sort(rng.choice(keys.size, T, replace=False))]
+    keys = keys[rng.permutation(T)]
+    o = (keys % E).astype(np.int32)
+    r = ((keys // E) % R).astype(np.int32)
+    s = (keys // E // R).astype(np.int32)
+    return s, r, o
+
+
+def c4_graph(seed: int = 4):
+    E, T, R = C4_DIMS
+    s, r, o = powerlaw_graph(E, T, R, seed)
+    return s, r, o, E, R
