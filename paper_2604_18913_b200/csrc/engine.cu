@@ -488,12 +488,13 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
       std::max<int64_t>(kChunkRows, ceil_div(ceil_div(rows, target), kChunkRows) * kChunkRows);
   const int nblk = (int)ceil_div(rows, blk_rows);
   const unsigned grid = (unsigned)(nblk * NG);
+  constexpr size_t smem_c = mat_smem_bytes<W, false>();
   if (es.out)
-    mat_kernel<W, Src, false, true><<<grid, 32 * NW, 0, s->st>>>(src, blk_rows, nblk, b.counts,
-                                                                 nullptr, nullptr, 0, es);
+    mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, blk_rows, nblk, b.counts,
+                                                                      nullptr, nullptr, 0, es);
   else
-    mat_kernel<W, Src, false><<<grid, 32 * NW, 0, s->st>>>(src, blk_rows, nblk, b.counts, nullptr,
-                                                           nullptr, 0);
+    mat_kernel<W, Src, false><<<grid, 32 * NW, smem_c, s->st>>>(src, blk_rows, nblk, b.counts,
+                                                                nullptr, nullptr, 0);
   TH_LAUNCHED();
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
   TH_LAUNCHED();

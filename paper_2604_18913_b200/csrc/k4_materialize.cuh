@@ -94,12 +94,19 @@ constexpr int mat_warps() {
   return W < kMatWordsPerCta ? W : kMatWordsPerCta;
 }
 
-// S (33 x 32 words) + staging run (kChunkRows ids) per warp
-constexpr size_t kMatWarpSmem = (size_t)(32 * kSStride + kChunkRows) * sizeof(uint32_t);
+constexpr unsigned kSparseBits = 5;       // tiles with <= this many bits per lane skip the transpose
+constexpr unsigned kCoopIdsPerQuery = 48;  // chunk ids per touched query for the cooperative write
+
+// per-warp shared words: WRITE = S (32 x kSStride) + staging run (kChunkRows
+// ids); COUNT = per-query id counters + degree sums (2 x 32)
+template <bool WRITE>
+constexpr size_t mat_warp_words() {
+  return WRITE ? (size_t)(32 * kSStride + kChunkRows) : 64;
+}
 
 template <int W, bool WRITE>
 constexpr size_t mat_smem_bytes() {
-  return (size_t)mat_warps<W>() * kMatWarpSmem;
+  return (size_t)mat_warps<W>() * mat_warp_words<WRITE>() * sizeof(uint32_t);
 }
 
 // EDGES (COUNT pass over an entity layer): also sum the out-degrees of each
@@ -136,8 +143,16 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
   const int j = (blockIdx.x % NG) * NW + warp;
   const int q = 32 * j + lane;
   if (blk >= nblk) return;
-  uint32_t* S = mat_smem + (size_t)warp * (kMatWarpSmem / sizeof(uint32_t));
+  // WRITE: S[32][kSStride] + staging run; COUNT: per-query counters
+  uint32_t* S = mat_smem + (size_t)warp * (mat_warp_words<WRITE>());
   int32_t* stg = reinterpret_cast<int32_t*>(S + 32 * kSStride);
+  uint32_t* cnt = S;        // COUNT: [32] ids per query (sparse tiles)
+  uint32_t* ecnt = S + 32;  // COUNT+EDGES: [32] degree sums per query (sparse tiles)
+  if (!WRITE) {
+    cnt[lane] = 0u;
+    ecnt[lane] = 0u;
+    __syncwarp();
+  }
   int64_t pos = 0;
   int32_t total = 0;
   unsigned long long esum = 0;
@@ -149,8 +164,12 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
     // ---- A: tile masks of this chunk, S[b][t] = rows of tile t in query b.
     // Loads of 8 tiles are issued before their transposes (memory-level
     // parallelism); dense sources get all 32 tile flags from one load.
-    int32_t ccount = 0;
-    uint32_t cflags = 0u;  // lane t: flags of tile t (dense sources)
+    // Dense tiles go through the 32x32 butterfly transpose; sparse tiles
+    // (at most kSparseBits bits on any lane) scatter their few bits with
+    // shared-memory atomics instead, so a tile costs O(set bits) there.
+    uint32_t touched = 0u;  // WRITE: queries with ids in this chunk
+    uint32_t nbits = 0u;    // WRITE: set bits seen by this lane (its rows)
+    uint32_t cflags = 0u;   // lane t: flags of tile t (dense sources)
     if constexpr (Src::kDense) cflags = src.chunk_flags(c0, rend);
 #pragma unroll 1
     for (int t0 = 0; t0 < 32; t0 += 8) {
@@ -169,28 +188,75 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int64_t r0 = c0 + 32 * (t0 + u);
-        uint32_t m = 0u;
-        if (__any_sync(TH_FULL, x[u] != 0u)) {
-          m = transpose32(x[u]);
+        const int t = t0 + u;
+        const int64_t r = c0 + 32 * t + lane;
+        const uint32_t xu = x[u];
+        if (WRITE) nbits += __popc(xu);
+        const bool anyx = __any_sync(TH_FULL, xu != 0u);
+        const unsigned mx = anyx ? __reduce_max_sync(TH_FULL, (unsigned)__popc(xu)) : 0u;
+        if (mx > kSparseBits) {
+          const uint32_t m = transpose32(xu);
           if (EDGES) {
-            const int64_t r = r0 + lane;
             const uint32_t d =
                 ((fl[u] >> lane) & 1u) ? (uint32_t)(es.indptr[r + 1] - es.indptr[r]) : 0u;
             const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d));
             for (int k = 0; k < np; ++k)
               esum += (unsigned long long)__popc(m & __ballot_sync(TH_FULL, (d >> k) & 1u)) << k;
           }
+          if (WRITE) {
+            S[lane * kSStride + t] = m;
+            touched |= __ballot_sync(TH_FULL, m != 0u);
+          } else {
+            total += __popc(m);
+          }
+        } else {
+          if (WRITE) S[lane * kSStride + t] = 0u;
+          if (anyx) {
+            uint32_t d = 0u;
+            if (EDGES && xu) d = (uint32_t)(es.indptr[r + 1] - es.indptr[r]);
+            if (WRITE) {
+              __syncwarp();
+              touched |= __reduce_or_sync(TH_FULL, xu);
+            }
+            uint32_t y = xu;
+            while (y) {
+              const int b = 31 - __clz((int)y);
+              if (WRITE) {
+                atomicOr(&S[b * kSStride + t], 1u << lane);
+              } else {
+                atomicAdd(&cnt[b], 1u);
+                if (EDGES) atomicAdd(&ecnt[b], d);
+              }
+              y ^= 1u << b;
+            }
+          }
         }
-        ccount += __popc(m);
-        if (WRITE) S[lane * kSStride + t0 + u] = m;
       }
     }
-    total += ccount;
     if (!WRITE) continue;
     __syncwarp();
-    // ---- WRITE: query by query, lane t extracts tile t's rows
-    unsigned todo = __ballot_sync(TH_FULL, ccount != 0);
+    // ---- WRITE.  Dense chunks (many ids per query): query by query, lane
+    // t extracts tile t's rows into a staging run stored coalesced.  Sparse
+    // chunks (a few ids per query, e.g. the C4 layers): every lane walks its
+    // own query's 32 tile masks and stores its ids directly -- one pass per
+    // chunk instead of a scan + copy per query.
+    const unsigned ids = __reduce_add_sync(TH_FULL, nbits);
+    if (ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
+      if (q < src.nq) {
+        for (int t = 0; t < 32; ++t) {
+          uint32_t m = S[lane * kSStride + t];
+          const int32_t rb = (int32_t)(c0 + 32 * t);
+          while (m) {
+            if (pos < cap) out[pos] = rb + __ffs(m) - 1;
+            ++pos;
+            m &= m - 1u;
+          }
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    unsigned todo = touched;
     while (todo) {
       const int b = __ffs(todo) - 1;
       todo &= todo - 1u;
@@ -220,8 +286,13 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
       __syncwarp();
     }
   }
-  if (!WRITE && q < src.nq) {
-    counts[(size_t)q * nblk + blk] = total;
-    if (EDGES && esum) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), esum);
+  if (!WRITE) {
+    __syncwarp();
+    total += (int32_t)cnt[lane];
+    if (EDGES) esum += ecnt[lane];
+    if (q < src.nq) {
+      counts[(size_t)q * nblk + blk] = total;
+      if (EDGES && esum) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), esum);
+    }
   }
 }

@@ -1,0 +1,31 @@
+"""Short C4 run for ncu captures: one warm-up k=3 batch of 1,024 seeds,
+then one more.  Per batch (k=3, frontier): 3 pull_kernel, 3 mat_kernel
+count passes and 3 write passes, so `-k regex:"mat_kernel|pull_kernel"
+-s 9 -c 9` captures the second batch."""
+
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import paper_2604_18913_b200 as th  # noqa: E402
+import workloads  # noqa: E402
+
+
+def main():
+    k = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+    s, r, o, E, R = workloads.c4_graph()
+    g = th.build_incidence((s, r, o), E, R)
+    del s, r, o
+    ret = th.Retriever(g)
+    seeds = torch.from_numpy(workloads.seed_batches(E, 1024, 1, seed=400)[0]).cuda()
+    for _ in range(2):
+        res = ret.retrieve(seeds, k, copy=False)
+    torch.cuda.synchronize()
+    print("ids", res.frontier_len.sum(1).tolist(), "edges", int(res.edges.sum()))
+
+
+if __name__ == "__main__":
+    main()

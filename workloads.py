@@ -24,8 +24,10 @@ C4  54.4M entities / exactly 86.5M distinct triples / 1,000 uniform
     incident "base" edge (as subject or object, coin flip) so nothing else
     is isolated; the remaining endpoints are drawn with weights whose tail
     is P(w >= x) ~ x^-1.3 (the config's "Zipf 1.3"), sampled in closed form
-    by inverse CDF over rank (rank = N * U^(1/(1-1/1.3))), with independent
-    random rank->id permutations for the subject and object sides.
+    by inverse CDF over rank (rank = N * U^(1/(1-1/1.3))).  One random
+    rank->id permutation serves both sides, so prolific subjects are also
+    popular objects (a hub core, as in C2; independent permutations leave
+    the hubs unreachable, with k=3 frontiers of a few entities per seed).
     Duplicates are topped up to exactly T; triple order is shuffled.
 """
 
@@ -135,7 +137,7 @@ def _sorted_unique(keys: np.ndarray) -> np.ndarray:
 
 
 def powerlaw_graph(n_entities: int, n_triples: int, n_relations: int, seed: int,
-                   alpha: float = 1.3, isolated: float = 0.01):
+                   alpha: float = 1.3, isolated: float = 0.01, shared_ranks: bool = True):
     """Exactly ``n_triples`` distinct (s, r, o); ``isolated`` of entities untouched."""
     rng = np.random.default_rng(seed)
     E, T, R = n_entities, n_triples, n_relations
@@ -143,7 +145,7 @@ def powerlaw_graph(n_entities: int, n_triples: int, n_relations: int, seed: int,
     act = perm[int(round(E * isolated)):]
     N = act.size
     by_rank_out = act
-    by_rank_in = act[rng.permutation(N)]
+    by_rank_in = act if shared_ranks else act[rng.permutation(N)]
     ex = 1.0 / (1.0 - 1.0 / alpha)
 
     def draw(by_rank, n):
