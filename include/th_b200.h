@@ -142,6 +142,11 @@ int th_finish(th_session* s, th_result* out);
  * out-edge total exceeds n_triples / pull_divisor; 0 = never pull,
  * <0 = always pull. */
 int th_session_set_pull_divisor(th_session* s, double pull_divisor);
+/* K4 materialisation strategy: graphs with at least `min_entities` entities
+ * first compact each layer's flag bitmap into an ascending row list (work
+ * follows the reached rows); smaller graphs scan the flag bitmap directly.
+ * Default 4 Mi.  0 = always list-driven. */
+int th_session_set_list_min_entities(th_session* s, int64_t min_entities);
 /* Number of kernels this session has launched since creation. */
 int64_t th_session_launch_count(const th_session* s);
 

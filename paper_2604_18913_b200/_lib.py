@@ -24,6 +24,7 @@ EXPORTS = (
     "th_abi_version", "th_last_error", "th_graph_create", "th_graph_destroy",
     "th_graph_info_get", "th_session_create", "th_session_destroy", "th_run", "th_finish",
     "th_session_set_pull_divisor", "th_session_launch_count", "th_plan_owner_hash",
+    "th_session_set_list_min_entities",
     "th_session_set_profiling", "th_session_profile", "th_session_wave_lists",
 )
 PROF_CATEGORIES = ("setup", "edges", "activated", "push", "pull", "frontier", "clear", "paths")
@@ -90,6 +91,7 @@ def load():
         "th_run": (ctypes.c_int, [_vp, ctypes.POINTER(Query)]),
         "th_finish": (ctypes.c_int, [_vp, ctypes.POINTER(Result)]),
         "th_session_set_pull_divisor": (ctypes.c_int, [_vp, ctypes.c_double]),
+        "th_session_set_list_min_entities": (ctypes.c_int, [_vp, ctypes.c_int64]),
         "th_session_launch_count": (ctypes.c_int64, [_vp]),
         "th_plan_owner_hash": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp]),
         "th_session_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),

@@ -173,6 +173,15 @@ int th_session_set_pull_divisor(th_session* s, double pull_divisor) {
   return TH_OK;
 }
 
+int th_session_set_list_min_entities(th_session* s, int64_t min_entities) {
+  if (!s) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  s->s.list_min_entities = min_entities;
+  return TH_OK;
+}
+
 int64_t th_session_launch_count(const th_session* s) { return s ? s->s.launches : -1; }
 
 int th_session_set_profiling(th_session* s, int on) {

@@ -428,6 +428,95 @@ __global__ void mat_scan_queries_kernel(const int64_t* totals, int nq, int64_t* 
   if (q == 0) *cursor = base + ws[(blockDim.x >> 5) - 1];
 }
 
+// ---------------------------------------------- flag bitmap -> row list
+
+// Ascending list of the set bits of a flag bitmap (rows reached by a layer):
+// per-block popcounts, one exclusive scan, then an ordered write.  Feeds K4's
+// ListSrc so materialisation work follows the reached rows, not E.
+constexpr int kCompactThreads = 256;
+constexpr int kCompactPerThread = 8;
+constexpr int kCompactWords = kCompactThreads * kCompactPerThread;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* ws, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(TH_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(TH_FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  const int ex = (warp ? ws[warp - 1] : 0) + x - v;
+  *total = ws[(blockDim.x >> 5) - 1];
+  __syncthreads();
+  return ex;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) flag_count_kernel(const uint32_t* __restrict__ flags,
+                                                                      int64_t nwords, int32_t* bcount) {
+  __shared__ int ws[32];
+  const int64_t w0 = (int64_t)blockIdx.x * kCompactWords + threadIdx.x * kCompactPerThread;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kCompactPerThread; ++i)
+    if (w0 + i < nwords) c += __popc(flags[w0 + i]);
+  int total;
+  block_excl_scan(c, ws, &total);
+  if (threadIdx.x == 0) bcount[blockIdx.x] = total;
+}
+
+// single block: exclusive scan of the block counts in place; total -> *n_out
+__global__ void flag_scan_kernel(int32_t* bcount, int nb, int32_t* n_out) {
+  __shared__ int ws[32];
+  int carry = 0;
+  for (int b0 = 0; b0 < nb; b0 += blockDim.x) {
+    const int i = b0 + threadIdx.x;
+    const int v = i < nb ? bcount[i] : 0;
+    int total;
+    const int ex = block_excl_scan(v, ws, &total);
+    if (i < nb) bcount[i] = carry + ex;
+    carry += total;
+  }
+  if (threadIdx.x == 0) *n_out = carry;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) flag_write_kernel(const uint32_t* __restrict__ flags,
+                                                                      int64_t nwords,
+                                                                      const int32_t* __restrict__ boff,
+                                                                      int32_t* rows) {
+  __shared__ int ws[32];
+  const int64_t w0 = (int64_t)blockIdx.x * kCompactWords + threadIdx.x * kCompactPerThread;
+  uint32_t f[kCompactPerThread];
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kCompactPerThread; ++i) {
+    f[i] = w0 + i < nwords ? flags[w0 + i] : 0u;
+    c += __popc(f[i]);
+  }
+  int total;
+  int o = boff[blockIdx.x] + block_excl_scan(c, ws, &total);
+#pragma unroll
+  for (int i = 0; i < kCompactPerThread; ++i) {
+    uint32_t m = f[i];
+    const int32_t base = (int32_t)((w0 + i) * 32);
+    while (m) {
+      rows[o++] = base + __ffs(m) - 1;
+      m &= m - 1u;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host
 
 template <typename T>
@@ -490,27 +579,50 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   const unsigned grid = (unsigned)(nblk * NG);
   constexpr size_t smem_c = mat_smem_bytes<W, false>();
   if (es.out)
-    mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, blk_rows, nblk, b.counts,
+    mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, b.counts,
                                                                       nullptr, nullptr, 0, es);
   else
-    mat_kernel<W, Src, false><<<grid, 32 * NW, smem_c, s->st>>>(src, blk_rows, nblk, b.counts,
-                                                                nullptr, nullptr, 0);
+    mat_kernel<W, Src, false><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, b.counts, nullptr,
+                                                                nullptr, 0);
   TH_LAUNCHED();
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
   TH_LAUNCHED();
   mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
   TH_LAUNCHED();
-  mat_kernel<W, Src, true><<<grid, 32 * NW, smem_w, s->st>>>(src, blk_rows, nblk, b.counts, off,
-                                                             out, cap);
+  mat_kernel<W, Src, true><<<grid, 32 * NW, smem_w, s->st>>>(src, nblk, b.counts, off, out,
+                                                             cap);
   TH_LAUNCHED();
   s->launches += 4;
 }
 
+// Rows of A (minus neg) whose flag is set.  Small graphs scan the flag
+// bitmap directly (the whole state matrix is L2-resident and most rows of a
+// layer are live); large graphs first compact the flags into an ascending
+// row list so the work follows the rows a layer reached (C4: 10x fewer
+// tiles at hop 2, 2x at hop 3).
 template <int W>
 void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
                        const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
                        int64_t cap, int64_t* cursor, EdgeSum es = {}) {
-  DenseSrc<W> src{A, neg, flags, s->g->E, nq};
+  const int64_t E = s->g->E;
+  if (E < s->list_min_entities) {
+    DenseSrc<W> src{A, neg, flags, E, nq};
+    materialize<W>(s, b, src, nq, off, len, out, cap, cursor, es);
+    return;
+  }
+  const int64_t nwords = ceil_div(E, 32);
+  const int nb = (int)ceil_div(nwords, kCompactWords);
+  int32_t* rows = ensure<int32_t>(s->rowlist, E, s->st);
+  int32_t* bsum = ensure<int32_t>(s->rowscan, nb, s->st);
+  int32_t* n_dev = &b.ctl->mat_rows;
+  flag_count_kernel<<<nb, kCompactThreads, 0, s->st>>>(flags, nwords, bsum);
+  TH_LAUNCHED();
+  flag_scan_kernel<<<1, 1024, 0, s->st>>>(bsum, nb, n_dev);
+  TH_LAUNCHED();
+  flag_write_kernel<<<nb, kCompactThreads, 0, s->st>>>(flags, nwords, bsum, rows);
+  TH_LAUNCHED();
+  s->launches += 3;
+  ListSrc<W> src{A, neg, rows, n_dev, E, nq};
   materialize<W>(s, b, src, nq, off, len, out, cap, cursor, es);
 }
 
@@ -944,7 +1056,7 @@ void session_free(Session* s) {
   for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
                   &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
-                  &s->p_scratch}) {
+                  &s->p_scratch, &s->rowlist, &s->rowscan}) {
     if (d->p) cudaFreeAsync(d->p, s->st);
     d->p = nullptr;
     d->bytes = 0;

@@ -24,6 +24,7 @@ struct Ctl {
   int64_t act_used;
   int32_t push_hops, pull_hops;
   int64_t path_used;
+  int32_t mat_rows;  // length of the compacted row list of the layer being materialised
 };
 
 struct DBuf {
@@ -35,9 +36,10 @@ struct Session {
   Graph* g = nullptr;
   cudaStream_t st = nullptr;
   double pull_divisor = 8.0;
+  int64_t list_min_entities = int64_t(4) << 20;  // K4 list-driven above this E
   int64_t launches = 0;
   // wave state
-  DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals;
+  DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals, rowlist, rowscan;
   DBuf ctl;
   // outputs
   DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch;

@@ -57,6 +57,37 @@ struct DenseSrc {
     if (neg) x &= ~neg[(size_t)r * W + j];
     return x & valid_word(j, nq);
   }
+  __device__ __forceinline__ int64_t rows_dev() const { return nrows; }
+  __device__ __forceinline__ int32_t id(int64_t r) const { return (int32_t)r; }
+};
+
+// rows = the ascending list of nonzero entity rows of a layer (compacted
+// from its flag bitmap), so the work is proportional to the rows a layer
+// actually reached rather than to E; the list length lives on the device
+template <int W>
+struct ListSrc {
+  const uint32_t* A;
+  const uint32_t* neg;
+  const int32_t* rows;
+  const int32_t* n_dev;
+  int64_t nrows;  // capacity (host-side grid sizing)
+  int nq;
+  static constexpr bool kDense = true;
+  __device__ __forceinline__ uint32_t chunk_flags(int64_t r0, int64_t rend) const {
+    const int64_t t0 = r0 + 32 * (int64_t)lane_id();
+    if (t0 >= rend) return 0u;
+    const int64_t left = rend - t0;
+    return left >= 32 ? TH_FULL : ((1u << left) - 1u);
+  }
+  __device__ __forceinline__ bool chunk_any(int64_t r0, int64_t rend) const { return r0 < rend; }
+  __device__ __forceinline__ uint32_t word(int64_t r, int64_t, int j) const {
+    const size_t v = (size_t)rows[r];
+    uint32_t x = A[v * W + j];
+    if (neg) x &= ~neg[v * W + j];
+    return x & valid_word(j, nq);
+  }
+  __device__ __forceinline__ int64_t rows_dev() const { return *n_dev; }
+  __device__ __forceinline__ int32_t id(int64_t r) const { return rows[r]; }
 };
 
 // rows = triples in tid order; word j of row t = X[subj[t]] & M[rel[t]]
@@ -87,6 +118,8 @@ struct TripleSrc {
     if (M) x &= M[(size_t)(aux >> 32) * W + j];
     return x & valid_word(j, nq);
   }
+  __device__ __forceinline__ int64_t rows_dev() const { return nrows; }
+  __device__ __forceinline__ int32_t id(int64_t r) const { return (int32_t)r; }
 };
 
 template <int W>
@@ -120,6 +153,10 @@ struct EdgeSum {
   int64_t* out = nullptr;  // [nq], accumulated with atomics
 };
 
+__device__ __forceinline__ uint32_t degree(const EdgeSum& es, int32_t v) {
+  return (uint32_t)(es.indptr[v + 1] - es.indptr[v]);
+}
+
 __device__ __forceinline__ int warp_incl_scan(int v) {
   const unsigned lane = lane_id();
 #pragma unroll
@@ -131,8 +168,8 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 }
 
 template <int W, class Src, bool WRITE, bool EDGES = false>
-__global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int64_t blk_rows,
-                                                                   int nblk, int32_t* counts,
+__global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int nblk,
+                                                                   int32_t* counts,
                                                                    const int64_t* base, int32_t* out,
                                                                    int64_t cap, EdgeSum es = {}) {
   extern __shared__ uint32_t mat_smem[];
@@ -157,8 +194,12 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
   int32_t total = 0;
   unsigned long long esum = 0;
   if (WRITE && q < src.nq) pos = base[q] + counts[(size_t)q * nblk + blk];
+  // rows per block from the device-side row count (whole 1024-row chunks)
+  const int64_t nrows = src.rows_dev();
+  int64_t blk_rows = (nrows + nblk - 1) / nblk;
+  blk_rows = blk_rows < kChunkRows ? kChunkRows : (blk_rows + kChunkRows - 1) / kChunkRows * kChunkRows;
   const int64_t r_begin = (int64_t)blk * blk_rows;
-  const int64_t rend = src.nrows < r_begin + blk_rows ? src.nrows : r_begin + blk_rows;
+  const int64_t rend = nrows < r_begin + blk_rows ? nrows : r_begin + blk_rows;
   for (int64_t c0 = r_begin; c0 < rend; c0 += kChunkRows) {
     if (!src.chunk_any(c0, rend)) continue;
     // ---- A: tile masks of this chunk, S[b][t] = rows of tile t in query b.
@@ -198,7 +239,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
           const uint32_t m = transpose32(xu);
           if (EDGES) {
             const uint32_t d =
-                ((fl[u] >> lane) & 1u) ? (uint32_t)(es.indptr[r + 1] - es.indptr[r]) : 0u;
+                ((fl[u] >> lane) & 1u) ? degree(es, src.id(r)) : 0u;
             const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d));
             for (int k = 0; k < np; ++k)
               esum += (unsigned long long)__popc(m & __ballot_sync(TH_FULL, (d >> k) & 1u)) << k;
@@ -213,7 +254,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
           if (WRITE) S[lane * kSStride + t] = 0u;
           if (anyx) {
             uint32_t d = 0u;
-            if (EDGES && xu) d = (uint32_t)(es.indptr[r + 1] - es.indptr[r]);
+            if (EDGES && xu) d = degree(es, src.id(r));
             if (WRITE) {
               __syncwarp();
               touched |= __reduce_or_sync(TH_FULL, xu);
@@ -245,9 +286,9 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
       if (q < src.nq) {
         for (int t = 0; t < 32; ++t) {
           uint32_t m = S[lane * kSStride + t];
-          const int32_t rb = (int32_t)(c0 + 32 * t);
+          const int64_t rb = c0 + 32 * t;
           while (m) {
-            if (pos < cap) out[pos] = rb + __ffs(m) - 1;
+            if (pos < cap) out[pos] = src.id(rb + __ffs(m) - 1);
             ++pos;
             m &= m - 1u;
           }
@@ -265,8 +306,9 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
       const int incl = warp_incl_scan(c);
       const int n = __shfl_sync(TH_FULL, incl, 31);
       // highest set bit first, filling the lane's run from its end (FLO
-      // gives the top bit directly; no bit reversal per id)
-      const int32_t rbase = (int32_t)(c0 + 32 * lane);
+      // gives the top bit directly; no bit reversal per id).  The run holds
+      // chunk-relative row positions; ids are resolved on the way out.
+      const int32_t rbase = 32 * lane;
       int32_t* dst = stg + incl - 1;
       while (m) {
         const int bit = 31 - __clz((int)m);
@@ -277,10 +319,10 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int6
       const int64_t pb = __shfl_sync(TH_FULL, pos, b);
       if (pb + n <= cap) {
         int32_t* o = out + pb;
-        for (int i = lane; i < n; i += 32) o[i] = stg[i];
+        for (int i = lane; i < n; i += 32) o[i] = src.id(c0 + stg[i]);
       } else {
         for (int i = lane; i < n; i += 32)
-          if (pb + i < cap) out[pb + i] = stg[i];
+          if (pb + i < cap) out[pb + i] = src.id(c0 + stg[i]);
       }
       if (lane == b) pos += n;
       __syncwarp();

@@ -181,6 +181,10 @@ class Retriever:
     def set_pull_divisor(self, divisor: float) -> None:
         _lib.check(_lib.load().th_session_set_pull_divisor(self._handle, float(divisor)))
 
+    def set_list_min_entities(self, n: int) -> None:
+        """K4 strategy knob: list-driven materialisation for graphs with >= n entities."""
+        _lib.check(_lib.load().th_session_set_list_min_entities(self._handle, int(n)))
+
     def launch_count(self) -> int:
         return int(_lib.load().th_session_launch_count(self._handle))
 

@@ -127,11 +127,12 @@ def _hub_graph(E, T, R, seed, alpha=1.2):
     return key // E // R, (key // E) % R, key % E
 
 
+@pytest.mark.parametrize("k4", ["dense", "list"])
 @pytest.mark.parametrize("divisor", [0.0, -1.0, 8.0], ids=["push", "pull", "auto"])
 @pytest.mark.parametrize("sem", ["exact", "frontier", "cumulative"])
-def test_hub_graph_two_waves_vs_oracle(th, sem, divisor):
+def test_hub_graph_two_waves_vs_oracle(th, sem, divisor, k4):
     """1,100 seeds (two waves), hub rows above the heavy thresholds, every
-    direction policy; checked against the oracle seed by seed."""
+    direction policy, both K4 strategies; checked against the oracle seed by seed."""
     s, r, o = _hub_graph(3000, 100000, 64, seed=11)
     E, R = 3000, 64
     g = th.build_incidence((s, r, o), E, R)
@@ -142,6 +143,7 @@ def test_hub_graph_two_waves_vs_oracle(th, sem, divisor):
     seeds = rng.integers(0, E, 1100)
     ret = th.Retriever(g)
     ret.set_pull_divisor(divisor)
+    ret.set_list_min_entities(0 if k4 == "list" else 1 << 40)
     k = 3
     res = ret.retrieve(seeds, k, semantics=sem)
     if divisor == 0.0:
@@ -164,9 +166,10 @@ def test_filtered_hub_graph_vs_oracle(th):
     rng = np.random.default_rng(9)
     seeds = rng.integers(0, E, 300)
     filt = [sorted(rng.choice(R, 6, replace=False).tolist()) for _ in seeds]
-    for divisor in (0.0, -1.0):
+    for divisor, k4 in ((0.0, 1 << 40), (-1.0, 0)):
         ret = th.Retriever(g)
         ret.set_pull_divisor(divisor)
+        ret.set_list_min_entities(k4)
         res = ret.retrieve(seeds, 2, relation_filter=filt, semantics="frontier", paths=True,
                            max_paths=300, activated=True)
         for i in range(0, 300, 7):
