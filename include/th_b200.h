@@ -13,6 +13,9 @@
  *   th_run (paths)    <- reconstruct_paths / assemble_paths
  *                                                   incidence.py:361-408
  *   th_plan_owner     <- plan_partitions            partition.py:49-98
+ *   th_shard_*        <- materialize_subgraphs / route / _partitioned_expand /
+ *                        cross_graph_k_hop          partition.py:101-181,
+ *                                                   engine.py:94-154
  *
  * Conventions
  *   - plain C types only; every pointer argument documented as device (d_)
@@ -176,6 +179,57 @@ int th_session_wave_lists(const th_session* s, int64_t* lens, int n);
  * device; entities with no out-edges get -1 (UNASSIGNED, partition.py:23).
  * d_owner: int32[E].  Asynchronous. */
 int th_plan_owner_hash(const th_graph* g, int32_t m, int32_t* d_owner, void* stream);
+
+/* ---- partitioned graphs (multi-GPU; one shard per rank) ---------------- */
+
+/* Ownership: own(v) = ((v * 0x9E3779B1) mod 2^32) mod world for every
+ * entity (the reference hash plan, partition.py:80-84).  own(v) stores v's
+ * out-row (subject-cohesive, partition.py:125-154) and v's per-query
+ * visited/next bits.  Hub entities (d_hub_index[v] >= 0) are the exception:
+ * their rows are edge-split, triple t of a hub living on rank own(t), and a
+ * hub in the frontier is expanded by every rank.
+ *   d_subj/d_rel/d_obj  the FULL graph's columns in tid order (device int32)
+ *   d_lidx[E]           row of every entity at its owner (an owner's rows
+ *                       number its entities in ascending id order)
+ *   d_hub_index[E]      -1 or hub number < n_hubs; d_hub_ids[n_hubs] inverse
+ *   d_l2g[n_local]      this rank's owned entities, ascending
+ * The shard copies what it keeps; inputs may be freed afterwards. */
+typedef struct th_shard th_shard;
+int th_shard_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
+                    int64_t n_triples, int64_t n_entities, int64_t n_relations,
+                    const int32_t* d_lidx, const int32_t* d_hub_index, const int32_t* d_hub_ids,
+                    int64_t n_hubs, const int32_t* d_l2g, int64_t n_local, int32_t rank,
+                    int32_t world, void* stream, th_shard** out);
+int th_shard_destroy(th_shard* s);
+int64_t th_shard_local_triples(const th_shard* s);
+int64_t th_shard_launch_count(const th_shard* s);
+
+/* One wave of <= 1024 queries, hop h = 1..k in order; every rank makes the
+ * same calls with the same query arrays:
+ *   th_shard_begin(q)                     seeds (hub seeds on every rank)
+ *   th_shard_expand(h, counts, &send)     push over local rows + hub slices;
+ *       send[] = records bucketed by owner rank, counts[world] records per
+ *       owner (host).  Record = ((row_at_owner * W + word) << 32) | bits,
+ *       W = 32-bit words per row (queries rounded up to a power of two / 32)
+ *   -- caller: all-to-all of the records --
+ *   th_shard_absorb(h, recv, n)           apply received records
+ *   th_shard_hub_rows(h, &rows, &words)   uint32 [n_hubs][W]: owned hubs'
+ *       next-layer rows, zero elsewhere
+ *   -- caller: sum `rows` over ranks in place (one owner per hub) --
+ *   th_shard_hub_merge(h)                 install hub frontier rows
+ *   th_shard_end_hop(h)                   materialise owned frontier ids
+ *   th_shard_finish(&result)              after hop k; like th_finish, with
+ *       frontier ids = owned entities (global ids, sorted), activated =
+ *       local triples (global tids, sorted), edges = this rank's share
+ *       (sum over ranks = |T_h|).  TH_ERR_OVERFLOW: capacities grew, every
+ *       rank must run the wave again.  Paths are not available here. */
+int th_shard_begin(th_shard* s, const th_query* q);
+int th_shard_expand(th_shard* s, int32_t hop, int64_t* h_send_counts, const uint64_t** d_send);
+int th_shard_absorb(th_shard* s, int32_t hop, const uint64_t* d_recv, int64_t n_recv);
+int th_shard_hub_rows(th_shard* s, int32_t hop, uint32_t** d_rows, int64_t* n_words);
+int th_shard_hub_merge(th_shard* s, int32_t hop);
+int th_shard_end_hop(th_shard* s, int32_t hop);
+int th_shard_finish(th_shard* s, th_result* out);
 
 #ifdef __cplusplus
 }

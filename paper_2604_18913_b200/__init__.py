@@ -22,9 +22,38 @@ from .core_types import (
     jaccard,
 )
 from .device_graph import IncidenceGraph, build_incidence
+from .errors import DataError, IntegrityError, TripleHopError, UsageError
+from .partition import (
+    UNASSIGNED,
+    DistExchange,
+    LoopbackExchange,
+    PartitionedGraph,
+    PartitionPlan,
+    RouteResult,
+    ShardPlan,
+    cross_graph_k_hop,
+    plan_partitions,
+    plan_sharding,
+    route,
+)
 from .retriever import RetrievalResult, Retriever, k_hop, one_hop, reconstruct_paths, retrieve
 
 __all__ = [
+    "UNASSIGNED",
+    "DataError",
+    "DistExchange",
+    "IntegrityError",
+    "LoopbackExchange",
+    "PartitionPlan",
+    "PartitionedGraph",
+    "RouteResult",
+    "ShardPlan",
+    "TripleHopError",
+    "UsageError",
+    "cross_graph_k_hop",
+    "plan_partitions",
+    "plan_sharding",
+    "route",
     "DEFAULT_MAX_PATHS",
     "EntityVector",
     "HopSemantics",

@@ -15,6 +15,9 @@ struct th_graph {
 struct th_session {
   th::Session s;
 };
+struct th_shard {
+  th::Shard* sh = nullptr;
+};
 
 namespace th {
 static thread_local std::string g_last_error;
@@ -222,6 +225,151 @@ int th_plan_owner_hash(const th_graph* g, int32_t m, int32_t* d_owner, void* str
     th::plan_owner_hash(&g->g, m, d_owner, static_cast<cudaStream_t>(stream));
     return TH_OK;
   });
+}
+
+// ---- partitioned graphs ----------------------------------------------------
+
+int th_shard_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
+                    int64_t n_triples, int64_t n_entities, int64_t n_relations,
+                    const int32_t* d_lidx, const int32_t* d_hub_index, const int32_t* d_hub_ids,
+                    int64_t n_hubs, const int32_t* d_l2g, int64_t n_local, int32_t rank,
+                    int32_t world, void* stream, th_shard** out) {
+  return guarded([&]() -> int {
+    if (!out) {
+      th::set_error("out is NULL");
+      return TH_ERR_INVALID;
+    }
+    *out = nullptr;
+    if (n_triples < 0 || n_entities < 0 || n_relations < 0 || n_hubs < 0 || n_local < 0 ||
+        n_local > n_entities || n_hubs > n_entities) {
+      th::set_error("bad sizes");
+      return TH_ERR_INVALID;
+    }
+    if (n_triples >= INT32_MAX || n_entities >= INT32_MAX || n_relations > 65535) {
+      th::set_error("id space exceeded (int32 entities/triples, uint16 relations)");
+      return TH_ERR_INVALID;
+    }
+    if (world < 1 || rank < 0 || rank >= world) {
+      th::set_error("rank must be in [0, world)");
+      return TH_ERR_INVALID;
+    }
+    if ((n_triples > 0 && (!d_subj || !d_rel || !d_obj)) ||
+        (n_entities > 0 && (!d_lidx || !d_hub_index)) || (n_hubs > 0 && !d_hub_ids) ||
+        (n_local > 0 && !d_l2g)) {
+      th::set_error("NULL input array");
+      return TH_ERR_INVALID;
+    }
+    auto* h = new th_shard();
+    th::Shard* sh = nullptr;
+    int rc = TH_OK;
+    try {
+      rc = th::shard_create(&sh, d_subj, d_rel, d_obj, n_triples, n_entities, n_relations, d_lidx,
+                            d_hub_index, d_hub_ids, n_hubs, d_l2g, n_local, rank, world,
+                            static_cast<cudaStream_t>(stream));
+    } catch (...) {
+      if (sh) th::shard_free(sh);
+      delete h;
+      throw;
+    }
+    if (rc != TH_OK) {
+      if (sh) th::shard_free(sh);
+      delete h;
+      return rc;
+    }
+    h->sh = sh;
+    *out = h;
+    return TH_OK;
+  });
+}
+
+int th_shard_destroy(th_shard* s) {
+  if (!s) return TH_OK;
+  if (s->sh) th::shard_free(s->sh);
+  delete s;
+  return TH_OK;
+}
+
+int64_t th_shard_local_triples(const th_shard* s) {
+  return (s && s->sh) ? th::shard_local_triples(s->sh) : -1;
+}
+
+#define TH_SHARD_GUARD(s)            \
+  if (!(s) || !(s)->sh) {            \
+    th::set_error("NULL handle");    \
+    return TH_ERR_INVALID;           \
+  }
+
+int th_shard_begin(th_shard* s, const th_query* q) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    if (!q) {
+      th::set_error("NULL query");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_begin(s->sh, q);
+  });
+}
+
+int th_shard_expand(th_shard* s, int32_t hop, int64_t* h_send_counts, const uint64_t** d_send) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    if (!h_send_counts || !d_send) {
+      th::set_error("NULL output");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_expand(s->sh, hop, h_send_counts, d_send);
+  });
+}
+
+int th_shard_absorb(th_shard* s, int32_t hop, const uint64_t* d_recv, int64_t n_recv) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    if (n_recv < 0 || (n_recv > 0 && !d_recv)) {
+      th::set_error("bad receive buffer");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_absorb(s->sh, hop, d_recv, n_recv);
+  });
+}
+
+int th_shard_hub_rows(th_shard* s, int32_t hop, uint32_t** d_rows, int64_t* n_words) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    if (!d_rows || !n_words) {
+      th::set_error("NULL output");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_hub_rows(s->sh, hop, d_rows, n_words);
+  });
+}
+
+int th_shard_hub_merge(th_shard* s, int32_t hop) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    return th::shard_hub_merge(s->sh, hop);
+  });
+}
+
+int th_shard_end_hop(th_shard* s, int32_t hop) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    return th::shard_end_hop(s->sh, hop);
+  });
+}
+
+int th_shard_finish(th_shard* s, th_result* out) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    if (!out) {
+      th::set_error("NULL output");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_finish(s->sh, out);
+  });
+}
+
+int64_t th_shard_launch_count(const th_shard* s) {
+  return (s && s->sh) ? th::shard_session(s->sh)->launches : -1;
 }
 
 }  // extern "C"

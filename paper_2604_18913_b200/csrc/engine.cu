@@ -463,14 +463,21 @@ __device__ __forceinline__ int block_excl_scan(int v, int* ws, int* total) {
   return ex;
 }
 
+// flag word w restricted to bits below nbits
+__device__ __forceinline__ uint32_t flag_word(const uint32_t* flags, int64_t w, int64_t nbits) {
+  if (w * 32 >= nbits) return 0u;
+  const uint32_t f = flags[w];
+  const int64_t left = nbits - w * 32;
+  return left >= 32 ? f : f & ((1u << left) - 1u);
+}
+
 __global__ void __launch_bounds__(kCompactThreads) flag_count_kernel(const uint32_t* __restrict__ flags,
-                                                                      int64_t nwords, int32_t* bcount) {
+                                                                      int64_t nbits, int32_t* bcount) {
   __shared__ int ws[32];
   const int64_t w0 = (int64_t)blockIdx.x * kCompactWords + threadIdx.x * kCompactPerThread;
   int c = 0;
 #pragma unroll
-  for (int i = 0; i < kCompactPerThread; ++i)
-    if (w0 + i < nwords) c += __popc(flags[w0 + i]);
+  for (int i = 0; i < kCompactPerThread; ++i) c += __popc(flag_word(flags, w0 + i, nbits));
   int total;
   block_excl_scan(c, ws, &total);
   if (threadIdx.x == 0) bcount[blockIdx.x] = total;
@@ -492,7 +499,7 @@ __global__ void flag_scan_kernel(int32_t* bcount, int nb, int32_t* n_out) {
 }
 
 __global__ void __launch_bounds__(kCompactThreads) flag_write_kernel(const uint32_t* __restrict__ flags,
-                                                                      int64_t nwords,
+                                                                      int64_t nbits,
                                                                       const int32_t* __restrict__ boff,
                                                                       int32_t* rows) {
   __shared__ int ws[32];
@@ -501,7 +508,7 @@ __global__ void __launch_bounds__(kCompactThreads) flag_write_kernel(const uint3
   int c = 0;
 #pragma unroll
   for (int i = 0; i < kCompactPerThread; ++i) {
-    f[i] = w0 + i < nwords ? flags[w0 + i] : 0u;
+    f[i] = flag_word(flags, w0 + i, nbits);
     c += __popc(f[i]);
   }
   int total;
@@ -604,9 +611,9 @@ template <int W>
 void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
                        const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
                        int64_t cap, int64_t* cursor, EdgeSum es = {}) {
-  const int64_t E = s->g->E;
-  if (E < s->list_min_entities) {
-    DenseSrc<W> src{A, neg, flags, E, nq};
+  const int64_t E = s->mat_rows >= 0 ? s->mat_rows : s->g->E;
+  if (E < s->list_min_entities || E == 0) {
+    DenseSrc<W> src{A, neg, flags, E, nq, s->row_map};
     materialize<W>(s, b, src, nq, off, len, out, cap, cursor, es);
     return;
   }
@@ -615,14 +622,14 @@ void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_
   int32_t* rows = ensure<int32_t>(s->rowlist, E, s->st);
   int32_t* bsum = ensure<int32_t>(s->rowscan, nb, s->st);
   int32_t* n_dev = &b.ctl->mat_rows;
-  flag_count_kernel<<<nb, kCompactThreads, 0, s->st>>>(flags, nwords, bsum);
+  flag_count_kernel<<<nb, kCompactThreads, 0, s->st>>>(flags, E, bsum);
   TH_LAUNCHED();
   flag_scan_kernel<<<1, 1024, 0, s->st>>>(bsum, nb, n_dev);
   TH_LAUNCHED();
-  flag_write_kernel<<<nb, kCompactThreads, 0, s->st>>>(flags, nwords, bsum, rows);
+  flag_write_kernel<<<nb, kCompactThreads, 0, s->st>>>(flags, E, bsum, rows);
   TH_LAUNCHED();
   s->launches += 3;
-  ListSrc<W> src{A, neg, rows, n_dev, E, nq};
+  ListSrc<W> src{A, neg, rows, n_dev, E, nq, s->row_map};
   materialize<W>(s, b, src, nq, off, len, out, cap, cursor, es);
 }
 
@@ -630,7 +637,8 @@ template <int W>
 void materialize_triples(Session* s, WaveBufs& b, int nq, int64_t* off, int64_t* len, int32_t* out,
                          int64_t cap, int64_t* cursor) {
   const Graph* g = s->g;
-  TripleSrc<W> src{b.X, b.Xf, s->last.d_rel_masks ? b.M : nullptr, g->subj, g->rel, g->T, nq};
+  TripleSrc<W> src{b.X, b.Xf, s->last.d_rel_masks ? b.M : nullptr, g->subj, g->rel, g->T, nq,
+                   s->tid_map};
   materialize<W>(s, b, src, nq, off, len, out, cap, cursor);
 }
 
@@ -825,6 +833,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   }
 }
 
+
+#include "k6_shard.cuh"
 
 }  // namespace
 
@@ -1028,6 +1038,10 @@ int session_finish(Session* s, th_result* out) {
     out->path_tids = static_cast<const int32_t*>(s->p_tids.p);
     out->path_total = c.path_used;
   }
+  if (c.err == 2) {
+    set_error("malformed exchange record (row not owned by this rank)");
+    return TH_ERR_STATE;
+  }
   if (c.err) {
     set_error("seed id out of range for the graph's entity count");
     return TH_ERR_RANGE;
@@ -1081,6 +1095,518 @@ void plan_owner_hash(const Graph* g, int32_t m, int32_t* d_owner, cudaStream_t s
   if (g->E == 0) return;
   plan_owner_hash_kernel<<<grid_for(g->E), kThreads, 0, st>>>(g->indptr, g->E, m, d_owner);
   TH_LAUNCHED();
+}
+
+
+// ============================================================ K6 shards
+// One rank's partitioned-graph session (see k6_shard.cuh).  The host drives
+// a wave hop by hop -- expand / (exchange) / absorb / hub rows / (all-reduce)
+// / hub merge / end hop -- so the collectives stay with the caller
+// (torch.distributed over NCCL, or an in-process loopback).
+
+struct Shard {
+  Graph g;                         // rows [0,n_local) owned, then hub slices
+  int32_t* tid_l2g = nullptr;      // local triple -> global tid (ascending)
+  int32_t* lidx = nullptr;         // [E] row at the owner
+  int32_t* hub_index = nullptr;    // [E]
+  int32_t* hub_ids = nullptr;      // [H]
+  int32_t* l2g = nullptr;          // [n_local] owned rows -> global ids (ascending)
+  int64_t E = 0, n_local = 0, H = 0;
+  int32_t rank = 0, world = 1;
+  Session s;
+  DBuf O, Of, olist, send, pcnt, hubbuf;
+  int W = 0;
+  bool in_wave = false;
+  int next_hop = 0;
+  int64_t rows() const { return n_local + H; }
+};
+
+namespace {
+
+template <typename T>
+T* dcopy(const T* src, int64_t n, cudaStream_t st) {
+  T* p = nullptr;
+  TH_CUDA(cudaMalloc(&p, sizeof(T) * std::max<int64_t>(n, 1)));
+  if (n > 0) TH_CUDA(cudaMemcpyAsync(p, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
+  return p;
+}
+
+template <int W>
+ShardArgs shard_args(Shard* sh) {
+  Session* s = &sh->s;
+  const Graph* g = &sh->g;
+  ShardArgs sa{};
+  WaveArgs& a = sa.a;
+  a.indptr = g->indptr;
+  a.csr_obj = g->csr_obj;
+  a.csr_rel = g->csr_rel;
+  a.E = sh->rows();
+  a.T = g->T;
+  a.X = static_cast<uint32_t*>(s->X.p);
+  a.N = static_cast<uint32_t*>(s->N.p);
+  a.V = static_cast<uint32_t*>(s->V.p);
+  a.S = static_cast<uint32_t*>(s->S.p);
+  a.Xf = static_cast<uint32_t*>(s->Xf.p);
+  a.Nf = static_cast<uint32_t*>(s->Nf.p);
+  a.Vf = static_cast<uint32_t*>(s->Vf.p);
+  a.M = s->last.d_rel_masks ? static_cast<uint32_t*>(s->M.p) : nullptr;
+  a.lists = static_cast<int32_t*>(s->lists.p);
+  a.heavy = static_cast<int32_t*>(s->heavy.p);
+  a.ctl = static_cast<Ctl*>(s->ctl.p);
+  a.nq = s->last.n_queries;
+  a.sem = s->last.semantics;
+  a.h = sh->next_hop;
+  sa.lidx = sh->lidx;
+  sa.hub_index = sh->hub_index;
+  sa.hub_ids = sh->hub_ids;
+  sa.O = static_cast<uint32_t*>(sh->O.p);
+  sa.Of = static_cast<uint32_t*>(sh->Of.p);
+  sa.olist = static_cast<int32_t*>(sh->olist.p);
+  sa.olen = &a.ctl->olen;
+  sa.E_global = sh->E;
+  sa.n_local = sh->n_local;
+  sa.n_hubs = sh->H;
+  sa.rank = sh->rank;
+  sa.world = sh->world;
+  return sa;
+}
+
+template <int W>
+WaveBufs shard_bufs(Shard* sh) {
+  Session* s = &sh->s;
+  WaveBufs b{};
+  b.W = W;
+  b.X = static_cast<uint32_t*>(s->X.p);
+  b.N = static_cast<uint32_t*>(s->N.p);
+  b.V = static_cast<uint32_t*>(s->V.p);
+  b.S = static_cast<uint32_t*>(s->S.p);
+  b.Xf = static_cast<uint32_t*>(s->Xf.p);
+  b.Nf = static_cast<uint32_t*>(s->Nf.p);
+  b.Vf = static_cast<uint32_t*>(s->Vf.p);
+  b.M = static_cast<uint32_t*>(s->M.p);
+  b.lists = static_cast<int32_t*>(s->lists.p);
+  b.heavy = static_cast<int32_t*>(s->heavy.p);
+  b.counts = static_cast<int32_t*>(s->counts.p);
+  b.totals = static_cast<int64_t*>(s->totals.p);
+  b.ctl = static_cast<Ctl*>(s->ctl.p);
+  return b;
+}
+
+template <int W>
+void shard_begin_w(Shard* sh, const th_query* q) {
+  Session* s = &sh->s;
+  cudaStream_t st = s->st;
+  const int64_t rows = std::max<int64_t>(sh->rows(), 1);
+  const int64_t k = q->k;
+  const int64_t fwords = ceil_div(rows, 32) + 1;
+  for (DBuf* d : {&s->X, &s->N, &s->V, &s->S}) {
+    if (d == &s->S && q->semantics != TH_CUMULATIVE) continue;
+    if (d->bytes < (size_t)rows * W * 4) {
+      ensure<uint32_t>(*d, rows * W, st);
+      TH_CUDA(cudaMemsetAsync(d->p, 0, d->bytes, st));
+    }
+  }
+  ensure<uint32_t>(s->Xf, fwords, st);
+  ensure<uint32_t>(s->Nf, fwords, st);
+  ensure<uint32_t>(s->Vf, fwords, st);
+  ensure<int32_t>(s->lists, (k + 1) * rows, st);
+  ensure<int32_t>(s->heavy, rows, st);
+  if (q->d_rel_masks) ensure<uint32_t>(s->M, std::max<int64_t>(sh->g.R, 1) * W, st);
+  ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
+  ensure<int64_t>(s->totals, kMaxWave, st);
+  const int64_t E = std::max<int64_t>(sh->E, 1);
+  if (sh->O.bytes < (size_t)E * W * 4) {
+    ensure<uint32_t>(sh->O, E * W, st);
+    TH_CUDA(cudaMemsetAsync(sh->O.p, 0, sh->O.bytes, st));
+  }
+  if (sh->Of.bytes < (size_t)(ceil_div(E, 32) + 1) * 4) {
+    ensure<uint32_t>(sh->Of, ceil_div(E, 32) + 1, st);
+    TH_CUDA(cudaMemsetAsync(sh->Of.p, 0, sh->Of.bytes, st));
+  }
+  ensure<int32_t>(sh->olist, E, st);
+  ensure<unsigned long long>(sh->pcnt, std::max(sh->world, 1), st);
+  ensure<uint32_t>(sh->hubbuf, std::max<int64_t>(sh->H, 1) * W, st);
+  Ctl* ctl = static_cast<Ctl*>(s->ctl.p);
+  TH_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+  TH_CUDA(cudaMemsetAsync(s->Xf.p, 0, fwords * 4, st));
+  TH_CUDA(cudaMemsetAsync(s->Nf.p, 0, fwords * 4, st));
+  TH_CUDA(cudaMemsetAsync(s->Vf.p, 0, fwords * 4, st));
+  sh->next_hop = 0;
+  ShardArgs sa = shard_args<W>(sh);
+  if (q->d_rel_masks) {
+    build_mask_kernel<W><<<grid_for(sh->g.R * W), kThreads, 0, st>>>(
+        q->d_rel_masks, q->mask_words, 0, q->n_queries, sh->g.R, static_cast<uint32_t*>(s->M.p));
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+  shard_seed_kernel<W><<<grid_for((int64_t)q->n_queries * 32), kThreads, 0, st>>>(
+      sa, q->d_seed_offsets, q->d_seeds);
+  TH_LAUNCHED();
+  s->launches += 1;
+  sh->next_hop = 1;
+}
+
+template <int W>
+void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send) {
+  Session* s = &sh->s;
+  cudaStream_t st = s->st;
+  const th_query& q = s->last;
+  const bool filter = q.d_rel_masks != nullptr;
+  const int64_t B = q.n_queries;
+  WaveBufs b = shard_bufs<W>(sh);
+  ShardArgs sa = shard_args<W>(sh);
+  sa.a.h = h;
+  const unsigned pg = persistent_grid();
+  begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, sh->g.T, 0.0, 0);
+  TH_LAUNCHED();
+  TH_CUDA(cudaMemsetAsync(&b.ctl->olen, 0, sizeof(int32_t), st));
+  int64_t* e_out = static_cast<int64_t*>(s->edges.p) + (h - 1) * B;
+  {
+    ProfScope ps(s, TH_PROF_EDGES);
+    if (filter) {
+      edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out, 0);
+      TH_LAUNCHED();
+      edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out, 1);
+      TH_LAUNCHED();
+      s->launches += 2;
+    } else {
+      edge_count_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out);
+      TH_LAUNCHED();
+      s->launches += 1;
+    }
+  }
+  if (q.flags & TH_WANT_ACTIVATED) {
+    ProfScope ps(s, TH_PROF_ACTIVATED);
+    materialize_triples<W>(s, b, (int)B, static_cast<int64_t*>(s->a_off.p) + (h - 1) * B,
+                           static_cast<int64_t*>(s->a_len.p) + (h - 1) * B,
+                           static_cast<int32_t*>(s->a_ids.p), s->a_cap, &b.ctl->act_used);
+  }
+  {
+    ProfScope ps(s, TH_PROF_PUSH);
+    const int sem = q.semantics == TH_EXACT ? TH_EXACT : TH_FRONTIER;
+#define TH_SHARD_PUSH(SEM, F)                                                      \
+  shard_push_light_kernel<W, SEM, F><<<pg, kThreads, 0, st>>>(sa);               \
+  TH_LAUNCHED();                                                                 \
+  shard_push_heavy_kernel<W, SEM, F><<<pg, kThreads, 0, st>>>(sa);               \
+  TH_LAUNCHED();
+    if (filter) {
+      if (sem == TH_EXACT) { TH_SHARD_PUSH(TH_EXACT, true) } else { TH_SHARD_PUSH(TH_FRONTIER, true) }
+    } else {
+      if (sem == TH_EXACT) { TH_SHARD_PUSH(TH_EXACT, false) } else { TH_SHARD_PUSH(TH_FRONTIER, false) }
+    }
+#undef TH_SHARD_PUSH
+    s->launches += 3;
+  }
+  // pack: per-owner totals -> host -> offsets -> records
+  const int G = sh->world;
+  unsigned long long* pc = static_cast<unsigned long long*>(sh->pcnt.p);
+  TH_CUDA(cudaMemsetAsync(pc, 0, sizeof(unsigned long long) * G, st));
+  shard_pack_kernel<W, false><<<pg, kThreads, 0, st>>>(sa, pc, nullptr);
+  TH_LAUNCHED();
+  std::vector<unsigned long long> cnt(G);
+  TH_CUDA(cudaMemcpyAsync(cnt.data(), pc, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost, st));
+  TH_CUDA(cudaStreamSynchronize(st));
+  std::vector<unsigned long long> off(G);
+  unsigned long long tot = 0;
+  for (int d = 0; d < G; ++d) {
+    off[d] = tot;
+    tot += cnt[d];
+    h_counts[d] = (int64_t)cnt[d];
+  }
+  uint64_t* send = ensure<uint64_t>(sh->send, (int64_t)std::max<unsigned long long>(tot, 1), st);
+  TH_CUDA(cudaMemcpyAsync(pc, off.data(), sizeof(unsigned long long) * G, cudaMemcpyHostToDevice, st));
+  shard_pack_kernel<W, true><<<pg, kThreads, 0, st>>>(sa, pc, send);
+  TH_LAUNCHED();
+  TH_CUDA(cudaStreamSynchronize(st));  // `off` is a host temporary
+  s->launches += 3;
+  *d_send = send;
+}
+
+template <int W>
+void shard_absorb_w(Shard* sh, int h, const uint64_t* recs, int64_t n) {
+  Session* s = &sh->s;
+  ShardArgs sa = shard_args<W>(sh);
+  sa.a.h = h;
+  if (n > 0) {
+    const int sem = s->last.semantics;
+    const unsigned grid = grid_for(n);
+    if (sem == TH_EXACT) shard_absorb_kernel<W, TH_EXACT><<<grid, kThreads, 0, s->st>>>(sa, recs, n);
+    else shard_absorb_kernel<W, TH_FRONTIER><<<grid, kThreads, 0, s->st>>>(sa, recs, n);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+}
+
+template <int W>
+uint32_t* shard_hub_rows_w(Shard* sh, int h) {
+  Session* s = &sh->s;
+  ShardArgs sa = shard_args<W>(sh);
+  sa.a.h = h;
+  uint32_t* buf = static_cast<uint32_t*>(sh->hubbuf.p);
+  if (sh->H > 0) {
+    shard_hub_out_kernel<W><<<grid_for(sh->H * W), kThreads, 0, s->st>>>(sa, buf);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+  return buf;
+}
+
+template <int W>
+void shard_hub_merge_w(Shard* sh, int h) {
+  Session* s = &sh->s;
+  ShardArgs sa = shard_args<W>(sh);
+  sa.a.h = h;
+  if (sh->H > 0) {
+    shard_hub_in_kernel<W><<<grid_for(sh->H), kThreads, 0, s->st>>>(
+        sa, static_cast<const uint32_t*>(sh->hubbuf.p));
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+}
+
+template <int W>
+void shard_end_hop_w(Shard* sh, int h) {
+  Session* s = &sh->s;
+  cudaStream_t st = s->st;
+  const th_query& q = s->last;
+  const int64_t B = q.n_queries;
+  WaveBufs b = shard_bufs<W>(sh);
+  const int64_t rows = std::max<int64_t>(sh->rows(), 1);
+  const int64_t fwords = ceil_div(rows, 32) + 1;
+  if (q.flags & TH_WANT_FRONTIERS) {
+    ProfScope ps(s, TH_PROF_FRONTIER);
+    int64_t* f_off = static_cast<int64_t*>(s->f_off.p) + (h - 1) * B;
+    int64_t* f_len = static_cast<int64_t*>(s->f_len.p) + (h - 1) * B;
+    int32_t* ids = static_cast<int32_t*>(s->f_ids.p);
+    if (q.semantics == TH_CUMULATIVE)
+      materialize_dense<W>(s, b, b.V, b.S, b.Vf, (int)B, f_off, f_len, ids, s->f_cap, &b.ctl->ids_used);
+    else
+      materialize_dense<W>(s, b, b.N, nullptr, b.Nf, (int)B, f_off, f_len, ids, s->f_cap,
+                           &b.ctl->ids_used);
+  }
+  {
+    ProfScope ps(s, TH_PROF_CLEAR);
+    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1);
+    TH_LAUNCHED();
+    TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
+    s->launches += 1;
+  }
+  std::swap(s->X, s->N);
+  std::swap(s->Xf, s->Nf);
+  sh->next_hop = h + 1;
+}
+
+template <int W>
+void shard_retire_w(Shard* sh) {
+  Session* s = &sh->s;
+  cudaStream_t st = s->st;
+  const th_query& q = s->last;
+  const int k = q.k;
+  WaveBufs b = shard_bufs<W>(sh);
+  const int64_t rows = std::max<int64_t>(sh->rows(), 1);
+  clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, k, k);
+  TH_LAUNCHED();
+  if (q.semantics != TH_EXACT) {
+    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, k);
+    TH_LAUNCHED();
+  }
+  if (q.semantics == TH_CUMULATIVE) {
+    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0);
+    TH_LAUNCHED();
+  }
+  s->launches += 3;
+}
+
+#define TH_W_DISPATCH(W_, CALL)             \
+  switch (W_) {                             \
+    case 1: { constexpr int WW = 1; CALL; } break;   \
+    case 2: { constexpr int WW = 2; CALL; } break;   \
+    case 4: { constexpr int WW = 4; CALL; } break;   \
+    case 8: { constexpr int WW = 8; CALL; } break;   \
+    case 16: { constexpr int WW = 16; CALL; } break; \
+    default: { constexpr int WW = 32; CALL; } break; \
+  }
+
+}  // namespace
+
+int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
+                 int64_t T, int64_t E, int64_t R, const int32_t* d_lidx,
+                 const int32_t* d_hub_index, const int32_t* d_hub_ids, int64_t H,
+                 const int32_t* d_l2g, int64_t n_local, int32_t rank, int32_t world,
+                 cudaStream_t st) {
+  auto* sh = new Shard();
+  *out = sh;
+  sh->E = E;
+  sh->n_local = n_local;
+  sh->H = H;
+  sh->rank = rank;
+  sh->world = world;
+  sh->lidx = dcopy(d_lidx, E, st);
+  sh->hub_index = dcopy(d_hub_index, E, st);
+  sh->hub_ids = dcopy(d_hub_ids, H, st);
+  sh->l2g = dcopy(d_l2g, n_local, st);
+  // select + compact this rank's triples (tid order kept)
+  int32_t* key = nullptr;
+  TH_CUDA(cudaMalloc(&key, sizeof(int32_t) * std::max<int64_t>(T, 1)));
+  const int nb = (int)std::max<int64_t>(1, ceil_div(T, kCompactWords));
+  int32_t* bsum = nullptr;
+  TH_CUDA(cudaMalloc(&bsum, sizeof(int32_t) * (nb + 1)));
+  if (T > 0) {
+    shard_select_kernel<<<grid_for(T), kThreads, 0, st>>>(d_subj, T, sh->lidx, sh->hub_index,
+                                                         n_local, rank, world, key);
+    TH_LAUNCHED();
+    shard_count_kernel<<<nb, kCompactThreads, 0, st>>>(key, T, bsum);
+    TH_LAUNCHED();
+    flag_scan_kernel<<<1, 1024, 0, st>>>(bsum, nb, bsum + nb);
+    TH_LAUNCHED();
+  } else {
+    TH_CUDA(cudaMemsetAsync(bsum + nb, 0, sizeof(int32_t), st));
+  }
+  int32_t tl = 0;
+  TH_CUDA(cudaMemcpyAsync(&tl, bsum + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  TH_CUDA(cudaStreamSynchronize(st));
+  int32_t *okey = nullptr, *orel = nullptr, *oobj = nullptr;
+  const int64_t tcap = std::max<int32_t>(tl, 1);
+  TH_CUDA(cudaMalloc(&okey, sizeof(int32_t) * tcap));
+  TH_CUDA(cudaMalloc(&orel, sizeof(int32_t) * tcap));
+  TH_CUDA(cudaMalloc(&oobj, sizeof(int32_t) * tcap));
+  TH_CUDA(cudaMalloc(&sh->tid_l2g, sizeof(int32_t) * tcap));
+  if (T > 0) {
+    shard_gather_kernel<<<nb, kCompactThreads, 0, st>>>(key, T, bsum, d_rel, d_obj, okey, orel, oobj,
+                                                        sh->tid_l2g);
+    TH_LAUNCHED();
+  }
+  const int rc = graph_build(&sh->g, okey, orel, oobj, tl, n_local + H, R, false, st, E);
+  TH_CUDA(cudaStreamSynchronize(st));
+  for (void* p : {(void*)key, (void*)bsum, (void*)okey, (void*)orel, (void*)oobj}) cudaFree(p);
+  if (rc != TH_OK) return rc;
+  Session* s = &sh->s;
+  s->g = &sh->g;
+  s->st = st;
+  s->pull_divisor = 0.0;
+  s->mat_rows = n_local;
+  s->row_map = sh->l2g;
+  s->tid_map = sh->tid_l2g;
+  return TH_OK;
+}
+
+int64_t shard_local_triples(const Shard* sh) { return sh->g.T; }
+
+int shard_begin(Shard* sh, const th_query* q) {
+  Session* s = &sh->s;
+  if (q->k < 1 || q->k > kMaxK) {
+    set_error("hop count must be in [1, " + std::to_string(kMaxK) + "]");
+    return TH_ERR_INVALID;
+  }
+  if (q->semantics < TH_EXACT || q->semantics > TH_CUMULATIVE) {
+    set_error("unknown hop semantics");
+    return TH_ERR_INVALID;
+  }
+  if (q->n_queries < 0 || q->n_queries > kMaxWave ||
+      (q->n_queries > 0 && (!q->d_seed_offsets || !q->d_seeds))) {
+    set_error("a partitioned wave takes 0..1024 queries with device seed arrays");
+    return TH_ERR_INVALID;
+  }
+  if (q->d_rel_masks && q->mask_words < ceil_div(sh->g.R, 32)) {
+    set_error("mask_words too small for the relation count");
+    return TH_ERR_INVALID;
+  }
+  if (q->flags & TH_WANT_PATHS) {
+    set_error("path reconstruction is not available on partitioned graphs");
+    return TH_ERR_INVALID;
+  }
+  cudaStream_t st = s->st;
+  const int64_t B = q->n_queries, k = q->k;
+  const int64_t kb = std::max<int64_t>(k * B, 1);
+  ensure<Ctl>(s->ctl, 1, st);
+  for (DBuf* d : {&s->f_off, &s->f_len, &s->a_off, &s->a_len, &s->edges}) {
+    ensure<int64_t>(*d, kb, st);
+    TH_CUDA(cudaMemsetAsync(d->p, 0, sizeof(int64_t) * kb, st));
+  }
+  s->f_cap = std::max<int64_t>({s->f_cap, s->last_f_need, 1 << 16});
+  s->a_cap = std::max<int64_t>({s->a_cap, s->last_a_need, 1 << 16});
+  ensure<int32_t>(s->f_ids, s->f_cap, st);
+  ensure<int32_t>(s->a_ids, s->a_cap, st);
+  s->last = *q;
+  s->has_run = true;
+  sh->W = pick_words((int)std::max<int64_t>(B, 1));
+  if ((sh->rows() + 1) * (int64_t)sh->W >= (int64_t(1) << 32)) {
+    set_error("shard too large for 32-bit exchange keys (rows * W >= 2^32)");
+    return TH_ERR_INVALID;
+  }
+  sh->in_wave = true;
+  TH_W_DISPATCH(sh->W, shard_begin_w<WW>(sh, q));
+  return TH_OK;
+}
+
+static int shard_check_hop(Shard* sh, int h) {
+  if (!sh->in_wave) {
+    set_error("no wave in progress (th_shard_begin first)");
+    return TH_ERR_STATE;
+  }
+  if (h != sh->next_hop || h > sh->s.last.k) {
+    set_error("hop out of sequence");
+    return TH_ERR_STATE;
+  }
+  return TH_OK;
+}
+
+int shard_expand(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send) {
+  if (int rc = shard_check_hop(sh, h)) return rc;
+  TH_W_DISPATCH(sh->W, shard_expand_w<WW>(sh, h, h_counts, d_send));
+  return TH_OK;
+}
+
+int shard_absorb(Shard* sh, int h, const uint64_t* d_recv, int64_t n) {
+  if (int rc = shard_check_hop(sh, h)) return rc;
+  TH_W_DISPATCH(sh->W, shard_absorb_w<WW>(sh, h, d_recv, n));
+  return TH_OK;
+}
+
+int shard_hub_rows(Shard* sh, int h, uint32_t** d_rows, int64_t* words) {
+  if (int rc = shard_check_hop(sh, h)) return rc;
+  uint32_t* p = nullptr;
+  TH_W_DISPATCH(sh->W, p = shard_hub_rows_w<WW>(sh, h));
+  *d_rows = p;
+  *words = sh->H * sh->W;
+  return TH_OK;
+}
+
+int shard_hub_merge(Shard* sh, int h) {
+  if (int rc = shard_check_hop(sh, h)) return rc;
+  TH_W_DISPATCH(sh->W, shard_hub_merge_w<WW>(sh, h));
+  return TH_OK;
+}
+
+int shard_end_hop(Shard* sh, int h) {
+  if (int rc = shard_check_hop(sh, h)) return rc;
+  TH_W_DISPATCH(sh->W, shard_end_hop_w<WW>(sh, h));
+  return TH_OK;
+}
+
+int shard_finish(Shard* sh, th_result* out) {
+  if (!sh->in_wave || sh->next_hop != sh->s.last.k + 1) {
+    set_error("th_shard_finish before the last hop ended");
+    return TH_ERR_STATE;
+  }
+  TH_W_DISPATCH(sh->W, shard_retire_w<WW>(sh));
+  sh->in_wave = false;
+  return session_finish(&sh->s, out);
+}
+
+Session* shard_session(Shard* sh) { return &sh->s; }
+
+void shard_free(Shard* sh) {
+  session_free(&sh->s);
+  for (DBuf* d : {&sh->O, &sh->Of, &sh->olist, &sh->send, &sh->pcnt, &sh->hubbuf}) {
+    if (d->p) cudaFree(d->p);
+    d->p = nullptr;
+  }
+  for (void* p : {(void*)sh->tid_l2g, (void*)sh->lidx, (void*)sh->hub_index, (void*)sh->hub_ids,
+                  (void*)sh->l2g})
+    if (p) cudaFree(p);
+  graph_free(&sh->g);
+  delete sh;
 }
 
 }  // namespace th

@@ -25,6 +25,7 @@ struct Ctl {
   int32_t push_hops, pull_hops;
   int64_t path_used;
   int32_t mat_rows;  // length of the compacted row list of the layer being materialised
+  int32_t olen;      // shards: staged remote rows this hop
 };
 
 struct DBuf {
@@ -37,6 +38,11 @@ struct Session {
   cudaStream_t st = nullptr;
   double pull_divisor = 8.0;
   int64_t list_min_entities = int64_t(4) << 20;  // K4 list-driven above this E
+  // shards: K4 covers rows [0, mat_rows) (owned entities) and maps rows /
+  // local triples to global ids; defaults cover the whole single graph
+  int64_t mat_rows = -1;
+  const int32_t* row_map = nullptr;
+  const int32_t* tid_map = nullptr;
   int64_t launches = 0;
   // wave state
   DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals, rowlist, rowscan;
@@ -76,5 +82,23 @@ int session_run(Session* s, const th_query* q);
 int session_finish(Session* s, th_result* out);
 void session_free(Session* s);
 void plan_owner_hash(const Graph* g, int32_t m, int32_t* d_owner, cudaStream_t st);
+
+// ---- K6 partitioned graphs (one rank's shard; see k6_shard.cuh) ----
+struct Shard;
+int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
+                 int64_t T, int64_t E, int64_t R, const int32_t* d_lidx,
+                 const int32_t* d_hub_index, const int32_t* d_hub_ids, int64_t H,
+                 const int32_t* d_l2g, int64_t n_local, int32_t rank, int32_t world,
+                 cudaStream_t st);
+int64_t shard_local_triples(const Shard* sh);
+int shard_begin(Shard* sh, const th_query* q);
+int shard_expand(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send);
+int shard_absorb(Shard* sh, int h, const uint64_t* d_recv, int64_t n);
+int shard_hub_rows(Shard* sh, int h, uint32_t** d_rows, int64_t* words);
+int shard_hub_merge(Shard* sh, int h);
+int shard_end_hop(Shard* sh, int h);
+int shard_finish(Shard* sh, th_result* out);
+Session* shard_session(Shard* sh);
+void shard_free(Shard* sh);
 
 }  // namespace th

@@ -170,7 +170,8 @@ void sorted_rows(Graph* g, const int32_t* key, int64_t T, int64_t E, int32_t* pt
 }  // namespace
 
 int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
-                int64_t T, int64_t E, int64_t R, bool reverse, cudaStream_t st) {
+                int64_t T, int64_t E, int64_t R, bool reverse, cudaStream_t st, int64_t obj_bound) {
+  if (obj_bound < 0) obj_bound = E;
   g->E = E;
   g->T = T;
   g->R = R;
@@ -187,7 +188,7 @@ int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int
     TH_CUDA(cudaStreamSynchronize(st));
     cudaFree(mm);
     const char* names[3] = {"subject", "relation", "object"};
-    const int64_t bound[3] = {E, R, E};
+    const int64_t bound[3] = {E, R, obj_bound};
     for (int c = 0; c < 3; ++c) {
       if (h[2 * c] < 0 || h[2 * c + 1] >= bound[c]) {
         set_error(std::string(names[c]) + " id out of range (bound " + std::to_string(bound[c]) +

@@ -40,8 +40,11 @@ struct Graph {
 
 // Builds everything; throws CudaError / std::invalid_argument-like status via
 // the return code (TH_ERR_RANGE for out-of-range ids).
+// obj_bound: object ids must be < obj_bound (default E; a shard's rows are
+// local while its objects keep global ids)
 int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
-                int64_t T, int64_t E, int64_t R, bool reverse, cudaStream_t st);
+                int64_t T, int64_t E, int64_t R, bool reverse, cudaStream_t st,
+                int64_t obj_bound = -1);
 void graph_free(Graph* g);
 
 }  // namespace th

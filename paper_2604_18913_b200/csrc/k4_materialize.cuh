@@ -33,6 +33,7 @@ struct DenseSrc {
   const uint32_t* flags;
   int64_t nrows;
   int nq;
+  const int32_t* map = nullptr;  // optional row -> output id (ascending), e.g. shard local -> global
   static constexpr bool kDense = true;
   // lane t: flags of rows [r0+32t, r0+32t+32) below `rend` (r0 % 32 == 0)
   __device__ __forceinline__ uint32_t chunk_flags(int64_t r0, int64_t rend) const {
@@ -58,7 +59,7 @@ struct DenseSrc {
     return x & valid_word(j, nq);
   }
   __device__ __forceinline__ int64_t rows_dev() const { return nrows; }
-  __device__ __forceinline__ int32_t id(int64_t r) const { return (int32_t)r; }
+  __device__ __forceinline__ int32_t id(int64_t r) const { return map ? map[r] : (int32_t)r; }
 };
 
 // rows = the ascending list of nonzero entity rows of a layer (compacted
@@ -72,6 +73,7 @@ struct ListSrc {
   const int32_t* n_dev;
   int64_t nrows;  // capacity (host-side grid sizing)
   int nq;
+  const int32_t* map = nullptr;
   static constexpr bool kDense = true;
   __device__ __forceinline__ uint32_t chunk_flags(int64_t r0, int64_t rend) const {
     const int64_t t0 = r0 + 32 * (int64_t)lane_id();
@@ -87,7 +89,10 @@ struct ListSrc {
     return x & valid_word(j, nq);
   }
   __device__ __forceinline__ int64_t rows_dev() const { return *n_dev; }
-  __device__ __forceinline__ int32_t id(int64_t r) const { return rows[r]; }
+  __device__ __forceinline__ int32_t id(int64_t r) const {
+    const int32_t v = rows[r];
+    return map ? map[v] : v;
+  }
 };
 
 // rows = triples in tid order; word j of row t = X[subj[t]] & M[rel[t]]
@@ -100,6 +105,7 @@ struct TripleSrc {
   const uint16_t* rel;
   int64_t nrows;
   int nq;
+  const int32_t* map = nullptr;  // local triple -> global tid (shards)
   static constexpr bool kDense = false;
   __device__ __forceinline__ bool chunk_any(int64_t, int64_t) const { return true; }
   __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
@@ -119,7 +125,7 @@ struct TripleSrc {
     return x & valid_word(j, nq);
   }
   __device__ __forceinline__ int64_t rows_dev() const { return nrows; }
-  __device__ __forceinline__ int32_t id(int64_t r) const { return (int32_t)r; }
+  __device__ __forceinline__ int32_t id(int64_t r) const { return map ? map[r] : (int32_t)r; }
 };
 
 template <int W>

@@ -1,0 +1,385 @@
+// Part of engine.cu (included inside namespace th::{anonymous}).
+//
+// K6: one rank's side of the partitioned (multi-GPU) hop, the B200 form of
+// the reference's Algorithm 1 (engine.py:94-135 _partitioned_expand: route
+// -> local expand -> union).  One owner map serves both roles
+//   own(v) = ((v * 0x9E3779B1) mod 2^32) mod world     (partition.py:80-84)
+// -- the rank that stores v's out-row (subject-cohesive, partition.py:3-4)
+// and the rank that holds v's per-query visited/next bits.  Hubs (the top
+// out-degree entities) are the exception to subject cohesion: their rows
+// are edge-split over all ranks (triple t of a hub lives on rank
+// hash(t) mod world), and a hub in the frontier is expanded by every rank on
+// its slice.  Per hop, for one wave of <= 1024 queries:
+//   expand   push over the local frontier rows + the hub slices; targets
+//            owned here are test-and-set directly (as in K2); others are
+//            OR-ed into a staging matrix O (global rows) -- the local
+//            pre-dedupe, every (query, target) pair leaves a rank at most
+//            once per hop
+//   pack     staged rows -> (row-at-owner * W + word, bits) records bucketed
+//            by owner rank; the host exchanges them (NCCL all-to-all)
+//   absorb   received records are test-and-set like local targets
+//   hubs     owners publish their hubs' next-layer rows; the host sums the
+//            [hubs][W] buffer over ranks (one owner per hub, so the sum is
+//            the row) and every rank installs them as hub frontier rows
+//   end      K4 over the owned rows (ids mapped to global), retire X.
+// Local row space: [0, n_local) owned entities in ascending id order, then
+// [n_local, n_local + n_hubs) hub slices.
+
+struct ShardArgs {
+  WaveArgs a;              // local rows = n_local + n_hubs
+  const int32_t* lidx;     // [E_global] row of an entity at its owner
+  const int32_t* hub_index;  // [E_global] -1 or hub number
+  const int32_t* hub_ids;  // [n_hubs]
+  uint32_t* O;             // [E_global][W] staged remote bits
+  uint32_t* Of;            // [E_global / 32] staged-row flags
+  int32_t* olist;          // staged global ids
+  int32_t* olen;
+  int64_t E_global, n_local, n_hubs;
+  int32_t rank, world;
+};
+
+__device__ __forceinline__ int32_t owner_of(int64_t v, int32_t world) {
+  return (int32_t)((uint32_t)((uint64_t)v * 0x9E3779B1ull) % (uint32_t)world);
+}
+
+// test-and-set of (local row, word j) with bits w (K2's PushOp on a row)
+template <int W, int SEM>
+__device__ __forceinline__ bool local_set(const WaveArgs& a, int32_t row, int j, uint32_t w) {
+  const size_t r = (size_t)row * W + j;
+  if (SEM == TH_EXACT) {
+    if (!(w & ~__ldcg(&a.N[r]))) return false;
+    const uint32_t old = atomicOr(&a.N[r], w);
+    return old == 0u && flag_next(a, row);
+  }
+  if (!(w & ~__ldcg(&a.V[r]))) return false;
+  const uint32_t old = atomicOr(&a.V[r], w);
+  const uint32_t nb = w & ~old;
+  if (!nb) return false;
+  atomicOr(&a.N[r], nb);
+  return flag_next(a, row);
+}
+
+// stage bits for a remote target; true for the first toucher of v this hop
+template <int W>
+__device__ __forceinline__ bool remote_stage(const ShardArgs& sa, int32_t v, int j, uint32_t w) {
+  uint32_t* o = &sa.O[(size_t)v * W + j];
+  if (!(w & ~__ldcg(o))) return false;
+  atomicOr(o, w);
+  const uint32_t fb = 1u << (v & 31);
+  return !(atomicOr(&sa.Of[v >> 5], fb) & fb);
+}
+
+// seeds: owned seeds set local rows; hub seeds set their hub rows (every rank
+// sees every seed, so hub rows need no exchange at hop 0)
+template <int W>
+__global__ void shard_seed_kernel(ShardArgs sa, const int32_t* __restrict__ qoff,
+                                  const int32_t* __restrict__ seeds) {
+  const WaveArgs& a = sa.a;
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int q = gw; q < a.nq; q += nw) {
+    const int32_t lo = qoff[q], hi = qoff[q + 1];
+    const uint32_t qb = 1u << (q & 31);
+    const int qw = q >> 5;
+    for (int32_t i0 = lo; i0 < hi; i0 += 32) {
+      const int32_t i = i0 + lane;
+      int32_t row = -1, hrow = -1;
+      if (i < hi) {
+        const int32_t e = seeds[i];
+        if (e < 0 || e >= sa.E_global) {
+          a.ctl->err = 1;
+        } else {
+          if (owner_of(e, sa.world) == sa.rank) row = sa.lidx[e];
+          const int32_t hx = sa.hub_index[e];
+          if (hx >= 0) hrow = (int32_t)(sa.n_local + hx);
+        }
+      }
+      bool fresh = false, hfresh = false;
+      if (row >= 0) {
+        const size_t r = (size_t)row * W + qw;
+        atomicOr(&a.X[r], qb);
+        if (a.sem != TH_EXACT) atomicOr(&a.V[r], qb);
+        if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
+        const uint32_t fb = 1u << (row & 31);
+        fresh = !(atomicOr(&a.Xf[row >> 5], fb) & fb);
+        if (fresh && a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[row >> 5], fb);
+      }
+      if (hrow >= 0) {
+        atomicOr(&a.X[(size_t)hrow * W + qw], qb);
+        const uint32_t fb = 1u << (hrow & 31);
+        hfresh = !(atomicOr(&a.Xf[hrow >> 5], fb) & fb);
+      }
+      const uint32_t d = fresh ? (uint32_t)(a.indptr[row + 1] - a.indptr[row]) : 0u;
+      warp_append_all(fresh, row, d, a.lists, &a.ctl->list_len[0], a.E, &a.ctl->push_cost[0]);
+      const uint32_t hd = hfresh ? (uint32_t)(a.indptr[hrow + 1] - a.indptr[hrow]) : 0u;
+      warp_append_all(hfresh, hrow, hd, a.lists, &a.ctl->list_len[0], a.E, &a.ctl->push_cost[0]);
+    }
+  }
+}
+
+// K2's pair enumeration over CSR slots [lo, hi) of local row u, with the
+// owner split of every target
+template <int W, int SEM, bool FILTER>
+__device__ __forceinline__ void shard_row_pairs(const ShardArgs& sa, int32_t u, int32_t lo,
+                                                int32_t hi) {
+  const WaveArgs& a = sa.a;
+  const unsigned lane = lane_id();
+  const uint32_t xw = lane < (unsigned)W ? a.X[(size_t)u * W + lane] : 0u;
+  const unsigned nz = __ballot_sync(TH_FULL, xw != 0u);
+  if (!nz || hi <= lo) return;
+  const int nzw = __popc(nz);
+  const int pairs = (hi - lo) * nzw;
+  const int j1 = __ffs(nz) - 1;
+  for (int p0 = 0; p0 < pairs; p0 += 32) {
+    const int p = p0 + (int)lane;
+    int e, j;
+    if (nzw == 1) {
+      e = p;
+      j = j1;
+    } else {
+      e = p / nzw;
+      j = (int)__fns(nz, 0, p - e * nzw + 1);
+    }
+    const uint32_t x = __shfl_sync(TH_FULL, xw, j & 31);
+    bool fresh = false, rfresh = false;
+    int32_t row = 0, v = 0;
+    if (p < pairs) {
+      const int32_t pos = lo + e;
+      uint32_t w = x;
+      if (FILTER) w &= a.M[(size_t)a.csr_rel[pos] * W + j];
+      if (w) {
+        v = a.csr_obj[pos];
+        if (owner_of(v, sa.world) == sa.rank) {
+          row = sa.lidx[v];
+          fresh = local_set<W, SEM>(a, row, j, w);
+        } else {
+          rfresh = remote_stage<W>(sa, v, j, w);
+        }
+      }
+    }
+    append_next(a, fresh, row);
+    warp_append_all(rfresh, v, 0u, sa.olist, sa.olen, sa.E_global, (unsigned long long*)nullptr);
+  }
+}
+
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) shard_push_light_kernel(ShardArgs sa) {
+  const WaveArgs& a = sa.a;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int32_t n = a.ctl->list_len[a.h - 1];
+  const int32_t* list = a.lists + a.ctl->list_off[a.h - 1];
+  for (int32_t i = gw; i < n; i += nw) {
+    const int32_t u = list[i];
+    const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
+    if (hi - lo > kHeavyPush) {
+      // with a relation filter the edge-count pass already built the heavy list
+      if (!FILTER && lane_id() == 0) a.heavy[atomicAdd(&a.ctl->heavy_len, 1)] = u;
+      continue;
+    }
+    shard_row_pairs<W, SEM, FILTER>(sa, u, lo, hi);
+  }
+}
+
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa) {
+  const WaveArgs& a = sa.a;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int32_t nh = a.ctl->heavy_len;
+  int64_t base = 0;
+  for (int32_t i = 0; i < nh; ++i) {
+    const int32_t u = a.heavy[i];
+    const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
+    const int32_t nc = (hi - lo + kPushChunk - 1) / kPushChunk;
+    int64_t c = ((gw - base) % nw + nw) % nw;
+    for (; c < nc; c += nw) {
+      const int32_t clo = lo + (int32_t)c * kPushChunk;
+      shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk));
+    }
+    base += nc;
+  }
+}
+
+// staged rows -> records bucketed by owner.  COUNT: per-owner record totals
+// into cnt[world]; WRITE: records at cursor[owner] (pre-set to the owner's
+// exclusive offset), staged rows and flags cleared.  Warp-aggregated: one
+// atomic per (warp, owner).
+template <int W, bool WRITE>
+__global__ void __launch_bounds__(kThreads) shard_pack_kernel(ShardArgs sa,
+                                                              unsigned long long* cnt_or_cursor,
+                                                              uint64_t* send) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t n = *sa.olen;
+  for (int64_t base = gw * 32; base < n; base += nw * 32) {
+    const int64_t i = base + lane;
+    int32_t v = -1, dest = -1;
+    uint32_t words[W];
+    int nzc = 0;
+    if (i < n) {
+      v = sa.olist[i];
+      dest = owner_of(v, sa.world);
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        words[j] = sa.O[(size_t)v * W + j];
+        nzc += words[j] != 0u;
+      }
+    }
+    for (int d = 0; d < sa.world; ++d) {
+      const bool mine = dest == d;
+      const unsigned m = __ballot_sync(TH_FULL, mine && nzc > 0);
+      if (!m) continue;
+      int incl = mine ? nzc : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(TH_FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int tot = __shfl_sync(TH_FULL, incl, 31);
+      unsigned long long b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&cnt_or_cursor[d], (unsigned long long)tot);
+      b0 = __shfl_sync(TH_FULL, b0, 0);
+      if (WRITE && mine) {
+        uint64_t o = b0 + (uint64_t)(incl - nzc);
+        const uint64_t key0 = (uint64_t)sa.lidx[v] * W;
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+          if (words[j]) send[o++] = ((key0 + j) << 32) | words[j];
+      }
+    }
+    if (WRITE && v >= 0) {
+#pragma unroll
+      for (int j = 0; j < W; ++j) sa.O[(size_t)v * W + j] = 0u;
+      atomicAnd(&sa.Of[v >> 5], ~(1u << (v & 31)));
+    }
+  }
+}
+
+// received records -> local test-and-set, appended to the hop's list
+template <int W, int SEM>
+__global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa,
+                                                                const uint64_t* __restrict__ recs,
+                                                                int64_t n) {
+  const WaveArgs& a = sa.a;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = gw * 32; base < n; base += nw * 32) {
+    const int64_t i = base + lane;
+    bool fresh = false;
+    int32_t row = 0;
+    if (i < n) {
+      const uint64_t rec = recs[i];
+      const uint32_t key = (uint32_t)(rec >> 32);
+      row = (int32_t)(key / W);
+      if (row >= sa.n_local) {
+        a.ctl->err = 2;  // malformed record: not an owned row
+      } else {
+        fresh = local_set<W, SEM>(a, row, (int)(key % W), (uint32_t)rec);
+      }
+    }
+    append_next(a, fresh, row);
+  }
+}
+
+// owners publish their hubs' next-layer rows ([n_hubs][W], zero elsewhere)
+template <int W>
+__global__ void shard_hub_out_kernel(ShardArgs sa, uint32_t* out) {
+  const int64_t n = sa.n_hubs * W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = i / W;
+    const int j = (int)(i % W);
+    const int32_t v = sa.hub_ids[h];
+    out[i] = owner_of(v, sa.world) == sa.rank ? sa.a.N[(size_t)sa.lidx[v] * W + j] : 0u;
+  }
+}
+
+// install the summed hub rows as next-layer hub slice rows (frontier only:
+// a hub's visited bits stay with its owner)
+template <int W>
+__global__ void shard_hub_in_kernel(ShardArgs sa, const uint32_t* __restrict__ rows) {
+  const WaveArgs& a = sa.a;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = gw * 32; base < sa.n_hubs; base += nw * 32) {
+    const int64_t h = base + lane;
+    bool any = false;
+    int32_t row = 0;
+    if (h < sa.n_hubs) {
+      row = (int32_t)(sa.n_local + h);
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        const uint32_t w = rows[h * W + j];
+        a.N[(size_t)row * W + j] = w;
+        any |= w != 0u;
+      }
+      if (any) {
+        const uint32_t fb = 1u << (row & 31);
+        any = !(atomicOr(&a.Nf[row >> 5], fb) & fb);
+      }
+    }
+    const uint32_t d = any ? (uint32_t)(a.indptr[row + 1] - a.indptr[row]) : 0u;
+    warp_append_all(any, row, d, a.lists + a.ctl->list_off[a.h], &a.ctl->list_len[a.h], a.E,
+                    &a.ctl->push_cost[a.h]);
+  }
+}
+
+// mark the local triples of the rank and their local row keys, in tid order
+__global__ void shard_select_kernel(const int32_t* __restrict__ subj, int64_t T,
+                                    const int32_t* __restrict__ lidx,
+                                    const int32_t* __restrict__ hub_index, int64_t n_local,
+                                    int32_t rank, int32_t world, int32_t* key) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = subj[t];
+    const int32_t hx = hub_index[u];
+    int32_t k = -1;
+    if (hx >= 0) {
+      if (owner_of(t, world) == rank) k = (int32_t)(n_local + hx);
+    } else if (owner_of(u, world) == rank) {
+      k = lidx[u];
+    }
+    key[t] = k;
+  }
+}
+
+// ordered compaction of the selected triples (key >= 0) via per-block scans
+__global__ void __launch_bounds__(kCompactThreads) shard_count_kernel(const int32_t* __restrict__ key,
+                                                                       int64_t T, int32_t* bcount) {
+  __shared__ int ws[32];
+  const int64_t t0 = (int64_t)blockIdx.x * kCompactWords + threadIdx.x * kCompactPerThread;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kCompactPerThread; ++i) c += (t0 + i < T && key[t0 + i] >= 0);
+  int total;
+  block_excl_scan(c, ws, &total);
+  if (threadIdx.x == 0) bcount[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) shard_gather_kernel(
+    const int32_t* __restrict__ key, int64_t T, const int32_t* __restrict__ boff,
+    const int32_t* __restrict__ rel, const int32_t* __restrict__ obj, int32_t* okey, int32_t* orel,
+    int32_t* oobj, int32_t* otid) {
+  __shared__ int ws[32];
+  const int64_t t0 = (int64_t)blockIdx.x * kCompactWords + threadIdx.x * kCompactPerThread;
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < kCompactPerThread; ++i) c += (t0 + i < T && key[t0 + i] >= 0);
+  int total;
+  int o = boff[blockIdx.x] + block_excl_scan(c, ws, &total);
+  for (int i = 0; i < kCompactPerThread; ++i) {
+    const int64_t t = t0 + i;
+    if (t < T && key[t] >= 0) {
+      okey[o] = key[t];
+      orel[o] = rel[t];
+      oobj[o] = obj[t];
+      otid[o] = (int32_t)t;
+      ++o;
+    }
+  }
+}

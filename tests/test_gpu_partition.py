@@ -1,0 +1,122 @@
+"""GPU parity of the partitioned engine (K6, th_shard_*): every rank of a
+small world hosted on one B200 through LoopbackExchange.  Bit-exact against
+the single-graph engine, the oracle and the reference's golden traces --
+frontier AND activated sets, mirroring test_engine.py:68-82 (cross-graph
+traces bit-identical to single-graph ones)."""
+
+import numpy as np
+import pytest
+
+from golden_io import HERE as GOLDEN
+from golden_io import load_case
+from oracle import khop_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def th(cuda_device):
+    import paper_2604_18913_b200 as th
+
+    return th
+
+
+def _hub_graph(E, T, R, seed, alpha=1.2):
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(E)
+    w = np.cumsum(1.0 / np.arange(1, E + 1) ** alpha)
+    w /= w[-1]
+    s = perm[np.minimum(np.searchsorted(w, rng.random(T)), E - 1)]
+    o = perm[np.minimum(np.searchsorted(w, rng.random(T)), E - 1)]
+    r = rng.integers(0, R, T)
+    key = np.unique((s.astype(np.int64) * R + r) * E + o)
+    key = rng.permutation(key)
+    return key // E // R, (key // E) % R, key % E
+
+
+@pytest.mark.parametrize("world,n_hubs", [(1, 0), (2, 0), (2, 5), (3, 7), (4, 16)])
+@pytest.mark.parametrize("sem", ["exact", "frontier", "cumulative"])
+def test_partitioned_equals_single_and_oracle(th, world, n_hubs, sem):
+    s, r, o = _hub_graph(1500, 30000, 24, seed=21)
+    E, R = 1500, 24
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(world), n_hubs=n_hubs)
+    assert sum(sh.local_triples for sh in pg.shards) == s.size  # each triple on one rank
+    rng = np.random.default_rng(4)
+    seeds = rng.integers(0, E, 300)
+    part = pg.retrieve(seeds, 3, semantics=sem, activated=True)
+    single = th.retrieve(g, seeds, 3, semantics=sem, activated=True)
+    for i in range(seeds.size):
+        for h in range(1, 4):
+            assert np.array_equal(part.frontier(i, h), single.frontier(i, h)), (i, h)
+            assert np.array_equal(part.activated(i, h), single.activated(i, h)), (i, h)
+    assert np.array_equal(part.edges.numpy(), single.edges.cpu().numpy())
+    for i in range(0, seeds.size, 23):
+        ref = orc.retrieve_one(og, int(seeds[i]), 3, sem)
+        for h in range(3):
+            assert np.array_equal(part.frontier(i, h + 1), ref["frontiers"][h])
+            assert int(part.edges[h, i]) == ref["edges"][h]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_partitioned_relation_filter(th, world):
+    s, r, o = _hub_graph(1200, 20000, 30, seed=8)
+    E, R = 1200, 30
+    og = orc.build_csr(s, r, o, E, R)
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(world), n_hubs=6)
+    rng = np.random.default_rng(2)
+    seeds = rng.integers(0, E, 200)
+    filt = [sorted(rng.choice(R, 5, replace=False).tolist()) for _ in seeds]
+    part = pg.retrieve(seeds, 2, relation_filter=filt, semantics="frontier", activated=True)
+    for i in range(0, 200, 9):
+        ref = orc.retrieve_one(og, int(seeds[i]), 2, "frontier", filt[i])
+        for h in range(2):
+            assert np.array_equal(part.frontier(i, h + 1), ref["frontiers"][h])
+            assert np.array_equal(part.activated(i, h + 1), ref["activated"][h])
+            assert int(part.edges[h, i]) == ref["edges"][h]
+
+
+def test_two_waves_and_overflow_rerun(th):
+    """1,300 seeds = two waves; the first run of each wave overflows the
+    initial result capacity on every rank and is re-run transparently."""
+    s, r, o = _hub_graph(3000, 90000, 16, seed=3)
+    E, R = 3000, 16
+    g = th.build_incidence((s, r, o), E, R)
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(3), n_hubs=10)
+    seeds = np.random.default_rng(5).integers(0, E, 1300)
+    part = pg.retrieve(seeds, 3)
+    single = th.retrieve(g, seeds, 3)
+    for i in range(0, 1300, 13):
+        for h in range(1, 4):
+            assert np.array_equal(part.frontier(i, h), single.frontier(i, h))
+
+
+@pytest.mark.parametrize("name", ["tiny", "er30_s0", "er60_s12", "pl500_hubs", "selfloop", "objonly"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_cross_graph_k_hop_golden(th, name, world):
+    """The reference's own traces (frontier and activated per hop) through
+    cross_graph_k_hop on a partitioned graph."""
+    case = load_case(GOLDEN / f"{name}.npz")
+    pg = th.PartitionedGraph((case.subj, case.rel, case.obj), case.n_entities, case.n_relations,
+                             th.LoopbackExchange(world), n_hubs=2)
+    for q in case.queries:
+        if q.relations is not None:
+            continue
+        tr = th.cross_graph_k_hop(th.EntityVector(q.seeds, case.n_entities), q.k, pg, q.semantics)
+        for h in range(q.k):
+            assert np.array_equal(tr.frontier(h + 1).ids, q.frontiers[h]), (name, q.seeds, h)
+            assert np.array_equal(tr.activated(h + 1).ids, q.activated[h]), (name, q.seeds, h)
+
+
+def test_bad_partition_inputs(th):
+    s, r, o = _hub_graph(100, 500, 4, seed=1)
+    with pytest.raises(ValueError):
+        th.PartitionedGraph((s, r, o + 1000), 100, 4, th.LoopbackExchange(2))
+    pg = th.PartitionedGraph((s, r, o), 100, 4, th.LoopbackExchange(2))
+    with pytest.raises(ValueError):
+        pg.retrieve([5, 100], 2)
+    with pytest.raises(ValueError):
+        pg.retrieve([5], 0)
+    with pytest.raises(ValueError):
+        th.cross_graph_k_hop(th.EntityVector([1], 99), 2, pg)
