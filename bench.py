@@ -202,6 +202,197 @@ def run_reference(args, world, rank):
 
 # --------------------------------------------------------------- GPU side
 
+def _timed(stream, fn):
+    """Device milliseconds of fn() on `stream` (CUDA events, synchronised)."""
+    import torch
+
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record(stream)
+    out = fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b), out
+
+
+def run_c3_leg(th, g, s, E, R, stream, peaks):
+    """BASELINE configs[2]: relation-constrained k=2 with capped paths on the
+    C2 graph; 2,048 uniform + 2,048 top-1% hub seeds, per-seed 32-of-400 masks."""
+    import torch
+
+    from paper_2604_18913_b200.retriever import _relation_masks
+
+    seeds, rel_ids = workloads.c3_queries(s, E, R)
+    B = seeds.size
+    words = _relation_masks(list(rel_ids), B, R)
+    dev = g.device
+    d_seeds = torch.from_numpy(seeds).to(dev)
+    d_masks = torch.from_numpy(words.view(np.int32)).to(dev)
+    offs = torch.arange(B + 1, dtype=torch.int32, device=dev)
+    ret = th.Retriever(g, stream)
+
+    def step():
+        return ret.run(offs, d_seeds, 2, "frontier", d_masks, paths=True, max_paths=10_000,
+                       singleton=True, copy=False)
+
+    step()
+    ret.set_profiling(True)
+    ret.profile()
+    reps = 3
+    times, res = [], None
+    for _ in range(reps):
+        ms, res = _timed(stream, step)
+        times.append(ms)
+    prof = ret.profile()
+    ret.set_profiling(False)
+    t = sum(times) / reps
+    paths = int(res.path_count.sum().item())
+    edges = int(res.edges.sum().item())
+    # e2e: host seed/relation lists in, host frontiers + path tids out
+    e2e = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rr = ret.retrieve(seeds, 2, relation_filter=list(rel_ids), paths=True, max_paths=10_000,
+                          copy=False)
+        host = [x.cpu() for x in (rr.frontier_off, rr.frontier_len, rr.frontier_ids, rr.edges,
+                                  rr.path_off, rr.path_count, rr.path_tids, rr.path_truncated)]
+        e2e.append(time.perf_counter() - t0)
+    d2h = sum(x.numel() * x.element_size() for x in host)
+    return {"workload": "C3 (BASELINE configs[2]): C2 graph, 2,048 uniform + 2,048 top-1% hub seeds, "
+                        "per-seed random 32-of-400 relation masks, k=2 FRONTIER, full path "
+                        "reconstruction capped at 10,000 paths per seed",
+            "seeds_per_s": B / (t / 1e3), "ms_per_batch": t, "paths_per_s": paths / (t / 1e3),
+            "paths": paths, "truncated_seeds": int(res.path_truncated.sum().item()),
+            "edges_per_s": edges / (t / 1e3),
+            "kernel_ms_per_batch": {c: v[0] / reps for c, v in prof.items() if v[0]},
+            "e2e": {"value": B / statistics.median(e2e), "unit": "seeds/s",
+                    "h2d_bytes_per_step": int(seeds.nbytes + words.nbytes), "d2h_bytes_per_step": d2h}}
+
+
+def run_c4_leg(th, stream, peaks, n_batches=8):
+    """BASELINE configs[3] on one GPU: 54.4M entities / 86.5M triples, 8,192
+    uniform seeds as 8 waves of 1,024, k=2 and k=3, FRONTIER, frontiers
+    materialised per wave (the state and results of a wave are far above L2)."""
+    import torch
+
+    t0 = time.perf_counter()
+    s, r, o, E, R = workloads.c4_graph()
+    gen_s = time.perf_counter() - t0
+    stats = workloads.graph_stats(s, o, E)
+    g = th.build_incidence((s, r, o), E, R)
+    del s, r, o
+    ret = th.Retriever(g, stream)
+    batches = torch.from_numpy(workloads.seed_batches(E, BATCH, n_batches, seed=400)).to(g.device)
+    offs = torch.arange(BATCH + 1, dtype=torch.int32, device=g.device)
+    out = {"workload": "C4 (BASELINE configs[3]) on 1 GPU: 54.4M entities, 86.5M triples, 1,000 "
+                       "relations, power law P(w>=x)~x^-1.3 with a shared hub core, 1% isolated; "
+                       f"{n_batches * BATCH} uniform seeds in waves of {BATCH}, FRONTIER, no filter",
+           "graph": stats, "gen_s": gen_s}
+    peaks_leg = peaks
+    for k in (2, 3):
+        step = lambda i: ret.run(offs, batches[i], k, "frontier", None, singleton=True,  # noqa: E731
+                                 copy=False)
+        step(0)  # sizes the result buffers
+        ret.set_profiling(True)
+        ret.profile()
+        tot_ms, seeds, edges, ids, lists = 0.0, 0, 0, 0, 0
+        for i in range(n_batches):
+            ms, res = _timed(stream, lambda: step(i))
+            tot_ms += ms
+            seeds += BATCH
+            edges += int(res.edges.sum().item())
+            ids += int(res.frontier_len.sum().item())
+            lists += sum(ret.wave_lists(k)[1:])
+        prof = ret.profile()
+        ret.set_profiling(False)
+        kms = {c: v[0] / n_batches for c, v in prof.items() if v[0]}
+        dom = max(("frontier", "pull", "push"), key=lambda c: kms.get(c, 0.0))
+        leg = {"seeds_per_s": seeds / (tot_ms / 1e3), "edges_per_s": edges / (tot_ms / 1e3),
+               "ms_per_batch": tot_ms / n_batches, "frontier_ids_per_batch": ids / n_batches,
+               "kernel_ms_per_batch": kms, "dominant": dom}
+        if dom == "frontier":
+            W = 32
+            kbytes = 4 * ids + 4 * W * lists + 16 * k * seeds
+            a = kbytes / (prof["frontier"][0] / 1e3) / 1e9
+            leg["roofline"] = {"bound": "hbm", "achieved": a, "peak": peaks_leg["hbm_gbs"], "unit": "GB/s",
+                               "frac": a / peaks_leg["hbm_gbs"], "kernel": "K4 frontier",
+                               "alg_bytes_per_batch": kbytes / n_batches,
+                               "note": "4 B per output id + 4W B per nonzero layer row + offsets"}
+        out[f"k{k}"] = leg
+    del ret, g
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_partitioned(args, world, rank, local):
+    """C4 on a graph partitioned over the N ranks (hash owners + edge-split
+    hubs, NCCL all-to-all of candidate records per hop); every rank takes
+    part in every wave, so total work is fixed: strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_18913_b200 as th
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    s, r, o, E, R = workloads.c4_graph()
+    xch = th.DistExchange()
+    pg = th.PartitionedGraph((s, r, o), E, R, xch)
+    del s, r, o
+    batches = workloads.seed_batches(E, BATCH, args.warmup + args.steps, seed=400)
+    k = args.part_k
+    stream = torch.cuda.current_stream(dev)
+
+    def wave(i):
+        q = th.partition.WaveQuery(np.arange(BATCH + 1, dtype=np.int32), batches[i], k,
+                                   th.HopSemantics.FRONTIER)
+        return pg.run(q)
+
+    for i in range(args.warmup):
+        wave(i)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    b0 = xch.bytes_sent
+    launches0 = sum(sh.launch_count() for sh in pg.shards)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    edges = 0
+    for i in range(args.steps):
+        parts = wave(args.warmup + i)
+        edges += int(parts[0].edges.sum())
+    b.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    t_ms = a.elapsed_time(b)
+    tt = torch.tensor([t_ms, float(edges), float(xch.bytes_sent - b0)], dtype=torch.float64, device=dev)
+    tmax = tt.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+    t_ms = float(tmax[0].item())
+    if rank == 0:
+        value = BATCH * args.steps / (t_ms / 1e3)
+        print(json.dumps({
+            "metric": f"partitioned C4 k-hop seeds/s at k={k}", "value": value, "unit": "seeds/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": "C4 partitioned (BASELINE configs[3]): hash owners, top-0.01% hubs "
+                                   f"edge-split; one wave of {BATCH} uniform seeds per step, k={k}, FRONTIER",
+                       "parallelism": f"graph-partitioned x{world}"},
+            "edges_per_s": float(tt[1].item()) / (t_ms / 1e3),
+            "nvlink": {"bytes_per_step": float(tt[2].item()) / args.steps,
+                       "GBps": float(tt[2].item()) / (t_ms / 1e3) / 1e9, "peak_per_direction": 900.0},
+            "gpu_launches": sum(sh.launch_count() for sh in pg.shards) - launches0,
+            "clocks": clk}), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args, world, rank, local):
     import torch
 
@@ -346,6 +537,9 @@ def run_ours(args, world, rank, local):
                          f"oracle hop_trace per seed, fork pool, {dt:.1f} s)",
                "edges_per_s": e / dt}
 
+    c3 = run_c3_leg(th, g, s, E, R, stream, peaks) if (rank == 0 and not args.no_c3) else None
+    c4 = run_c4_leg(th, stream, peaks) if (rank == 0 and not args.no_c4) else None
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "seeds/s", "n_gpus": world, "steps": args.steps,
@@ -377,6 +571,8 @@ def run_ours(args, world, rank, local):
             "wall_s_timed": wall,
             "clocks": clk,
             "cpu_baseline": cpu,
+            "c3": c3,
+            "c4": c4,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -392,10 +588,17 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-step-seeds", type=int, default=64)
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 (filter + paths) leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 (54.4M-entity) leg")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="C4 on a graph partitioned over the ranks (NCCL exchange per hop)")
+    ap.add_argument("--part-k", type=int, default=2)
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
+    elif args.partitioned:
+        run_partitioned(args, world, rank, local)
     else:
         run_ours(args, world, rank, local)
 

@@ -1317,7 +1317,8 @@ void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send
   TH_CUDA(cudaMemcpyAsync(pc, off.data(), sizeof(unsigned long long) * G, cudaMemcpyHostToDevice, st));
   shard_pack_kernel<W, true><<<pg, kThreads, 0, st>>>(sa, pc, send);
   TH_LAUNCHED();
-  TH_CUDA(cudaStreamSynchronize(st));  // `off` is a host temporary
+  // (a pageable H2D copy is staged before cudaMemcpyAsync returns, so the
+  // host temporary `off` may go out of scope without a sync)
   s->launches += 3;
   *d_send = send;
 }

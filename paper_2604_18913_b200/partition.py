@@ -405,18 +405,22 @@ class GraphShard:
         return "ok", self._host_result(res)
 
     def _host_result(self, res) -> "ShardResult":
+        """Device views of the shard's results (valid until its next wave)."""
         B, k = res.n_queries, res.k
         t = _lib.as_tensor
         out = ShardResult(B, k)
-        out.edges = t(res.edges, (k, B), "<i8", self).cpu().numpy()
-        out.f_off = t(res.frontier_off, (k, B), "<i8", self).cpu().numpy()
-        out.f_len = t(res.frontier_len, (k, B), "<i8", self).cpu().numpy()
-        out.f_ids = t(res.frontier_ids, (res.frontier_total,), "<i4", self).cpu().numpy()
+        out.edges = t(res.edges, (k, B), "<i8", self)
+        out.f_off = t(res.frontier_off, (k, B), "<i8", self)
+        out.f_len = t(res.frontier_len, (k, B), "<i8", self)
+        out.f_ids = t(res.frontier_ids, (res.frontier_total,), "<i4", self)
         if self._q.flags & _lib.TH_WANT_ACTIVATED:
-            out.a_off = t(res.act_off, (k, B), "<i8", self).cpu().numpy()
-            out.a_len = t(res.act_len, (k, B), "<i8", self).cpu().numpy()
-            out.a_ids = t(res.act_ids, (res.act_total,), "<i4", self).cpu().numpy()
+            out.a_off = t(res.act_off, (k, B), "<i8", self)
+            out.a_len = t(res.act_len, (k, B), "<i8", self)
+            out.a_ids = t(res.act_ids, (res.act_total,), "<i4", self)
         return out
+
+    def _to_host(self, r: "ShardResult") -> "ShardResult":
+        return r.to_host()
 
 
 @dataclass
@@ -438,7 +442,8 @@ class WaveQuery:
 @dataclass
 class ShardResult:
     """One rank's share of a wave: owned frontier ids, local activated tids,
-    partial edge counts (host numpy, CSR per (hop, query))."""
+    partial edge counts (CSR per (hop, query)); device tensors from a CUDA
+    shard until ``to_host``."""
 
     n_queries: int
     k: int
@@ -449,6 +454,12 @@ class ShardResult:
     a_off: np.ndarray = None
     a_len: np.ndarray = None
     a_ids: np.ndarray = None
+
+    def to_host(self) -> "ShardResult":
+        conv = lambda x: x if x is None or isinstance(x, np.ndarray) else x.cpu().numpy()  # noqa: E731
+        return ShardResult(self.n_queries, self.k, *(conv(getattr(self, f)) for f in
+                                                      ("edges", "f_off", "f_len", "f_ids", "a_off", "a_len",
+                                                       "a_ids")))
 
 
 def run_wave(shards, xch: Exchange, query: WaveQuery, stats: dict | None = None):
@@ -571,7 +582,7 @@ class PartitionedGraph:
             nq = q1 - q0
             wq = WaveQuery(np.arange(nq + 1, dtype=np.int32), arr[q0:q1].astype(np.int32), k, sem,
                            None if words is None else words[q0:q1], activated)
-            parts = self.exchange.gather(self.run(wq))
+            parts = self.exchange.gather([r.to_host() for r in self.run(wq)])
             m = merge_results(parts, nq, k, activated)
             merged["edges"].append(m["edges"])
             merged["f_off"].append(m["f_off"] + fbase)
@@ -607,7 +618,7 @@ def cross_graph_k_hop(q0: EntityVector, k: int, pg: PartitionedGraph,
     sem = HopSemantics.parse(semantics)
     ids = q0.ids.astype(np.int32)
     wq = WaveQuery(np.array([0, ids.size], dtype=np.int32), ids, k, sem, None, True)
-    parts = pg.exchange.gather(pg.run(wq))
+    parts = pg.exchange.gather([r.to_host() for r in pg.run(wq)])
     m = merge_results(parts, 1, k, True)
     steps = []
     for h in range(k):

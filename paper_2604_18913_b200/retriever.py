@@ -158,7 +158,17 @@ def _relation_masks(relation_filter, n_queries: int, n_relations: int):
         rows = list(relation_filter)
         if len(rows) != n_queries:
             raise ValueError("per-seed relation filter needs one entry per seed")
-        words = np.stack([words_from_ids(r) for r in rows]) if rows else np.zeros((0, mw), np.uint32)
+        lens = {np.size(r) for r in rows}
+        if len(lens) == 1 and rows and next(iter(lens)) > 0:
+            # equal-length id rows: one vectorised scatter + pack for the batch
+            ids = np.asarray(rows, dtype=np.int64).reshape(n_queries, -1)
+            if ids.min() < 0 or ids.max() >= n_relations:
+                raise ValueError(f"relation id out of range (bound {n_relations})")
+            bits = np.zeros((n_queries, mw * 32), dtype=bool)
+            bits[np.arange(n_queries)[:, None], ids] = True
+            words = np.packbits(bits, axis=1, bitorder="little").view(np.uint32)
+        else:
+            words = np.stack([words_from_ids(r) for r in rows]) if rows else np.zeros((0, mw), np.uint32)
     return np.ascontiguousarray(words, dtype=np.uint32).reshape(n_queries, mw)
 
 
