@@ -150,6 +150,9 @@ int th_session_set_pull_divisor(th_session* s, double pull_divisor);
  * follows the reached rows); smaller graphs scan the flag bitmap directly.
  * Default 4 Mi.  0 = always list-driven. */
 int th_session_set_list_min_entities(th_session* s, int64_t min_entities);
+/* Overlap hop h's frontier materialisation (K4) with hop h+1's expansion
+ * on an internal stream (frontier-only runs).  Default on. */
+int th_session_set_overlap(th_session* s, int on);
 /* Number of kernels this session has launched since creation. */
 int64_t th_session_launch_count(const th_session* s);
 

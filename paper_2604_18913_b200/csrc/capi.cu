@@ -185,6 +185,15 @@ int th_session_set_list_min_entities(th_session* s, int64_t min_entities) {
   return TH_OK;
 }
 
+int th_session_set_overlap(th_session* s, int on) {
+  if (!s) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  s->s.overlap = on != 0;
+  return TH_OK;
+}
+
 int64_t th_session_launch_count(const th_session* s) { return s ? s->s.launches : -1; }
 
 int th_session_set_profiling(th_session* s, int on) {

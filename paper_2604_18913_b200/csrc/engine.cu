@@ -661,6 +661,23 @@ void expand_hop(Session* s, const WaveArgs& a) {
   }
 }
 
+// route a scope's launches to another stream of the session
+struct StreamScope {
+  Session* s;
+  cudaStream_t saved;
+  StreamScope(Session* s_, cudaStream_t to) : s(s_), saved(s_->st) { s->st = to; }
+  ~StreamScope() { s->st = saved; }
+};
+
+void ensure_side_stream(Session* s) {
+  if (s->side) return;
+  TH_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+  for (int i = 0; i < kMaxK + 2; ++i) {
+    TH_CUDA(cudaEventCreateWithFlags(&s->ev_expand[i], cudaEventDisableTiming));
+    TH_CUDA(cudaEventCreateWithFlags(&s->ev_mat[i], cudaEventDisableTiming));
+  }
+}
+
 template <int W>
 void run_wave(Session* s, const th_query* q, int q0, int nq) {
   const Graph* g = s->g;
@@ -741,6 +758,9 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   const bool want_a = q->flags & TH_WANT_ACTIVATED;
   const bool paths_need_l0 = (q->flags & TH_WANT_PATHS) && !(q->flags & TH_SINGLETON_SEEDS);
   const unsigned pg = persistent_grid();
+  const bool overlap = s->overlap && want_f && !want_a && !(q->flags & TH_WANT_PATHS) &&
+                       sem != TH_CUMULATIVE;
+  if (overlap) ensure_side_stream(s);
 
   int nplanes = 0;
   while (nplanes < 31 && (int64_t(1) << nplanes) <= g->max_out) ++nplanes;
@@ -783,6 +803,11 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
       else expand_hop<W, TH_FRONTIER, false>(s, a);
     }
     if (want_f) {
+      if (overlap) {
+        TH_CUDA(cudaEventRecord(s->ev_expand[h], st));
+        TH_CUDA(cudaStreamWaitEvent(s->side, s->ev_expand[h], 0));
+      }
+      StreamScope sc(s, overlap ? s->side : st);
       ProfScope ps(s, TH_PROF_FRONTIER);
       if (sem == TH_CUMULATIVE)
         materialize_dense<W>(s, b, b.V, b.S, b.Vf, nq, f_off + (h - 1) * B + q0,
@@ -802,9 +827,12 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
                              &b.ctl->ids_used, es);
         next_edges_done = es.out != nullptr;
       }
+      if (overlap) TH_CUDA(cudaEventRecord(s->ev_mat[h], s->side));
     }
     {
-      // retire X (rows of list segment h-1) and swap roles
+      // retire X (rows of list segment h-1) and swap roles; with overlap the
+      // layer's K4 (side stream) must be done reading it first
+      if (overlap && h > 1) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[h - 1], 0));
       ProfScope ps(s, TH_PROF_CLEAR);
       clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1);
       TH_LAUNCHED();
@@ -817,6 +845,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
     std::swap(a.Xf, a.Nf);
   }
   // leave every matrix zero for the next wave
+  if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k], 0));
   ProfScope ps(s, TH_PROF_CLEAR);
   clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, (int)k, (int)k);
   TH_LAUNCHED();
@@ -1078,6 +1107,15 @@ void session_free(Session* s) {
   cudaStreamSynchronize(s->st);
   for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
   s->ev_pool.clear();
+  if (s->side) {
+    cudaStreamSynchronize(s->side);
+    for (int i = 0; i < kMaxK + 2; ++i) {
+      cudaEventDestroy(s->ev_expand[i]);
+      cudaEventDestroy(s->ev_mat[i]);
+    }
+    cudaStreamDestroy(s->side);
+    s->side = nullptr;
+  }
 }
 
 // partition.py:80-84 multiplicative hash; -1 for entities without out-edges

@@ -40,6 +40,12 @@ struct Session {
   int64_t list_min_entities = int64_t(4) << 20;  // K4 list-driven above this E
   // shards: K4 covers rows [0, mat_rows) (owned entities) and maps rows /
   // local triples to global ids; defaults cover the whole single graph
+  // K4 of hop h overlaps hop h+1's expansion on a side stream (frontier-only
+  // runs; the main stream joins before it recycles the layer's rows)
+  bool overlap = true;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_expand[kMaxK + 2] = {};
+  cudaEvent_t ev_mat[kMaxK + 2] = {};
   int64_t mat_rows = -1;
   const int32_t* row_map = nullptr;
   const int32_t* tid_map = nullptr;

@@ -195,6 +195,10 @@ class Retriever:
         """K4 strategy knob: list-driven materialisation for graphs with >= n entities."""
         _lib.check(_lib.load().th_session_set_list_min_entities(self._handle, int(n)))
 
+    def set_overlap(self, on: bool) -> None:
+        """Overlap hop h's K4 with hop h+1's expansion (frontier-only runs)."""
+        _lib.check(_lib.load().th_session_set_overlap(self._handle, int(bool(on))))
+
     def launch_count(self) -> int:
         return int(_lib.load().th_session_launch_count(self._handle))
 
