@@ -47,6 +47,7 @@ extern "C" {
 #define TH_ERR_NOMEM 4    /* device allocation failed    -> MemoryError   */
 #define TH_ERR_OVERFLOW 5 /* result capacity too small: call th_run again  */
 #define TH_ERR_STATE 6    /* misuse of handles           -> RuntimeError  */
+#define TH_ERR_DATA 7     /* malformed archive payload   -> ArchiveError  */
 
 /* hop semantics, incidence.py:52-75 */
 #define TH_EXACT 0
@@ -78,6 +79,17 @@ int th_graph_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* 
                     int64_t n_triples, int64_t n_entities, int64_t n_relations,
                     uint32_t flags, void* stream, th_graph** out);
 int th_graph_destroy(th_graph* g);
+
+/* Build from the payload of an LKG1 archive (archive.py:1-24,66-133) copied
+ * verbatim to the device: d_indptr = u64[E+1] row offsets, d_tids = the
+ * row-ordered triple ids, d_obj / d_rel in triple-id order, each id_width
+ * (4 or 8) bytes.  The header and CRC32 are the host's job.  Structural
+ * errors (offsets, permutation, ranges, row order) return TH_ERR_DATA with
+ * the reference's message.  Synchronises `stream`. */
+int th_graph_create_lkg(const void* d_indptr, const void* d_tids, const void* d_obj,
+                        const void* d_rel, int32_t id_width, int64_t n_triples,
+                        int64_t n_entities, int64_t n_relations, uint32_t flags, void* stream,
+                        th_graph** out);
 
 typedef struct {
   int64_t n_entities, n_triples, n_relations;

@@ -21,6 +21,7 @@ from .core_types import (
     TripleVector,
     jaccard,
 )
+from .archive import graph_from_bytes, graph_to_bytes, load_graph, save_graph
 from .device_graph import IncidenceGraph, build_incidence
 from .errors import DataError, IntegrityError, TripleHopError, UsageError
 from .partition import (
@@ -37,8 +38,15 @@ from .partition import (
     route,
 )
 from .retriever import RetrievalResult, Retriever, k_hop, one_hop, reconstruct_paths, retrieve
+from .targets import GpuTarget, PartitionedGpuTarget
 
 __all__ = [
+    "GpuTarget",
+    "PartitionedGpuTarget",
+    "graph_from_bytes",
+    "graph_to_bytes",
+    "load_graph",
+    "save_graph",
     "UNASSIGNED",
     "DataError",
     "DistExchange",

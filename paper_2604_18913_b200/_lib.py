@@ -13,7 +13,8 @@ from pathlib import Path
 
 LIB_PATH = Path(os.environ.get("TH_B200_LIB", Path(__file__).resolve().parent / "lib" / "libth_b200.so"))
 
-TH_OK, TH_ERR_INVALID, TH_ERR_RANGE, TH_ERR_CUDA, TH_ERR_NOMEM, TH_ERR_OVERFLOW, TH_ERR_STATE = range(7)
+(TH_OK, TH_ERR_INVALID, TH_ERR_RANGE, TH_ERR_CUDA, TH_ERR_NOMEM, TH_ERR_OVERFLOW, TH_ERR_STATE,
+ TH_ERR_DATA) = range(8)
 TH_EXACT, TH_FRONTIER, TH_CUMULATIVE = 0, 1, 2
 TH_WANT_FRONTIERS, TH_WANT_ACTIVATED, TH_WANT_PATHS, TH_SINGLETON_SEEDS = 0x1, 0x2, 0x4, 0x8
 TH_GRAPH_NO_REVERSE = 0x1
@@ -21,7 +22,7 @@ ABI_VERSION = 1
 
 # every symbol include/th_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "th_abi_version", "th_last_error", "th_graph_create", "th_graph_destroy",
+    "th_abi_version", "th_last_error", "th_graph_create", "th_graph_create_lkg", "th_graph_destroy",
     "th_graph_info_get", "th_session_create", "th_session_destroy", "th_run", "th_finish",
     "th_session_set_pull_divisor", "th_session_launch_count", "th_plan_owner_hash",
     "th_session_set_list_min_entities", "th_session_set_overlap",
@@ -88,6 +89,9 @@ def load():
         "th_graph_create": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64,
                                            ctypes.c_int64, ctypes.c_uint32, _vp, ctypes.POINTER(_vp)]),
         "th_graph_destroy": (ctypes.c_int, [_vp]),
+        "th_graph_create_lkg": (ctypes.c_int, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int64,
+                                               ctypes.c_int64, ctypes.c_int64, ctypes.c_uint32, _vp,
+                                               ctypes.POINTER(_vp)]),
         "th_graph_info_get": (ctypes.c_int, [_vp, ctypes.POINTER(GraphInfo)]),
         "th_session_create": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(_vp)]),
         "th_session_destroy": (ctypes.c_int, [_vp]),
@@ -139,6 +143,10 @@ def check(rc: int) -> None:
         raise MemoryError(msg)
     if rc == TH_ERR_OVERFLOW:
         raise OverflowError(msg)
+    if rc == TH_ERR_DATA:
+        from .errors import ArchiveError
+
+        raise ArchiveError(msg)
     raise RuntimeError(f"th_b200 error {rc}: {msg}")
 
 

@@ -89,6 +89,46 @@ int th_graph_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* 
   });
 }
 
+int th_graph_create_lkg(const void* d_indptr, const void* d_tids, const void* d_obj,
+                        const void* d_rel, int32_t id_width, int64_t n_triples,
+                        int64_t n_entities, int64_t n_relations, uint32_t flags, void* stream,
+                        th_graph** out) {
+  return guarded([&]() -> int {
+    if (!out) {
+      th::set_error("out is NULL");
+      return TH_ERR_INVALID;
+    }
+    *out = nullptr;
+    if (id_width != 4 && id_width != 8) {
+      th::set_error("unsupported id width " + std::to_string(id_width));
+      return TH_ERR_DATA;
+    }
+    if (n_triples < 0 || n_entities < 0 || n_relations < 0) {
+      th::set_error("negative size");
+      return TH_ERR_INVALID;
+    }
+    if (n_triples >= INT32_MAX || n_entities >= INT32_MAX || n_relations > 65535) {
+      th::set_error("archive exceeds the device id space (int32 entities/triples, uint16 relations)");
+      return TH_ERR_INVALID;
+    }
+    if (!d_indptr || (n_triples > 0 && (!d_tids || !d_obj || !d_rel))) {
+      th::set_error("NULL payload array");
+      return TH_ERR_INVALID;
+    }
+    auto* h = new th_graph();
+    const int rc = th::graph_build_lkg(&h->g, d_indptr, d_tids, d_obj, d_rel, id_width, n_triples,
+                                       n_entities, n_relations, !(flags & TH_GRAPH_NO_REVERSE),
+                                       static_cast<cudaStream_t>(stream));
+    if (rc != TH_OK) {
+      th::graph_free(&h->g);
+      delete h;
+      return rc;
+    }
+    *out = h;
+    return TH_OK;
+  });
+}
+
 int th_graph_destroy(th_graph* g) {
   return guarded([&]() -> int {
     if (!g) return TH_OK;

@@ -47,4 +47,10 @@ int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int
                 int64_t obj_bound = -1);
 void graph_free(Graph* g);
 
+// LKG1 archive payload already on the device (archive.cu): narrow, validate
+// (TH_ERR_DATA + message on a structural error), recover subjects, build.
+int graph_build_lkg(Graph* g, const void* d_indptr, const void* d_tids, const void* d_obj,
+                    const void* d_rel, int width, int64_t T, int64_t E, int64_t R, bool reverse,
+                    cudaStream_t st);
+
 }  // namespace th

@@ -19,5 +19,25 @@ class DataError(TripleHopError):
     """Malformed input data."""
 
 
+class ArchiveError(DataError):
+    """Base for binary archive load failures (archive.py)."""
+
+
+class BadMagicError(ArchiveError):
+    """The file does not start with the LKG1 magic."""
+
+
+class VersionError(ArchiveError):
+    """Unsupported archive format version."""
+
+
+class TruncatedError(ArchiveError):
+    """The archive is shorter (or longer) than its header says."""
+
+
+class ChecksumError(ArchiveError):
+    """CRC32 mismatch over header + payload."""
+
+
 class IntegrityError(DataError):
     """Cross-rank inconsistency (plan/world mismatch, malformed exchange)."""

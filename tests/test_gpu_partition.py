@@ -120,3 +120,20 @@ def test_bad_partition_inputs(th):
         pg.retrieve([5], 0)
     with pytest.raises(ValueError):
         th.cross_graph_k_hop(th.EntityVector([1], 99), 2, pg)
+
+
+def test_bench_targets_expand_like_reference(th):
+    """GpuTarget / PartitionedGpuTarget answer the reference harness's
+    expand(frontier) (bench.py:98-137) with one device hop."""
+    s, r, o = _hub_graph(400, 3000, 6, seed=12)
+    E, R = 400, 6
+    og = orc.build_csr(s, r, o, E, R)
+    g = th.build_incidence((s, r, o), E, R)
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(2), n_hubs=3)
+    for tgt in (th.GpuTarget(g), th.PartitionedGpuTarget(pg, (s, r, o))):
+        assert (tgt.n_entities, tgt.n_triples) == (E, s.size)
+        for f in ([0, 5, 17], [3], list(range(0, 400, 7))):
+            act, nxt = tgt.expand(np.array(f))
+            ref_act, ref_nxt = orc.raw_hop(og, np.array(f, dtype=np.int64))
+            assert np.array_equal(act, ref_act) and np.array_equal(nxt, ref_nxt)
+        assert len(tgt.triples()) == s.size
