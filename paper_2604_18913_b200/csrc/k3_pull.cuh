@@ -100,39 +100,84 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
     int maxlen = len;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(TH_FULL, maxlen, o));
-    for (int e0 = 0; e0 < maxlen; e0 += 4) {
-      int32_t u[4];
-      uint32_t rr[4];
-      bool act[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        act[k] = !done && e0 + k < len;
-        u[k] = act[k] ? __ldg(a.rsrc + lo + e0 + k) : 0;
-        rr[k] = (FILTER && act[k]) ? (uint32_t)__ldg(a.rrel + lo + e0 + k) : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (act[k]) act[k] = (__ldg(a.Xf + (u[k] >> 5)) >> (u[k] & 31)) & 1u;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (act[k]) {
-          uint32_t x[VEC];
-          ldg_words<VEC>(a.X + (size_t)u[k] * W + part * VEC, x);
-          if (FILTER) {
-            uint32_t m[VEC];
-            ldg_words<VEC>(a.M + (size_t)rr[k] * W + part * VEC, m);
-#pragma unroll
-            for (int c = 0; c < VEC; ++c) x[c] &= m[c];
-          }
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
+    if constexpr (LPR >= 4) {
+      // LPR in-edges per step: lane p of a group loads edge e0+p and tests
+      // its frontier flag (coalesced, no redundant loads), the group's
+      // active edges are compacted with one __fns per lane, then their
+      // frontier rows are loaded back to back (up to LPR loads in flight)
+      for (int e0 = 0; e0 < maxlen; e0 += LPR) {
+        const int ei = e0 + part;
+        bool act = !done && ei < len;
+        int32_t u = 0;
+        uint32_t rr = 0u;
+        if (act) {
+          u = __ldg(a.rsrc + lo + ei);
+          if (FILTER) rr = (uint32_t)__ldg(a.rrel + lo + ei);
+          act = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
         }
-      }
-      bool full = true;
+        const unsigned gm = (__ballot_sync(TH_FULL, act) & gbits) >> (grp * LPR);
+        const int cnt = __popc(gm);
+        const int srcp = part < cnt ? (int)__fns(gm, 0, part + 1) : 0;
+        const int32_t uc = __shfl_sync(TH_FULL, u, grp * LPR + srcp);
+        const uint32_t rc = FILTER ? __shfl_sync(TH_FULL, rr, grp * LPR + srcp) : 0u;
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) full &= ((acc[c] | seen[c]) & valid[c]) == valid[c];
-      if ((__ballot_sync(TH_FULL, full) & gbits) == gbits) done = true;
-      if (__all_sync(TH_FULL, done)) break;
+        for (int it = 0; it < LPR; ++it) {
+          const int32_t uu = __shfl_sync(TH_FULL, uc, grp * LPR + it);
+          const uint32_t r2 = FILTER ? __shfl_sync(TH_FULL, rc, grp * LPR + it) : 0u;
+          if (it < cnt) {
+            uint32_t x[VEC];
+            ldg_words<VEC>(a.X + (size_t)uu * W + part * VEC, x);
+            if (FILTER) {
+              uint32_t m[VEC];
+              ldg_words<VEC>(a.M + (size_t)r2 * W + part * VEC, m);
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) x[c] &= m[c];
+            }
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
+          }
+        }
+        bool full = true;
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) full &= ((acc[c] | seen[c]) & valid[c]) == valid[c];
+        if ((__ballot_sync(TH_FULL, full) & gbits) == gbits) done = true;
+        if (__all_sync(TH_FULL, done)) break;
+      }
+    } else {
+      for (int e0 = 0; e0 < maxlen; e0 += 4) {
+        int32_t u[4];
+        uint32_t rr[4];
+        bool act[4];
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          act[k] = !done && e0 + k < len;
+          u[k] = act[k] ? __ldg(a.rsrc + lo + e0 + k) : 0;
+          rr[k] = (FILTER && act[k]) ? (uint32_t)__ldg(a.rrel + lo + e0 + k) : 0u;
+        }
+  #pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (act[k]) act[k] = (__ldg(a.Xf + (u[k] >> 5)) >> (u[k] & 31)) & 1u;
+  #pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (act[k]) {
+            uint32_t x[VEC];
+            ldg_words<VEC>(a.X + (size_t)u[k] * W + part * VEC, x);
+            if (FILTER) {
+              uint32_t m[VEC];
+              ldg_words<VEC>(a.M + (size_t)rr[k] * W + part * VEC, m);
+  #pragma unroll
+              for (int c = 0; c < VEC; ++c) x[c] &= m[c];
+            }
+  #pragma unroll
+            for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
+          }
+        }
+        bool full = true;
+  #pragma unroll
+        for (int c = 0; c < VEC; ++c) full &= ((acc[c] | seen[c]) & valid[c]) == valid[c];
+        if ((__ballot_sync(TH_FULL, full) & gbits) == gbits) done = true;
+        if (__all_sync(TH_FULL, done)) break;
+      }
     }
     uint32_t nb[VEC];
     bool any = false;
