@@ -326,16 +326,40 @@ __global__ void __launch_bounds__(kThreads) edge_count_filtered_kernel(WaveArgs 
 
 // ------------------------------------------------------------- clearing
 
-// zero rows listed in list segments [s0, s1] of matrix A
+// zero rows listed in list segments [s0, s1] of matrix A (nrows rows); when
+// the segments cover more than half of the rows, one streaming memset of the
+// whole matrix is cheaper than the row gathers
 template <int W>
-__global__ void clear_rows_kernel(uint32_t* A, const int32_t* lists, const Ctl* ctl, int s0, int s1) {
+__global__ void clear_rows_kernel(uint32_t* A, const int32_t* lists, const Ctl* ctl, int s0, int s1,
+                                  int64_t nrows) {
   const int64_t lo = ctl->list_off[s0];
   const int64_t hi = ctl->list_off[s1] + ctl->list_len[s1];
-  const int64_t n = (hi - lo) * W;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t u = lists[lo + i / W];
-    A[(size_t)u * W + (i % W)] = 0u;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if ((hi - lo) * 2 > nrows) {
+    if constexpr (W % 4 == 0) {
+      uint4* p = reinterpret_cast<uint4*>(A);
+      const int64_t n = nrows * (W / 4);
+      for (int64_t i = t0; i < n; i += stride) p[i] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      const int64_t n = nrows * W;
+      for (int64_t i = t0; i < n; i += stride) A[i] = 0u;
+    }
+    return;
+  }
+  if constexpr (W % 4 == 0) {
+    constexpr int Q = W / 4;  // 16-byte stores per row
+    const int64_t n = (hi - lo) * Q;
+    for (int64_t i = t0; i < n; i += stride) {
+      const int32_t u = lists[lo + i / Q];
+      reinterpret_cast<uint4*>(A + (size_t)u * W)[i % Q] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  } else {
+    const int64_t n = (hi - lo) * W;
+    for (int64_t i = t0; i < n; i += stride) {
+      const int32_t u = lists[lo + i / W];
+      A[(size_t)u * W + (i % W)] = 0u;
+    }
   }
 }
 
@@ -834,7 +858,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
       // layer's K4 (side stream) must be done reading it first
       if (overlap && h > 1) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[h - 1], 0));
       ProfScope ps(s, TH_PROF_CLEAR);
-      clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1);
+      clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1, E);
       TH_LAUNCHED();
       TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
       s->launches += 1;
@@ -847,16 +871,16 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   // leave every matrix zero for the next wave
   if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k], 0));
   ProfScope ps(s, TH_PROF_CLEAR);
-  clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, (int)k, (int)k);
+  clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, (int)k, (int)k, E);
   TH_LAUNCHED();
   s->launches += 1;
   if (sem != TH_EXACT) {
-    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k);
+    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k, E);
     TH_LAUNCHED();
     s->launches += 1;
   }
   if (sem == TH_CUMULATIVE) {
-    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0);
+    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0, E);
     TH_LAUNCHED();
     s->launches += 1;
   }
@@ -1425,7 +1449,7 @@ void shard_end_hop_w(Shard* sh, int h) {
   }
   {
     ProfScope ps(s, TH_PROF_CLEAR);
-    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1);
+    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1, rows);
     TH_LAUNCHED();
     TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
     s->launches += 1;
@@ -1443,14 +1467,14 @@ void shard_retire_w(Shard* sh) {
   const int k = q.k;
   WaveBufs b = shard_bufs<W>(sh);
   const int64_t rows = std::max<int64_t>(sh->rows(), 1);
-  clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, k, k);
+  clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, k, k, rows);
   TH_LAUNCHED();
   if (q.semantics != TH_EXACT) {
-    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, k);
+    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, k, rows);
     TH_LAUNCHED();
   }
   if (q.semantics == TH_CUMULATIVE) {
-    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0);
+    clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0, rows);
     TH_LAUNCHED();
   }
   s->launches += 3;
