@@ -13,7 +13,7 @@ HEADER = ROOT / "include" / "th_b200.h"
 
 def header_symbols():
     text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(th_[a-z_]+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(th_[a-z_0-9]+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_binding_list():
