@@ -136,11 +136,61 @@ constexpr int mat_warps() {
 constexpr unsigned kSparseBits = 5;       // tiles with <= this many bits per lane skip the transpose
 constexpr unsigned kCoopIdsPerQuery = 48;  // chunk ids per touched query for the cooperative write
 
-// per-warp shared words: WRITE = S (32 x kSStride) + staging run (kChunkRows
-// ids); COUNT = per-query id counters + degree sums (2 x 32)
+// sparse-chunk staging: a 64-slot ring per query (lane), flushed by the
+// whole warp 32 ids at a time so every store is a full coalesced run (no
+// scattered 4-byte stores, whose partially written sectors cost DRAM fills)
+constexpr int kRing = 64;
+constexpr int kRingStride = kRing + 1;
+constexpr int kRingWords = 32 * kRingStride;
+
+// per-warp shared words: WRITE = S (32 x kSStride) + a region shared by the
+// dense-chunk staging run (kChunkRows ids) and the sparse-chunk rings
+// (emptied before a dense chunk); COUNT = per-query counters + degree sums
 template <bool WRITE>
 constexpr size_t mat_warp_words() {
-  return WRITE ? (size_t)(32 * kSStride + kChunkRows) : 64;
+  return WRITE ? (size_t)(32 * kSStride + (kChunkRows > kRingWords ? kChunkRows : kRingWords)) : 64;
+}
+
+// lanes whose ring holds >= 32 ids store 32 of them (all 32 lanes, converged)
+__device__ __forceinline__ void ring_flush_full(const int32_t* ring, int& head, int& fill,
+                                                int64_t& pos, int32_t* out, int64_t cap) {
+  const unsigned lane = lane_id();
+  unsigned need = __ballot_sync(TH_FULL, fill >= 32);
+  while (need) {
+    const int b = __ffs(need) - 1;
+    need &= need - 1u;
+    const int hb = __shfl_sync(TH_FULL, head, b);
+    const int64_t pb = __shfl_sync(TH_FULL, pos, b);
+    const int32_t id = ring[b * kRingStride + ((hb + (int)lane) & (kRing - 1))];
+    if (pb + (int64_t)lane < cap) out[pb + lane] = id;
+    if ((int)lane == b) {
+      head = (head + 32) & (kRing - 1);
+      fill -= 32;
+      pos += 32;
+    }
+  }
+}
+
+// every lane's remaining (< 32) ids
+__device__ __forceinline__ void ring_flush_all(const int32_t* ring, int& head, int& fill,
+                                               int64_t& pos, int32_t* out, int64_t cap) {
+  const unsigned lane = lane_id();
+  unsigned need = __ballot_sync(TH_FULL, fill > 0);
+  while (need) {
+    const int b = __ffs(need) - 1;
+    need &= need - 1u;
+    const int nb = __shfl_sync(TH_FULL, fill, b);
+    const int hb = __shfl_sync(TH_FULL, head, b);
+    const int64_t pb = __shfl_sync(TH_FULL, pos, b);
+    if ((int)lane < nb && pb + (int64_t)lane < cap)
+      out[pb + lane] = ring[b * kRingStride + ((hb + (int)lane) & (kRing - 1))];
+    if ((int)lane == b) {
+      head = (head + nb) & (kRing - 1);
+      fill = 0;
+      pos += nb;
+    }
+  }
+  __syncwarp();
 }
 
 template <int W, bool WRITE>
@@ -189,6 +239,8 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
   // WRITE: S[32][kSStride] + staging run; COUNT: per-query counters
   uint32_t* S = mat_smem + (size_t)warp * (mat_warp_words<WRITE>());
   int32_t* stg = reinterpret_cast<int32_t*>(S + 32 * kSStride);
+  int32_t* ring = stg;  // sparse chunks (empty whenever stg is in use)
+  int head = 0, fill = 0;
   uint32_t* cnt = S;        // COUNT: [32] ids per query (sparse tiles)
   uint32_t* ecnt = S + 32;  // COUNT+EDGES: [32] degree sums per query (sparse tiles)
   if (!WRITE) {
@@ -285,24 +337,25 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
     // ---- WRITE.  Dense chunks (many ids per query): query by query, lane
     // t extracts tile t's rows into a staging run stored coalesced.  Sparse
     // chunks (a few ids per query, e.g. the C4 layers): every lane walks its
-    // own query's 32 tile masks and stores its ids directly -- one pass per
-    // chunk instead of a scan + copy per query.
+    // own query's 32 tile masks into its ring, and full rings are stored 32
+    // ids at a time by the whole warp.
     const unsigned ids = __reduce_add_sync(TH_FULL, nbits);
     if (ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
-      if (q < src.nq) {
-        for (int t = 0; t < 32; ++t) {
-          uint32_t m = S[lane * kSStride + t];
-          const int64_t rb = c0 + 32 * t;
-          while (m) {
-            if (pos < cap) out[pos] = src.id(rb + __ffs(m) - 1);
-            ++pos;
-            m &= m - 1u;
-          }
+      for (int t = 0; t < 32; ++t) {
+        uint32_t m = q < src.nq ? S[lane * kSStride + t] : 0u;
+        const int64_t rb = c0 + 32 * t;
+        while (m) {
+          ring[lane * kRingStride + ((head + fill) & (kRing - 1))] = src.id(rb + __ffs(m) - 1);
+          ++fill;
+          m &= m - 1u;
         }
+        __syncwarp();
+        ring_flush_full(ring, head, fill, pos, out, cap);
       }
       __syncwarp();
       continue;
     }
+    ring_flush_all(ring, head, fill, pos, out, cap);  // keep order; frees stg
     unsigned todo = touched;
     while (todo) {
       const int b = __ffs(todo) - 1;
@@ -334,6 +387,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
       __syncwarp();
     }
   }
+  if (WRITE) ring_flush_all(ring, head, fill, pos, out, cap);
   if (!WRITE) {
     __syncwarp();
     total += (int32_t)cnt[lane];
