@@ -194,6 +194,7 @@ __device__ __forceinline__ void row_pairs(const WaveArgs& a, int32_t u, int32_t 
 template <int W, int SEM>
 struct PushOp {
   static constexpr bool kAppends = true;
+  static constexpr bool kRowWise = false;
   const WaveArgs& a;
   // returns true when v entered the next layer's list through this lane
   __device__ __forceinline__ bool operator()(int32_t v, int j, uint32_t w) const {
@@ -215,13 +216,30 @@ struct PushOp {
 template <int W>
 struct CountOp {
   static constexpr bool kAppends = false;
+  static constexpr bool kRowWise = true;
   uint32_t* sc;
-  __device__ __forceinline__ bool operator()(int32_t, int j, uint32_t w) const {
-    while (w) {
-      atomicAdd(&sc[32 * j + __ffs(w) - 1], 1u);
-      w &= w - 1u;
+  // Filtered |T_h(q)| over CSR slots [lo, hi) of frontier row u: per nonzero
+  // frontier word j, 32 edges at a time, lane i holds the passing queries of
+  // edge i (x_j & M[rel_i]); a 32x32 bit transpose hands lane b the edges
+  // query 32j+b keeps, so one popcount + one shared atomic per lane per 32
+  // edges replaces one atomic per (query, edge).
+  template <int W_>
+  __device__ __forceinline__ void row(const WaveArgs& a, int32_t u, int32_t lo, int32_t hi) const {
+    const unsigned lane = lane_id();
+    const uint32_t xw = lane < (unsigned)W_ ? a.X[(size_t)u * W_ + lane] : 0u;
+    unsigned nz = __ballot_sync(TH_FULL, xw != 0u);
+    while (nz) {
+      const int j = __ffs(nz) - 1;
+      nz &= nz - 1u;
+      const uint32_t x = __shfl_sync(TH_FULL, xw, j);
+      for (int32_t e0 = lo; e0 < hi; e0 += 32) {
+        const int32_t e = e0 + (int32_t)lane;
+        const uint32_t w = e < hi ? x & a.M[(size_t)a.csr_rel[e] * W_ + j] : 0u;
+        if (!__any_sync(TH_FULL, w != 0u)) continue;
+        const int c = __popc(transpose32(w));
+        if (c) atomicAdd(&sc[32 * j + lane], (uint32_t)c);
+      }
     }
-    return false;
   }
 };
 
@@ -239,7 +257,8 @@ __device__ void drive_light(const WaveArgs& a, int seg, Op& op, bool build_heavy
       if (build_heavy && lane_id() == 0) a.heavy[atomicAdd(&a.ctl->heavy_len, 1)] = u;
       continue;
     }
-    row_pairs<W, FILTER>(a, u, lo, hi, op);
+    if constexpr (Op::kRowWise) op.template row<W>(a, u, lo, hi);
+    else row_pairs<W, FILTER>(a, u, lo, hi, op);
   }
 }
 
@@ -257,7 +276,8 @@ __device__ void drive_heavy(const WaveArgs& a, Op& op) {
     int64_t c = ((gw - base) % nw + nw) % nw;
     for (; c < nc; c += nw) {
       const int32_t clo = lo + (int32_t)c * kPushChunk;
-      row_pairs<W, FILTER>(a, u, clo, min(hi, clo + kPushChunk), op);
+      if constexpr (Op::kRowWise) op.template row<W>(a, u, clo, min(hi, clo + kPushChunk));
+      else row_pairs<W, FILTER>(a, u, clo, min(hi, clo + kPushChunk), op);
     }
     base += nc;
   }
