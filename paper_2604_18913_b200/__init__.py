@@ -33,6 +33,7 @@ from .partition import (
     RouteResult,
     ShardPlan,
     cross_graph_k_hop,
+    cross_graph_paths,
     plan_partitions,
     plan_sharding,
     route,
@@ -59,6 +60,7 @@ __all__ = [
     "TripleHopError",
     "UsageError",
     "cross_graph_k_hop",
+    "cross_graph_paths",
     "plan_partitions",
     "plan_sharding",
     "route",

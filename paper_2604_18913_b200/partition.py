@@ -550,6 +550,11 @@ class PartitionedGraph:
         self.n_entities = int(n_entities)
         self.n_relations = int(n_relations)
         self.n_triples = int(len(subj))
+        # host copy of the columns: cross_graph_paths gathers the (s, r, o)
+        # of a query's activated triples from it (the reference keeps its
+        # shards on disk and maps tids through tid_to_global the same way)
+        self._cols = tuple(np.asarray(c.cpu().numpy() if hasattr(c, "cpu") else c, dtype=np.int32)
+                           for c in cols)
         factory = shard_factory or GraphShard
         self.shards = [factory(cols, n_entities, n_relations, plan, r) for r in exchange.ranks]
 
@@ -627,3 +632,37 @@ def cross_graph_k_hop(q0: EntityVector, k: int, pg: PartitionedGraph,
         steps.append(HopStep(EntityVector(m["f_ids"][fo:fo + fl], pg.n_entities, _canonical_ids=True),
                              TripleVector(m["a_ids"][ao:ao + al], pg.n_triples, _canonical_ids=True)))
     return HopTrace(sem, q0, steps)
+
+
+def cross_graph_paths(q0: EntityVector, k: int, pg: PartitionedGraph,
+                      max_paths: int | None = 10_000):
+    """All length-k walks from q0 across the partitions, lexicographic in the
+    triple ids, capped (engine.py:157-182 -> assemble_paths).
+
+    Every step of a walk is a triple activated at its hop under exact-walk
+    semantics, so the walks of the full graph are exactly the walks of the
+    subgraph of activated triples.  The partitioned exact-walk trace
+    supplies those triples; their subgraph (local tids a monotone renumbering
+    of the global ones, the reference's tid_to_global idea,
+    partition.py:145-153) is enumerated by the device path kernel (K5) and
+    mapped back -- identical paths, order and truncation flag.
+    """
+    from .core_types import PathResult
+    from .device_graph import build_incidence
+    from .retriever import reconstruct_paths
+
+    if q0.width != pg.n_entities:
+        raise ValueError(f"query width {q0.width} != graph entity count {pg.n_entities}")
+    if k < 1:
+        raise ValueError("hop count must be >= 1")
+    if max_paths is not None and max_paths < 0:
+        raise ValueError("max_paths must be >= 0")
+    tr = cross_graph_k_hop(q0, k, pg, HopSemantics.EXACT_WALK)
+    act = [tr.activated(h).ids for h in range(1, k + 1)]
+    tids = np.unique(np.concatenate(act)) if act else np.empty(0, np.int64)
+    s, r, o = (c[tids] for c in pg._cols)
+    sub = build_incidence((s, r, o), pg.n_entities, pg.n_relations)
+    res = reconstruct_paths(q0, k, sub, max_paths)
+    # entity and relation ids are global in the subgraph, so its Triples are
+    # the full graph's
+    return PathResult(res.paths, res.truncated)

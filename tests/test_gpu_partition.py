@@ -137,3 +137,23 @@ def test_bench_targets_expand_like_reference(th):
             ref_act, ref_nxt = orc.raw_hop(og, np.array(f, dtype=np.int64))
             assert np.array_equal(act, ref_act) and np.array_equal(nxt, ref_nxt)
         assert len(tgt.triples()) == s.size
+
+
+@pytest.mark.parametrize("name", ["tiny", "er30_s1", "pl500_hubs", "interleave", "selfloop"])
+def test_cross_graph_paths_golden(th, name):
+    """Paths across partitions == the reference's reconstruct_paths goldens
+    (engine.py:157-182 / test_engine.py:99-123: cross paths == single paths)."""
+    case = load_case(GOLDEN / f"{name}.npz")
+    pg = th.PartitionedGraph((case.subj, case.rel, case.obj), case.n_entities, case.n_relations,
+                             th.LoopbackExchange(3), n_hubs=2)
+    n = 0
+    for q in case.queries:
+        if not q.want_paths or q.relations is not None:
+            continue
+        pr = th.cross_graph_paths(th.EntityVector(q.seeds, case.n_entities), q.k, pg, q.max_paths)
+        want = [tuple(th.Triple(int(case.subj[t]), int(case.rel[t]), int(case.obj[t])) for t in p)
+                for p in q.paths]
+        assert pr.paths == want, (name, q.seeds, q.max_paths)
+        assert pr.truncated == q.truncated
+        n += 1
+    assert n > 0
