@@ -614,7 +614,7 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   }
   constexpr int NW = mat_warps<W>();
   constexpr int NG = W / NW;
-  constexpr size_t smem_w = mat_smem_bytes<W, true>();
+  constexpr size_t smem_w = mat_smem_bytes<W, true, Src::kRing>();
   static bool attr_done = false;  // one per template instantiation
   if (!attr_done) {
     TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, true>,

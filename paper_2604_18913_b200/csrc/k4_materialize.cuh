@@ -35,6 +35,7 @@ struct DenseSrc {
   int nq;
   const int32_t* map = nullptr;  // optional row -> output id (ascending), e.g. shard local -> global
   static constexpr bool kDense = true;
+  static constexpr bool kRing = false;
   // lane t: flags of rows [r0+32t, r0+32t+32) below `rend` (r0 % 32 == 0)
   __device__ __forceinline__ uint32_t chunk_flags(int64_t r0, int64_t rend) const {
     const int64_t t0 = r0 + 32 * (int64_t)lane_id();
@@ -75,6 +76,7 @@ struct ListSrc {
   int nq;
   const int32_t* map = nullptr;
   static constexpr bool kDense = true;
+  static constexpr bool kRing = true;
   __device__ __forceinline__ uint32_t chunk_flags(int64_t r0, int64_t rend) const {
     const int64_t t0 = r0 + 32 * (int64_t)lane_id();
     if (t0 >= rend) return 0u;
@@ -107,6 +109,7 @@ struct TripleSrc {
   int nq;
   const int32_t* map = nullptr;  // local triple -> global tid (shards)
   static constexpr bool kDense = false;
+  static constexpr bool kRing = false;
   __device__ __forceinline__ bool chunk_any(int64_t, int64_t) const { return true; }
   __device__ __forceinline__ uint32_t prep(int64_t r0, int64_t& aux) const {
     const int64_t t = r0 + lane_id();
@@ -146,9 +149,10 @@ constexpr int kRingWords = 32 * kRingStride;
 // per-warp shared words: WRITE = S (32 x kSStride) + a region shared by the
 // dense-chunk staging run (kChunkRows ids) and the sparse-chunk rings
 // (emptied before a dense chunk); COUNT = per-query counters + degree sums
-template <bool WRITE>
+template <bool WRITE, bool RING = false>
 constexpr size_t mat_warp_words() {
-  return WRITE ? (size_t)(32 * kSStride + (kChunkRows > kRingWords ? kChunkRows : kRingWords)) : 64;
+  return WRITE ? (size_t)(32 * kSStride + (RING && kRingWords > kChunkRows ? kRingWords : kChunkRows))
+               : 64;
 }
 
 // lanes whose ring holds >= 32 ids store 32 of them (all 32 lanes, converged)
@@ -193,9 +197,9 @@ __device__ __forceinline__ void ring_flush_all(const int32_t* ring, int& head, i
   __syncwarp();
 }
 
-template <int W, bool WRITE>
+template <int W, bool WRITE, bool RING = false>
 constexpr size_t mat_smem_bytes() {
-  return (size_t)mat_warps<W>() * mat_warp_words<WRITE>() * sizeof(uint32_t);
+  return (size_t)mat_warps<W>() * mat_warp_words<WRITE, RING>() * sizeof(uint32_t);
 }
 
 // EDGES (COUNT pass over an entity layer): also sum the out-degrees of each
@@ -237,7 +241,10 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
   const int q = 32 * j + lane;
   if (blk >= nblk) return;
   // WRITE: S[32][kSStride] + staging run; COUNT: per-query counters
-  uint32_t* S = mat_smem + (size_t)warp * (mat_warp_words<WRITE>());
+  // rings (sparse chunks of large, list-driven layers) need more staging
+  // space; small graphs write sparse chunks directly and keep 6 CTAs/SM
+  constexpr bool RING = Src::kRing;
+  uint32_t* S = mat_smem + (size_t)warp * (mat_warp_words<WRITE, RING>());
   int32_t* stg = reinterpret_cast<int32_t*>(S + 32 * kSStride);
   int32_t* ring = stg;  // sparse chunks (empty whenever stg is in use)
   int head = 0, fill = 0;
@@ -340,7 +347,22 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
     // own query's 32 tile masks into its ring, and full rings are stored 32
     // ids at a time by the whole warp.
     const unsigned ids = __reduce_add_sync(TH_FULL, nbits);
-    if (ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
+    if (!RING && ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
+      if (q < src.nq) {
+        for (int t = 0; t < 32; ++t) {
+          uint32_t m = S[lane * kSStride + t];
+          const int64_t rb = c0 + 32 * t;
+          while (m) {
+            if (pos < cap) out[pos] = src.id(rb + __ffs(m) - 1);
+            ++pos;
+            m &= m - 1u;
+          }
+        }
+      }
+      __syncwarp();
+      continue;
+    }
+    if (RING && ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
       for (int t = 0; t < 32; ++t) {
         uint32_t m = q < src.nq ? S[lane * kSStride + t] : 0u;
         const int64_t rb = c0 + 32 * t;
@@ -355,7 +377,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
       __syncwarp();
       continue;
     }
-    ring_flush_all(ring, head, fill, pos, out, cap);  // keep order; frees stg
+    if (RING) ring_flush_all(ring, head, fill, pos, out, cap);  // keep order; frees stg
     unsigned todo = touched;
     while (todo) {
       const int b = __ffs(todo) - 1;
@@ -387,7 +409,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
       __syncwarp();
     }
   }
-  if (WRITE) ring_flush_all(ring, head, fill, pos, out, cap);
+  if (WRITE && RING) ring_flush_all(ring, head, fill, pos, out, cap);
   if (!WRITE) {
     __syncwarp();
     total += (int32_t)cnt[lane];
