@@ -267,6 +267,10 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
   const int64_t rend = nrows < r_begin + blk_rows ? nrows : r_begin + blk_rows;
   for (int64_t c0 = r_begin; c0 < rend; c0 += kChunkRows) {
     if (!src.chunk_any(c0, rend)) continue;
+    // keep the CTA's warps (words of the same rows) on the same chunk so
+    // each row sector they share is fetched from L2 once and hit in L1
+    // by the others (the write phase otherwise drifts them apart)
+    if (WRITE && NW > 1) __syncthreads();
     // ---- A: tile masks of this chunk, S[b][t] = rows of tile t in query b.
     // Loads of 8 tiles are issued before their transposes (memory-level
     // parallelism); dense sources get all 32 tile flags from one load.
