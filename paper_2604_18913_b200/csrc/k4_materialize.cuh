@@ -21,7 +21,7 @@
 // append with ring flushes.
 #pragma once
 
-constexpr int kMatWordsPerCta = 4;          // warps per CTA (one row word each)
+constexpr int kMatWordsPerCta = 8;          // warps per CTA (one row word each)
 constexpr int kChunkRows = 1024;            // 32 tiles of 32 rows
 constexpr int kSStride = 33;                // S[b][t] row stride (bank-conflict free)
 
