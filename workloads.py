@@ -29,6 +29,12 @@ C4  54.4M entities / exactly 86.5M distinct triples / 1,000 uniform
     popular objects (a hub core, as in C2; independent permutations leave
     the hubs unreachable, with k=3 frontiers of a few entities per seed).
     Duplicates are topped up to exactly T; triple order is shuffled.
+C5  200M entities / exactly 1e9 distinct triples / 2,000 uniform relations,
+    R-MAT(a=.57, b=.19, c=.19, d=.05) at scale 2^28 with ids >= 2e8
+    rejected, then one random id permutation; 16,384 seeds with per-seed
+    64-of-2,000 relation masks.  Generated on the GPU with torch (numpy
+    would need ~60 GB and minutes); deterministic for a given seed on a
+    given device and software stack.
 """
 
 
@@ -181,3 +187,76 @@ def c4_graph(seed: int = 4):
     E, T, R = C4_DIMS
     s, r, o = powerlaw_graph(E, T, R, seed)
     return s, r, o, E, R
+
+
+C5_DIMS = (200_000_000, 1_000_000_000, 2_000)
+
+
+def rmat_graph_gpu(n_entities: int, n_triples: int, n_relations: int, seed: int = 5,
+                   abcd=(0.57, 0.19, 0.19, 0.05), chunk: int = 1 << 27, device="cuda"):
+    """Exactly ``n_triples`` distinct R-MAT triples as int32 CUDA tensors."""
+    import torch
+
+    E, T, R = n_entities, n_triples, n_relations
+    scale = max(1, (E - 1).bit_length())
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    a, b, c, _ = abcd
+    cut = torch.tensor([a, a + b, a + b + c], device=device, dtype=torch.float32)
+
+    def draw(n):
+        s = torch.zeros(n, dtype=torch.int64, device=device)
+        o = torch.zeros(n, dtype=torch.int64, device=device)
+        for _ in range(scale):
+            u = torch.rand(n, generator=gen, device=device)
+            q = torch.bucketize(u, cut)  # 0..3 = quadrant (a, b, c, d)
+            s = (s << 1) | (q >> 1)
+            o = (o << 1) | (q & 1)
+        keep = (s < E) & (o < E)
+        return s[keep], o[keep]
+
+    perm = torch.randperm(E, generator=gen, device=device)
+    parts_s, parts_o, parts_r, got = [], [], [], 0
+    target = int(T * 1.05)
+    while True:
+        while got < target:
+            s, o = draw(chunk)
+            parts_s.append(perm[s].to(torch.int32))
+            parts_o.append(perm[o].to(torch.int32))
+            parts_r.append(torch.randint(0, R, (s.numel(),), generator=gen, device=device,
+                                         dtype=torch.int32))
+            got += s.numel()
+        s = torch.cat(parts_s)
+        o = torch.cat(parts_o)
+        r = torch.cat(parts_r)
+        parts_s, parts_o, parts_r = [s], [o], [r]
+        # distinct (s, r, o): stable sort by r, then by (s, o) -> lexicographic
+        key = (s.to(torch.int64) << 28) | o.to(torch.int64)
+        order = torch.sort(r, stable=True).indices
+        order = order[torch.sort(key[order], stable=True).indices]
+        ks, rs = key[order], r[order]
+        first = torch.ones(ks.numel(), dtype=torch.bool, device=device)
+        first[1:] = (ks[1:] != ks[:-1]) | (rs[1:] != rs[:-1])
+        idx = order[first]
+        del key, order, ks, rs, first
+        if idx.numel() >= T:
+            break
+        target = got + int((T - idx.numel()) * 1.5) + chunk // 4  # top up and re-deduplicate
+        del idx
+    # exactly T: a random subset, in random triple order
+    pick = torch.randperm(idx.numel(), generator=gen, device=device)[:T]
+    idx = idx[pick]
+    return s[idx].contiguous(), r[idx].contiguous(), o[idx].contiguous()
+
+
+def c5_graph_gpu(seed: int = 5):
+    E, T, R = C5_DIMS
+    s, r, o = rmat_graph_gpu(E, T, R, seed)
+    return s, r, o, E, R
+
+
+def c5_queries(n_entities: int, n_relations: int, seed: int = 6, n: int = 16_384, mask_size: int = 64):
+    rng = np.random.default_rng(seed)
+    seeds = rng.choice(n_entities, n, replace=False).astype(np.int32)
+    masks = np.argsort(rng.random((n, n_relations)), axis=1)[:, :mask_size]
+    return seeds, masks
