@@ -309,9 +309,18 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
           if (EDGES) {
             const uint32_t d =
                 ((fl[u] >> lane) & 1u) ? degree(es, src.id(r)) : 0u;
-            const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d));
+            // low 8 bits by bit planes (one ballot each); the rare rows of
+            // degree >= 256 add their high part row by row
+            const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d & 0xffu));
             for (int k = 0; k < np; ++k)
               esum += (unsigned long long)__popc(m & __ballot_sync(TH_FULL, (d >> k) & 1u)) << k;
+            unsigned big = __ballot_sync(TH_FULL, d > 0xffu);
+            while (big) {
+              const int i = __ffs(big) - 1;
+              big &= big - 1u;
+              const uint32_t hi = __shfl_sync(TH_FULL, d >> 8, i);
+              if ((m >> i) & 1u) esum += (unsigned long long)hi << 8;
+            }
           }
           if (WRITE) {
             S[lane * kSStride + t] = m;
