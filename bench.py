@@ -46,6 +46,19 @@ BATCH = 1024
 
 # ----------------------------------------------------------------- helpers
 
+def load_traffic(group: str) -> dict:
+    """DRAM bytes per step of a kernel group from the latest committed ncu
+    capture of one C2 k=3 step (profiles/r*_c2_traffic.json, written by
+    tools/ncu_traffic.py from `ncu --set full`)."""
+    files = sorted((ROOT / "profiles").glob("r*_c2_traffic.json"))
+    if not files:
+        return {}
+    d = json.loads(files[-1].read_text())
+    if group not in d:
+        return {}
+    return {"bytes": d[group]["bytes"], "source": f"{files[-1].name} (ncu --set full, one step)"}
+
+
 def load_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -502,6 +515,7 @@ def run_ours(args, world, rank, local):
         note = "push hop lower bound: 4 B object id per traversed (seed,edge)"
     kms = prof[dominant][0]
     achieved = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
+    traffic = load_traffic(dominant)
 
     # e2e through the public API: pinned host seeds in, host results out
     e2e_times, h2d, d2h = [], 0, 0
@@ -560,7 +574,8 @@ def run_ours(args, world, rank, local):
                                "note": "SURVEY 8d per-seed algorithmic bytes / step time; the bit-parallel "
                                        "engine shares each edge read across up to 1024 seeds"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dominant,
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic.get("bytes"),
+                         "traffic_source": traffic.get("source"), "kernel": dominant,
                          "kernel_ms_per_step": kms / args.steps, "alg_bytes_per_step": kbytes / args.steps,
                          "peak_source": peaks["source"], "note": note},
             "kernel_ms_per_step": {c: v[0] / args.steps for c, v in prof.items()},
