@@ -20,6 +20,7 @@
 // by a bit-transpose materialisation (K4), giving exactly the canonical
 // sorted/unique EntityVector / TripleVector form (incidence.py:83-91).
 #include <algorithm>
+#include <atomic>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -615,11 +616,16 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   constexpr int NW = mat_warps<W>();
   constexpr int NG = W / NW;
   constexpr size_t smem_w = mat_smem_bytes<W, true, Src::kRing>();
-  static bool attr_done = false;  // one per template instantiation
-  if (!attr_done) {
+  // the attribute is per device: remember which devices have it (one mask
+  // per template instantiation; an idempotent race at worst)
+  static std::atomic<uint64_t> attr_devices{0};
+  int dev = 0;
+  TH_CUDA(cudaGetDevice(&dev));
+  const uint64_t bit = uint64_t(1) << (dev & 63);
+  if (!(attr_devices.load(std::memory_order_relaxed) & bit)) {
     TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_w));
-    attr_done = true;
+    attr_devices.fetch_or(bit, std::memory_order_relaxed);
   }
   // about twelve CTAs per SM in total (two waves of the write pass, six
   // resident CTAs per SM); blocks are whole 1024-row chunks
