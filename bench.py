@@ -551,8 +551,10 @@ def run_ours(args, world, rank, local):
                          f"oracle hop_trace per seed, fork pool, {dt:.1f} s)",
                "edges_per_s": e / dt}
 
-    c3 = run_c3_leg(th, g, s, E, R, stream, peaks) if (rank == 0 and not args.no_c3) else None
-    c4 = run_c4_leg(th, stream, peaks) if (rank == 0 and not args.no_c4) else None
+    # the extra legs run at N=1 only (like the CPU baseline), so multi-rank
+    # runs stay symmetric and short
+    c3 = run_c3_leg(th, g, s, E, R, stream, peaks) if (world == 1 and not args.no_c3) else None
+    c4 = run_c4_leg(th, stream, peaks) if (world == 1 and not args.no_c4) else None
 
     if rank == 0:
         line = {
