@@ -105,16 +105,25 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
       // its frontier flag (coalesced, no redundant loads), the group's
       // active edges are compacted with one __fns per lane, then their
       // frontier rows are loaded back to back (up to LPR loads in flight)
+      // the next step's in-edge sources are loaded one step ahead, so their
+      // latency hides behind this step's flag and row loads
+      int32_t u_nx = 0;
+      uint32_t rr_nx = 0u;
+      if (!done && part < len) {
+        u_nx = __ldg(a.rsrc + lo + part);
+        if (FILTER) rr_nx = (uint32_t)__ldg(a.rrel + lo + part);
+      }
       for (int e0 = 0; e0 < maxlen; e0 += LPR) {
         const int ei = e0 + part;
         bool act = !done && ei < len;
-        int32_t u = 0;
-        uint32_t rr = 0u;
-        if (act) {
-          u = __ldg(a.rsrc + lo + ei);
-          if (FILTER) rr = (uint32_t)__ldg(a.rrel + lo + ei);
-          act = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
+        const int32_t u = u_nx;
+        const uint32_t rr = rr_nx;
+        const int en = ei + LPR;
+        if (!done && en < len) {
+          u_nx = __ldg(a.rsrc + lo + en);
+          if (FILTER) rr_nx = (uint32_t)__ldg(a.rrel + lo + en);
         }
+        if (act) act = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
         const unsigned gm = (__ballot_sync(TH_FULL, act) & gbits) >> (grp * LPR);
         const int cnt = __popc(gm);
         const int srcp = part < cnt ? (int)__fns(gm, 0, part + 1) : 0;
