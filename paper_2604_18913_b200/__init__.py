@@ -22,6 +22,7 @@ from .core_types import (
     jaccard,
 )
 from .archive import graph_from_bytes, graph_to_bytes, load_graph, save_graph
+from .cache import CacheCounters, SubgraphCache, simulate_lru
 from .device_graph import IncidenceGraph, build_incidence
 from .errors import DataError, IntegrityError, TripleHopError, UsageError
 from .partition import (
@@ -42,6 +43,9 @@ from .retriever import RetrievalResult, Retriever, k_hop, one_hop, reconstruct_p
 from .targets import GpuTarget, PartitionedGpuTarget
 
 __all__ = [
+    "CacheCounters",
+    "SubgraphCache",
+    "simulate_lru",
     "GpuTarget",
     "PartitionedGpuTarget",
     "graph_from_bytes",
