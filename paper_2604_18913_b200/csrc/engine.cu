@@ -634,6 +634,44 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
       std::max<int64_t>(kChunkRows, ceil_div(ceil_div(rows, target), kChunkRows) * kChunkRows);
   const int nblk = (int)ceil_div(rows, blk_rows);
   const unsigned grid = (unsigned)(nblk * NG);
+  // small dense layers: the count pass caches the chunks' tile masks (one
+  // layer-sized buffer, L2-resident at these sizes) for the write pass
+  if constexpr (Src::kDense && !Src::kRing) {
+    const int64_t nchunks = ceil_div(rows, kChunkRows);
+    if (s->k4_cache && nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
+      SCache sc;
+      sc.S = ensure<uint32_t>(s->k4_S, nchunks * W * 1024, s->st);
+      sc.meta = ensure<uint2>(s->k4_meta, nchunks * W, s->st);
+      constexpr size_t smem_cc = (size_t)NW * (mat_warp_words<true, false>() + 64) * sizeof(uint32_t);
+      constexpr size_t smem_wc = (size_t)NW * kChunkRows * sizeof(uint32_t);
+      static std::atomic<uint64_t> attr_c{0};
+      if (!(attr_c.load(std::memory_order_relaxed) & bit)) {
+        TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, false, false, 1>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cc));
+        TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, false, true, 1>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cc));
+        TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, true, false, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_wc));
+        attr_c.fetch_or(bit, std::memory_order_relaxed);
+      }
+      if (es.out)
+        mat_kernel<W, Src, false, true, 1><<<grid, 32 * NW, smem_cc, s->st>>>(
+            src, nblk, b.counts, nullptr, nullptr, 0, es, sc);
+      else
+        mat_kernel<W, Src, false, false, 1><<<grid, 32 * NW, smem_cc, s->st>>>(
+            src, nblk, b.counts, nullptr, nullptr, 0, EdgeSum{}, sc);
+      TH_LAUNCHED();
+      mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
+      TH_LAUNCHED();
+      mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
+      TH_LAUNCHED();
+      mat_kernel<W, Src, true, false, 2><<<grid, 32 * NW, smem_wc, s->st>>>(
+          src, nblk, b.counts, off, out, cap, EdgeSum{}, sc);
+      TH_LAUNCHED();
+      s->launches += 4;
+      return;
+    }
+  }
   constexpr size_t smem_c = mat_smem_bytes<W, false>();
   if (es.out)
     mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, b.counts,
@@ -1149,7 +1187,7 @@ void session_free(Session* s) {
   for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
                   &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
-                  &s->p_scratch, &s->rowlist, &s->rowscan}) {
+                  &s->p_scratch, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta}) {
     if (d->p) cudaFreeAsync(d->p, s->st);
     d->p = nullptr;
     d->bytes = 0;

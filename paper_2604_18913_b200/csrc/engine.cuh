@@ -43,6 +43,7 @@ struct Session {
   // K4 of hop h overlaps hop h+1's expansion on a side stream (frontier-only
   // runs; the main stream joins before it recycles the layer's rows)
   bool overlap = true;
+  bool k4_cache = true;  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr;
   cudaEvent_t ev_expand[kMaxK + 2] = {};
   cudaEvent_t ev_mat[kMaxK + 2] = {};
@@ -51,7 +52,7 @@ struct Session {
   const int32_t* tid_map = nullptr;
   int64_t launches = 0;
   // wave state
-  DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals, rowlist, rowscan;
+  DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals, rowlist, rowscan, k4_S, k4_meta;
   DBuf ctl;
   // outputs
   DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch;

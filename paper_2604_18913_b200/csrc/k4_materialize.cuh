@@ -227,11 +227,24 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
   return v;
 }
 
-template <int W, class Src, bool WRITE, bool EDGES = false>
+// Cached tile masks (small graphs): the count pass also stores each chunk's
+// transposed masks S and its (touched queries, ids) summary to global
+// memory, and the write pass starts from them instead of redoing the
+// loads and transposes.  Layout: Sg[((chunk * W + j) * 32 + b) * 32 + t].
+struct SCache {
+  uint32_t* S = nullptr;
+  uint2* meta = nullptr;
+};
+
+template <int W, class Src, bool WRITE, bool EDGES = false, int CACHE = 0>
 __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int nblk,
                                                                    int32_t* counts,
                                                                    const int64_t* base, int32_t* out,
-                                                                   int64_t cap, EdgeSum es = {}) {
+                                                                   int64_t cap, EdgeSum es = {},
+                                                                   SCache sc = {}) {
+  // CACHE 1 = count pass that stores S, CACHE 2 = write pass that loads it
+  constexpr bool BUILD_S = WRITE ? CACHE != 2 : CACHE == 1;
+  constexpr bool LOAD_S = WRITE && CACHE == 2;
   extern __shared__ uint32_t mat_smem[];
   constexpr int NW = mat_warps<W>();
   constexpr int NG = W / NW;  // word groups
@@ -244,12 +257,16 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
   // rings (sparse chunks of large, list-driven layers) need more staging
   // space; small graphs write sparse chunks directly and keep 6 CTAs/SM
   constexpr bool RING = Src::kRing;
-  uint32_t* S = mat_smem + (size_t)warp * (mat_warp_words<WRITE, RING>());
-  int32_t* stg = reinterpret_cast<int32_t*>(S + 32 * kSStride);
+  uint32_t* S = LOAD_S ? nullptr : mat_smem + (size_t)warp * (mat_warp_words<WRITE || BUILD_S, RING>() +
+                                                                 (BUILD_S && !WRITE ? 64 : 0));
+  int32_t* stg = LOAD_S ? reinterpret_cast<int32_t*>(mat_smem + (size_t)warp * kChunkRows)
+                        : reinterpret_cast<int32_t*>(S + 32 * kSStride);
   int32_t* ring = stg;  // sparse chunks (empty whenever stg is in use)
   int head = 0, fill = 0;
-  uint32_t* cnt = S;        // COUNT: [32] ids per query (sparse tiles)
-  uint32_t* ecnt = S + 32;  // COUNT+EDGES: [32] degree sums per query (sparse tiles)
+  // COUNT: [32] ids + [32] degree sums per query (sparse tiles), after S
+  // when the pass also builds S
+  uint32_t* cnt = BUILD_S && !WRITE ? S + 32 * kSStride : S;
+  uint32_t* ecnt = cnt + 32;
   if (!WRITE) {
     cnt[lane] = 0u;
     ecnt[lane] = 0u;
@@ -270,7 +287,8 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
     // keep the CTA's warps (words of the same rows) on the same chunk so
     // each row sector they share is fetched from L2 once and hit in L1
     // by the others (the write phase otherwise drifts them apart)
-    if (WRITE && NW > 1) __syncthreads();
+    if (WRITE && !LOAD_S && NW > 1) __syncthreads();
+    const size_t sbase = ((size_t)(c0 / kChunkRows) * W + j) * 1024;
     // ---- A: tile masks of this chunk, S[b][t] = rows of tile t in query b.
     // Loads of 8 tiles are issued before their transposes (memory-level
     // parallelism); dense sources get all 32 tile flags from one load.
@@ -280,9 +298,14 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
     uint32_t touched = 0u;  // WRITE: queries with ids in this chunk
     uint32_t nbits = 0u;    // WRITE: set bits seen by this lane (its rows)
     uint32_t cflags = 0u;   // lane t: flags of tile t (dense sources)
-    if constexpr (Src::kDense) cflags = src.chunk_flags(c0, rend);
+    if constexpr (LOAD_S) {
+      const uint2 mt = sc.meta[(size_t)(c0 / kChunkRows) * W + j];
+      touched = mt.x;
+      nbits = lane == 0 ? mt.y : 0u;  // the warp sum below restores the chunk's ids
+    }
+    if constexpr (Src::kDense && !LOAD_S) cflags = src.chunk_flags(c0, rend);
 #pragma unroll 1
-    for (int t0 = 0; t0 < 32; t0 += 8) {
+    for (int t0 = 0; t0 < (LOAD_S ? 0 : 32); t0 += 8) {
       uint32_t x[8], fl[8];
       int64_t aux[8];
 #pragma unroll
@@ -301,7 +324,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
         const int t = t0 + u;
         const int64_t r = c0 + 32 * t + lane;
         const uint32_t xu = x[u];
-        if (WRITE) nbits += __popc(xu);
+        if (WRITE || BUILD_S) nbits += __popc(xu);
         const bool anyx = __any_sync(TH_FULL, xu != 0u);
         const unsigned mx = anyx ? __reduce_max_sync(TH_FULL, (unsigned)__popc(xu)) : 0u;
         if (mx > kSparseBits) {
@@ -322,27 +345,25 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
               if ((m >> i) & 1u) esum += (unsigned long long)hi << 8;
             }
           }
-          if (WRITE) {
+          if (BUILD_S) {
             S[lane * kSStride + t] = m;
             touched |= __ballot_sync(TH_FULL, m != 0u);
-          } else {
-            total += __popc(m);
           }
+          if (!WRITE) total += __popc(m);
         } else {
-          if (WRITE) S[lane * kSStride + t] = 0u;
+          if (BUILD_S) S[lane * kSStride + t] = 0u;
           if (anyx) {
             uint32_t d = 0u;
             if (EDGES && xu) d = degree(es, src.id(r));
-            if (WRITE) {
+            if (BUILD_S) {
               __syncwarp();
               touched |= __reduce_or_sync(TH_FULL, xu);
             }
             uint32_t y = xu;
             while (y) {
               const int b = 31 - __clz((int)y);
-              if (WRITE) {
-                atomicOr(&S[b * kSStride + t], 1u << lane);
-              } else {
+              if (BUILD_S) atomicOr(&S[b * kSStride + t], 1u << lane);
+              if (!WRITE) {
                 atomicAdd(&cnt[b], 1u);
                 if (EDGES) atomicAdd(&ecnt[b], d);
               }
@@ -352,7 +373,17 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
         }
       }
     }
-    if (!WRITE) continue;
+    if (!WRITE) {
+      if constexpr (BUILD_S) {
+        // publish the chunk's masks (one coalesced 128-byte row per query)
+        __syncwarp();
+        for (int b = 0; b < 32; ++b) sc.S[sbase + b * 32 + lane] = S[b * kSStride + lane];
+        const unsigned ids = __reduce_add_sync(TH_FULL, nbits);
+        if (lane == 0) sc.meta[(size_t)(c0 / kChunkRows) * W + j] = make_uint2(touched, ids);
+        __syncwarp();
+      }
+      continue;
+    }
     __syncwarp();
     // ---- WRITE.  Dense chunks (many ids per query): query by query, lane
     // t extracts tile t's rows into a staging run stored coalesced.  Sparse
@@ -363,7 +394,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
     if (!RING && ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
       if (q < src.nq) {
         for (int t = 0; t < 32; ++t) {
-          uint32_t m = S[lane * kSStride + t];
+          uint32_t m = LOAD_S ? sc.S[sbase + lane * 32 + t] : S[lane * kSStride + t];
           const int64_t rb = c0 + 32 * t;
           while (m) {
             if (pos < cap) out[pos] = src.id(rb + __ffs(m) - 1);
@@ -395,7 +426,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
     while (todo) {
       const int b = __ffs(todo) - 1;
       todo &= todo - 1u;
-      uint32_t m = S[b * kSStride + lane];
+      uint32_t m = LOAD_S ? sc.S[sbase + b * 32 + lane] : S[b * kSStride + lane];
       const int c = __popc(m);
       const int incl = warp_incl_scan(c);
       const int n = __shfl_sync(TH_FULL, incl, 31);
