@@ -36,8 +36,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int32_t kHeavyPush = 256;  // rows longer than this are split across warps
-constexpr int32_t kPushChunk = 256;
+constexpr int32_t kHeavyPush = 64;   // rows longer than this are split across warps
+constexpr int32_t kPushChunk = 64;
 constexpr int kMatBlocks = 4096;      // target materialisation blocks
 
 __device__ __forceinline__ uint32_t valid_word(int j, int nq) {
