@@ -8,7 +8,7 @@ namespace th {
 
 // pull hops walk in-rows in items of at most kPullChunk in-edges; a lane
 // group owns one item (see engine.cu pull_kernel)
-constexpr int32_t kPullChunk = 64;
+constexpr int32_t kPullChunk = 32;
 
 struct Graph {
   int64_t E = 0, T = 0, R = 0;
