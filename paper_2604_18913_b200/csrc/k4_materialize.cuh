@@ -257,15 +257,17 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
   // rings (sparse chunks of large, list-driven layers) need more staging
   // space; small graphs write sparse chunks directly and keep 6 CTAs/SM
   constexpr bool RING = Src::kRing;
-  uint32_t* S = LOAD_S ? nullptr : mat_smem + (size_t)warp * (mat_warp_words<WRITE || BUILD_S, RING>() +
-                                                                 (BUILD_S && !WRITE ? 64 : 0));
+  // count pass that builds S: S + per-query counters only (no staging run)
+  constexpr size_t kWarpWords = BUILD_S && !WRITE ? (size_t)(32 * kSStride + 64)
+                                                  : mat_warp_words<WRITE, RING>();
+  uint32_t* S = LOAD_S ? nullptr : mat_smem + (size_t)warp * kWarpWords;
   int32_t* stg = LOAD_S ? reinterpret_cast<int32_t*>(mat_smem + (size_t)warp * kChunkRows)
                         : reinterpret_cast<int32_t*>(S + 32 * kSStride);
   int32_t* ring = stg;  // sparse chunks (empty whenever stg is in use)
   int head = 0, fill = 0;
   // COUNT: [32] ids + [32] degree sums per query (sparse tiles), after S
   // when the pass also builds S
-  uint32_t* cnt = BUILD_S && !WRITE ? S + 32 * kSStride : S;
+  uint32_t* cnt = BUILD_S && !WRITE ? S + 32 * kSStride : S;  // (unused when LOAD_S)
   uint32_t* ecnt = cnt + 32;
   if (!WRITE) {
     cnt[lane] = 0u;
