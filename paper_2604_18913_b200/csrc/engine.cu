@@ -63,6 +63,7 @@ struct WaveArgs {
   const uint32_t* M;
   int32_t* lists;
   int32_t* heavy;
+  int64_t* heavy_off;  // [heavy_len + 1] exclusive chunk prefix of the heavy rows
   Ctl* ctl;
   int nq, sem, h;
 };
@@ -263,24 +264,95 @@ __device__ void drive_light(const WaveArgs& a, int seg, Op& op, bool build_heavy
   }
 }
 
-// all warps split every heavy row into kPushChunk-slot chunks
+constexpr int32_t kSmallHeavy = 1024;
+
+// walk a short heavy list: every warp visits every row, taking the chunks
+// of a global round-robin numbering
 template <int W, bool FILTER, class Op>
-__device__ void drive_heavy(const WaveArgs& a, Op& op) {
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  const int32_t nh = a.ctl->heavy_len;
-  int64_t base = 0;  // global chunk numbering keeps all warps busy
+__device__ void drive_heavy_short(const WaveArgs& a, Op& op, int32_t nh, int gw, int nw) {
+  int64_t base = 0;
   for (int32_t i = 0; i < nh; ++i) {
     const int32_t u = a.heavy[i];
     const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
     const int32_t nc = (hi - lo + kPushChunk - 1) / kPushChunk;
-    int64_t c = ((gw - base) % nw + nw) % nw;
-    for (; c < nc; c += nw) {
+    for (int64_t c = ((gw - base) % nw + nw) % nw; c < nc; c += nw) {
       const int32_t clo = lo + (int32_t)c * kPushChunk;
       if constexpr (Op::kRowWise) op.template row<W>(a, u, clo, min(hi, clo + kPushChunk));
       else row_pairs<W, FILTER>(a, u, clo, min(hi, clo + kPushChunk), op);
     }
     base += nc;
+  }
+}
+
+// single block: exclusive prefix of the heavy rows' chunk counts, so the
+// heavy kernels can map a global chunk index to its row by binary search
+// (push_hop >= 0: skipped when that hop pulls)
+__global__ void heavy_scan_kernel(const int32_t* __restrict__ indptr, const int32_t* __restrict__ heavy,
+                                  const Ctl* ctl, int64_t* off, int push_hop) {
+  __shared__ int64_t ws[32];
+  if (push_hop >= 0 && ctl->mode[push_hop] != 0) return;
+  if (ctl->heavy_len <= kSmallHeavy) return;  // drive_heavy walks short lists directly
+  const int32_t nh = ctl->heavy_len;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  int64_t carry = 0;
+  for (int32_t i0 = 0; i0 < nh; i0 += blockDim.x) {
+    const int32_t i = i0 + threadIdx.x;
+    int64_t v = 0;
+    if (i < nh) {
+      const int32_t u = heavy[i];
+      v = (indptr[u + 1] - indptr[u] + kPushChunk - 1) / kPushChunk;
+    }
+    int64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(TH_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < nwarp ? ws[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(TH_FULL, w, o);
+        if (lane >= o) w += y;
+      }
+      ws[lane] = w;
+    }
+    __syncthreads();
+    if (i < nh) off[i] = carry + (warp ? ws[warp - 1] : 0) + x - v;
+    carry += ws[nwarp - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[nh] = carry;
+}
+
+// all warps split the heavy rows into kPushChunk-slot chunks: a global chunk
+// index maps to (row, chunk) through the prefix (binary search), so each
+// warp only visits its own chunks
+template <int W, bool FILTER, class Op>
+__device__ void drive_heavy(const WaveArgs& a, Op& op) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int32_t nh = a.ctl->heavy_len;
+  if (nh == 0) return;
+  if (nh <= kSmallHeavy) {
+    drive_heavy_short<W, FILTER>(a, op, nh, gw, nw);
+    return;
+  }
+  const int64_t total = a.heavy_off[nh];
+  for (int64_t g = gw; g < total; g += nw) {
+    int32_t lo_i = 0, hi_i = nh - 1;  // last i with heavy_off[i] <= g
+    while (lo_i < hi_i) {
+      const int32_t mid = (lo_i + hi_i + 1) >> 1;
+      if (a.heavy_off[mid] <= g) lo_i = mid;
+      else hi_i = mid - 1;
+    }
+    const int32_t u = a.heavy[lo_i];
+    const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
+    const int32_t clo = lo + (int32_t)(g - a.heavy_off[lo_i]) * kPushChunk;
+    if constexpr (Op::kRowWise) op.template row<W>(a, u, clo, min(hi, clo + kPushChunk));
+    else row_pairs<W, FILTER>(a, u, clo, min(hi, clo + kPushChunk), op);
   }
 }
 
@@ -737,6 +809,8 @@ void expand_hop(Session* s, const WaveArgs& a) {
     ProfScope ps(s, TH_PROF_PUSH);
     push_light_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
     TH_LAUNCHED();
+    heavy_scan_kernel<<<1, 1024, 0, s->st>>>(a.indptr, a.heavy, a.ctl, a.heavy_off, a.h);
+    TH_LAUNCHED();
     push_heavy_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
     TH_LAUNCHED();
     s->launches += 2;
@@ -818,6 +892,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   a.M = b.M;
   a.lists = b.lists;
   a.heavy = b.heavy;
+  a.heavy_off = ensure<int64_t>(s->heavy_off, std::max<int64_t>(E, 1) + 1, st);
   a.ctl = b.ctl;
   a.nq = nq;
   a.sem = sem;
@@ -868,6 +943,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
       int64_t* e_out = edges + (h - 1) * B + q0;
       if (filter) {
         edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(a, e_out, 0);
+        TH_LAUNCHED();
+        heavy_scan_kernel<<<1, 1024, 0, st>>>(a.indptr, a.heavy, a.ctl, a.heavy_off, -1);
         TH_LAUNCHED();
         edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(a, e_out, 1);
         TH_LAUNCHED();
@@ -1187,7 +1264,8 @@ void session_free(Session* s) {
   for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
                   &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
-                  &s->p_scratch, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta}) {
+                  &s->p_scratch, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta,
+                  &s->heavy_off}) {
     if (d->p) cudaFreeAsync(d->p, s->st);
     d->p = nullptr;
     d->bytes = 0;
@@ -1278,6 +1356,7 @@ ShardArgs shard_args(Shard* sh) {
   a.M = s->last.d_rel_masks ? static_cast<uint32_t*>(s->M.p) : nullptr;
   a.lists = static_cast<int32_t*>(s->lists.p);
   a.heavy = static_cast<int32_t*>(s->heavy.p);
+  a.heavy_off = static_cast<int64_t*>(s->heavy_off.p);
   a.ctl = static_cast<Ctl*>(s->ctl.p);
   a.nq = s->last.n_queries;
   a.sem = s->last.semantics;
@@ -1337,6 +1416,7 @@ void shard_begin_w(Shard* sh, const th_query* q) {
   ensure<uint32_t>(s->Vf, fwords, st);
   ensure<int32_t>(s->lists, (k + 1) * rows, st);
   ensure<int32_t>(s->heavy, rows, st);
+  ensure<int64_t>(s->heavy_off, rows + 1, st);
   if (q->d_rel_masks) ensure<uint32_t>(s->M, std::max<int64_t>(sh->g.R, 1) * W, st);
   ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
   ensure<int64_t>(s->totals, kMaxWave, st);
@@ -1392,6 +1472,8 @@ void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send
     if (filter) {
       edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out, 0);
       TH_LAUNCHED();
+      heavy_scan_kernel<<<1, 1024, 0, st>>>(sa.a.indptr, sa.a.heavy, sa.a.ctl, sa.a.heavy_off, -1);
+      TH_LAUNCHED();
       edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out, 1);
       TH_LAUNCHED();
       s->launches += 2;
@@ -1412,6 +1494,9 @@ void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send
     const int sem = q.semantics == TH_EXACT ? TH_EXACT : TH_FRONTIER;
 #define TH_SHARD_PUSH(SEM, F)                                                      \
   shard_push_light_kernel<W, SEM, F><<<pg, kThreads, 0, st>>>(sa);               \
+  TH_LAUNCHED();                                                                 \
+  heavy_scan_kernel<<<1, 1024, 0, st>>>(sa.a.indptr, sa.a.heavy, sa.a.ctl,         \
+                                       sa.a.heavy_off, h);                       \
   TH_LAUNCHED();                                                                 \
   shard_push_heavy_kernel<W, SEM, F><<<pg, kThreads, 0, st>>>(sa);               \
   TH_LAUNCHED();

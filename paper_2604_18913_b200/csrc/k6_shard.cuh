@@ -188,17 +188,33 @@ __global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int32_t nh = a.ctl->heavy_len;
-  int64_t base = 0;
-  for (int32_t i = 0; i < nh; ++i) {
-    const int32_t u = a.heavy[i];
-    const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
-    const int32_t nc = (hi - lo + kPushChunk - 1) / kPushChunk;
-    int64_t c = ((gw - base) % nw + nw) % nw;
-    for (; c < nc; c += nw) {
-      const int32_t clo = lo + (int32_t)c * kPushChunk;
-      shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk));
+  if (nh == 0) return;
+  if (nh <= kSmallHeavy) {
+    int64_t base = 0;
+    for (int32_t i = 0; i < nh; ++i) {
+      const int32_t u = a.heavy[i];
+      const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
+      const int32_t nc = (hi - lo + kPushChunk - 1) / kPushChunk;
+      for (int64_t c = ((gw - base) % nw + nw) % nw; c < nc; c += nw) {
+        const int32_t clo = lo + (int32_t)c * kPushChunk;
+        shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk));
+      }
+      base += nc;
     }
-    base += nc;
+    return;
+  }
+  const int64_t total = a.heavy_off[nh];
+  for (int64_t g = gw; g < total; g += nw) {
+    int32_t lo_i = 0, hi_i = nh - 1;
+    while (lo_i < hi_i) {
+      const int32_t mid = (lo_i + hi_i + 1) >> 1;
+      if (a.heavy_off[mid] <= g) lo_i = mid;
+      else hi_i = mid - 1;
+    }
+    const int32_t u = a.heavy[lo_i];
+    const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
+    const int32_t clo = lo + (int32_t)(g - a.heavy_off[lo_i]) * kPushChunk;
+    shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk));
   }
 }
 
