@@ -813,7 +813,7 @@ void expand_hop(Session* s, const WaveArgs& a) {
     TH_LAUNCHED();
     push_heavy_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
     TH_LAUNCHED();
-    s->launches += 2;
+    s->launches += 3;
   }
   if (s->g->rindptr) {
     ProfScope ps(s, TH_PROF_PULL);
@@ -948,7 +948,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
         TH_LAUNCHED();
         edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(a, e_out, 1);
         TH_LAUNCHED();
-        s->launches += 2;
+        s->launches += 3;
       } else {
         edge_count_kernel<W><<<pg, kThreads, 0, st>>>(a, e_out);
         TH_LAUNCHED();
@@ -1476,7 +1476,7 @@ void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send
       TH_LAUNCHED();
       edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out, 1);
       TH_LAUNCHED();
-      s->launches += 2;
+      s->launches += 3;
     } else {
       edge_count_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out);
       TH_LAUNCHED();
@@ -1506,7 +1506,7 @@ void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send
       if (sem == TH_EXACT) { TH_SHARD_PUSH(TH_EXACT, false) } else { TH_SHARD_PUSH(TH_FRONTIER, false) }
     }
 #undef TH_SHARD_PUSH
-    s->launches += 3;
+    s->launches += 3;  // light, heavy-chunk scan, heavy
   }
   // pack: per-owner totals -> host -> offsets -> records
   const int G = sh->world;
