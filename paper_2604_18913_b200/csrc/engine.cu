@@ -708,6 +708,8 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   const unsigned grid = (unsigned)(nblk * NG);
   // small dense layers: the count pass caches the chunks' tile masks (one
   // layer-sized buffer, L2-resident at these sizes) for the write pass
+  // (list-driven large layers re-read the layer instead: caching S there
+  // streams a layer-sized buffer through HBM twice, C4 k=3 18.5 -> 20.9 ms)
   if constexpr (Src::kDense && !Src::kRing) {
     const int64_t nchunks = ceil_div(rows, kChunkRows);
     if (s->k4_cache && nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
@@ -715,7 +717,7 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
       sc.S = ensure<uint32_t>(s->k4_S, nchunks * W * 1024, s->st);
       sc.meta = ensure<uint2>(s->k4_meta, nchunks * W, s->st);
       constexpr size_t smem_cc = (size_t)NW * (32 * kSStride + 64) * sizeof(uint32_t);
-      constexpr size_t smem_wc = (size_t)NW * kChunkRows * sizeof(uint32_t);
+      constexpr size_t smem_wc = (size_t)NW * mat_load_words<Src::kRing>() * sizeof(uint32_t);
       static std::atomic<uint64_t> attr_c{0};
       if (!(attr_c.load(std::memory_order_relaxed) & bit)) {
         TH_CUDA(cudaFuncSetAttribute(mat_kernel<W, Src, false, false, 1>,

@@ -197,6 +197,12 @@ __device__ __forceinline__ void ring_flush_all(const int32_t* ring, int& head, i
   __syncwarp();
 }
 
+// per-warp words of a write pass that loads cached masks: staging run or rings
+template <bool RING>
+constexpr size_t mat_load_words() {
+  return RING && kRingWords > kChunkRows ? kRingWords : kChunkRows;
+}
+
 template <int W, bool WRITE, bool RING = false>
 constexpr size_t mat_smem_bytes() {
   return (size_t)mat_warps<W>() * mat_warp_words<WRITE, RING>() * sizeof(uint32_t);
@@ -261,7 +267,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
   constexpr size_t kWarpWords = BUILD_S && !WRITE ? (size_t)(32 * kSStride + 64)
                                                   : mat_warp_words<WRITE, RING>();
   uint32_t* S = LOAD_S ? nullptr : mat_smem + (size_t)warp * kWarpWords;
-  int32_t* stg = LOAD_S ? reinterpret_cast<int32_t*>(mat_smem + (size_t)warp * kChunkRows)
+  int32_t* stg = LOAD_S ? reinterpret_cast<int32_t*>(mat_smem + (size_t)warp * mat_load_words<RING>())
                         : reinterpret_cast<int32_t*>(S + 32 * kSStride);
   int32_t* ring = stg;  // sparse chunks (empty whenever stg is in use)
   int head = 0, fill = 0;
@@ -410,7 +416,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
     }
     if (RING && ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
       for (int t = 0; t < 32; ++t) {
-        uint32_t m = q < src.nq ? S[lane * kSStride + t] : 0u;
+        uint32_t m = q >= src.nq ? 0u : LOAD_S ? sc.S[sbase + lane * 32 + t] : S[lane * kSStride + t];
         const int64_t rb = c0 + 32 * t;
         while (m) {
           ring[lane * kRingStride + ((head + fill) & (kRing - 1))] = src.id(rb + __ffs(m) - 1);
