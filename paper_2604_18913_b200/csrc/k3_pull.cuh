@@ -129,8 +129,12 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
         const int srcp = part < cnt ? (int)__fns(gm, 0, part + 1) : 0;
         const int32_t uc = __shfl_sync(TH_FULL, u, grp * LPR + srcp);
         const uint32_t rc = FILTER ? __shfl_sync(TH_FULL, rr, grp * LPR + srcp) : 0u;
-#pragma unroll
-        for (int it = 0; it < LPR; ++it) {
+        // steps where no group of the warp found a frontier in-edge skip the
+        // (fully unrolled, up to LPR loads in flight) row gathers entirely;
+        // bounding the unrolled loop by the busiest group measured slower at
+        // C4 (serialised or branchy loads)
+        const int maxcnt = (int)__reduce_max_sync(TH_FULL, (unsigned)cnt);
+        auto take = [&](int it) {
           const int32_t uu = __shfl_sync(TH_FULL, uc, grp * LPR + it);
           const uint32_t r2 = FILTER ? __shfl_sync(TH_FULL, rc, grp * LPR + it) : 0u;
           if (it < cnt) {
@@ -145,6 +149,10 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
 #pragma unroll
             for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
           }
+        };
+        if (maxcnt > 0) {
+#pragma unroll
+          for (int it = 0; it < LPR; ++it) take(it);
         }
         bool full = true;
 #pragma unroll
