@@ -257,7 +257,13 @@ class LoopbackExchange(Exchange):
 
 
 class DistExchange(Exchange):
-    """One rank per process over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+    """One rank per process over torch.distributed.
+
+    NCCL moves device buffers directly (the B200 path).  With gloo (CPU
+    tests, or several ranks sharing one GPU in a functional test, where
+    NCCL refuses duplicate devices) device tensors are staged through host
+    memory, so no rank's kernels ever wait on another rank's.
+    """
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -267,32 +273,41 @@ class DistExchange(Exchange):
         self.world = dist.get_world_size(group)
         self.ranks = [dist.get_rank(group)]
         self.bytes_sent = 0
+        self.staged = dist.get_backend(group) != "nccl"
+
+    def _host(self, t):
+        return t.cpu() if (self.staged and t.is_cuda) else t
 
     def all_to_all(self, sends):
         import torch
 
         (send, counts), = sends
         dev = send.device
-        cnt = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=dev)
+        cdev = "cpu" if self.staged else dev
+        cnt = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=cdev)
         rcnt = torch.empty_like(cnt)
         self.dist.all_to_all_single(rcnt, cnt, group=self.group)
         rc = [int(x) for x in rcnt.tolist()]
-        recv = torch.empty(sum(rc), dtype=torch.int64, device=dev)
         n = int(sum(counts))
-        self.dist.all_to_all_single(recv, send[:n].contiguous(), output_split_sizes=rc,
+        src = self._host(send[:n].contiguous())
+        recv = torch.empty(sum(rc), dtype=torch.int64, device=src.device)
+        self.dist.all_to_all_single(recv, src, output_split_sizes=rc,
                                     input_split_sizes=[int(c) for c in counts], group=self.group)
         self.bytes_sent += 8 * (n - int(counts[self.ranks[0]]))
-        return [recv]
+        return [recv.to(dev) if recv.device != dev else recv]
 
     def sum_(self, tensors):
         (t,) = tensors
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        h = self._host(t)
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
+        if h is not t:
+            t.copy_(h)
 
     def any(self, flags):
         import torch
 
         (f,) = flags
-        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        dev = "cpu" if self.staged else "cuda"
         t = torch.tensor([1 if f else 0], dtype=torch.int32, device=dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return bool(t.item())

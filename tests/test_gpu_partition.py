@@ -157,3 +157,57 @@ def test_cross_graph_paths_golden(th, name):
         assert pr.truncated == q.truncated
         n += 1
     assert n > 0
+
+
+def _gpu_dist_worker(rank, world, port, errfile):
+    """One rank with a REAL CUDA shard; gloo carries the exchange (host-staged)
+    because NCCL refuses two ranks on one device.  No kernel of one rank waits
+    on another rank."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_18913_b200 as th
+
+        s, r, o = _hub_graph(1500, 30000, 16, seed=33)
+        E, R = 1500, 16
+        og = orc.build_csr(s, r, o, E, R)
+        xch = th.DistExchange()
+        pg = th.PartitionedGraph((s, r, o), E, R, xch, n_hubs=8)
+        assert isinstance(pg.shards[0], th.partition.GraphShard)
+        seeds = np.random.default_rng(8).integers(0, E, 150)
+        for sem in ("exact", "frontier", "cumulative"):
+            res = pg.retrieve(seeds, 3, semantics=sem, activated=True)
+            for i in range(0, 150, 7):
+                ref = orc.retrieve_one(og, int(seeds[i]), 3, sem)
+                for h in range(3):
+                    assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h])
+                    assert np.array_equal(res.activated(i, h + 1), ref["activated"][h])
+                    assert int(res.edges[h, i]) == ref["edges"][h]
+        assert xch.bytes_sent > 0
+    except BaseException as e:  # pragma: no cover - reported to the parent
+        with open(errfile, "a") as f:
+            f.write(f"rank {rank}: {type(e).__name__}: {e}\n")
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_with_cuda_shards(tmp_path):
+    import socket
+
+    import torch
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    errfile = str(tmp_path / "err.txt")
+    torch.multiprocessing.spawn(_gpu_dist_worker, args=(2, port, errfile), nprocs=2, join=True)
+    import os
+
+    assert not os.path.exists(errfile), open(errfile).read()
