@@ -222,12 +222,19 @@ int64_t th_shard_launch_count(const th_shard* s);
 /* One wave of <= 1024 queries, hop h = 1..k in order; every rank makes the
  * same calls with the same query arrays:
  *   th_shard_begin(q)                     seeds (hub seeds on every rank)
- *   th_shard_expand(h, counts, &send)     push over local rows + hub slices;
- *       send[] = records bucketed by owner rank, counts[world] records per
- *       owner (host).  Record = ((row_at_owner * W + word) << 32) | bits,
- *       W = 32-bit words per row (queries rounded up to a power of two / 32)
- *   -- caller: all-to-all of the records --
- *   th_shard_absorb(h, recv, n)           apply received records
+ *   th_shard_plan(h, &cost)               optional: this rank's frontier
+ *       out-edge total; the caller sums it over ranks to pick the direction
+ *   th_shard_expand(h, mode, counts, &send)
+ *       mode 0 (push): push over local rows + hub slices; send[] = records
+ *       bucketed by owner rank, counts[world] records per owner (host).
+ *       Record = ((row_at_owner * W + word) << 32) | bits, W = 32-bit words
+ *       per row (queries rounded up to a power of two / 32).
+ *       mode 1 (pull, th_shard_can_pull): send[] = this rank's owned
+ *       frontier rows as ((global_id * W + word) << 32) | bits, the same for
+ *       every rank (counts[d] = their number)
+ *   -- caller: mode 0 all-to-all, mode 1 all-gather of the records --
+ *   th_shard_absorb(h, recv, n)           mode 0: apply received records;
+ *       mode 1: stage all ranks' frontier rows, pull over the owned in-edges
  *   th_shard_hub_rows(h, &rows, &words)   uint32 [n_hubs][W]: owned hubs'
  *       next-layer rows, zero elsewhere
  *   -- caller: sum `rows` over ranks in place (one owner per hub) --
@@ -239,7 +246,10 @@ int64_t th_shard_launch_count(const th_shard* s);
  *       (sum over ranks = |T_h|).  TH_ERR_OVERFLOW: capacities grew, every
  *       rank must run the wave again.  Paths are not available here. */
 int th_shard_begin(th_shard* s, const th_query* q);
-int th_shard_expand(th_shard* s, int32_t hop, int64_t* h_send_counts, const uint64_t** d_send);
+int th_shard_plan(th_shard* s, int32_t hop, int64_t* h_cost);
+int th_shard_can_pull(const th_shard* s);
+int th_shard_expand(th_shard* s, int32_t hop, int32_t mode, int64_t* h_send_counts,
+                    const uint64_t** d_send);
 int th_shard_absorb(th_shard* s, int32_t hop, const uint64_t* d_recv, int64_t n_recv);
 int th_shard_hub_rows(th_shard* s, int32_t hop, uint32_t** d_rows, int64_t* n_words);
 int th_shard_hub_merge(th_shard* s, int32_t hop);

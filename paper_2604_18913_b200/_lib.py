@@ -28,7 +28,8 @@ EXPORTS = (
     "th_session_set_list_min_entities", "th_session_set_overlap",
     "th_session_set_profiling", "th_session_profile", "th_session_wave_lists",
     "th_shard_create", "th_shard_destroy", "th_shard_local_triples", "th_shard_launch_count",
-    "th_shard_begin", "th_shard_expand", "th_shard_absorb", "th_shard_hub_rows",
+    "th_shard_begin", "th_shard_plan", "th_shard_can_pull", "th_shard_expand", "th_shard_absorb",
+    "th_shard_hub_rows",
     "th_shard_hub_merge", "th_shard_end_hop", "th_shard_finish",
 )
 PROF_CATEGORIES = ("setup", "edges", "activated", "push", "pull", "frontier", "clear", "paths")
@@ -113,8 +114,10 @@ def load():
         "th_shard_local_triples": (ctypes.c_int64, [_vp]),
         "th_shard_launch_count": (ctypes.c_int64, [_vp]),
         "th_shard_begin": (ctypes.c_int, [_vp, ctypes.POINTER(Query)]),
-        "th_shard_expand": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
-                                           ctypes.POINTER(_vp)]),
+        "th_shard_plan": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
+        "th_shard_can_pull": (ctypes.c_int, [_vp]),
+        "th_shard_expand": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32,
+                                           ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_vp)]),
         "th_shard_absorb": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, ctypes.c_int64]),
         "th_shard_hub_rows": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(_vp),
                                              ctypes.POINTER(ctypes.c_int64)]),

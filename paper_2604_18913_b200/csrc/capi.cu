@@ -359,14 +359,28 @@ int th_shard_begin(th_shard* s, const th_query* q) {
   });
 }
 
-int th_shard_expand(th_shard* s, int32_t hop, int64_t* h_send_counts, const uint64_t** d_send) {
+int th_shard_plan(th_shard* s, int32_t hop, int64_t* h_cost) {
   return guarded([&]() -> int {
     TH_SHARD_GUARD(s);
-    if (!h_send_counts || !d_send) {
+    if (!h_cost) {
       th::set_error("NULL output");
       return TH_ERR_INVALID;
     }
-    return th::shard_expand(s->sh, hop, h_send_counts, d_send);
+    return th::shard_plan(s->sh, hop, h_cost);
+  });
+}
+
+int th_shard_can_pull(const th_shard* s) { return (s && s->sh) ? th::shard_can_pull(s->sh) : 0; }
+
+int th_shard_expand(th_shard* s, int32_t hop, int32_t mode, int64_t* h_send_counts,
+                    const uint64_t** d_send) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    if (!h_send_counts || !d_send || (mode != 0 && mode != 1)) {
+      th::set_error("NULL output or bad mode");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_expand(s->sh, hop, mode, h_send_counts, d_send);
   });
 }
 

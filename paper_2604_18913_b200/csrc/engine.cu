@@ -1321,6 +1321,10 @@ struct Shard {
   int32_t rank = 0, world = 1;
   Session s;
   DBuf O, Of, olist, send, pcnt, hubbuf;
+  Graph gin;                       // in-edges of owned objects (pull hops)
+  bool can_pull = false;
+  int planned = 0;                 // hop whose bookkeeping th_shard_plan ran
+  int hop_mode[kMaxK + 2] = {};    // 0 push, 1 pull
   int W = 0;
   bool in_wave = false;
   int next_hop = 0;
@@ -1455,7 +1459,7 @@ void shard_begin_w(Shard* sh, const th_query* q) {
 }
 
 template <int W>
-void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send) {
+void shard_expand_w(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_t** d_send) {
   Session* s = &sh->s;
   cudaStream_t st = s->st;
   const th_query& q = s->last;
@@ -1465,8 +1469,11 @@ void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send
   ShardArgs sa = shard_args<W>(sh);
   sa.a.h = h;
   const unsigned pg = persistent_grid();
-  begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, sh->g.T, 0.0, 0);
-  TH_LAUNCHED();
+  if (sh->planned != h) {
+    begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, sh->g.T, 0.0, 0);
+    TH_LAUNCHED();
+  }
+  sh->hop_mode[h] = mode;
   TH_CUDA(cudaMemsetAsync(&b.ctl->olen, 0, sizeof(int32_t), st));
   int64_t* e_out = static_cast<int64_t*>(s->edges.p) + (h - 1) * B;
   {
@@ -1490,6 +1497,26 @@ void shard_expand_w(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send
     materialize_triples<W>(s, b, (int)B, static_cast<int64_t*>(s->a_off.p) + (h - 1) * B,
                            static_cast<int64_t*>(s->a_len.p) + (h - 1) * B,
                            static_cast<int32_t*>(s->a_ids.p), s->a_cap, &b.ctl->act_used);
+  }
+  if (mode == 1) {
+    // pull hop: publish the owned frontier rows (same records for every rank)
+    const int32_t one = 1;
+    TH_CUDA(cudaMemcpyAsync(&b.ctl->mode[h], &one, sizeof(int32_t), cudaMemcpyHostToDevice, st));
+    unsigned long long* pc = static_cast<unsigned long long*>(sh->pcnt.p);
+    TH_CUDA(cudaMemsetAsync(pc, 0, sizeof(unsigned long long), st));
+    shard_frontier_pack_kernel<W, false><<<pg, kThreads, 0, st>>>(sa, h - 1, sh->l2g, pc, nullptr);
+    TH_LAUNCHED();
+    unsigned long long tot = 0;
+    TH_CUDA(cudaMemcpyAsync(&tot, pc, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    TH_CUDA(cudaStreamSynchronize(st));
+    uint64_t* send = ensure<uint64_t>(sh->send, (int64_t)std::max<unsigned long long>(tot, 1), st);
+    TH_CUDA(cudaMemsetAsync(pc, 0, sizeof(unsigned long long), st));
+    shard_frontier_pack_kernel<W, true><<<pg, kThreads, 0, st>>>(sa, h - 1, sh->l2g, pc, send);
+    TH_LAUNCHED();
+    s->launches += 2;
+    for (int d = 0; d < sh->world; ++d) h_counts[d] = (int64_t)tot;
+    *d_send = send;
+    return;
   }
   {
     ProfScope ps(s, TH_PROF_PUSH);
@@ -1541,6 +1568,41 @@ void shard_absorb_w(Shard* sh, int h, const uint64_t* recs, int64_t n) {
   Session* s = &sh->s;
   ShardArgs sa = shard_args<W>(sh);
   sa.a.h = h;
+  if (sh->hop_mode[h] == 1) {
+    // pull hop: all ranks' frontier rows (+ local hub rows) -> global staging,
+    // pull over the owned in-edges, then undo the staging
+    cudaStream_t st = s->st;
+    const unsigned grid = persistent_grid();
+    shard_gather_frontier_kernel<W><<<grid, kThreads, 0, st>>>(sa, h - 1, recs, n);
+    TH_LAUNCHED();
+    WaveArgs pa = sa.a;
+    pa.X = sa.O;
+    pa.Xf = sa.Of;
+    pa.rsrc = sh->gin.rsrc;
+    pa.rrel = sh->gin.rrel;
+    pa.item_v = sh->gin.item_v;
+    pa.item_lo = sh->gin.item_lo;
+    pa.item_hi = sh->gin.item_hi;
+    pa.n_items = sh->gin.n_items;
+    const unsigned pg = persistent_grid();
+    const bool filter = s->last.d_rel_masks != nullptr;
+    {
+      ProfScope ps(s, TH_PROF_PULL);
+      if (s->last.semantics == TH_EXACT) {
+        if (filter) pull_kernel<W, TH_EXACT, true><<<pg, kThreads, 0, st>>>(pa);
+        else pull_kernel<W, TH_EXACT, false><<<pg, kThreads, 0, st>>>(pa);
+      } else {
+        if (filter) pull_kernel<W, TH_FRONTIER, true><<<pg, kThreads, 0, st>>>(pa);
+        else pull_kernel<W, TH_FRONTIER, false><<<pg, kThreads, 0, st>>>(pa);
+      }
+      TH_LAUNCHED();
+    }
+    shard_clear_frontier_kernel<W><<<grid, kThreads, 0, st>>>(sa, h - 1, recs, n);
+    TH_LAUNCHED();
+    TH_CUDA(cudaMemsetAsync(sa.Of, 0, (size_t)(ceil_div(sh->E, 32) + 1) * 4, st));
+    s->launches += 3;
+    return;
+  }
   if (n > 0) {
     const int sem = s->last.semantics;
     const unsigned grid = grid_for(n);
@@ -1690,10 +1752,49 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
                                                         sh->tid_l2g);
     TH_LAUNCHED();
   }
-  const int rc = graph_build(&sh->g, okey, orel, oobj, tl, n_local + H, R, false, st, E);
+  int rc = graph_build(&sh->g, okey, orel, oobj, tl, n_local + H, R, false, st, E);
   TH_CUDA(cudaStreamSynchronize(st));
-  for (void* p : {(void*)key, (void*)bsum, (void*)okey, (void*)orel, (void*)oobj}) cudaFree(p);
-  if (rc != TH_OK) return rc;
+  for (void* p : {(void*)okey, (void*)orel, (void*)oobj}) cudaFree(p);
+  if (rc != TH_OK) {
+    cudaFree(key);
+    cudaFree(bsum);
+    return rc;
+  }
+  // in-edges of the owned objects (global sources) for pull hops: records
+  // key (gid * W + word) must fit 32 bits for W = 32
+  if (E * 32 < (int64_t(1) << 32) && T > 0) {
+    shard_select_in_kernel<<<grid_for(T), kThreads, 0, st>>>(d_obj, T, sh->lidx, rank, world, key);
+    TH_LAUNCHED();
+    shard_count_kernel<<<nb, kCompactThreads, 0, st>>>(key, T, bsum);
+    TH_LAUNCHED();
+    flag_scan_kernel<<<1, 1024, 0, st>>>(bsum, nb, bsum + nb);
+    TH_LAUNCHED();
+    int32_t ti = 0;
+    TH_CUDA(cudaMemcpyAsync(&ti, bsum + nb, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    TH_CUDA(cudaStreamSynchronize(st));
+    const int64_t icap = std::max<int32_t>(ti, 1);
+    int32_t *ikey = nullptr, *irel = nullptr, *isub = nullptr, *itid = nullptr;
+    TH_CUDA(cudaMalloc(&ikey, sizeof(int32_t) * icap));
+    TH_CUDA(cudaMalloc(&irel, sizeof(int32_t) * icap));
+    TH_CUDA(cudaMalloc(&isub, sizeof(int32_t) * icap));
+    TH_CUDA(cudaMalloc(&itid, sizeof(int32_t) * icap));
+    shard_gather_kernel<<<nb, kCompactThreads, 0, st>>>(key, T, bsum, d_rel, d_subj, ikey, irel, isub,
+                                                        itid);
+    TH_LAUNCHED();
+    // forward side keyed by the global subject (unused), reverse side by the
+    // object's local row: items cover the owned rows
+    rc = graph_build(&sh->gin, isub, irel, ikey, ti, E, R, true, st, E);
+    TH_CUDA(cudaStreamSynchronize(st));
+    for (void* p : {(void*)ikey, (void*)irel, (void*)isub, (void*)itid}) cudaFree(p);
+    if (rc != TH_OK) {
+      cudaFree(key);
+      cudaFree(bsum);
+      return rc;
+    }
+    sh->can_pull = true;
+  }
+  cudaFree(key);
+  cudaFree(bsum);
   Session* s = &sh->s;
   s->g = &sh->g;
   s->st = st;
@@ -1765,11 +1866,31 @@ static int shard_check_hop(Shard* sh, int h) {
   return TH_OK;
 }
 
-int shard_expand(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send) {
+int shard_plan(Shard* sh, int h, int64_t* h_cost) {
   if (int rc = shard_check_hop(sh, h)) return rc;
-  TH_W_DISPATCH(sh->W, shard_expand_w<WW>(sh, h, h_counts, d_send));
+  Session* s = &sh->s;
+  Ctl* ctl = static_cast<Ctl*>(s->ctl.p);
+  begin_hop_kernel<<<1, 1, 0, s->st>>>(ctl, h, sh->g.T, 0.0, 0);
+  TH_LAUNCHED();
+  unsigned long long c = 0;
+  TH_CUDA(cudaMemcpyAsync(&c, &ctl->push_cost[h - 1], sizeof(c), cudaMemcpyDeviceToHost, s->st));
+  TH_CUDA(cudaStreamSynchronize(s->st));
+  *h_cost = (int64_t)c;
+  sh->planned = h;
   return TH_OK;
 }
+
+int shard_expand(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_t** d_send) {
+  if (int rc = shard_check_hop(sh, h)) return rc;
+  if (mode == 1 && !sh->can_pull) {
+    set_error("this shard has no in-edge index for pull hops");
+    return TH_ERR_INVALID;
+  }
+  TH_W_DISPATCH(sh->W, shard_expand_w<WW>(sh, h, mode, h_counts, d_send));
+  return TH_OK;
+}
+
+int shard_can_pull(const Shard* sh) { return sh->can_pull ? 1 : 0; }
 
 int shard_absorb(Shard* sh, int h, const uint64_t* d_recv, int64_t n) {
   if (int rc = shard_check_hop(sh, h)) return rc;
@@ -1820,6 +1941,7 @@ void shard_free(Shard* sh) {
                   (void*)sh->l2g})
     if (p) cudaFree(p);
   graph_free(&sh->g);
+  graph_free(&sh->gin);
   delete sh;
 }
 

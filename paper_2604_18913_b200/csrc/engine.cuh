@@ -99,7 +99,9 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
                  cudaStream_t st);
 int64_t shard_local_triples(const Shard* sh);
 int shard_begin(Shard* sh, const th_query* q);
-int shard_expand(Shard* sh, int h, int64_t* h_counts, const uint64_t** d_send);
+int shard_plan(Shard* sh, int h, int64_t* h_cost);
+int shard_expand(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_t** d_send);
+int shard_can_pull(const Shard* sh);
 int shard_absorb(Shard* sh, int h, const uint64_t* d_recv, int64_t n);
 int shard_hub_rows(Shard* sh, int h, uint32_t** d_rows, int64_t* words);
 int shard_hub_merge(Shard* sh, int h);

@@ -399,3 +399,120 @@ __global__ void __launch_bounds__(kCompactThreads) shard_gather_kernel(
     }
   }
 }
+
+// ---------------------------------------------------------------------------
+// Pull hops across partitions (dense frontiers).  Instead of pushing every
+// frontier edge's candidates to the target's owner, every rank publishes its
+// owned frontier rows -- records ((gid * W + word) << 32) | bits -- and all
+// ranks all-gather them into a global-indexed staging copy of the frontier
+// (the push staging matrix O, empty between hops); each rank then pulls for
+// the entities it owns over its in-edge CSR (global sources).  Hub frontier
+// rows are already replicated and are copied in locally.
+
+// in-edges of owned objects: key = object's local row, or -1
+__global__ void shard_select_in_kernel(const int32_t* __restrict__ obj, int64_t T,
+                                       const int32_t* __restrict__ lidx, int32_t rank,
+                                       int32_t world, int32_t* key) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < T;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = obj[t];
+    key[t] = owner_of(v, world) == rank ? lidx[v] : -1;
+  }
+}
+
+// owned frontier rows of list segment `seg` -> records (COUNT: totals only)
+template <int W, bool WRITE>
+__global__ void __launch_bounds__(kThreads) shard_frontier_pack_kernel(ShardArgs sa, int seg,
+                                                                       const int32_t* __restrict__ l2g,
+                                                                       unsigned long long* cursor,
+                                                                       uint64_t* out) {
+  const WaveArgs& a = sa.a;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int32_t n = a.ctl->list_len[seg];
+  const int32_t* list = a.lists + a.ctl->list_off[seg];
+  for (int64_t base = gw * 32; base < n; base += nw * 32) {
+    const int64_t i = base + lane;
+    int32_t row = -1;
+    uint32_t words[W];
+    int nzc = 0;
+    if (i < n) {
+      row = list[i];
+      if (row < sa.n_local) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          words[j] = a.X[(size_t)row * W + j];
+          nzc += words[j] != 0u;
+        }
+      } else {
+        row = -1;  // hub rows: every rank holds them already
+      }
+    }
+    int incl = nzc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(TH_FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int tot = __shfl_sync(TH_FULL, incl, 31);
+    unsigned long long b0 = 0;
+    if (lane == 0 && tot) b0 = atomicAdd(cursor, (unsigned long long)tot);
+    b0 = __shfl_sync(TH_FULL, b0, 0);
+    if (WRITE && row >= 0) {
+      uint64_t o = b0 + (uint64_t)(incl - nzc);
+      const uint64_t key0 = (uint64_t)l2g[row] * W;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (words[j]) out[o++] = ((key0 + j) << 32) | words[j];
+    }
+  }
+}
+
+// gathered records (and the local hub frontier rows) -> global staging G, Gf
+template <int W>
+__global__ void shard_gather_frontier_kernel(ShardArgs sa, int seg, const uint64_t* __restrict__ recs,
+                                             int64_t n) {
+  const WaveArgs& a = sa.a;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t rec = recs[i];
+    const uint32_t key = (uint32_t)(rec >> 32);
+    const int32_t g = (int32_t)(key / W);
+    sa.O[(size_t)key] = (uint32_t)rec;
+    atomicOr(&sa.Of[g >> 5], 1u << (g & 31));
+  }
+  // hub rows of the segment (rows >= n_local), one thread per (row, word)
+  const int32_t nl = a.ctl->list_len[seg];
+  const int32_t* list = a.lists + a.ctl->list_off[seg];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nl * W;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t row = list[i / W];
+    if (row < sa.n_local) continue;
+    const int j = (int)(i % W);
+    const int32_t g = sa.hub_ids[row - sa.n_local];
+    const uint32_t w = a.X[(size_t)row * W + j];
+    if (w) {
+      sa.O[(size_t)g * W + j] = w;
+      atomicOr(&sa.Of[g >> 5], 1u << (g & 31));
+    }
+  }
+}
+
+// undo the staging: zero the gathered words and the hub rows' words
+template <int W>
+__global__ void shard_clear_frontier_kernel(ShardArgs sa, int seg, const uint64_t* __restrict__ recs,
+                                            int64_t n) {
+  const WaveArgs& a = sa.a;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    sa.O[(size_t)(uint32_t)(recs[i] >> 32)] = 0u;
+  const int32_t nl = a.ctl->list_len[seg];
+  const int32_t* list = a.lists + a.ctl->list_off[seg];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nl * W;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t row = list[i / W];
+    if (row < sa.n_local) continue;
+    sa.O[(size_t)sa.hub_ids[row - sa.n_local] * W + (i % W)] = 0u;
+  }
+}

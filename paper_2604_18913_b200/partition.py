@@ -213,6 +213,12 @@ class Exchange:
     def sum_(self, tensors) -> None:  # in place, over ranks
         raise NotImplementedError
 
+    def all_gather(self, sends):  # [(int64 tensor, counts)] -> [concat of all ranks' tensors]
+        raise NotImplementedError
+
+    def sum_int(self, values) -> int:  # sum of one int per hosted rank over all ranks
+        raise NotImplementedError
+
     def any(self, flags) -> bool:
         raise NotImplementedError
 
@@ -239,6 +245,17 @@ class LoopbackExchange(Exchange):
             out.append(torch.cat(parts) if parts else sends[0][0][:0])
         self.bytes_sent += 8 * sum(int(sum(c)) for _, c in sends)
         return out
+
+    def all_gather(self, sends):
+        import torch
+
+        parts = [t[: int(c[0])] if len(c) else t[:0] for t, c in sends]
+        full = torch.cat(parts) if parts else sends[0][0][:0]
+        self.bytes_sent += 8 * (self.world - 1) * sum(int(p.numel()) for p in parts)
+        return [full for _ in sends]
+
+    def sum_int(self, values):
+        return int(sum(int(v) for v in values))
 
     def sum_(self, tensors):
         if len(tensors) <= 1:
@@ -295,6 +312,35 @@ class DistExchange(Exchange):
                                     input_split_sizes=[int(c) for c in counts], group=self.group)
         self.bytes_sent += 8 * (n - int(counts[self.ranks[0]]))
         return [recv.to(dev) if recv.device != dev else recv]
+
+    def all_gather(self, sends):
+        import torch
+
+        (send, counts), = sends
+        dev = send.device
+        n = int(counts[0]) if len(counts) else 0
+        cdev = "cpu" if self.staged else dev
+        sizes = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(self.world)]
+        self.dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=cdev), group=self.group)
+        sizes = [int(x.item()) for x in sizes]
+        m = max(sizes) if sizes else 0
+        src = self._host(send[:n])
+        padded = torch.zeros(max(m, 1), dtype=torch.int64, device=src.device)
+        padded[:n] = src
+        out = torch.empty(self.world * max(m, 1), dtype=torch.int64, device=src.device)
+        self.dist.all_gather_into_tensor(out, padded, group=self.group)
+        parts = [out[r * max(m, 1): r * max(m, 1) + sizes[r]] for r in range(self.world)]
+        full = torch.cat(parts)
+        self.bytes_sent += 8 * n * (self.world - 1)
+        return [full.to(dev) if full.device != dev else full]
+
+    def sum_int(self, values):
+        import torch
+
+        (v,) = values
+        t = torch.tensor([int(v)], dtype=torch.int64, device="cpu" if self.staged else "cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return int(t.item())
 
     def sum_(self, tensors):
         (t,) = tensors
@@ -356,6 +402,7 @@ class GraphShard:
         self._handle = h.value
         self._finalizer = weakref.finalize(self, lib.th_shard_destroy, self._handle)
         self.local_triples = int(lib.th_shard_local_triples(self._handle))
+        self.can_pull = bool(lib.th_shard_can_pull(self._handle))
         self._keep = None
 
     def launch_count(self) -> int:
@@ -384,10 +431,16 @@ class GraphShard:
         self._q = q
         _lib.check(_lib.load().th_shard_begin(self._handle, ctypes.byref(q)))
 
-    def expand(self, hop: int):
+    def frontier_cost(self, hop: int) -> int:
+        """This rank's frontier out-edge total (direction choice)."""
+        c = ctypes.c_int64()
+        _lib.check(_lib.load().th_shard_plan(self._handle, hop, ctypes.byref(c)))
+        return int(c.value)
+
+    def expand(self, hop: int, mode: int = 0):
         counts = (ctypes.c_int64 * self.plan.world)()
         ptr = ctypes.c_void_p()
-        _lib.check(_lib.load().th_shard_expand(self._handle, hop, counts, ctypes.byref(ptr)))
+        _lib.check(_lib.load().th_shard_expand(self._handle, hop, mode, counts, ctypes.byref(ptr)))
         cnt = [int(c) for c in counts]
         n = sum(cnt)
         send = _lib.as_tensor(ptr.value, (n,), "<i8", owner=self)
@@ -477,20 +530,34 @@ class ShardResult:
                                                        "a_ids")))
 
 
-def run_wave(shards, xch: Exchange, query: WaveQuery, stats: dict | None = None):
+PULL_DIVISOR = 8.0  # pull when the frontier's out-edges exceed T / 8 (as K2/K3)
+
+
+def run_wave(shards, xch: Exchange, query: WaveQuery, stats: dict | None = None,
+             n_triples: int | None = None, pull_divisor: float = PULL_DIVISOR):
     """Drive one wave through every hosted shard (Algorithm 1 per hop).
 
+    Per hop the ranks agree on a direction: push (candidate records to
+    their owners, all-to-all) or, for dense frontiers, pull (every rank's
+    owned frontier rows all-gathered, each owner pulls over its in-edges).
     Returns the hosted shards' ShardResults.  An output overflow on any
     rank makes every rank run the wave again with grown capacities.
     """
+    can_pull = n_triples is not None and pull_divisor > 0 and all(
+        getattr(sh, "can_pull", False) for sh in shards)
     for _attempt in range(4):
         for sh in shards:
             sh.begin(query)
         for h in range(1, query.k + 1):
-            sends = [sh.expand(h) for sh in shards]
+            mode = 0
+            if can_pull:
+                cost = xch.sum_int([sh.frontier_cost(h) for sh in shards])
+                mode = 1 if cost * pull_divisor > n_triples else 0
+            sends = [sh.expand(h, mode) if mode else sh.expand(h) for sh in shards]
             if stats is not None:
                 stats.setdefault("records", []).append(sum(sum(c) for _, c in sends))
-            recvs = xch.all_to_all(sends)
+                stats.setdefault("modes", []).append(mode)
+            recvs = xch.all_gather(sends) if mode else xch.all_to_all(sends)
             for sh, rv in zip(shards, recvs):
                 sh.absorb(h, rv)
             if h < query.k:  # the last layer is never expanded
@@ -570,12 +637,13 @@ class PartitionedGraph:
         # shards on disk and maps tids through tid_to_global the same way)
         self._cols = tuple(np.asarray(c.cpu().numpy() if hasattr(c, "cpu") else c, dtype=np.int32)
                            for c in cols)
+        self.pull_divisor = PULL_DIVISOR  # 0 = push only
         factory = shard_factory or GraphShard
         self.shards = [factory(cols, n_entities, n_relations, plan, r) for r in exchange.ranks]
 
     def run(self, query: WaveQuery, stats: dict | None = None):
         """One wave; the hosted ranks' partial results (kept sharded)."""
-        return run_wave(self.shards, self.exchange, query, stats)
+        return run_wave(self.shards, self.exchange, query, stats, self.n_triples, self.pull_divisor)
 
     def retrieve(self, seeds, k: int, relation_filter=None, semantics="frontier",
                  activated: bool = False):

@@ -34,14 +34,16 @@ def _hub_graph(E, T, R, seed, alpha=1.2):
     return key // E // R, (key // E) % R, key % E
 
 
+@pytest.mark.parametrize("direction", ["push", "auto", "pull"])
 @pytest.mark.parametrize("world,n_hubs", [(1, 0), (2, 0), (2, 5), (3, 7), (4, 16)])
 @pytest.mark.parametrize("sem", ["exact", "frontier", "cumulative"])
-def test_partitioned_equals_single_and_oracle(th, world, n_hubs, sem):
+def test_partitioned_equals_single_and_oracle(th, world, n_hubs, sem, direction):
     s, r, o = _hub_graph(1500, 30000, 24, seed=21)
     E, R = 1500, 24
     g = th.build_incidence((s, r, o), E, R)
     og = orc.build_csr(s, r, o, E, R)
     pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(world), n_hubs=n_hubs)
+    pg.pull_divisor = {"push": 0.0, "auto": 8.0, "pull": 1e18}[direction]
     assert sum(sh.local_triples for sh in pg.shards) == s.size  # each triple on one rank
     rng = np.random.default_rng(4)
     seeds = rng.integers(0, E, 300)
@@ -61,10 +63,12 @@ def test_partitioned_equals_single_and_oracle(th, world, n_hubs, sem):
 
 @pytest.mark.parametrize("world", [2, 4])
 def test_partitioned_relation_filter(th, world):
+    """Relation masks on push hops (world 2, auto) and on pull hops (world 4)."""
     s, r, o = _hub_graph(1200, 20000, 30, seed=8)
     E, R = 1200, 30
     og = orc.build_csr(s, r, o, E, R)
     pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(world), n_hubs=6)
+    pg.pull_divisor = 1e18 if world == 4 else 8.0  # world 4: every hop pulls
     rng = np.random.default_rng(2)
     seeds = rng.integers(0, E, 200)
     filt = [sorted(rng.choice(R, 5, replace=False).tolist()) for _ in seeds]
