@@ -139,15 +139,19 @@ constexpr int mat_warps() {
 constexpr unsigned kSparseBits = 5;       // tiles with <= this many bits per lane skip the transpose
 constexpr unsigned kCoopIdsPerQuery = 48;  // chunk ids per touched query for the cooperative write
 
-// sparse-chunk staging: a 64-slot ring per query (lane), flushed by the
-// whole warp 32 ids at a time so every store is a full coalesced run (no
-// scattered 4-byte stores, whose partially written sectors cost DRAM fills)
-constexpr int kRing = 64;
-constexpr int kRingStride = kRing + 1;
+// sparse-chunk staging: a small linear buffer per query (lane).  After every
+// tile (at most 32 new ids per lane) the lanes holding >= kFlushAt ids store
+// them as one coalesced run (no scattered 4-byte stores, whose partially
+// written sectors cost DRAM fills), so a buffer never exceeds
+// kFlushAt - 1 + 32 ids and the whole per-warp staging stays small enough
+// for three 8-warp CTAs per SM.
+constexpr int kFlushAt = 8;
+constexpr int kBuf = kFlushAt + 32;
+constexpr int kRingStride = kBuf + 1;
 constexpr int kRingWords = 32 * kRingStride;
 
 // per-warp shared words: WRITE = S (32 x kSStride) + a region shared by the
-// dense-chunk staging run (kChunkRows ids) and the sparse-chunk rings
+// dense-chunk staging run (kChunkRows ids) and the sparse-chunk buffers
 // (emptied before a dense chunk); COUNT = per-query counters + degree sums
 template <bool WRITE, bool RING = false>
 constexpr size_t mat_warp_words() {
@@ -155,43 +159,23 @@ constexpr size_t mat_warp_words() {
                : 64;
 }
 
-// lanes whose ring holds >= 32 ids store 32 of them (all 32 lanes, converged)
-__device__ __forceinline__ void ring_flush_full(const int32_t* ring, int& head, int& fill,
-                                                int64_t& pos, int32_t* out, int64_t cap) {
+// lanes whose buffer holds >= `at` ids store all of them (all 32 lanes, converged)
+__device__ __forceinline__ void buf_flush(const int32_t* buf, int& fill, int64_t& pos, int32_t* out,
+                                          int64_t cap, int at) {
   const unsigned lane = lane_id();
-  unsigned need = __ballot_sync(TH_FULL, fill >= 32);
-  while (need) {
-    const int b = __ffs(need) - 1;
-    need &= need - 1u;
-    const int hb = __shfl_sync(TH_FULL, head, b);
-    const int64_t pb = __shfl_sync(TH_FULL, pos, b);
-    const int32_t id = ring[b * kRingStride + ((hb + (int)lane) & (kRing - 1))];
-    if (pb + (int64_t)lane < cap) out[pb + lane] = id;
-    if ((int)lane == b) {
-      head = (head + 32) & (kRing - 1);
-      fill -= 32;
-      pos += 32;
-    }
-  }
-}
-
-// every lane's remaining (< 32) ids
-__device__ __forceinline__ void ring_flush_all(const int32_t* ring, int& head, int& fill,
-                                               int64_t& pos, int32_t* out, int64_t cap) {
-  const unsigned lane = lane_id();
-  unsigned need = __ballot_sync(TH_FULL, fill > 0);
+  unsigned need = __ballot_sync(TH_FULL, fill >= at && fill > 0);
   while (need) {
     const int b = __ffs(need) - 1;
     need &= need - 1u;
     const int nb = __shfl_sync(TH_FULL, fill, b);
-    const int hb = __shfl_sync(TH_FULL, head, b);
     const int64_t pb = __shfl_sync(TH_FULL, pos, b);
-    if ((int)lane < nb && pb + (int64_t)lane < cap)
-      out[pb + lane] = ring[b * kRingStride + ((hb + (int)lane) & (kRing - 1))];
+    for (int o = 0; o < nb; o += 32) {
+      const int i = o + (int)lane;
+      if (i < nb && pb + i < cap) out[pb + i] = buf[b * kRingStride + i];
+    }
     if ((int)lane == b) {
-      head = (head + nb) & (kRing - 1);
-      fill = 0;
       pos += nb;
+      fill = 0;
     }
   }
   __syncwarp();
@@ -270,7 +254,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
   int32_t* stg = LOAD_S ? reinterpret_cast<int32_t*>(mat_smem + (size_t)warp * mat_load_words<RING>())
                         : reinterpret_cast<int32_t*>(S + 32 * kSStride);
   int32_t* ring = stg;  // sparse chunks (empty whenever stg is in use)
-  int head = 0, fill = 0;
+  int fill = 0;  // sparse-chunk buffer of this lane's query
   // COUNT: [32] ids + [32] degree sums per query (sparse tiles), after S
   // when the pass also builds S
   uint32_t* cnt = BUILD_S && !WRITE ? S + 32 * kSStride : S;  // (unused when LOAD_S)
@@ -419,17 +403,17 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
         uint32_t m = q >= src.nq ? 0u : LOAD_S ? sc.S[sbase + lane * 32 + t] : S[lane * kSStride + t];
         const int64_t rb = c0 + 32 * t;
         while (m) {
-          ring[lane * kRingStride + ((head + fill) & (kRing - 1))] = src.id(rb + __ffs(m) - 1);
+          ring[lane * kRingStride + fill] = src.id(rb + __ffs(m) - 1);
           ++fill;
           m &= m - 1u;
         }
         __syncwarp();
-        ring_flush_full(ring, head, fill, pos, out, cap);
+        buf_flush(ring, fill, pos, out, cap, kFlushAt);
       }
       __syncwarp();
       continue;
     }
-    if (RING) ring_flush_all(ring, head, fill, pos, out, cap);  // keep order; frees stg
+    if (RING) buf_flush(ring, fill, pos, out, cap, 1);  // keep order; frees stg
     unsigned todo = touched;
     while (todo) {
       const int b = __ffs(todo) - 1;
@@ -461,7 +445,7 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
       __syncwarp();
     }
   }
-  if (WRITE && RING) ring_flush_all(ring, head, fill, pos, out, cap);
+  if (WRITE && RING) buf_flush(ring, fill, pos, out, cap, 1);
   if (!WRITE) {
     __syncwarp();
     total += (int32_t)cnt[lane];
