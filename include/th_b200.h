@@ -165,6 +165,14 @@ int th_session_set_list_min_entities(th_session* s, int64_t min_entities);
 /* Overlap hop h's frontier materialisation (K4) with hop h+1's expansion
  * on an internal stream (frontier-only runs).  Default on. */
 int th_session_set_overlap(th_session* s, int on);
+/* CUDA-graph replay (default on): a TH_SINGLETON_SEEDS query with the same
+ * shape (B, k, semantics, flags, masks, max_paths, capacities, knobs) as the
+ * previous run is captured once and then replayed as one graph launch.
+ * Inputs are copied into session buffers first, so callers may reuse or
+ * free theirs after th_run as before.  Under profiling the timing events are
+ * part of the graph; a run whose previous events were not yet drained
+ * (th_finish / th_session_profile) runs eagerly. */
+int th_session_set_graphs(th_session* s, int on);
 /* Number of kernels this session has launched since creation. */
 int64_t th_session_launch_count(const th_session* s);
 

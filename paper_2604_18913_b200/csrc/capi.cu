@@ -225,6 +225,15 @@ int th_session_set_list_min_entities(th_session* s, int64_t min_entities) {
   return TH_OK;
 }
 
+int th_session_set_graphs(th_session* s, int on) {
+  if (!s) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  s->s.use_graphs = on != 0;
+  return TH_OK;
+}
+
 int th_session_set_overlap(th_session* s, int on) {
   if (!s) {
     th::set_error("NULL handle");

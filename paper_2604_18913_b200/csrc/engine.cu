@@ -643,6 +643,8 @@ __global__ void __launch_bounds__(kCompactThreads) flag_write_kernel(const uint3
 
 // ---------------------------------------------------------------- host
 
+std::atomic<uint64_t> g_alloc_epoch{0};
+
 template <typename T>
 T* ensure(DBuf& b, int64_t n, cudaStream_t st) {
   const size_t need = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
@@ -651,6 +653,7 @@ T* ensure(DBuf& b, int64_t n, cudaStream_t st) {
     b.p = nullptr;
     TH_CUDA(cudaMallocAsync(&b.p, need, st));
     b.bytes = need;
+    g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
   }
   return static_cast<T*>(b.p);
 }
@@ -975,6 +978,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
         TH_CUDA(cudaStreamWaitEvent(s->side, s->ev_expand[h], 0));
       }
       StreamScope sc(s, overlap ? s->side : st);
+      {
+      // (the scope's end event must precede the join event below)
       ProfScope ps(s, TH_PROF_FRONTIER);
       if (sem == TH_CUMULATIVE)
         materialize_dense<W>(s, b, b.V, b.S, b.Vf, nq, f_off + (h - 1) * B + q0,
@@ -993,6 +998,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
                              f_len + (h - 1) * B + q0, static_cast<int32_t*>(s->f_ids.p), s->f_cap,
                              &b.ctl->ids_used, es);
         next_edges_done = es.out != nullptr;
+      }
       }
       if (overlap) TH_CUDA(cudaEventRecord(s->ev_mat[h], s->side));
     }
@@ -1043,7 +1049,9 @@ ProfScope::ProfScope(Session* s_, int c) : s(s_), cat(c), l0(s_->launches) {
       s->ev_pool.push_back(e);
     }
   }
-  TH_CUDA(cudaEventRecord(s->ev_pool[s->ev_used], s->st));
+  // external: a captured record becomes a real event node of the graph
+  TH_CUDA(cudaEventRecordWithFlags(s->ev_pool[s->ev_used], s->st,
+                                   s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
 }
 
 ProfScope::~ProfScope() noexcept(false) {
@@ -1057,7 +1065,8 @@ ProfScope::~ProfScope() noexcept(false) {
     std::fprintf(stderr, "[th] done %s\n", names[cat]);
   }
   if (!s->prof) return;
-  TH_CUDA(cudaEventRecord(s->ev_pool[s->ev_used + 1], s->st));
+  TH_CUDA(cudaEventRecordWithFlags(s->ev_pool[s->ev_used + 1], s->st,
+                                   s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
   s->ev_used += 2;
   s->pending_cat.push_back(cat);
   s->pending_launch.push_back(s->launches - l0);
@@ -1096,6 +1105,152 @@ int session_wave_lists(Session* s, int64_t* lens, int n) {
   return TH_OK;
 }
 
+static int run_body(Session* s, const th_query* q);
+
+// ---- CUDA-graph replay of repeated batch shapes ----
+// A wave is ~30 short launches whose grids and arguments depend only on the
+// query shape, the session buffers and the knobs (all control flow past the
+// seeds lives on the device in Ctl).  A query repeating the previous run's
+// key is captured once into a graph and replayed with one cudaGraphLaunch;
+// its inputs are first copied into session-owned staging buffers so the
+// graph's pointers stay valid.  Any buffer (re)allocation anywhere bumps
+// g_alloc_epoch and invalidates the graph.
+static bool graph_eligible(const Session* s, const th_query* q) {
+  static const bool debug_sync = std::getenv("TH_DEBUG_SYNC") != nullptr;
+  // profiling: event records are captured too, so a replay needs the
+  // previous run's events drained (th_finish / th_session_profile)
+  return s->use_graphs && !debug_sync && q->n_queries > 0 &&
+         (q->flags & TH_SINGLETON_SEEDS) && s->mat_rows < 0 &&
+         (!s->prof || (s->ev_used == 0 && s->pending_cat.empty()));
+}
+
+static GraphKey graph_key(const Session* s, const th_query* q) {
+  GraphKey k{};
+  k.B = q->n_queries;
+  k.k = q->k;
+  k.semantics = q->semantics;
+  k.flags = q->flags;
+  k.mask_words = q->d_rel_masks ? q->mask_words : -1;
+  k.max_paths = q->max_paths;
+  k.f_cap = std::max<int64_t>({s->f_cap, s->last_f_need, 1 << 16});
+  k.a_cap = std::max<int64_t>({s->a_cap, s->last_a_need, 1 << 16});
+  k.p_cap = std::max<int64_t>({s->p_cap, s->last_p_need, 1 << 12});
+  k.pull_divisor = s->pull_divisor;
+  k.list_min = s->list_min_entities;
+  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0);
+  k.epoch = g_alloc_epoch.load(std::memory_order_relaxed);
+  return k;
+}
+
+template <typename T>
+static const T* stage(DBuf& b, const T* src, int64_t n, cudaStream_t st) {
+  T* p = ensure<T>(b, n, st);
+  if (n > 0) TH_CUDA(cudaMemcpyAsync(p, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
+  return p;
+}
+
+static void drop_graph(Session* s) {
+  if (s->gexec) cudaGraphExecDestroy(s->gexec);
+  s->gexec = nullptr;
+  s->g_valid = false;
+}
+
+static int run_graphed(Session* s, const th_query* q) {
+  cudaStream_t st = s->st;
+  const int64_t B = q->n_queries;
+  th_query qs = *q;
+  // stage inputs (seeds: one per query under TH_SINGLETON_SEEDS)
+  qs.d_seed_offsets = stage(s->in_offs, q->d_seed_offsets, B + 1, st);
+  qs.d_seeds = stage(s->in_seeds, q->d_seeds, B, st);
+  if (q->d_rel_masks)
+    qs.d_rel_masks = stage(s->in_masks, q->d_rel_masks, B * (int64_t)q->mask_words, st);
+  const GraphKey key = graph_key(s, &qs);
+  if (s->gexec && s->g_valid && key == s->gkey) {
+    TH_CUDA(cudaGraphLaunch(s->gexec, st));
+    s->launches += s->g_launches;
+    if (s->prof) {
+      s->pending_cat = s->g_pend_cat;
+      s->pending_launch = s->g_pend_launch;
+      s->ev_used = s->g_ev_used;
+    }
+    s->last = qs;
+    s->has_run = true;
+    return TH_OK;
+  }
+  if (!(s->g_seen && key == s->gkey)) {
+    // first run of this shape: run eagerly (sizes every buffer), remember it
+    drop_graph(s);
+    const int rc = run_body(s, &qs);
+    s->gkey = graph_key(s, &qs);
+    s->g_seen = rc == TH_OK;
+    return rc;
+  }
+  // second run of the same shape: capture, instantiate, launch
+  drop_graph(s);
+  const int64_t l0 = s->launches;
+  cudaGraph_t graph = nullptr;
+  // capture on a session-owned stream (the caller's may be the legacy
+  // default stream, which cannot capture); nothing runs during capture, and
+  // the graph is launched on the caller's stream
+  if (!s->cap) TH_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
+  TH_CUDA(cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal));
+  int rc = TH_OK;
+  const char* fail = nullptr;
+  cudaError_t fail_code = cudaSuccess;
+  s->st = s->cap;
+  s->capturing = true;
+  try {
+    rc = run_body(s, &qs);
+  } catch (const CudaError& e) {
+    fail = e.where;
+    fail_code = e.code;
+  }
+  s->capturing = false;
+  s->st = st;
+  cudaError_t ce = cudaStreamEndCapture(s->cap, &graph);
+  if (fail || rc != TH_OK || ce != cudaSuccess) {
+    // capture is a pure optimisation: drop it and run this query eagerly
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    static const bool dbg = std::getenv("TH_GRAPH_DEBUG") != nullptr;
+    if (dbg)
+      std::fprintf(stderr, "[th] graph capture failed: %s: %s (end: %s)\n", fail ? fail : "rc",
+                   cudaGetErrorString(fail_code), cudaGetErrorString(ce));
+    s->g_seen = false;
+    s->launches = l0;
+    s->pending_cat.clear();
+    s->pending_launch.clear();
+    s->ev_used = 0;
+    if (rc != TH_OK && !fail) return rc;
+    s->g_failures += 1;
+    if (s->g_failures >= 3) s->use_graphs = false;
+    return run_body(s, &qs);
+  }
+  const uint64_t epoch = g_alloc_epoch.load(std::memory_order_relaxed);
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  TH_CUDA(ie);
+  s->gexec = exec;
+  s->g_launches = s->launches - l0;
+  s->g_pend_cat = s->pending_cat;
+  s->g_pend_launch = s->pending_launch;
+  s->g_ev_used = s->ev_used;
+  s->launches = l0 + s->g_launches;
+  s->gkey = key;
+  // an allocation inside the capture would leave the graph pointing at
+  // freed memory: never replay such a graph (sizes are stable on a repeat,
+  // so this is a guard, not a path)
+  s->g_valid = epoch == key.epoch;
+  if (!s->g_valid) {
+    drop_graph(s);
+    s->g_seen = false;
+    return run_body(s, &qs);
+  }
+  TH_CUDA(cudaGraphLaunch(s->gexec, st));
+  return TH_OK;
+}
+
 int session_run(Session* s, const th_query* q) {
   const Graph* g = s->g;
   if (q->k < 1) {
@@ -1122,6 +1277,12 @@ int session_run(Session* s, const th_query* q) {
     set_error("max_paths must be >= 0");
     return TH_ERR_INVALID;
   }
+  if (graph_eligible(s, q)) return run_graphed(s, q);
+  return run_body(s, q);
+}
+
+static int run_body(Session* s, const th_query* q) {
+  const Graph* g = s->g;
   cudaStream_t st = s->st;
   const int64_t B = q->n_queries, k = q->k;
   const int64_t kb = std::max<int64_t>(k * B, 1);
@@ -1263,11 +1424,12 @@ int session_finish(Session* s, th_result* out) {
 }
 
 void session_free(Session* s) {
+  drop_graph(s);
   for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
                   &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
                   &s->p_scratch, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta,
-                  &s->heavy_off}) {
+                  &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks}) {
     if (d->p) cudaFreeAsync(d->p, s->st);
     d->p = nullptr;
     d->bytes = 0;
@@ -1283,6 +1445,10 @@ void session_free(Session* s) {
     }
     cudaStreamDestroy(s->side);
     s->side = nullptr;
+  }
+  if (s->cap) {
+    cudaStreamDestroy(s->cap);
+    s->cap = nullptr;
   }
 }
 

@@ -33,6 +33,19 @@ struct DBuf {
   size_t bytes = 0;
 };
 
+// shape of a run a captured CUDA graph is valid for (engine.cu run_graphed)
+struct GraphKey {
+  int64_t B, k, semantics, flags, mask_words, max_paths, f_cap, a_cap, p_cap, list_min, knobs;
+  double pull_divisor;
+  uint64_t epoch;
+  bool operator==(const GraphKey& o) const {
+    return B == o.B && k == o.k && semantics == o.semantics && flags == o.flags &&
+           mask_words == o.mask_words && max_paths == o.max_paths && f_cap == o.f_cap &&
+           a_cap == o.a_cap && p_cap == o.p_cap && list_min == o.list_min && knobs == o.knobs &&
+           pull_divisor == o.pull_divisor && epoch == o.epoch;
+  }
+};
+
 struct Session {
   Graph* g = nullptr;
   cudaStream_t st = nullptr;
@@ -71,6 +84,19 @@ struct Session {
   int64_t prof_launches[TH_PROF_CATEGORIES] = {};
   int64_t wave_lists[kMaxK + 2] = {};
   int last_k = 0;
+  // CUDA-graph replay of repeated shapes
+  bool use_graphs = true;
+  cudaStream_t cap = nullptr;       // capture stream
+  bool capturing = false;
+  DBuf in_offs, in_seeds, in_masks;
+  cudaGraphExec_t gexec = nullptr;
+  GraphKey gkey{};
+  bool g_seen = false, g_valid = false;
+  int64_t g_launches = 0;
+  std::vector<int> g_pend_cat;     // profile scopes the graph records
+  std::vector<int64_t> g_pend_launch;
+  size_t g_ev_used = 0;
+  int g_failures = 0;               // captures that fell back to eager runs
 };
 
 // RAII timing scope for one kernel group

@@ -199,6 +199,10 @@ class Retriever:
         """Overlap hop h's K4 with hop h+1's expansion (frontier-only runs)."""
         _lib.check(_lib.load().th_session_set_overlap(self._handle, int(bool(on))))
 
+    def set_graphs(self, on: bool) -> None:
+        """Replay repeated batch shapes as one captured CUDA graph."""
+        _lib.check(_lib.load().th_session_set_graphs(self._handle, int(bool(on))))
+
     def launch_count(self) -> int:
         return int(_lib.load().th_session_launch_count(self._handle))
 

@@ -1,0 +1,98 @@
+"""CUDA-graph replay of repeated batch shapes (engine.cu run_graphed).
+
+A session captures the second run of a shape and replays it from then on;
+every replayed result must equal an eager session's, bit for bit, while the
+seeds, masks and output capacities change underneath it."""
+
+import numpy as np
+import pytest
+
+from oracle import khop_oracle as orc
+from test_gpu_parity import _hub_graph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def th(cuda_device):
+    import paper_2604_18913_b200 as th
+
+    return th
+
+
+def _same(a, b):
+    for name in ("edges", "frontier_off", "frontier_len", "frontier_ids", "act_off", "act_len",
+                 "act_ids", "path_off", "path_count", "path_tids", "path_truncated"):
+        x, y = getattr(a, name), getattr(b, name)
+        assert (x is None) == (y is None), name
+        if x is not None:
+            assert x.shape == y.shape and bool((x == y).all()), name
+
+
+@pytest.mark.parametrize("paths", [False, True], ids=["frontier", "paths"])
+@pytest.mark.parametrize("sem", ["exact", "frontier", "cumulative"])
+def test_replay_matches_eager(th, sem, paths):
+    s, r, o = _hub_graph(3000, 60000, 48, seed=21)
+    E, R = 3000, 48
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    graphed, eager = th.Retriever(g), th.Retriever(g)
+    eager.set_graphs(False)
+    rng = np.random.default_rng(4)
+    B, k = 700, 3 if not paths else 2
+    for it in range(6):
+        seeds = rng.integers(0, E, B)
+        filt = None
+        if it >= 3:  # three runs of each shape: eager, capture, replay
+            filt = [sorted(rng.choice(R, 8, replace=False).tolist()) for _ in range(B)]
+        kw = dict(relation_filter=filt, semantics=sem, paths=paths, max_paths=200, activated=paths)
+        l0 = graphed.launch_count()
+        a = graphed.retrieve(seeds, k, **kw)
+        b = eager.retrieve(seeds, k, **kw)
+        _same(a, b)
+        assert graphed.launch_count() > l0
+        for i in (0, B // 2, B - 1):
+            ref = orc.retrieve_one(og, int(seeds[i]), k, sem, None if filt is None else filt[i],
+                                   paths=paths, max_paths=200)
+            for h in range(k):
+                assert np.array_equal(a.frontier(i, h + 1), ref["frontiers"][h]), (it, i, h)
+            if paths:
+                assert a.path_tid_tuples(i) == ref["paths"]
+
+
+def test_replay_grows_capacity_and_shape_changes(th):
+    """Small outputs first (graph captured with small capacities), then a batch
+    of hub seeds with the same shape overflows them: the run is redone
+    eagerly and later replays use the grown buffers; a new B re-captures."""
+    s, r, o = _hub_graph(4000, 120000, 16, seed=8)
+    E, R = 4000, 16
+    g = th.build_incidence((s, r, o), E, R)
+    graphed, eager = th.Retriever(g), th.Retriever(g)
+    eager.set_graphs(False)
+    deg = np.bincount(s, minlength=E)
+    leaves = np.flatnonzero(deg == 0)
+    hubs = np.argsort(-deg)[:64]
+    rng = np.random.default_rng(1)
+    B = 1024
+    batches = [rng.choice(leaves, B)] * 3 + [rng.choice(hubs, B)] * 3
+    batches += [rng.integers(0, E, 300)] * 3 + [rng.integers(0, E, B)]
+    for seeds in batches:
+        _same(graphed.retrieve(seeds, 3), eager.retrieve(seeds, 3))
+
+
+def test_profiling_under_replay(th):
+    """Timing events are captured with the kernels: every replay reports the
+    same launch counts per category as the eager run, with real times."""
+    s, r, o = _hub_graph(1000, 10000, 8, seed=2)
+    g = th.build_incidence((s, r, o), 1000, 8)
+    ret = th.Retriever(g)
+    ret.set_profiling(True)
+    seeds = np.arange(200)
+    first = ret.retrieve(seeds, 2)
+    eager = ret.profile()
+    assert sum(n for _ms, n in eager.values()) > 0
+    for _ in range(3):
+        _same(ret.retrieve(seeds, 2), first)
+        prof = ret.profile()
+        assert {c: n for c, (_ms, n) in prof.items()} == {c: n for c, (_ms, n) in eager.items()}
+        assert sum(ms for ms, _n in prof.values()) > 0
