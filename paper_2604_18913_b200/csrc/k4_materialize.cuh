@@ -414,18 +414,28 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
       continue;
     }
     if (RING) buf_flush(ring, fill, pos, out, cap, 1);  // keep order; frees stg
+    // entity layers without a row map stage final ids (the copy-out is then
+    // a plain move); otherwise chunk-relative positions resolved on the way out
+    const bool direct = !Src::kRing && Src::kDense && src.map == nullptr;
+    const int32_t rbase = direct ? (int32_t)(c0 + 32 * lane) : 32 * lane;
     unsigned todo = touched;
+    // the next query's masks are loaded while the current one is written
+    int nb_ = todo ? __ffs(todo) - 1 : 0;
+    uint32_t m_next = 0u;
+    if (todo) m_next = LOAD_S ? sc.S[sbase + nb_ * 32 + lane] : S[nb_ * kSStride + lane];
     while (todo) {
-      const int b = __ffs(todo) - 1;
+      const int b = nb_;
+      uint32_t m = m_next;
       todo &= todo - 1u;
-      uint32_t m = LOAD_S ? sc.S[sbase + b * 32 + lane] : S[b * kSStride + lane];
+      if (todo) {
+        nb_ = __ffs(todo) - 1;
+        m_next = LOAD_S ? sc.S[sbase + nb_ * 32 + lane] : S[nb_ * kSStride + lane];
+      }
       const int c = __popc(m);
       const int incl = warp_incl_scan(c);
       const int n = __shfl_sync(TH_FULL, incl, 31);
       // highest set bit first, filling the lane's run from its end (FLO
-      // gives the top bit directly; no bit reversal per id).  The run holds
-      // chunk-relative row positions; ids are resolved on the way out.
-      const int32_t rbase = 32 * lane;
+      // gives the top bit directly; no bit reversal per id)
       int32_t* dst = stg + incl - 1;
       while (m) {
         const int bit = 31 - __clz((int)m);
@@ -434,7 +444,22 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
       }
       __syncwarp();
       const int64_t pb = __shfl_sync(TH_FULL, pos, b);
-      if (pb + n <= cap) {
+      if (direct && pb + n <= cap) {
+        int32_t* o = out + pb + lane;
+        const int32_t* sp = stg + lane;
+        int i = lane;
+        for (; i + 96 < n; i += 128, o += 128, sp += 128) {
+          const int32_t v0 = sp[0], v1 = sp[32], v2 = sp[64], v3 = sp[96];
+          o[0] = v0;
+          o[32] = v1;
+          o[64] = v2;
+          o[96] = v3;
+        }
+        for (; i < n; i += 32, o += 32, sp += 32) *o = *sp;
+      } else if (direct) {
+        for (int i = lane; i < n; i += 32)
+          if (pb + i < cap) out[pb + i] = stg[i];
+      } else if (pb + n <= cap) {
         int32_t* o = out + pb;
         for (int i = lane; i < n; i += 32) o[i] = src.id(c0 + stg[i]);
       } else {
