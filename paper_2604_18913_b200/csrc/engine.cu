@@ -718,7 +718,8 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
     if (s->k4_cache && nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
       SCache sc;
       sc.S = ensure<uint32_t>(s->k4_S, nchunks * W * 1024, s->st);
-      sc.meta = ensure<uint2>(s->k4_meta, nchunks * W, s->st);
+      sc.meta = ensure<uint2>(s->k4_meta, nchunks * W + 1, s->st);
+      sc.work = reinterpret_cast<unsigned*>(sc.meta + nchunks * W);
       constexpr size_t smem_cc = (size_t)NW * (32 * kSStride + 64) * sizeof(uint32_t);
       constexpr size_t smem_wc = (size_t)NW * mat_load_words<Src::kRing>() * sizeof(uint32_t);
       static std::atomic<uint64_t> attr_c{0};
@@ -742,7 +743,9 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
       TH_LAUNCHED();
       mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
       TH_LAUNCHED();
-      mat_kernel<W, Src, true, false, 2><<<grid, 32 * NW, smem_wc, s->st>>>(
+      // (warps pull units from a counter: at most one resident wave of CTAs)
+      const unsigned wgrid = std::min<unsigned>(grid, kNumSMs * (2048 / (32 * NW)));
+      mat_kernel<W, Src, true, false, 2><<<wgrid, 32 * NW, smem_wc, s->st>>>(
           src, nblk, b.counts, off, out, cap, EdgeSum{}, sc);
       TH_LAUNCHED();
       s->launches += 4;

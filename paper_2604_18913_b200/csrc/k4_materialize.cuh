@@ -224,23 +224,20 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 struct SCache {
   uint32_t* S = nullptr;
   uint2* meta = nullptr;
+  unsigned* work = nullptr;  // unit counter of the write pass (zeroed by the count pass)
 };
 
-template <int W, class Src, bool WRITE, bool EDGES = false, int CACHE = 0>
-__global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int nblk,
-                                                                   int32_t* counts,
-                                                                   const int64_t* base, int32_t* out,
-                                                                   int64_t cap, EdgeSum es = {},
-                                                                   SCache sc = {}) {
+// one (row block, word) unit of a pass: warp `warp` of its CTA, word j
+template <int W, class Src, bool WRITE, bool EDGES, int CACHE>
+__device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* counts,
+                                         const int64_t* base, int32_t* out, int64_t cap,
+                                         const EdgeSum& es, const SCache& sc, int blk, int j,
+                                         int warp, int lane) {
   // CACHE 1 = count pass that stores S, CACHE 2 = write pass that loads it
   constexpr bool BUILD_S = WRITE ? CACHE != 2 : CACHE == 1;
   constexpr bool LOAD_S = WRITE && CACHE == 2;
   extern __shared__ uint32_t mat_smem[];
   constexpr int NW = mat_warps<W>();
-  constexpr int NG = W / NW;  // word groups
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int blk = blockIdx.x / NG;
-  const int j = (blockIdx.x % NG) * NW + warp;
   const int q = 32 * j + lane;
   if (blk >= nblk) return;
   // WRITE: S[32][kSStride] + staging run; COUNT: per-query counters
@@ -479,5 +476,36 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
       counts[(size_t)q * nblk + blk] = total;
       if (EDGES && esum) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), esum);
     }
+  }
+}
+
+template <int W, class Src, bool WRITE, bool EDGES = false, int CACHE = 0>
+__global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int nblk,
+                                                                   int32_t* counts,
+                                                                   const int64_t* base, int32_t* out,
+                                                                   int64_t cap, EdgeSum es = {},
+                                                                   SCache sc = {}) {
+  constexpr int NW = mat_warps<W>();
+  constexpr int NG = W / NW;  // word groups
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (WRITE && CACHE == 2) {
+    // cached write pass: warps are independent (no shared row sectors), so
+    // each takes (block, word) units from a counter until none are left --
+    // no wave-quantisation tail, dense and sparse units balance out
+    const int units = nblk * W;
+    for (;;) {
+      int u = 0;
+      if (lane == 0) u = (int)atomicAdd(sc.work, 1u);
+      u = __shfl_sync(TH_FULL, u, 0);
+      if (u >= units) return;
+      mat_unit<W, Src, WRITE, EDGES, CACHE>(src, nblk, counts, base, out, cap, es, sc, u / W, u % W,
+                                            warp, lane);
+      __syncwarp();
+    }
+  } else {
+    if (CACHE == 1 && blockIdx.x == 0 && threadIdx.x == 0) *sc.work = 0u;  // for the write pass
+    mat_unit<W, Src, WRITE, EDGES, CACHE>(src, nblk, counts, base, out, cap, es, sc,
+                                          (int)blockIdx.x / NG, ((int)blockIdx.x % NG) * NW + warp,
+                                          warp, lane);
   }
 }
