@@ -720,7 +720,7 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
       sc.S = ensure<uint32_t>(s->k4_S, nchunks * W * 1024, s->st);
       sc.meta = ensure<uint2>(s->k4_meta, nchunks * W + 1, s->st);
       sc.work = reinterpret_cast<unsigned*>(sc.meta + nchunks * W);
-      constexpr size_t smem_cc = (size_t)NW * (32 * kSStride + 64) * sizeof(uint32_t);
+      constexpr size_t smem_cc = ((size_t)NW * (32 * kSStride + 64) + kEdgeWords) * sizeof(uint32_t);
       constexpr size_t smem_wc = (size_t)NW * mat_load_words<Src::kRing>() * sizeof(uint32_t);
       static std::atomic<uint64_t> attr_c{0};
       if (!(attr_c.load(std::memory_order_relaxed) & bit)) {

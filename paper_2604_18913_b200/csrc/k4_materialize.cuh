@@ -187,9 +187,13 @@ constexpr size_t mat_load_words() {
   return RING && kRingWords > kChunkRows ? kRingWords : kChunkRows;
 }
 
+// CTA-shared words of an EDGES count pass (degree planes, see mat_unit)
+constexpr size_t kEdgeWords = 32 * 8 + 64;
+
 template <int W, bool WRITE, bool RING = false>
 constexpr size_t mat_smem_bytes() {
-  return (size_t)mat_warps<W>() * mat_warp_words<WRITE, RING>() * sizeof(uint32_t);
+  return ((size_t)mat_warps<W>() * mat_warp_words<WRITE, RING>() + (WRITE ? 0 : kEdgeWords)) *
+         sizeof(uint32_t);
 }
 
 // EDGES (COUNT pass over an entity layer): also sum the out-degrees of each
@@ -256,6 +260,9 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
   // when the pass also builds S
   uint32_t* cnt = BUILD_S && !WRITE ? S + 32 * kSStride : S;  // (unused when LOAD_S)
   uint32_t* ecnt = cnt + 32;
+  // EDGES: CTA-shared degree planes [32 tiles][8], plane counts [32], big-row masks [32]
+  uint32_t* eplanes = mat_smem + (size_t)NW * kWarpWords;
+  uint32_t eplane_cnt[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
   if (!WRITE) {
     cnt[lane] = 0u;
     ecnt[lane] = 0u;
@@ -293,6 +300,28 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       nbits = lane == 0 ? mt.y : 0u;  // the warp sum below restores the chunk's ids
     }
     if constexpr (Src::kDense && !LOAD_S) cflags = src.chunk_flags(c0, rend);
+    if constexpr (EDGES) {
+      // degree bit planes of the chunk's rows, once per CTA (they depend on
+      // the rows only; every word-warp of the CTA reads them)
+      __syncthreads();  // the previous chunk's readers are done
+      for (int t = warp; t < 32; t += NW) {
+        const uint32_t ft = __shfl_sync(TH_FULL, cflags, t);
+        const uint32_t d = ((ft >> lane) & 1u) ? degree(es, src.id(c0 + 32 * t + lane)) : 0u;
+        const uint32_t lo = d & 0xffu;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t pk = __ballot_sync(TH_FULL, (lo >> k) & 1u);
+          if (lane == 0) eplanes[t * 8 + k] = pk;
+        }
+        const uint32_t big = __ballot_sync(TH_FULL, d > 0xffu);
+        const unsigned mx = __reduce_max_sync(TH_FULL, lo);
+        if (lane == 0) {
+          eplanes[256 + t] = 32 - __clz((int)mx);
+          eplanes[288 + t] = big;
+        }
+      }
+      __syncthreads();
+    }
 #pragma unroll 1
     for (int t0 = 0; t0 < (LOAD_S ? 0 : 32); t0 += 8) {
       uint32_t x[8], fl[8];
@@ -319,19 +348,17 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
         if (mx > kSparseBits) {
           const uint32_t m = transpose32(xu);
           if (EDGES) {
-            const uint32_t d =
-                ((fl[u] >> lane) & 1u) ? degree(es, src.id(r)) : 0u;
-            // low 8 bits by bit planes (one ballot each); the rare rows of
-            // degree >= 256 add their high part row by row
-            const int np = 32 - __clz((int)__reduce_max_sync(TH_FULL, d & 0xffu));
-            for (int k = 0; k < np; ++k)
-              esum += (unsigned long long)__popc(m & __ballot_sync(TH_FULL, (d >> k) & 1u)) << k;
-            unsigned big = __ballot_sync(TH_FULL, d > 0xffu);
-            while (big) {
-              const int i = __ffs(big) - 1;
-              big &= big - 1u;
-              const uint32_t hi = __shfl_sync(TH_FULL, d >> 8, i);
-              if ((m >> i) & 1u) esum += (unsigned long long)hi << 8;
+            // low 8 bits by the shared bit planes; the rare rows of degree
+            // >= 256 add their high part row by row
+            const int np = (int)eplanes[256 + t];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k < np) eplane_cnt[k] += __popc(m & eplanes[t * 8 + k]);
+            uint32_t bg = eplanes[288 + t] & m;
+            while (bg) {
+              const int i = __ffs(bg) - 1;
+              bg &= bg - 1u;
+              esum += (unsigned long long)(degree(es, src.id(c0 + 32 * t + i)) >> 8) << 8;
             }
           }
           if (BUILD_S) {
@@ -471,7 +498,11 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
   if (!WRITE) {
     __syncwarp();
     total += (int32_t)cnt[lane];
-    if (EDGES) esum += ecnt[lane];
+    if (EDGES) {
+      esum += ecnt[lane];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) esum += (unsigned long long)eplane_cnt[k] << k;
+    }
     if (q < src.nq) {
       counts[(size_t)q * nblk + blk] = total;
       if (EDGES && esum) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), esum);
