@@ -739,6 +739,12 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
         mat_kernel<W, Src, false, false, 1><<<grid, 32 * NW, smem_cc, s->st>>>(
             src, nblk, b.counts, nullptr, nullptr, 0, EdgeSum{}, sc);
       TH_LAUNCHED();
+      // the write pass reads only the cached masks: the layer itself is free
+      // (callers may clear it) once the count pass is done
+      if (s->mark_counted) {
+        TH_CUDA(cudaEventRecord(s->mark_counted, s->st));
+        s->counted_recorded = true;
+      }
       mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
       TH_LAUNCHED();
       mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
@@ -845,6 +851,7 @@ void ensure_side_stream(Session* s) {
   for (int i = 0; i < kMaxK + 2; ++i) {
     TH_CUDA(cudaEventCreateWithFlags(&s->ev_expand[i], cudaEventDisableTiming));
     TH_CUDA(cudaEventCreateWithFlags(&s->ev_mat[i], cudaEventDisableTiming));
+    TH_CUDA(cudaEventCreateWithFlags(&s->ev_cnt[i], cudaEventDisableTiming));
   }
 }
 
@@ -981,6 +988,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
         TH_CUDA(cudaStreamWaitEvent(s->side, s->ev_expand[h], 0));
       }
       StreamScope sc(s, overlap ? s->side : st);
+      s->mark_counted = overlap ? s->ev_cnt[h] : nullptr;
+      s->counted_recorded = false;
       {
       // (the scope's end event must precede the join event below)
       ProfScope ps(s, TH_PROF_FRONTIER);
@@ -1003,12 +1012,16 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
         next_edges_done = es.out != nullptr;
       }
       }
-      if (overlap) TH_CUDA(cudaEventRecord(s->ev_mat[h], s->side));
+      if (overlap) {
+        TH_CUDA(cudaEventRecord(s->ev_mat[h], s->side));
+        if (!s->counted_recorded) TH_CUDA(cudaEventRecord(s->ev_cnt[h], s->side));
+      }
+      s->mark_counted = nullptr;
     }
     {
       // retire X (rows of list segment h-1) and swap roles; with overlap the
       // layer's K4 (side stream) must be done reading it first
-      if (overlap && h > 1) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[h - 1], 0));
+      if (overlap && h > 1) TH_CUDA(cudaStreamWaitEvent(st, s->ev_cnt[h - 1], 0));
       ProfScope ps(s, TH_PROF_CLEAR);
       clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1, E);
       TH_LAUNCHED();
@@ -1020,17 +1033,22 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
     std::swap(a.X, a.N);
     std::swap(a.Xf, a.Nf);
   }
-  // leave every matrix zero for the next wave
-  if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k], 0));
-  ProfScope ps(s, TH_PROF_CLEAR);
-  clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, (int)k, (int)k, E);
-  TH_LAUNCHED();
-  s->launches += 1;
-  if (sem != TH_EXACT) {
-    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k, E);
+  // leave every matrix zero for the next wave (V is not read by the
+  // frontier K4, so its clear overlaps the last layer's materialisation)
+  {
+    ProfScope ps(s, TH_PROF_CLEAR);
+    if (sem != TH_EXACT) {
+      clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k, E);
+      TH_LAUNCHED();
+      s->launches += 1;
+    }
+    if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_cnt[k], 0));
+    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, (int)k, (int)k, E);
     TH_LAUNCHED();
     s->launches += 1;
   }
+  if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k], 0));
+  ProfScope ps(s, TH_PROF_CLEAR);
   if (sem == TH_CUMULATIVE) {
     clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0, E);
     TH_LAUNCHED();
@@ -1445,6 +1463,7 @@ void session_free(Session* s) {
     for (int i = 0; i < kMaxK + 2; ++i) {
       cudaEventDestroy(s->ev_expand[i]);
       cudaEventDestroy(s->ev_mat[i]);
+      cudaEventDestroy(s->ev_cnt[i]);
     }
     cudaStreamDestroy(s->side);
     s->side = nullptr;

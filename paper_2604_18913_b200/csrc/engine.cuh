@@ -60,6 +60,9 @@ struct Session {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_expand[kMaxK + 2] = {};
   cudaEvent_t ev_mat[kMaxK + 2] = {};
+  cudaEvent_t ev_cnt[kMaxK + 2] = {};  // K4 of the layer no longer reads it (count pass done)
+  cudaEvent_t mark_counted = nullptr;  // set by run_wave around a K4 call
+  bool counted_recorded = false;
   int64_t mat_rows = -1;
   const int32_t* row_map = nullptr;
   const int32_t* tid_map = nullptr;

@@ -279,7 +279,14 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
   const int64_t r_begin = (int64_t)blk * blk_rows;
   const int64_t rend = nrows < r_begin + blk_rows ? nrows : r_begin + blk_rows;
   for (int64_t c0 = r_begin; c0 < rend; c0 += kChunkRows) {
-    if (!src.chunk_any(c0, rend)) continue;
+    // (the cached write pass never reads the layer or its flags -- callers
+    // recycle both once the count pass is done -- so the count pass
+    // records empty chunks in the meta instead)
+    if (!LOAD_S && !src.chunk_any(c0, rend)) {
+      if (BUILD_S && !WRITE && lane == 0)
+        sc.meta[(size_t)(c0 / kChunkRows) * W + j] = make_uint2(0u, 0u);
+      continue;
+    }
     // keep the CTA's warps (words of the same rows) on the same chunk so
     // each row sector they share is fetched from L2 once and hit in L1
     // by the others (the write phase otherwise drifts them apart)

@@ -17,7 +17,10 @@ def main():
     for r in rows:
         if r and r[0].isdigit():
             f = lambda x: float(x) if x not in ("", "-") else 0.0  # noqa: E731
-            lines.append((int(r[0]), f(r[ii]), f(r[si]), r[1][:90]))
+            try:
+                lines.append((int(r[0]), f(r[ii]), f(r[si]), r[1][:90]))
+            except (ValueError, IndexError):
+                continue
     ti = sum(x[1] for x in lines) or 1
     ts = sum(x[2] for x in lines) or 1
     print(f"total inst {ti:.3e} samples {ts:.0f}")
