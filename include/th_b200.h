@@ -165,6 +165,10 @@ int th_session_set_list_min_entities(th_session* s, int64_t min_entities);
 /* Overlap hop h's frontier materialisation (K4) with hop h+1's expansion
  * on an internal stream (frontier-only runs).  Default on. */
 int th_session_set_overlap(th_session* s, int on);
+/* Pull hops whose frontier sources more than 1/divisor of all in-edges
+ * (by the frontier's out-degree sum) gather every in-neighbour row instead
+ * of testing frontier flags first (default 2; <= 0 never). */
+int th_session_set_dense_pull(th_session* s, double divisor);
 /* CUDA-graph replay (default on): a TH_SINGLETON_SEEDS query with the same
  * shape (B, k, semantics, flags, masks, max_paths, capacities, knobs) as the
  * previous run is captured once and then replayed as one graph launch.

@@ -25,7 +25,7 @@ EXPORTS = (
     "th_abi_version", "th_last_error", "th_graph_create", "th_graph_create_lkg", "th_graph_destroy",
     "th_graph_info_get", "th_session_create", "th_session_destroy", "th_run", "th_finish",
     "th_session_set_pull_divisor", "th_session_launch_count", "th_plan_owner_hash",
-    "th_session_set_list_min_entities", "th_session_set_overlap", "th_session_set_graphs",
+    "th_session_set_list_min_entities", "th_session_set_overlap", "th_session_set_graphs", "th_session_set_dense_pull",
     "th_session_set_profiling", "th_session_profile", "th_session_wave_lists",
     "th_shard_create", "th_shard_destroy", "th_shard_local_triples", "th_shard_launch_count",
     "th_shard_begin", "th_shard_plan", "th_shard_can_pull", "th_shard_expand", "th_shard_absorb",
@@ -102,6 +102,7 @@ def load():
         "th_session_set_list_min_entities": (ctypes.c_int, [_vp, ctypes.c_int64]),
         "th_session_set_overlap": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_session_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
+        "th_session_set_dense_pull": (ctypes.c_int, [_vp, ctypes.c_double]),
         "th_session_launch_count": (ctypes.c_int64, [_vp]),
         "th_plan_owner_hash": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, _vp]),
         "th_session_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),

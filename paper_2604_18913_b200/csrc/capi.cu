@@ -1,6 +1,7 @@
 // extern "C" boundary (include/th_b200.h).  No C++ exception crosses it:
 // every entry point converts failures into a status code plus a
 // thread-local message (th_last_error).
+#include <cstdlib>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -213,6 +214,15 @@ int th_session_set_pull_divisor(th_session* s, double pull_divisor) {
     return TH_ERR_INVALID;
   }
   s->s.pull_divisor = pull_divisor;
+  return TH_OK;
+}
+
+int th_session_set_dense_pull(th_session* s, double divisor) {
+  if (!s) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  s->s.dense_pull = divisor;
   return TH_OK;
 }
 

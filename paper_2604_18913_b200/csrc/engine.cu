@@ -120,7 +120,10 @@ __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
 }
 
 // begin hop h: place list segment h, choose the direction
-__global__ void begin_hop_kernel(Ctl* ctl, int h, int64_t T, double pull_divisor, int has_reverse) {
+// pull hops skip the per-edge frontier test when over 1/dense_div of the
+// in-edges come from the frontier (dense_div <= 0: never)
+__global__ void begin_hop_kernel(Ctl* ctl, int h, int64_t T, double pull_divisor, int has_reverse,
+                                 double dense_div = 0.0) {
   const int32_t prev = ctl->list_len[h - 1];
   ctl->list_off[h] = ctl->list_off[h - 1] + prev;
   ctl->list_len[h] = 0;
@@ -132,6 +135,8 @@ __global__ void begin_hop_kernel(Ctl* ctl, int h, int64_t T, double pull_divisor
     else if (pull_divisor > 0) pull = (double)ctl->push_cost[h - 1] * pull_divisor > (double)T;
   }
   ctl->mode[h] = pull;
+  // the frontier's out-degree sum is the number of in-edges it sources
+  ctl->dense[h] = pull && dense_div > 0 && (double)ctl->push_cost[h - 1] * dense_div > (double)T;
   if (pull) ctl->pull_hops++;
   else ctl->push_hops++;
 }
@@ -949,7 +954,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
     next_edges_done = false;
     {
       ProfScope ps(s, TH_PROF_SETUP);
-      begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, g->T, s->pull_divisor, g->rindptr != nullptr);
+      begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, g->T, s->pull_divisor, g->rindptr != nullptr,
+                                        s->dense_pull);
       TH_LAUNCHED();
       s->launches += 1;
     }
@@ -1035,14 +1041,16 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   }
   // leave every matrix zero for the next wave (V is not read by the
   // frontier K4, so its clear overlaps the last layer's materialisation)
-  {
+  if (sem != TH_EXACT) {
     ProfScope ps(s, TH_PROF_CLEAR);
-    if (sem != TH_EXACT) {
-      clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k, E);
-      TH_LAUNCHED();
-      s->launches += 1;
-    }
-    if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_cnt[k], 0));
+    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k, E);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
+  if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_cnt[k], 0));
+  {
+    // (outside the scope above: the wait is not clearing time)
+    ProfScope ps(s, TH_PROF_CLEAR);
     clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, (int)k, (int)k, E);
     TH_LAUNCHED();
     s->launches += 1;
@@ -1157,6 +1165,7 @@ static GraphKey graph_key(const Session* s, const th_query* q) {
   k.a_cap = std::max<int64_t>({s->a_cap, s->last_a_need, 1 << 16});
   k.p_cap = std::max<int64_t>({s->p_cap, s->last_p_need, 1 << 12});
   k.pull_divisor = s->pull_divisor;
+  k.dense_pull = s->dense_pull;
   k.list_min = s->list_min_entities;
   k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0);
   k.epoch = g_alloc_epoch.load(std::memory_order_relaxed);

@@ -18,6 +18,7 @@ struct Ctl {
   int64_t list_off[kMaxK + 2];
   unsigned long long push_cost[kMaxK + 2];
   int32_t mode[kMaxK + 2];  // 0 = push, 1 = pull
+  int32_t dense[kMaxK + 2]; // pull hop over a frontier that sources most in-edges
   int32_t heavy_len;
   int32_t err;
   int64_t ids_used;
@@ -36,13 +37,13 @@ struct DBuf {
 // shape of a run a captured CUDA graph is valid for (engine.cu run_graphed)
 struct GraphKey {
   int64_t B, k, semantics, flags, mask_words, max_paths, f_cap, a_cap, p_cap, list_min, knobs;
-  double pull_divisor;
+  double pull_divisor, dense_pull;
   uint64_t epoch;
   bool operator==(const GraphKey& o) const {
     return B == o.B && k == o.k && semantics == o.semantics && flags == o.flags &&
            mask_words == o.mask_words && max_paths == o.max_paths && f_cap == o.f_cap &&
            a_cap == o.a_cap && p_cap == o.p_cap && list_min == o.list_min && knobs == o.knobs &&
-           pull_divisor == o.pull_divisor && epoch == o.epoch;
+           pull_divisor == o.pull_divisor && dense_pull == o.dense_pull && epoch == o.epoch;
   }
 };
 
@@ -50,6 +51,7 @@ struct Session {
   Graph* g = nullptr;
   cudaStream_t st = nullptr;
   double pull_divisor = 8.0;
+  double dense_pull = 2.0;  // pull hops gather unconditionally above 1/dense_pull active in-edges
   int64_t list_min_entities = int64_t(4) << 20;  // K4 list-driven above this E
   // shards: K4 covers rows [0, mat_rows) (owned entities) and maps rows /
   // local triples to global ids; defaults cover the whole single graph

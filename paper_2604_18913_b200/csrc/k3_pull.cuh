@@ -60,6 +60,7 @@ __device__ __forceinline__ void st_words(uint32_t* p, const uint32_t (&v)[VEC]) 
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   if (a.ctl->mode[a.h] != 1) return;
+  const bool dense = a.ctl->dense[a.h] != 0;
   using RS = RowShape<W>;
   constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
   const unsigned lane = lane_id();
@@ -123,12 +124,24 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
           u_nx = __ldg(a.rsrc + lo + en);
           if (FILTER) rr_nx = (uint32_t)__ldg(a.rrel + lo + en);
         }
-        if (act) act = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
-        const unsigned gm = (__ballot_sync(TH_FULL, act) & gbits) >> (grp * LPR);
-        const int cnt = __popc(gm);
-        const int srcp = part < cnt ? (int)__fns(gm, 0, part + 1) : 0;
-        const int32_t uc = __shfl_sync(TH_FULL, u, grp * LPR + srcp);
-        const uint32_t rc = FILTER ? __shfl_sync(TH_FULL, rr, grp * LPR + srcp) : 0u;
+        int cnt;
+        int32_t uc;
+        uint32_t rc;
+        if (dense) {
+          // most in-edges come from the frontier: gather every source row
+          // (a non-frontier row is zero) instead of testing flags first,
+          // which saves a dependent L2 round trip and the compaction
+          cnt = done ? 0 : min(max(len - e0, 0), LPR);
+          uc = u;
+          rc = rr;
+        } else {
+          if (act) act = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
+          const unsigned gm = (__ballot_sync(TH_FULL, act) & gbits) >> (grp * LPR);
+          cnt = __popc(gm);
+          const int srcp = part < cnt ? (int)__fns(gm, 0, part + 1) : 0;
+          uc = __shfl_sync(TH_FULL, u, grp * LPR + srcp);
+          rc = FILTER ? __shfl_sync(TH_FULL, rr, grp * LPR + srcp) : 0u;
+        }
         // steps where no group of the warp found a frontier in-edge skip the
         // (fully unrolled, up to LPR loads in flight) row gathers entirely;
         // bounding the unrolled loop by the busiest group measured slower at

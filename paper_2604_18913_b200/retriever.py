@@ -199,6 +199,10 @@ class Retriever:
         """Overlap hop h's K4 with hop h+1's expansion (frontier-only runs)."""
         _lib.check(_lib.load().th_session_set_overlap(self._handle, int(bool(on))))
 
+    def set_dense_pull(self, divisor: float) -> None:
+        """Pull hops gather unconditionally above 1/divisor active in-edges (<= 0: never)."""
+        _lib.check(_lib.load().th_session_set_dense_pull(self._handle, float(divisor)))
+
     def set_graphs(self, on: bool) -> None:
         """Replay repeated batch shapes as one captured CUDA graph."""
         _lib.check(_lib.load().th_session_set_graphs(self._handle, int(bool(on))))

@@ -210,3 +210,28 @@ def test_empty_graph_and_isolated(th):
         for h in range(1, 4):
             assert r.frontier(i, h).size == 0
         assert r.path_tid_tuples(i) == [] and not r.truncated(i)
+
+
+@pytest.mark.parametrize("filtered", [False, True])
+def test_dense_pull_matches_flag_tested_pull(th, filtered):
+    """Pull hops with and without the per-edge frontier test (dense_pull
+    1e9 forces the unconditional gather, 0 disables it) agree with the oracle."""
+    s, r, o = _hub_graph(2500, 50000, 24, seed=17)
+    E, R = 2500, 24
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    rng = np.random.default_rng(2)
+    seeds = rng.integers(0, E, 400)
+    filt = [sorted(rng.choice(R, 10, replace=False).tolist()) for _ in seeds] if filtered else None
+    out = []
+    for dense in (0.0, 1e9):
+        ret = th.Retriever(g)
+        ret.set_pull_divisor(-1.0)
+        ret.set_dense_pull(dense)
+        out.append(ret.retrieve(seeds, 3, relation_filter=filt, semantics="frontier"))
+    a, b = out
+    assert bool((a.frontier_ids == b.frontier_ids).all()) and bool((a.edges == b.edges).all())
+    for i in range(0, 400, 23):
+        ref = orc.retrieve_one(og, int(seeds[i]), 3, "frontier", None if filt is None else filt[i])
+        for h in range(3):
+            assert np.array_equal(b.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
