@@ -268,6 +268,34 @@ int th_shard_hub_merge(th_shard* s, int32_t hop);
 int th_shard_end_hop(th_shard* s, int32_t hop);
 int th_shard_finish(th_shard* s, th_result* out);
 
+/* ---- id sets: store-backed partitioned retrieval ------------------------
+ * The per-hop glue of the reference's out-of-core Algorithm 1
+ * (engine.py:94-135: route the frontier, map to a partition's local ids,
+ * expand, map back, union sorted) on device bitmaps of nbits bits
+ * ((nbits + 31) / 32 uint32 words, caller-owned, zeroed by the caller).
+ * Calls that report a count or an error synchronise `stream`. */
+/* counts[p] = |{i : assign[ids[i]] == p}| (UNASSIGNED = -1 skipped);
+ * replaces route's bucketing (partition.py:170-181); TH_ERR_INVALID for ids
+ * outside [0, n_entities). */
+int th_ids_route_count(const int32_t* d_assign, int64_t n_entities, const int32_t* d_ids, int64_t n,
+                       int32_t m, int64_t* d_counts, void* stream);
+/* bits[map[ids[i]]] = 1, or bits[ids[i]] = 1 with d_map NULL (local -> global
+ * maps, ent_to_global / tid_to_global, partition.py:113-114). */
+int th_ids_map_scatter(const int32_t* d_map, int64_t map_len, const int32_t* d_ids, int64_t n,
+                       uint32_t* d_bits, int64_t nbits, void* stream);
+/* bits[j] = 1 for every ids[i] == sorted_map[j] (Subgraph.entities_to_local,
+ * partition.py:115-122: absent ids dropped). */
+int th_ids_to_local_bits(const int32_t* d_sorted_map, int64_t map_len, const int32_t* d_ids,
+                         int64_t n, uint32_t* d_bits, void* stream);
+/* fresh &= ~visited; visited |= fresh (run_hops, incidence.py:301-315). */
+int th_bits_andnot_update(uint32_t* d_fresh, uint32_t* d_visited, int64_t nbits, void* stream);
+/* dst |= src (CUMULATIVE union of layers, incidence.py:309-312). */
+int th_bits_or(uint32_t* d_dst, const uint32_t* d_src, int64_t nbits, void* stream);
+/* The set bits as an ascending int32 list; *n_out = their number.
+ * TH_ERR_OVERFLOW (nothing written) when it exceeds cap. */
+int th_bits_compact(const uint32_t* d_bits, int64_t nbits, int32_t* d_out, int64_t cap,
+                    int64_t* n_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,9 +40,45 @@ from .partition import (
     route,
 )
 from .retriever import RetrievalResult, Retriever, k_hop, one_hop, reconstruct_paths, retrieve
+from .store import (
+    BatchQuery,
+    BatchResult,
+    Dictionary,
+    DirectoryStore,
+    InMemoryStore,
+    QueryBatch,
+    StorePartitionedGraph,
+    Subgraph,
+    load_labels,
+    load_partition_plan,
+    materialize_subgraphs,
+    open_partitioned,
+    plan_batch,
+    run_batch,
+    save_labels,
+    save_partition_dir,
+    signature,
+)
 from .targets import GpuTarget, PartitionedGpuTarget
 
 __all__ = [
+    "BatchQuery",
+    "BatchResult",
+    "Dictionary",
+    "DirectoryStore",
+    "InMemoryStore",
+    "QueryBatch",
+    "StorePartitionedGraph",
+    "Subgraph",
+    "load_labels",
+    "load_partition_plan",
+    "materialize_subgraphs",
+    "open_partitioned",
+    "plan_batch",
+    "run_batch",
+    "save_labels",
+    "save_partition_dir",
+    "signature",
     "CacheCounters",
     "SubgraphCache",
     "simulate_lru",

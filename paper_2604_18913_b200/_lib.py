@@ -31,6 +31,8 @@ EXPORTS = (
     "th_shard_begin", "th_shard_plan", "th_shard_can_pull", "th_shard_expand", "th_shard_absorb",
     "th_shard_hub_rows",
     "th_shard_hub_merge", "th_shard_end_hop", "th_shard_finish",
+    "th_ids_route_count", "th_ids_map_scatter", "th_ids_to_local_bits", "th_bits_andnot_update",
+    "th_bits_or", "th_bits_compact",
 )
 PROF_CATEGORIES = ("setup", "edges", "activated", "push", "pull", "frontier", "clear", "paths")
 
@@ -126,6 +128,15 @@ def load():
         "th_shard_hub_merge": (ctypes.c_int, [_vp, ctypes.c_int32]),
         "th_shard_end_hop": (ctypes.c_int, [_vp, ctypes.c_int32]),
         "th_shard_finish": (ctypes.c_int, [_vp, ctypes.POINTER(Result)]),
+        "th_ids_route_count": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32,
+                                              _vp, _vp]),
+        "th_ids_map_scatter": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,
+                                              ctypes.c_int64, _vp]),
+        "th_ids_to_local_bits": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, _vp]),
+        "th_bits_andnot_update": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
+        "th_bits_or": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
+        "th_bits_compact": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                                           ctypes.POINTER(ctypes.c_int64), _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -108,4 +108,10 @@ def save_graph(g, path) -> None:
 
 
 def load_graph(path, **kw):
-    return graph_from_bytes(Path(path).read_bytes(), **kw)
+    """archive.py:140-144: a missing file is an IntegrityError."""
+    from .errors import IntegrityError
+
+    p = Path(path)
+    if not p.exists():
+        raise IntegrityError(f"no such archive: {p}")
+    return graph_from_bytes(p.read_bytes(), **kw)

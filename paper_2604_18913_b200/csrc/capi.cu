@@ -9,6 +9,7 @@
 #include "../../include/th_b200.h"
 #include "engine.cuh"
 #include "graph.cuh"
+#include "idset.cuh"
 
 struct th_graph {
   th::Graph g;
@@ -447,6 +448,80 @@ int th_shard_finish(th_shard* s, th_result* out) {
       return TH_ERR_INVALID;
     }
     return th::shard_finish(s->sh, out);
+  });
+}
+
+// ---- id sets (store-backed partitioned retrieval) ----
+
+#define TH_NONNULL(p)                 \
+  do {                                \
+    if (!(p)) {                       \
+      th::set_error("NULL argument"); \
+      return TH_ERR_INVALID;          \
+    }                                 \
+  } while (0)
+
+int th_ids_route_count(const int32_t* d_assign, int64_t n_entities, const int32_t* d_ids, int64_t n,
+                       int32_t m, int64_t* d_counts, void* stream) {
+  return guarded([&]() -> int {
+    TH_NONNULL(d_assign);
+    TH_NONNULL(d_counts);
+    if (n > 0) TH_NONNULL(d_ids);
+    const int rc = th::ids_route_count(d_assign, n_entities, d_ids, n, m, d_counts,
+                                       static_cast<cudaStream_t>(stream));
+    if (rc != TH_OK) th::set_error("id out of range for the partition plan");
+    return rc;
+  });
+}
+
+int th_ids_map_scatter(const int32_t* d_map, int64_t map_len, const int32_t* d_ids, int64_t n,
+                       uint32_t* d_bits, int64_t nbits, void* stream) {
+  return guarded([&]() -> int {
+    TH_NONNULL(d_bits);
+    if (n > 0) TH_NONNULL(d_ids);
+    const int rc = th::ids_map_scatter(d_map, map_len, d_ids, n, d_bits, nbits,
+                                       static_cast<cudaStream_t>(stream));
+    if (rc != TH_OK) th::set_error("id out of range for the map or bitmap");
+    return rc;
+  });
+}
+
+int th_ids_to_local_bits(const int32_t* d_sorted_map, int64_t map_len, const int32_t* d_ids,
+                         int64_t n, uint32_t* d_bits, void* stream) {
+  return guarded([&]() -> int {
+    TH_NONNULL(d_bits);
+    if (n > 0) TH_NONNULL(d_ids);
+    if (map_len > 0) TH_NONNULL(d_sorted_map);
+    return th::ids_to_local_bits(d_sorted_map, map_len, d_ids, n, d_bits,
+                                 static_cast<cudaStream_t>(stream));
+  });
+}
+
+int th_bits_andnot_update(uint32_t* d_fresh, uint32_t* d_visited, int64_t nbits, void* stream) {
+  return guarded([&]() -> int {
+    TH_NONNULL(d_fresh);
+    TH_NONNULL(d_visited);
+    return th::bits_andnot_update(d_fresh, d_visited, nbits, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int th_bits_or(uint32_t* d_dst, const uint32_t* d_src, int64_t nbits, void* stream) {
+  return guarded([&]() -> int {
+    TH_NONNULL(d_dst);
+    TH_NONNULL(d_src);
+    return th::bits_or(d_dst, d_src, nbits, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int th_bits_compact(const uint32_t* d_bits, int64_t nbits, int32_t* d_out, int64_t cap,
+                    int64_t* n_out, void* stream) {
+  return guarded([&]() -> int {
+    TH_NONNULL(d_bits);
+    TH_NONNULL(n_out);
+    if (cap > 0) TH_NONNULL(d_out);
+    const int rc = th::bits_compact(d_bits, nbits, d_out, cap, n_out, static_cast<cudaStream_t>(stream));
+    if (rc == TH_ERR_OVERFLOW) th::set_error("id list longer than the output capacity");
+    return rc;
   });
 }
 

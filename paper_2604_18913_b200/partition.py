@@ -608,7 +608,18 @@ def merge_results(parts, n_queries: int, k: int, activated: bool):
 
 class PartitionedGraph:
     """Shards of one graph over ``exchange.world`` ranks; this process hosts
-    ``exchange.ranks`` of them (engine.py:62-81's role)."""
+    ``exchange.ranks`` of them (engine.py:62-81's role).
+
+    ``PartitionedGraph(plan, store, cache)`` -- the reference's constructor
+    (engine.py:62-71) -- builds the store-backed, LRU-cached form instead
+    (``store.StorePartitionedGraph``)."""
+
+    def __new__(cls, *args, **kwargs):
+        if cls is PartitionedGraph and args and isinstance(args[0], PartitionPlan):
+            from .store import StorePartitionedGraph
+
+            return super().__new__(StorePartitionedGraph)
+        return super().__new__(cls)
 
     def __init__(self, triples, n_entities: int, n_relations: int, exchange: Exchange | None = None,
                  plan: ShardPlan | None = None, hub_fraction: float = DEFAULT_HUB_FRACTION,
@@ -699,6 +710,10 @@ def cross_graph_k_hop(q0: EntityVector, k: int, pg: PartitionedGraph,
                       semantics: HopSemantics = HopSemantics.FRONTIER) -> HopTrace:
     """k-hop retrieval of one seed set across the partitions (engine.py:138-154);
     bit-identical to single-graph ``k_hop`` (frontier and activated sets)."""
+    if getattr(pg, "store", None) is not None:
+        from .store import store_k_hop
+
+        return store_k_hop(q0, k, pg, semantics)
     if q0.width != pg.n_entities:
         raise ValueError(f"query width {q0.width} != graph entity count {pg.n_entities}")
     if k < 1:
@@ -734,6 +749,10 @@ def cross_graph_paths(q0: EntityVector, k: int, pg: PartitionedGraph,
     from .device_graph import build_incidence
     from .retriever import reconstruct_paths
 
+    if getattr(pg, "store", None) is not None:
+        from .store import store_paths
+
+        return store_paths(q0, k, pg, max_paths)
     if q0.width != pg.n_entities:
         raise ValueError(f"query width {q0.width} != graph entity count {pg.n_entities}")
     if k < 1:
