@@ -57,26 +57,7 @@ __device__ __forceinline__ void st_words(uint32_t* p, const uint32_t (&v)[VEC]) 
 // every live query has visited or reached the entity.  Whole in-rows are
 // finished with plain stores; rows split over several items merge with
 // atomicOr (the union of the pieces is exactly R_h & ~V_{h-1}).
-//
-// Appends of newly reached entities go through a per-warp shared buffer
-// (one global atomic per 32 entities instead of one per warp step) and the
-// push-cost sum stays in registers until the kernel ends: at low in-degree
-// (C4: 1.6 in-edges per entity) nearly every step reaches an entity, and
-// two same-address atomics per warp step serialised in L2.
-constexpr int kPullAppend = 32;
-
-// store a warp's buffered appends to the hop's list segment (all 32 lanes)
-__device__ __forceinline__ void pull_flush(const WaveArgs& a, int32_t* wbuf, int& afill) {
-  int32_t base = 0;
-  if (lane_id() == 0) base = atomicAdd(&a.ctl->list_len[a.h], afill);
-  base = __shfl_sync(TH_FULL, base, 0);
-  int32_t* list = a.lists + a.ctl->list_off[a.h];
-  for (int i = (int)lane_id(); i < afill; i += 32)
-    if (base + (int64_t)i < a.E) list[base + i] = wbuf[i];
-  afill = 0;
-  __syncwarp();
-}
-
+// (newly reached entities are appended through a WarpAppender)
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   if (a.ctl->mode[a.h] != 1) return;
@@ -87,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   // positions of m's set bits, ascending, one per nibble (replaces __fns,
   // a software loop)
   __shared__ uint32_t nth_bit[LPR >= 4 ? (1 << LPR) : 1];
-  __shared__ int32_t abuf[kThreads / 32][2 * kPullAppend];
+  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
   if constexpr (LPR >= 4) {
     for (int m = threadIdx.x; m < (1 << LPR); m += blockDim.x) {
       uint32_t e = 0u;
@@ -98,9 +79,7 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
     }
     __syncthreads();
   }
-  int32_t* wbuf = abuf[threadIdx.x >> 5];
-  int afill = 0;
-  unsigned long long cost = 0ull;
+  WarpAppender app{abuf[threadIdx.x >> 5]};
   const unsigned lane = lane_id();
   const int part = (int)lane % LPR, grp = (int)lane / LPR;
   const unsigned gbits = (LPR == 32 ? TH_FULL : ((1u << LPR) - 1u)) << (grp * LPR);
@@ -276,23 +255,8 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
       }
       if (part == 0) fresh = flag_next(a, v);
     }
-    // buffered append (converged): flush whole runs of >= kPullAppend
-    const unsigned fm = __ballot_sync(TH_FULL, fresh);
-    if (fresh) {
-      wbuf[afill + __popc(fm & lanemask_lt())] = v;
-      const uint32_t d = (uint32_t)(a.indptr[v + 1] - a.indptr[v]);
-      cost += d > (1u << 26) ? (1u << 26) : d;
-    }
-    afill += __popc(fm);
-    if (afill >= kPullAppend) {
-      __syncwarp();
-      pull_flush(a, wbuf, afill);
-    }
+    app.add(a, fresh, v);
   }
-  __syncwarp();
-  if (afill) pull_flush(a, wbuf, afill);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) cost += __shfl_xor_sync(TH_FULL, cost, o);
-  if (lane == 0 && cost) atomicAdd(&a.ctl->push_cost[a.h], cost);
+  app.finish(a);
 }
 
