@@ -92,8 +92,8 @@ struct ListSrc {
   }
   __device__ __forceinline__ int64_t rows_dev() const { return *n_dev; }
   __device__ __forceinline__ int32_t id(int64_t r) const {
-    const int32_t v = rows[r];
-    return map ? map[v] : v;
+    const int32_t v = __ldg(rows + r);
+    return map ? __ldg(map + v) : v;
   }
 };
 
@@ -288,9 +288,12 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       continue;
     }
     // keep the CTA's warps (words of the same rows) on the same chunk so
-    // each row sector they share is fetched from L2 once and hit in L1
-    // by the others (the write phase otherwise drifts them apart)
-    if (WRITE && !LOAD_S && NW > 1) __syncthreads();
+    // each row sector they share is fetched once and hit in L1 by the
+    // others (the write phase drifts them apart; so does the count pass
+    // over a list of scattered rows: C4's last layer read 5.65 GB from
+    // DRAM in the count pass against 1.93 GB in the synchronised write
+    // pass; EDGES passes synchronise for their degree planes anyway)
+    if ((WRITE ? !LOAD_S : !EDGES) && NW > 1) __syncthreads();
     const size_t sbase = ((size_t)(c0 / kChunkRows) * W + j) * 1024;
     // ---- A: tile masks of this chunk, S[b][t] = rows of tile t in query b.
     // Loads of 8 tiles are issued before their transposes (memory-level
@@ -491,8 +494,20 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
         for (int i = lane; i < n; i += 32)
           if (pb + i < cap) out[pb + i] = stg[i];
       } else if (pb + n <= cap) {
-        int32_t* o = out + pb;
-        for (int i = lane; i < n; i += 32) o[i] = src.id(c0 + stg[i]);
+        // ids resolve through the row list / map: four independent
+        // lookups in flight per lane before their stores
+        int32_t* o = out + pb + lane;
+        const int32_t* sp = stg + lane;
+        int i = lane;
+        for (; i + 96 < n; i += 128, o += 128, sp += 128) {
+          const int32_t v0 = src.id(c0 + sp[0]), v1 = src.id(c0 + sp[32]);
+          const int32_t v2 = src.id(c0 + sp[64]), v3 = src.id(c0 + sp[96]);
+          o[0] = v0;
+          o[32] = v1;
+          o[64] = v2;
+          o[96] = v3;
+        }
+        for (; i < n; i += 32, o += 32, sp += 32) *o = src.id(c0 + *sp);
       } else {
         for (int i = lane; i < n; i += 32)
           if (pb + i < cap) out[pb + i] = src.id(c0 + stg[i]);
