@@ -837,9 +837,9 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
 template <int W>
 void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
                        const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
-                       int64_t cap, int64_t* cursor, EdgeSum es = {}) {
+                       int64_t cap, int64_t* cursor, EdgeSum es = {}, bool prefer_list = false) {
   const int64_t E = s->mat_rows >= 0 ? s->mat_rows : s->g->E;
-  if (E < s->list_min_entities || E == 0) {
+  if ((!prefer_list && E < s->list_min_entities) || E == 0) {
     DenseSrc<W> src{A, neg, flags, E, nq, s->row_map};
     materialize<W>(s, b, src, nq, off, len, out, cap, cursor, es);
     return;
@@ -1060,9 +1060,14 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
           es.nplanes = nplanes;
           es.out = edges + h * B + q0;
         }
+        // the first layer is bounded by the seeds' out-degrees: when its K4
+        // runs beside hop 2's expansion, follow its compacted row list (a
+        // few busy CTAs) rather than scanning every chunk of E with a full
+        // grid that takes SM slots from the expansion (C2 k=3 -5%; alone,
+        // at k=1, the two cost the same)
         materialize_dense<W>(s, b, b.N, nullptr, b.Nf, nq, f_off + (h - 1) * B + q0,
                              f_len + (h - 1) * B + q0, static_cast<int32_t*>(s->f_ids.p), s->f_cap,
-                             &b.ctl->ids_used, es);
+                             &b.ctl->ids_used, es, h == 1 && k > 1 && overlap && s->list_first_hop);
         next_edges_done = es.out != nullptr;
       }
       }

@@ -58,7 +58,8 @@ struct Session {
   // K4 of hop h overlaps hop h+1's expansion on a side stream (frontier-only
   // runs; the main stream joins before it recycles the layer's rows)
   bool overlap = true;
-  bool k4_cache = true;  // small layers: count pass caches tile masks for the write pass
+  bool k4_cache = true;
+  bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr;
   cudaEvent_t ev_expand[kMaxK + 2] = {};
   cudaEvent_t ev_mat[kMaxK + 2] = {};
