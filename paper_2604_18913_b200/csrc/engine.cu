@@ -726,8 +726,8 @@ int pick_words(int nq) {
 struct WaveBufs {
   int W;
   uint32_t *X, *N, *V, *S, *Xf, *Nf, *Vf, *M;
-  int32_t *lists, *heavy, *counts;
-  int64_t* totals;
+  int32_t *lists, *heavy, *counts, *counts2;
+  int64_t *totals, *totals2;
   Ctl* ctl;
 };
 
@@ -736,6 +736,11 @@ template <int W, class Src>
 void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, int64_t* len,
                  int32_t* out, int64_t cap, int64_t* cursor, EdgeSum es = {}) {
   const int64_t rows = src.nrows;
+  // scratch of the K4 slot in use (consecutive layers' K4s may run at once)
+  int32_t* const counts = s->k4_slot ? b.counts2 : b.counts;
+  int64_t* const totals = s->k4_slot ? b.totals2 : b.totals;
+  DBuf& kS = s->k4_slot ? s->k4_S2 : s->k4_S;
+  DBuf& kMeta = s->k4_slot ? s->k4_meta2 : s->k4_meta;
   if (rows == 0) {
     TH_CUDA(cudaMemsetAsync(len, 0, sizeof(int64_t) * nq, s->st));
     TH_CUDA(cudaMemsetAsync(off, 0, sizeof(int64_t) * nq, s->st));
@@ -770,8 +775,8 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
     const int64_t nchunks = ceil_div(rows, kChunkRows);
     if (s->k4_cache && nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
       SCache sc;
-      sc.S = ensure<uint32_t>(s->k4_S, nchunks * W * 1024, s->st);
-      sc.meta = ensure<uint2>(s->k4_meta, nchunks * W + 1, s->st);
+      sc.S = ensure<uint32_t>(kS, nchunks * W * 1024, s->st);
+      sc.meta = ensure<uint2>(kMeta, nchunks * W + 1, s->st);
       sc.work = reinterpret_cast<unsigned*>(sc.meta + nchunks * W);
       constexpr size_t smem_cc = ((size_t)NW * (32 * kSStride + 64) + kEdgeWords) * sizeof(uint32_t);
       constexpr size_t smem_wc = (size_t)NW * mat_load_words<Src::kRing>() * sizeof(uint32_t);
@@ -787,10 +792,10 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
       }
       if (es.out)
         mat_kernel<W, Src, false, true, 1><<<grid, 32 * NW, smem_cc, s->st>>>(
-            src, nblk, b.counts, nullptr, nullptr, 0, es, sc);
+            src, nblk, counts, nullptr, nullptr, 0, es, sc);
       else
         mat_kernel<W, Src, false, false, 1><<<grid, 32 * NW, smem_cc, s->st>>>(
-            src, nblk, b.counts, nullptr, nullptr, 0, EdgeSum{}, sc);
+            src, nblk, counts, nullptr, nullptr, 0, EdgeSum{}, sc);
       TH_LAUNCHED();
       // the write pass reads only the cached masks: the layer itself is free
       // (callers may clear it) once the count pass is done
@@ -798,14 +803,14 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
         TH_CUDA(cudaEventRecord(s->mark_counted, s->st));
         s->counted_recorded = true;
       }
-      mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
+      mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(counts, nblk, totals);
       TH_LAUNCHED();
-      mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
+      mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(totals, nq, off, len, cursor);
       TH_LAUNCHED();
       // (warps pull units from a counter: at most one resident wave of CTAs)
       const unsigned wgrid = std::min<unsigned>(grid, kNumSMs * (2048 / (32 * NW)));
       mat_kernel<W, Src, true, false, 2><<<wgrid, 32 * NW, smem_wc, s->st>>>(
-          src, nblk, b.counts, off, out, cap, EdgeSum{}, sc);
+          src, nblk, counts, off, out, cap, EdgeSum{}, sc);
       TH_LAUNCHED();
       s->launches += 4;
       return;
@@ -813,17 +818,17 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   }
   constexpr size_t smem_c = mat_smem_bytes<W, false>();
   if (es.out)
-    mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, b.counts,
+    mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, counts,
                                                                       nullptr, nullptr, 0, es);
   else
-    mat_kernel<W, Src, false><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, b.counts, nullptr,
+    mat_kernel<W, Src, false><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, counts, nullptr,
                                                                 nullptr, 0);
   TH_LAUNCHED();
-  mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(b.counts, nblk, b.totals);
+  mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(counts, nblk, totals);
   TH_LAUNCHED();
-  mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(b.totals, nq, off, len, cursor);
+  mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(totals, nq, off, len, cursor);
   TH_LAUNCHED();
-  mat_kernel<W, Src, true><<<grid, 32 * NW, smem_w, s->st>>>(src, nblk, b.counts, off, out,
+  mat_kernel<W, Src, true><<<grid, 32 * NW, smem_w, s->st>>>(src, nblk, counts, off, out,
                                                              cap);
   TH_LAUNCHED();
   s->launches += 4;
@@ -846,9 +851,9 @@ void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_
   }
   const int64_t nwords = ceil_div(E, 32);
   const int nb = (int)ceil_div(nwords, kCompactWords);
-  int32_t* rows = ensure<int32_t>(s->rowlist, E, s->st);
-  int32_t* bsum = ensure<int32_t>(s->rowscan, nb, s->st);
-  int32_t* n_dev = &b.ctl->mat_rows;
+  int32_t* rows = ensure<int32_t>(s->k4_slot ? s->rowlist2 : s->rowlist, E, s->st);
+  int32_t* bsum = ensure<int32_t>(s->k4_slot ? s->rowscan2 : s->rowscan, nb, s->st);
+  int32_t* n_dev = s->k4_slot ? &b.ctl->mat_rows2 : &b.ctl->mat_rows;
   flag_count_kernel<<<nb, kCompactThreads, 0, s->st>>>(flags, E, bsum);
   TH_LAUNCHED();
   flag_scan_kernel<<<1, 1024, 0, s->st>>>(bsum, nb, n_dev);
@@ -901,6 +906,7 @@ struct StreamScope {
 void ensure_side_stream(Session* s) {
   if (s->side) return;
   TH_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+  TH_CUDA(cudaStreamCreateWithFlags(&s->side2, cudaStreamNonBlocking));
   for (int i = 0; i < kMaxK + 2; ++i) {
     TH_CUDA(cudaEventCreateWithFlags(&s->ev_expand[i], cudaEventDisableTiming));
     TH_CUDA(cudaEventCreateWithFlags(&s->ev_mat[i], cudaEventDisableTiming));
@@ -931,6 +937,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   b.M = filter ? ensure<uint32_t>(s->M, std::max<int64_t>(g->R, 1) * W, st) : nullptr;
   b.counts = ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
   b.totals = ensure<int64_t>(s->totals, kMaxWave, st);
+  b.counts2 = ensure<int32_t>(s->counts2, (int64_t)kMaxWave * (kMatBlocks + 64), st);
+  b.totals2 = ensure<int64_t>(s->totals2, kMaxWave, st);
   b.ctl = static_cast<Ctl*>(s->ctl.p);
   TH_CUDA(cudaMemsetAsync(b.ctl, 0, offsetof(Ctl, err), st));
   TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
@@ -1037,11 +1045,17 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
       else expand_hop<W, TH_FRONTIER, false>(s, a);
     }
     if (want_f) {
+      // consecutive layers alternate between two side streams with their
+      // own K4 scratch, so layer h+1's K4 starts as soon as its expansion
+      // ends instead of queueing behind layer h's
+      const int slot = overlap ? (int)(h & 1) : 0;
+      cudaStream_t kst = slot ? s->side2 : s->side;
       if (overlap) {
         TH_CUDA(cudaEventRecord(s->ev_expand[h], st));
-        TH_CUDA(cudaStreamWaitEvent(s->side, s->ev_expand[h], 0));
+        TH_CUDA(cudaStreamWaitEvent(kst, s->ev_expand[h], 0));
       }
-      StreamScope sc(s, overlap ? s->side : st);
+      StreamScope sc(s, overlap ? kst : st);
+      s->k4_slot = slot;
       s->mark_counted = overlap ? s->ev_cnt[h] : nullptr;
       s->counted_recorded = false;
       {
@@ -1072,10 +1086,11 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
       }
       }
       if (overlap) {
-        TH_CUDA(cudaEventRecord(s->ev_mat[h], s->side));
-        if (!s->counted_recorded) TH_CUDA(cudaEventRecord(s->ev_cnt[h], s->side));
+        TH_CUDA(cudaEventRecord(s->ev_mat[h], kst));
+        if (!s->counted_recorded) TH_CUDA(cudaEventRecord(s->ev_cnt[h], kst));
       }
       s->mark_counted = nullptr;
+      s->k4_slot = 0;
     }
     {
       // retire X (rows of list segment h-1) and swap roles; with overlap the
@@ -1108,7 +1123,10 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
     TH_LAUNCHED();
     s->launches += 1;
   }
-  if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k], 0));
+  if (overlap) {
+    TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k], 0));
+    if (k > 1) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k - 1], 0));
+  }
   ProfScope ps(s, TH_PROF_CLEAR);
   if (sem == TH_CUMULATIVE) {
     clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.S, b.lists, b.ctl, 0, 0, E);
@@ -1511,7 +1529,8 @@ void session_free(Session* s) {
   for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
                   &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
-                  &s->p_scratch, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta,
+                  &s->p_scratch, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta, &s->counts2,
+                  &s->totals2, &s->rowlist2, &s->rowscan2, &s->k4_S2, &s->k4_meta2,
                   &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks}) {
     if (d->p) cudaFreeAsync(d->p, s->st);
     d->p = nullptr;
@@ -1527,8 +1546,10 @@ void session_free(Session* s) {
       cudaEventDestroy(s->ev_mat[i]);
       cudaEventDestroy(s->ev_cnt[i]);
     }
+    cudaStreamSynchronize(s->side2);
     cudaStreamDestroy(s->side);
-    s->side = nullptr;
+    cudaStreamDestroy(s->side2);
+    s->side = s->side2 = nullptr;
   }
   if (s->cap) {
     cudaStreamDestroy(s->cap);
@@ -1649,6 +1670,8 @@ WaveBufs shard_bufs(Shard* sh) {
   b.heavy = static_cast<int32_t*>(s->heavy.p);
   b.counts = static_cast<int32_t*>(s->counts.p);
   b.totals = static_cast<int64_t*>(s->totals.p);
+  b.counts2 = b.counts;  // shards run K4 on one stream (slot 0 only)
+  b.totals2 = b.totals;
   b.ctl = static_cast<Ctl*>(s->ctl.p);
   return b;
 }

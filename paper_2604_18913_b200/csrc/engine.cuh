@@ -27,6 +27,7 @@ struct Ctl {
   int64_t path_used;
   int32_t mat_rows;  // length of the compacted row list of the layer being materialised
   int32_t olen;      // shards: staged remote rows this hop
+  int32_t mat_rows2; // compacted row count of the second K4 slot
 };
 
 struct DBuf {
@@ -60,7 +61,8 @@ struct Session {
   bool overlap = true;
   bool k4_cache = true;
   bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr, side2 = nullptr;  // K4 streams (odd / even layers)
+  int k4_slot = 0;                                // which K4 scratch set is in use
   cudaEvent_t ev_expand[kMaxK + 2] = {};
   cudaEvent_t ev_mat[kMaxK + 2] = {};
   cudaEvent_t ev_cnt[kMaxK + 2] = {};  // K4 of the layer no longer reads it (count pass done)
@@ -72,6 +74,7 @@ struct Session {
   int64_t launches = 0;
   // wave state
   DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals, rowlist, rowscan, k4_S, k4_meta, heavy_off;
+  DBuf counts2, totals2, rowlist2, rowscan2, k4_S2, k4_meta2;  // second K4 slot
   DBuf ctl;
   // outputs
   DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch;
