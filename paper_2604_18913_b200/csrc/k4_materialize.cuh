@@ -360,10 +360,22 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
           if (EDGES) {
             // low 8 bits by the shared bit planes; the rare rows of degree
             // >= 256 add their high part row by row
+            // (planes read as two broadcast 16-byte loads; the upper four
+            // only when a row of the tile has degree >= 16)
             const int np = (int)eplanes[256 + t];
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (k < np) eplane_cnt[k] += __popc(m & eplanes[t * 8 + k]);
+            const uint4* pp = reinterpret_cast<const uint4*>(eplanes + t * 8);
+            const uint4 p0 = pp[0];
+            eplane_cnt[0] += __popc(m & p0.x);
+            eplane_cnt[1] += __popc(m & p0.y);
+            eplane_cnt[2] += __popc(m & p0.z);
+            eplane_cnt[3] += __popc(m & p0.w);
+            if (np > 4) {
+              const uint4 p1 = pp[1];
+              eplane_cnt[4] += __popc(m & p1.x);
+              eplane_cnt[5] += __popc(m & p1.y);
+              eplane_cnt[6] += __popc(m & p1.z);
+              eplane_cnt[7] += __popc(m & p1.w);
+            }
             uint32_t bg = eplanes[288 + t] & m;
             while (bg) {
               const int i = __ffs(bg) - 1;
