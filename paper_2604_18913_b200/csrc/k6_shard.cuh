@@ -122,7 +122,7 @@ __global__ void shard_seed_kernel(ShardArgs sa, const int32_t* __restrict__ qoff
 // owner split of every target
 template <int W, int SEM, bool FILTER>
 __device__ __forceinline__ void shard_row_pairs(const ShardArgs& sa, int32_t u, int32_t lo,
-                                                int32_t hi) {
+                                                int32_t hi, WarpAppender& app) {
   const WaveArgs& a = sa.a;
   const unsigned lane = lane_id();
   const uint32_t xw = lane < (unsigned)W ? a.X[(size_t)u * W + lane] : 0u;
@@ -158,7 +158,7 @@ __device__ __forceinline__ void shard_row_pairs(const ShardArgs& sa, int32_t u, 
         }
       }
     }
-    append_next(a, fresh, row);
+    app.add(a, fresh, row);
     warp_append_all(rfresh, v, 0u, sa.olist, sa.olen, sa.E_global, (unsigned long long*)nullptr);
   }
 }
@@ -166,6 +166,8 @@ __device__ __forceinline__ void shard_row_pairs(const ShardArgs& sa, int32_t u, 
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) shard_push_light_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
+  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  WarpAppender app{abuf[threadIdx.x >> 5]};
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int32_t n = a.ctl->list_len[a.h - 1];
@@ -178,13 +180,16 @@ __global__ void __launch_bounds__(kThreads) shard_push_light_kernel(ShardArgs sa
       if (!FILTER && lane_id() == 0) a.heavy[atomicAdd(&a.ctl->heavy_len, 1)] = u;
       continue;
     }
-    shard_row_pairs<W, SEM, FILTER>(sa, u, lo, hi);
+    shard_row_pairs<W, SEM, FILTER>(sa, u, lo, hi, app);
   }
+  app.finish(a);
 }
 
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
+  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  WarpAppender app{abuf[threadIdx.x >> 5]};
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int32_t nh = a.ctl->heavy_len;
@@ -197,10 +202,11 @@ __global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa
       const int32_t nc = (hi - lo + kPushChunk - 1) / kPushChunk;
       for (int64_t c = ((gw - base) % nw + nw) % nw; c < nc; c += nw) {
         const int32_t clo = lo + (int32_t)c * kPushChunk;
-        shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk));
+        shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk), app);
       }
       base += nc;
     }
+    app.finish(a);
     return;
   }
   const int64_t total = a.heavy_off[nh];
@@ -214,8 +220,9 @@ __global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa
     const int32_t u = a.heavy[lo_i];
     const int32_t lo = a.indptr[u], hi = a.indptr[u + 1];
     const int32_t clo = lo + (int32_t)(g - a.heavy_off[lo_i]) * kPushChunk;
-    shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk));
+    shard_row_pairs<W, SEM, FILTER>(sa, u, clo, min(hi, clo + kPushChunk), app);
   }
+  app.finish(a);
 }
 
 // staged rows -> records bucketed by owner.  COUNT: per-owner record totals
@@ -281,6 +288,8 @@ __global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa,
                                                                 int64_t n) {
   const WaveArgs& a = sa.a;
   const int lane = threadIdx.x & 31;
+  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  WarpAppender app{abuf[threadIdx.x >> 5]};
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t base = gw * 32; base < n; base += nw * 32) {
@@ -297,8 +306,9 @@ __global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa,
         fresh = local_set<W, SEM>(a, row, (int)(key % W), (uint32_t)rec);
       }
     }
-    append_next(a, fresh, row);
+    app.add(a, fresh, row);
   }
+  app.finish(a);
 }
 
 // owners publish their hubs' next-layer rows ([n_hubs][W], zero elsewhere)
