@@ -283,6 +283,33 @@ struct CountOp {
       const int j = __ffs(nz) - 1;
       nz &= nz - 1u;
       const uint32_t x = __shfl_sync(TH_FULL, xw, j);
+      if (__popc(x) <= 4) {
+        // few queries in this word (seed rows, sparse frontiers): one
+        // ballot per query bit instead of a 32x32 transpose per 32 edges
+        uint32_t c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u;
+        const int b0 = __ffs(x) - 1;
+        const uint32_t x1 = x & (x - 1u);
+        const int b1 = __ffs(x1) - 1;
+        const uint32_t x2 = x1 & (x1 - 1u);
+        const int b2 = __ffs(x2) - 1;
+        const uint32_t x3 = x2 & (x2 - 1u);
+        const int b3 = __ffs(x3) - 1;
+        for (int32_t e0 = lo; e0 < hi; e0 += 32) {
+          const int32_t e = e0 + (int32_t)lane;
+          const uint32_t w = e < hi ? x & a.M[(size_t)a.csr_rel[e] * W_ + j] : 0u;
+          c0 += __popc(__ballot_sync(TH_FULL, (w >> (b0 & 31)) & 1u));
+          if (b1 >= 0) c1 += __popc(__ballot_sync(TH_FULL, (w >> b1) & 1u));
+          if (b2 >= 0) c2 += __popc(__ballot_sync(TH_FULL, (w >> b2) & 1u));
+          if (b3 >= 0) c3 += __popc(__ballot_sync(TH_FULL, (w >> b3) & 1u));
+        }
+        if (lane == 0) {
+          if (c0) atomicAdd(&sc[32 * j + b0], c0);
+          if (c1) atomicAdd(&sc[32 * j + b1], c1);
+          if (c2) atomicAdd(&sc[32 * j + b2], c2);
+          if (c3) atomicAdd(&sc[32 * j + b3], c3);
+        }
+        continue;
+      }
       for (int32_t e0 = lo; e0 < hi; e0 += 32) {
         const int32_t e = e0 + (int32_t)lane;
         const uint32_t w = e < hi ? x & a.M[(size_t)a.csr_rel[e] * W_ + j] : 0u;
@@ -313,7 +340,7 @@ __device__ void drive_light(const WaveArgs& a, int seg, Op& op, bool build_heavy
   }
 }
 
-constexpr int32_t kSmallHeavy = 1024;
+constexpr int32_t kSmallHeavy = 64;  // every warp walks a list this short (O(list) per warp)
 
 // walk a short heavy list: every warp visits every row, taking the chunks
 // of a global round-robin numbering
