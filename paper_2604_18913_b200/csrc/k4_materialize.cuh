@@ -155,7 +155,9 @@ constexpr int kRingWords = 32 * kRingStride;
 // (emptied before a dense chunk); COUNT = per-query counters + degree sums
 template <bool WRITE, bool RING = false>
 constexpr size_t mat_warp_words() {
-  return WRITE ? (size_t)(32 * kSStride + (RING && kRingWords > kChunkRows ? kRingWords : kChunkRows))
+  // (RING: + 32 words holding the current tile's row ids)
+  return WRITE ? (size_t)(32 * kSStride + (RING && kRingWords > kChunkRows ? kRingWords : kChunkRows) +
+                          (RING ? 32 : 0))
                : 64;
 }
 
@@ -445,11 +447,19 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       continue;
     }
     if (RING && ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
+      // the tile's 32 output ids are looked up once (one coalesced load of
+      // the row list) and shared through shared memory, so each id costs a
+      // shared load instead of a dependent global one
+      int32_t* tile_ids = ring + (kRingWords > kChunkRows ? kRingWords : kChunkRows);
       for (int t = 0; t < 32; ++t) {
         uint32_t m = q >= src.nq ? 0u : LOAD_S ? sc.S[sbase + lane * 32 + t] : S[lane * kSStride + t];
         const int64_t rb = c0 + 32 * t;
+        const unsigned any = __ballot_sync(TH_FULL, m != 0u);
+        if (!any) continue;
+        tile_ids[lane] = rb + lane < rend ? src.id(rb + lane) : 0;
+        __syncwarp();
         while (m) {
-          ring[lane * kRingStride + fill] = src.id(rb + __ffs(m) - 1);
+          ring[lane * kRingStride + fill] = tile_ids[__ffs(m) - 1];
           ++fill;
           m &= m - 1u;
         }
