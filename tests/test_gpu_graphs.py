@@ -96,3 +96,20 @@ def test_profiling_under_replay(th):
         prof = ret.profile()
         assert {c: n for c, (_ms, n) in prof.items()} == {c: n for c, (_ms, n) in eager.items()}
         assert sum(ms for ms, _n in prof.values()) > 0
+
+
+def test_replay_two_waves_and_filters(th):
+    """B = 1,500 (two waves of the bit-parallel engine) with per-seed filters:
+    the captured graph covers both waves and the masks are staged."""
+    s, r, o = _hub_graph(2500, 50000, 20, seed=13)
+    E, R = 2500, 20
+    g = th.build_incidence((s, r, o), E, R)
+    graphed, eager = th.Retriever(g), th.Retriever(g)
+    eager.set_graphs(False)
+    rng = np.random.default_rng(6)
+    for it in range(4):
+        seeds = rng.integers(0, E, 1500)
+        filt = [sorted(rng.choice(R, 5, replace=False).tolist()) for _ in range(1500)]
+        a = graphed.retrieve(seeds, 3, relation_filter=filt, activated=True)
+        b = eager.retrieve(seeds, 3, relation_filter=filt, activated=True)
+        _same(a, b)
