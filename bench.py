@@ -578,7 +578,15 @@ def run_ours(args, world, rank, local):
         e2e_times.append(time.perf_counter() - t0)
         h2d = host_seeds.numel() * 4 + (BATCH + 1) * 4
         d2h = sum(outs.values())
-    e2e_value = BATCH / statistics.median(e2e_times)
+    e2e_t = statistics.median(e2e_times)
+    if world > 1:
+        # whole job: every rank's batch over the slowest rank's time
+        import torch.distributed as dist
+
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    e2e_value = BATCH * world / e2e_t
 
     # CPU baseline: oracle on the host cores, rank 0 at N=1 only
     cpu = None
