@@ -113,3 +113,26 @@ def test_replay_two_waves_and_filters(th):
         a = graphed.retrieve(seeds, 3, relation_filter=filt, activated=True)
         b = eager.retrieve(seeds, 3, relation_filter=filt, activated=True)
         _same(a, b)
+
+
+@pytest.mark.parametrize("B", [1, 2, 33, 100, 1025])
+def test_replay_every_wave_width(th, B):
+    """Word widths W = 1 .. 32 (and a second wave): replayed graphs equal
+    eager runs for each width, with seeds that change between replays."""
+    s, r, o = _hub_graph(1200, 20000, 12, seed=31)
+    E, R = 1200, 12
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    graphed, eager = th.Retriever(g), th.Retriever(g)
+    eager.set_graphs(False)
+    rng = np.random.default_rng(B)
+    for it in range(6):  # per semantics: eager run, capture, replay
+        seeds = rng.integers(0, E, B)
+        sem = "frontier" if it < 3 else "cumulative"
+        a = graphed.retrieve(seeds, 3, semantics=sem)
+        b = eager.retrieve(seeds, 3, semantics=sem)
+        _same(a, b)
+    i = B - 1
+    ref = orc.retrieve_one(og, int(seeds[i]), 3, "cumulative")
+    for h in range(3):
+        assert np.array_equal(a.frontier(i, h + 1), ref["frontiers"][h])
