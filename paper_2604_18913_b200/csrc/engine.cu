@@ -1486,6 +1486,9 @@ static int run_body(Session* s, const th_query* q) {
     pa.scratch = ensure<int64_t>(s->p_scratch, scan_scratch_elems_i64(B + 1), st);
     pa.cap = s->p_cap;
     pa.used = const_cast<int64_t*>(&ctl->path_used);
+    // capped queries whose slots fit 2 GiB take the single-DFS form
+    if (q->max_paths > 0 && (int64_t)B * q->max_paths * k * 4 <= (int64_t(2) << 30))
+      pa.tmp = ensure<int32_t>(s->p_tmp, (int64_t)B * q->max_paths * k, st);
     ProfScope ps(s, TH_PROF_PATHS);
     s->launches += launch_paths(pa, st);
   }
@@ -1556,7 +1559,7 @@ void session_free(Session* s) {
   for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
                   &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
-                  &s->p_scratch, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta, &s->counts2,
+                  &s->p_scratch, &s->p_tmp, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta, &s->counts2,
                   &s->totals2, &s->rowlist2, &s->rowscan2, &s->k4_S2, &s->k4_meta2,
                   &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks}) {
     if (d->p) cudaFreeAsync(d->p, s->st);

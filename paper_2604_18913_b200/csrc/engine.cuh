@@ -77,7 +77,7 @@ struct Session {
   DBuf counts2, totals2, rowlist2, rowscan2, k4_S2, k4_meta2;  // second K4 slot
   DBuf ctl;
   // outputs
-  DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch;
+  DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch, p_tmp;
   int64_t f_cap = 0, a_cap = 0, p_cap = 0;
   // last run
   th_query last{};

@@ -64,7 +64,7 @@ __device__ __forceinline__ Cand cand_csr(const PathArgs& a, int64_t i) {
 // candidates [lo, hi) of level d in order: 4 x 32 per iteration, all loads
 // issued before the four ordered ballots (a huge filtered row is the DFS's
 // critical path; this cuts its dependent iterations 4x)
-template <bool WRITE>
+template <bool WRITE, bool SINGLE = false>
 __device__ __forceinline__ void emit_range(const PathArgs& a, int q, int d, bool list_mode,
                                            int64_t lo, int64_t hi, const int32_t* stack_tid,
                                            int64_t& count, int64_t limit, int64_t out_base) {
@@ -88,8 +88,9 @@ __device__ __forceinline__ void emit_range(const PathArgs& a, int q, int d, bool
       if (WRITE && pass[u]) {
         const int64_t idx = count + __popc(bal & lanemask_lt());
         const int64_t pp = out_base + idx;
-        if (idx < limit && pp < a.cap) {
-          int32_t* dst = a.p_tids + pp * a.k;
+        // SINGLE: counts run to max_paths + 1 (truncation), slots hold max_paths
+        if (SINGLE ? idx < a.max_paths : (idx < limit && pp < a.cap)) {
+          int32_t* dst = (SINGLE ? a.tmp : a.p_tids) + pp * a.k;
           for (int dd = 0; dd < d; ++dd) dst[dd] = stack_tid[dd];
           dst[d] = c[u].tid;
         }
@@ -99,7 +100,7 @@ __device__ __forceinline__ void emit_range(const PathArgs& a, int q, int d, bool
   }
 }
 
-template <bool WRITE>
+template <bool WRITE, bool SINGLE = false>
 __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
   __shared__ int32_t stack_tid_s[kPathThreads / 32][kMaxDepth];
   __shared__ int64_t cur_s[kPathThreads / 32][kMaxDepth];
@@ -129,7 +130,10 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
       }
     }
     int64_t limit, out_base = 0;
-    if (WRITE) {
+    if (SINGLE) {
+      limit = a.max_paths + 1;
+      out_base = (int64_t)q * a.max_paths;
+    } else if (WRITE) {
       limit = a.p_cnt[q];
       out_base = a.p_off[q];
     } else {
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
       __syncwarp();
       while (d >= 0 && count < limit) {
         if (d == k - 1) {
-          emit_range<WRITE>(a, q, d, list_mode, cur[d], end[d], stack_tid, count, limit, out_base);
+          emit_range<WRITE, SINGLE>(a, q, d, list_mode, cur[d], end[d], stack_tid, count, limit, out_base);
           --d;
           continue;
         }
@@ -172,7 +176,7 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
           if (lane == 0) cur[d] = b + 32;
           __syncwarp();
           unsigned nonempty = __ballot_sync(TH_FULL, pass && rhi > rlo);
-          if (!WRITE && !a.masks) {
+          if (!WRITE && !SINGLE && !a.masks) {
             int64_t n = rhi - rlo;
             for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(TH_FULL, n, o);
             count += n;
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
             const int64_t lo = __shfl_sync(TH_FULL, rlo, f), hi = __shfl_sync(TH_FULL, rhi, f);
             if (lane == 0) stack_tid[d] = t;
             __syncwarp();
-            emit_range<WRITE>(a, q, d + 1, false, lo, hi, stack_tid, count, limit, out_base);
+            emit_range<WRITE, SINGLE>(a, q, d + 1, false, lo, hi, stack_tid, count, limit, out_base);
             __syncwarp();
           }
           // drain the skipped lanes' state when the limit was hit
@@ -232,12 +236,27 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
         __syncwarp();
       }
     }
-    if (!WRITE && lane == 0) {
+    if ((!WRITE || SINGLE) && lane == 0) {
       const int64_t cap = a.max_paths;
       a.p_cnt[q] = cap < 0 ? count : min(count, cap);
       a.p_trunc[q] = cap >= 0 && count > cap;
     }
     __syncwarp();
+  }
+}
+
+// pack each query's slot of the single-pass buffer at its scanned offset
+// (warp per query); nothing is written past the capacity (th_finish then
+// reports the overflow and the run is repeated with room)
+__global__ void paths_compact_kernel(PathArgs a) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int q = gw; q < a.B; q += nw) {
+    const int64_t n = a.p_cnt[q], o = a.p_off[q];
+    if (o + n > a.cap) continue;
+    const int32_t* src = a.tmp + (int64_t)q * a.max_paths * a.k;
+    int32_t* dst = a.p_tids + o * a.k;
+    for (int64_t i = lane_id(); i < n * a.k; i += 32) dst[i] = src[i];
   }
 }
 
@@ -257,6 +276,23 @@ int launch_paths(const PathArgs& a, cudaStream_t st) {
   const unsigned grid =
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)a.B * 32, kPathThreads),
                                                        kNumSMs * 16));
+  if (a.tmp) {
+    // capped: one writing DFS into per-query slots, then pack
+    if (a.B > 0) {
+      paths_kernel<true, true><<<grid, kPathThreads, 0, st>>>(a);
+      TH_LAUNCHED();
+      launches += 1 + scan_exclusive<int64_t>(a.p_cnt, a.p_off, a.B, a.scratch, st);
+    }
+    paths_total_kernel<<<1, 1, 0, st>>>(a.p_off, a.p_cnt, a.B, a.used);
+    TH_LAUNCHED();
+    launches += 1;
+    if (a.B > 0) {
+      paths_compact_kernel<<<grid, kPathThreads, 0, st>>>(a);
+      TH_LAUNCHED();
+      launches += 1;
+    }
+    return launches;
+  }
   if (a.B > 0) {
     paths_kernel<false><<<grid, kPathThreads, 0, st>>>(a);
     TH_LAUNCHED();

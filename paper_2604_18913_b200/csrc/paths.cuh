@@ -31,6 +31,10 @@ struct PathArgs {
   int64_t* scratch;
   int64_t cap;        // capacity in paths
   int64_t* used;      // device: total paths
+  // capped queries: one DFS writes each query's paths into its own
+  // max_paths-sized slot of tmp ([B][max_paths][k]), a compaction packs
+  // them (instead of a counting DFS + a writing DFS); null = two passes
+  int32_t* tmp = nullptr;
 };
 
 int64_t scan_scratch_elems_i64(int64_t n);
