@@ -14,6 +14,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
 python tools/summarize_launches.py /tmp/launches.csv > gpurun_out/launches.txt
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:"mat_kernel|pull_kernel|push_|clear_rows|mat_scan" -s 52 -c 26 \
-  -o /tmp/step python tools/prof_c2.py > gpurun_out/ncu_step.log 2>&1; echo step=$?
+  -f -o /tmp/step python tools/prof_c2.py > gpurun_out/ncu_step.log 2>&1; echo step=$?
 python tools/ncu_summary.py /tmp/step.ncu-rep > gpurun_out/step_summary.txt
 python tools/ncu_traffic.py /tmp/step.ncu-rep gpurun_out/step_traffic.json
