@@ -129,6 +129,8 @@ typedef struct {
 /* Device-resident results of the last th_run on a session.
  * Frontier of query q at hop h (1-based):
  *   frontier_ids[frontier_off[(h-1)*B+q] .. +frontier_len[(h-1)*B+q]]
+ * (segments are found through the offsets only: their placement in the id
+ * array may differ from run to run; their contents are deterministic)
  * Activated triples likewise with act_*.  Paths of query q:
  *   path_tids[(path_off[q] + i) * k + d], i < path_count[q], d < k. */
 typedef struct {
