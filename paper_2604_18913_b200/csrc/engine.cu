@@ -66,6 +66,7 @@ struct WaveArgs {
   int64_t* heavy_off;  // [heavy_len + 1] exclusive chunk prefix of the heavy rows
   Ctl* ctl;
   int nq, sem, h;
+  int last_frontier;  // FRONTIER's last hop: nothing reads V afterwards
 };
 
 template <int W>
@@ -1033,6 +1034,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   bool next_edges_done = false;
   for (int h = 1; h <= k; ++h) {
     a.h = h;
+    a.last_frontier = h == k && sem == TH_FRONTIER;
     const bool edges_done = next_edges_done;
     next_edges_done = false;
     {

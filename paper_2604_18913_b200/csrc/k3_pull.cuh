@@ -236,9 +236,11 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
     any = (__ballot_sync(TH_FULL, any) & gbits) != 0u;
     bool fresh = false;
     if (live && any) {
+      // (FRONTIER's last hop skips the visited-row update: the wave ends
+      // with the layer, and the visited matrix is only cleared after it)
       if (!split) {
         st_words<VEC>(a.N + row, nb);
-        if (SEM != TH_EXACT) {
+        if (SEM != TH_EXACT && !a.last_frontier) {
           uint32_t nv[VEC];
 #pragma unroll
           for (int c = 0; c < VEC; ++c) nv[c] = seen[c] | nb[c];
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
         for (int c = 0; c < VEC; ++c) {
           if (nb[c]) {
             atomicOr(a.N + row + c, nb[c]);
-            if (SEM != TH_EXACT) atomicOr(a.V + row + c, nb[c]);
+            if (SEM != TH_EXACT && !a.last_frontier) atomicOr(a.V + row + c, nb[c]);
           }
         }
       }
