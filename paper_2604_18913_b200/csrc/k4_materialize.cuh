@@ -296,6 +296,44 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
     // DRAM in the count pass against 1.93 GB in the synchronised write
     // pass; EDGES passes synchronise for their degree planes anyway)
     if ((WRITE ? !LOAD_S : !EDGES) && NW > 1) __syncthreads();
+    if constexpr (!WRITE && !BUILD_S && !EDGES) {
+      // plain count pass: a bit-sliced vertical popcount -- every lane adds
+      // its row words of the chunk's 32 tiles into six counter planes
+      // (ripple carry, 12 ops per word, no divergence), and one transpose
+      // per plane at the end gives each query's count: 6 transposes per
+      // chunk instead of one per dense tile plus per-bit atomics on sparse
+      // ones
+      uint32_t c[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+      uint32_t cfl = 0u;
+      if constexpr (Src::kDense) cfl = src.chunk_flags(c0, rend);
+#pragma unroll 1
+      for (int t0 = 0; t0 < 32; t0 += 8) {
+        uint32_t x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t r0 = c0 + 32 * (t0 + u);
+          int64_t aux = 0;
+          uint32_t fl;
+          if constexpr (Src::kDense) fl = __shfl_sync(TH_FULL, cfl, t0 + u);
+          else fl = r0 < rend ? src.prep(r0, aux) : 0u;
+          x[u] = ((fl >> lane) & 1u) ? src.word(r0 + lane, aux, j) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          uint32_t cy = x[u];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            const uint32_t t = c[i] & cy;
+            c[i] ^= cy;
+            cy = t;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 6; ++i)
+        if (__any_sync(TH_FULL, c[i] != 0u)) total += __popc(transpose32(c[i])) << i;
+      continue;
+    }
     const size_t sbase = ((size_t)(c0 / kChunkRows) * W + j) * 1024;
     // ---- A: tile masks of this chunk, S[b][t] = rows of tile t in query b.
     // Loads of 8 tiles are issued before their transposes (memory-level
