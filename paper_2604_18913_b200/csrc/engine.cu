@@ -85,8 +85,10 @@ struct Grp {
 // ---------------------------------------------------------------- seeds
 
 template <int W>
+// (e_out: unfiltered |T_1(q)| = out-degree sum of q's distinct seeds,
+// written per query, so hop 1 needs no edge-count pass)
 __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
-                                 const int32_t* __restrict__ seeds, int q0) {
+                                 const int32_t* __restrict__ seeds, int q0, int64_t* e_out) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -94,6 +96,7 @@ __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
     const int32_t lo = qoff[q0 + q], hi = qoff[q0 + q + 1];
     const uint32_t qb = 1u << (q & 31);
     const int qw = q >> 5;
+    unsigned long long dsum = 0ull;
     for (int32_t i0 = lo; i0 < hi; i0 += 32) {
       const int32_t i = i0 + lane;
       int32_t e = -1;
@@ -107,7 +110,8 @@ __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
       }
       if (e >= 0) {
         const size_t r = (size_t)e * W + qw;
-        atomicOr(&a.X[r], qb);
+        const uint32_t old = atomicOr(&a.X[r], qb);
+        if (e_out && !(old & qb)) dsum += (unsigned long long)(a.indptr[e + 1] - a.indptr[e]);
         if (a.sem != TH_EXACT) atomicOr(&a.V[r], qb);
         if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
         const uint32_t fb = 1u << (e & 31);
@@ -116,6 +120,11 @@ __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
       }
       const uint32_t d = fresh ? (uint32_t)(a.indptr[e + 1] - a.indptr[e]) : 0u;
       warp_append_all(fresh, e, d, a.lists, &a.ctl->list_len[0], a.E, &a.ctl->push_cost[0]);
+    }
+    if (e_out) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) dsum += __shfl_xor_sync(TH_FULL, dsum, o);
+      if (lane == 0) e_out[q] = (int64_t)dsum;
     }
   }
 }
@@ -1011,7 +1020,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
       s->launches += 1;
     }
     seed_init_kernel<W><<<grid_for((int64_t)nq * 32), kThreads, 0, st>>>(a, q->d_seed_offsets,
-                                                                         q->d_seeds, q0);
+                                                                         q->d_seeds, q0,
+        filter ? nullptr : static_cast<int64_t*>(s->edges.p) + q0);
     TH_LAUNCHED();
     s->launches += 1;
   }
@@ -1031,7 +1041,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
 
   int nplanes = 0;
   while (nplanes < 31 && (int64_t(1) << nplanes) <= g->max_out) ++nplanes;
-  bool next_edges_done = false;
+  bool next_edges_done = !filter;  // hop 1's counts come from seed_init
   for (int h = 1; h <= k; ++h) {
     a.h = h;
     a.last_frontier = h == k && sem == TH_FRONTIER;
