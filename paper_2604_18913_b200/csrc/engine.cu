@@ -625,14 +625,19 @@ __global__ void mat_scan_queries_kernel(const int64_t* totals, int nq, int64_t* 
     ws[lane] = w;
   }
   __syncthreads();
-  const int64_t base = *cursor;
+  // reserve this layer's output range atomically: consecutive layers' K4s
+  // run on two streams and take their ranges from the same cursor
+  __shared__ int64_t base_s;
+  if (q == 0)
+    base_s = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(cursor),
+                                (unsigned long long)ws[(blockDim.x >> 5) - 1]);
+  __syncthreads();
+  const int64_t base = base_s;
   const int64_t ex = (warp ? ws[warp - 1] : 0) + x - v;
   if (q < nq) {
     off[q] = base + ex;
     len[q] = v;
   }
-  __syncthreads();
-  if (q == 0) *cursor = base + ws[(blockDim.x >> 5) - 1];
 }
 
 // ---------------------------------------------- flag bitmap -> row list

@@ -1,0 +1,64 @@
+"""Randomised parity sweep over the engine's strategy switches: wave widths
+(B from 1 to past one wave), k = 1..4, every semantics, relation filters,
+K4 dense (mask cache) / list-driven (incl. the bit-sliced count pass and
+the first-layer row list), push / pull / auto directions, CUDA-graph
+replay -- each case against the oracle on sampled seeds."""
+
+import numpy as np
+import pytest
+
+from oracle import khop_oracle as orc
+from test_gpu_parity import _hub_graph
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases():
+    rng = np.random.default_rng(2026)
+    out = []
+    for i in range(60):
+        out.append(dict(
+            E=int(rng.integers(50, 1500)), T=int(rng.integers(200, 20000)), R=int(rng.integers(1, 40)),
+            alpha=float(rng.choice([0.8, 1.1, 1.4])), B=int(rng.choice([1, 7, 32, 33, 200, 1024, 1100])),
+            k=int(rng.integers(1, 5)), sem=str(rng.choice(["exact", "frontier", "cumulative"])),
+            filt=bool(rng.random() < 0.35), list_mode=bool(rng.random() < 0.5),
+            divisor=float(rng.choice([0.0, -1.0, 8.0])),
+            paths=bool(rng.random() < 0.3), max_paths=[0, 5, 100, None][int(rng.integers(0, 4))], seed=i))
+    return out
+
+
+@pytest.mark.parametrize("c", _cases(), ids=lambda c: f"s{c['seed']}")
+def test_random_configuration(th_mod, c):
+    th = th_mod
+    s, r, o = _hub_graph(c["E"], c["T"], c["R"], seed=c["seed"], alpha=c["alpha"])
+    E, R = c["E"], c["R"]
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    rng = np.random.default_rng(c["seed"] + 100)
+    ret = th.Retriever(g)
+    ret.set_pull_divisor(c["divisor"])
+    ret.set_list_min_entities(0 if c["list_mode"] else 1 << 40)
+    for rep in range(3):  # eager run, graph capture, replay (new seeds each time)
+        seeds = rng.integers(0, E, c["B"])
+        filt = None
+        if c["filt"]:
+            filt = [sorted(rng.choice(R, max(1, R // 3), replace=False).tolist()) for _ in range(c["B"])]
+        paths = c["paths"] and c["k"] <= 3
+        res = ret.retrieve(seeds, c["k"], relation_filter=filt, semantics=c["sem"], paths=paths,
+                           max_paths=c["max_paths"])
+        for i in sorted(set([0, c["B"] - 1, c["B"] // 2])):
+            ref = orc.retrieve_one(og, int(seeds[i]), c["k"], c["sem"], None if filt is None else filt[i],
+                                   paths=paths, max_paths=c["max_paths"])
+            for h in range(c["k"]):
+                assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (rep, i, h)
+                assert int(res.edges[h, i]) == ref["edges"][h], (rep, i, h)
+            if paths:
+                assert res.path_tid_tuples(i) == ref["paths"], (rep, i)
+                assert res.truncated(i) == ref["truncated"], (rep, i)
+
+
+@pytest.fixture(scope="module")
+def th_mod(cuda_device):
+    import paper_2604_18913_b200 as th
+
+    return th
