@@ -62,3 +62,32 @@ def th_mod(cuda_device):
     import paper_2604_18913_b200 as th
 
     return th
+
+
+@pytest.mark.parametrize("direction", [0.0, -1.0, 8.0], ids=["push", "pull", "auto"])
+@pytest.mark.parametrize("list_mode", [False, True], ids=["dense", "list"])
+def test_overlapped_layers_repeatedly(th_mod, direction, list_mode):
+    """The overlapped K4s of consecutive layers (two streams) under many
+    repeats: FRONTIER, frontiers only, k = 4, graphs replayed -- every
+    segment checked against the oracle (races show up as wrong ids with the
+    right counts)."""
+    th = th_mod
+    s, r, o = _hub_graph(1400, 15000, 3, seed=77, alpha=1.1)
+    E, R = 1400, 3
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    ret = th.Retriever(g)
+    ret.set_pull_divisor(direction)
+    ret.set_list_min_entities(0 if list_mode else 1 << 40)
+    rng = np.random.default_rng(5)
+    refs = {}
+    for rep in range(12):
+        B = int(rng.choice([1, 3, 40]))
+        seeds = rng.integers(0, E, B)
+        res = ret.retrieve(seeds, 4)
+        for i in range(B):
+            sd = int(seeds[i])
+            if sd not in refs:
+                refs[sd] = orc.retrieve_one(og, sd, 4, "frontier")
+            for h in range(4):
+                assert np.array_equal(res.frontier(i, h + 1), refs[sd]["frontiers"][h]), (rep, i, h)
