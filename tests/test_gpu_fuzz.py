@@ -91,3 +91,30 @@ def test_overlapped_layers_repeatedly(th_mod, direction, list_mode):
                 refs[sd] = orc.retrieve_one(og, sd, 4, "frontier")
             for h in range(4):
                 assert np.array_equal(res.frontier(i, h + 1), refs[sd]["frontiers"][h]), (rep, i, h)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_seed_sets_reference_api(th_mod, seed):
+    """Multi-seed queries through the reference API (k_hop with activated
+    sets, reconstruct_paths with caps): the non-singleton engine path."""
+    th = th_mod
+    rng = np.random.default_rng(seed)
+    E, T, R = int(rng.integers(30, 600)), int(rng.integers(50, 5000)), int(rng.integers(1, 8))
+    s, r, o = _hub_graph(E, T, R, seed=seed + 300, alpha=float(rng.choice([0.9, 1.2])))
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    for _ in range(3):
+        ids = np.unique(rng.integers(0, E, int(rng.integers(1, 12))))
+        k = int(rng.integers(1, 4))
+        sem = str(rng.choice(["exact", "frontier", "cumulative"]))
+        tr = th.k_hop(th.EntityVector(ids, E), k, g, th.HopSemantics.parse(sem))
+        ref = orc.hop_trace(og, ids, k, sem)
+        for h in range(k):
+            assert np.array_equal(tr.frontier(h + 1).ids, ref[h][0]), (sem, h)
+            assert np.array_equal(tr.activated(h + 1).ids, ref[h][1]), (sem, h)
+        cap = [0, 3, 50, None][int(rng.integers(0, 4))]
+        pr = th.reconstruct_paths(th.EntityVector(ids, E), k, g, max_paths=cap)
+        want, trunc = orc.walk_paths(og, ids, k, cap)
+        got = [tuple(tuple(int(x) for x in t) for t in p) for p in pr.paths]
+        assert got == orc.paths_as_triples(og, want), (ids.tolist(), k, cap)
+        assert pr.truncated == trunc
