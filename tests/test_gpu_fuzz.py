@@ -118,3 +118,31 @@ def test_random_seed_sets_reference_api(th_mod, seed):
         got = [tuple(tuple(int(x) for x in t) for t in p) for p in pr.paths]
         assert got == orc.paths_as_triples(og, want), (ids.tolist(), k, cap)
         assert pr.truncated == trunc
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_partitioned_graphs(th_mod, seed):
+    """Random graphs on 1-4 loopback ranks (hash owners, edge-split hubs,
+    push/pull/auto directions across partitions) against the single-graph
+    engine: frontier and activated sets and edge counts per seed."""
+    th = th_mod
+    rng = np.random.default_rng(seed + 900)
+    E, T, R = int(rng.integers(100, 1500)), int(rng.integers(300, 15000)), int(rng.integers(1, 10))
+    s, r, o = _hub_graph(E, T, R, seed=seed + 500, alpha=float(rng.choice([0.9, 1.2, 1.4])))
+    world = int(rng.integers(1, 5))
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(world), n_hubs=int(rng.integers(0, 12)))
+    pg.pull_divisor = float(rng.choice([0.0, 8.0, 1e9]))
+    g = th.build_incidence((s, r, o), E, R)
+    seeds = rng.integers(0, E, int(rng.choice([1, 17, 300])))
+    k = int(rng.integers(1, 4))
+    sem = str(rng.choice(["exact", "frontier", "cumulative"]))
+    filt = None
+    if rng.random() < 0.3:
+        filt = [sorted(rng.choice(R, max(1, R // 2), replace=False).tolist()) for _ in seeds]
+    a = pg.retrieve(seeds, k, relation_filter=filt, semantics=sem, activated=True)
+    b = th.Retriever(g).retrieve(seeds, k, relation_filter=filt, semantics=sem, activated=True)
+    for i in range(len(seeds)):
+        for h in range(k):
+            assert np.array_equal(a.frontier(i, h + 1), b.frontier(i, h + 1)), (world, i, h)
+            assert np.array_equal(a.activated(i, h + 1), b.activated(i, h + 1)), (world, i, h)
+            assert int(a.edges[h, i]) == int(b.edges[h, i]), (world, i, h)
