@@ -233,7 +233,7 @@ __device__ __forceinline__ void row_pairs(const WaveArgs& a, int32_t u, int32_t 
       j = j1;
     } else {
       e = p / nzw;
-      j = (int)__fns(nz, 0, p - e * nzw + 1);
+      j = select_bit(nz, p - e * nzw);
     }
     const uint32_t x = __shfl_sync(TH_FULL, xw, j & 31);
     bool fresh = false;

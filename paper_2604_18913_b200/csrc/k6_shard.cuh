@@ -139,7 +139,7 @@ __device__ __forceinline__ void shard_row_pairs(const ShardArgs& sa, int32_t u, 
       j = j1;
     } else {
       e = p / nzw;
-      j = (int)__fns(nz, 0, p - e * nzw + 1);
+      j = select_bit(nz, p - e * nzw);
     }
     const uint32_t x = __shfl_sync(TH_FULL, xw, j & 31);
     bool fresh = false, rfresh = false;
