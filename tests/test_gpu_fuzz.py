@@ -146,3 +146,23 @@ def test_random_partitioned_graphs(th_mod, seed):
             assert np.array_equal(a.frontier(i, h + 1), b.frontier(i, h + 1)), (world, i, h)
             assert np.array_equal(a.activated(i, h + 1), b.activated(i, h + 1)), (world, i, h)
             assert int(a.edges[h, i]) == int(b.edges[h, i]), (world, i, h)
+
+
+def test_duplicate_seeds_in_a_query(th_mod):
+    """th_query allows duplicate seeds: a set query with repeats equals the
+    deduplicated one (frontiers and hop-1 edge counts from seed init)."""
+    import torch
+
+    th = th_mod
+    s, r, o = _hub_graph(300, 3000, 4, seed=3)
+    g = th.build_incidence((s, r, o), 300, 4)
+    ret = th.Retriever(g)
+    dev = g.device
+    dup = torch.tensor([5, 5, 7, 5, 7, 11], dtype=torch.int32, device=dev)
+    uniq = torch.tensor([5, 7, 11], dtype=torch.int32, device=dev)
+    for sem in ("exact", "frontier", "cumulative"):
+        a = ret.run(torch.tensor([0, 6], dtype=torch.int32, device=dev), dup, 3, sem, copy=True)
+        b = ret.run(torch.tensor([0, 3], dtype=torch.int32, device=dev), uniq, 3, sem, copy=True)
+        assert bool((a.edges == b.edges).all()), sem
+        for h in range(3):
+            assert np.array_equal(a.frontier(0, h + 1), b.frontier(0, h + 1)), (sem, h)
