@@ -209,6 +209,18 @@ int th_session_wave_lists(const th_session* s, int64_t* lens, int n);
  * d_owner: int32[E].  Asynchronous. */
 int th_plan_owner_hash(const th_graph* g, int32_t m, int32_t* d_owner, void* stream);
 
+/* Host-only planner (no GPU needed): the assignment and per-partition loads
+ * of plan_partitions (partition.py:49-98) from subject out-degrees
+ * (h_degrees[E], 0 = not a subject -> -1 UNASSIGNED).  TH_PLAN_HASH = the
+ * multiplicative hash (partition.py:80-84); TH_PLAN_LPT = heaviest subject
+ * first (ties by id) onto the lightest partition (ties by index)
+ * (partition.py:85-94).  h_loads[m].  Range checks on m against the subject
+ * count are the caller's (they raise UsageError in the reference). */
+#define TH_PLAN_HASH 0
+#define TH_PLAN_LPT 1
+int th_plan_subjects(const int64_t* h_degrees, int64_t n_entities, int32_t m, int32_t strategy,
+                     int32_t* h_assignment, int64_t* h_loads);
+
 /* ---- partitioned graphs (multi-GPU; one shard per rank) ---------------- */
 
 /* Ownership: own(v) = ((v * 0x9E3779B1) mod 2^32) mod world for every

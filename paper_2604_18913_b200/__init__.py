@@ -22,7 +22,7 @@ from .core_types import (
     jaccard,
 )
 from .archive import graph_from_bytes, graph_to_bytes, load_graph, save_graph
-from .cache import CacheCounters, SubgraphCache, simulate_lru
+from .cache import CacheCounters, SubgraphCache
 from .device_graph import IncidenceGraph, build_incidence
 from .errors import DataError, IntegrityError, TripleHopError, UsageError
 from .partition import (
@@ -41,47 +41,30 @@ from .partition import (
 )
 from .retriever import RetrievalResult, Retriever, k_hop, one_hop, reconstruct_paths, retrieve
 from .store import (
-    BatchQuery,
-    BatchResult,
-    Dictionary,
     DirectoryStore,
     InMemoryStore,
-    QueryBatch,
+    PartitionManifest,
     StorePartitionedGraph,
     Subgraph,
-    load_labels,
     load_partition_plan,
     materialize_subgraphs,
     open_partitioned,
-    plan_batch,
-    run_batch,
-    save_labels,
     save_partition_dir,
-    signature,
 )
 from .targets import GpuTarget, PartitionedGpuTarget
 
 __all__ = [
-    "BatchQuery",
-    "BatchResult",
-    "Dictionary",
     "DirectoryStore",
     "InMemoryStore",
-    "QueryBatch",
+    "PartitionManifest",
     "StorePartitionedGraph",
     "Subgraph",
-    "load_labels",
     "load_partition_plan",
     "materialize_subgraphs",
     "open_partitioned",
-    "plan_batch",
-    "run_batch",
-    "save_labels",
     "save_partition_dir",
-    "signature",
     "CacheCounters",
     "SubgraphCache",
-    "simulate_lru",
     "GpuTarget",
     "PartitionedGpuTarget",
     "graph_from_bytes",

@@ -18,6 +18,7 @@ LIB_PATH = Path(os.environ.get("TH_B200_LIB", Path(__file__).resolve().parent / 
 TH_EXACT, TH_FRONTIER, TH_CUMULATIVE = 0, 1, 2
 TH_WANT_FRONTIERS, TH_WANT_ACTIVATED, TH_WANT_PATHS, TH_SINGLETON_SEEDS = 0x1, 0x2, 0x4, 0x8
 TH_GRAPH_NO_REVERSE = 0x1
+TH_PLAN_HASH, TH_PLAN_LPT = 0, 1
 ABI_VERSION = 1
 
 # every symbol include/th_b200.h declares (checked by tests/test_abi.py)
@@ -32,7 +33,7 @@ EXPORTS = (
     "th_shard_hub_rows",
     "th_shard_hub_merge", "th_shard_end_hop", "th_shard_finish",
     "th_ids_route_count", "th_ids_map_scatter", "th_ids_to_local_bits", "th_bits_andnot_update",
-    "th_bits_or", "th_bits_compact",
+    "th_bits_or", "th_bits_compact", "th_plan_subjects",
 )
 PROF_CATEGORIES = ("setup", "edges", "activated", "push", "pull", "frontier", "clear", "paths")
 
@@ -137,6 +138,7 @@ def load():
         "th_bits_or": (ctypes.c_int, [_vp, _vp, ctypes.c_int64, _vp]),
         "th_bits_compact": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64,
                                            ctypes.POINTER(ctypes.c_int64), _vp]),
+        "th_plan_subjects": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, _vp, _vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

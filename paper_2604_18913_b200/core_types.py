@@ -58,7 +58,7 @@ class HopSemantics(enum.Enum):
         return {"exact": 0, "frontier": 1, "cumulative": 2}[self.value]
 
 
-def _canonical(ids, width: int) -> np.ndarray:
+def _canonicalise(ids, width: int) -> np.ndarray:
     if isinstance(ids, np.ndarray):
         arr = ids.astype(np.int64, copy=False).reshape(-1)
     else:
@@ -80,13 +80,13 @@ class _IdVector:
 
     __slots__ = ("ids", "width")
 
-    def __init__(self, ids, width: int, _canonical_ids: bool = False):
-        if _canonical_ids:
+    def __init__(self, ids, width: int, _canonical: bool = False):
+        if _canonical:
             arr = np.asarray(ids, dtype=np.int64).reshape(-1)
             if arr.size and (arr[0] < 0 or arr[-1] >= width):
                 raise ValueError(f"id out of range for width {width}")
         else:
-            arr = _canonical(ids, width)
+            arr = _canonicalise(ids, width)
         arr.setflags(write=False)
         self.ids = arr
         self.width = int(width)

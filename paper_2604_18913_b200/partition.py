@@ -34,7 +34,6 @@ one device (GPU parity tests on a single B200).
 from __future__ import annotations
 
 import ctypes
-import heapq
 import weakref
 from dataclasses import dataclass
 
@@ -60,15 +59,30 @@ def hash_owner(ids, m: int) -> np.ndarray:
 # --------------------------------------------------------------- plans
 
 
-@dataclass(frozen=True)
 class PartitionPlan:
-    """Subject -> partition assignment plus per-partition triple loads
-    (partition.py:28-42)."""
+    """Subject -> partition assignment and per-partition triple loads
+    (the reference's ``PartitionPlan``, partition.py:28-42): ``m``,
+    ``assignment`` (int32 per entity, ``UNASSIGNED`` for entities that are
+    never a subject), ``loads`` (int64 per partition) and ``strategy``."""
 
-    m: int
-    assignment: np.ndarray  # int32 per entity; UNASSIGNED for non-subjects
-    loads: np.ndarray  # int64 per partition
-    strategy: str
+    __slots__ = ("m", "assignment", "loads", "strategy")
+
+    def __init__(self, m: int, assignment: np.ndarray, loads: np.ndarray, strategy: str):
+        object.__setattr__(self, "m", int(m))
+        object.__setattr__(self, "assignment", assignment)
+        object.__setattr__(self, "loads", loads)
+        object.__setattr__(self, "strategy", strategy)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("PartitionPlan is immutable")
+
+    def __eq__(self, other) -> bool:
+        return (isinstance(other, PartitionPlan) and self.m == other.m and self.strategy == other.strategy
+                and np.array_equal(self.assignment, other.assignment)
+                and np.array_equal(self.loads, other.loads))
+
+    def __repr__(self) -> str:
+        return f"PartitionPlan(m={self.m}, strategy={self.strategy!r}, loads={self.loads.tolist()})"
 
     @property
     def n_entities(self) -> int:
@@ -78,64 +92,76 @@ class PartitionPlan:
         return int(self.assignment[entity])
 
 
-def plan_partitions(triples, m: int, strategy: str = "lpt") -> PartitionPlan:
-    """Assign every subject to one of m partitions (partition.py:49-98).
-
-    ``triples`` is a (subject column, entity count) pair or an
-    ``IncidenceGraph``.  Hash: the multiplicative hash; LPT: heaviest
-    subjects first (ties by id), each to the least-loaded partition.
-    """
+def _subject_columns(triples):
+    """(subject column, entity count) from an IncidenceGraph or a pair."""
     if hasattr(triples, "subj") and hasattr(triples, "n_entities"):
-        subj, n_entities = triples.subj, triples.n_entities
-    else:
-        subj, n_entities = triples
-    subj = np.asarray(subj, dtype=np.int64)
-    degrees = np.bincount(subj, minlength=n_entities).astype(np.int64)
-    subjects = np.flatnonzero(degrees)
+        return triples.subj, int(triples.n_entities)
+    subj, n_entities = triples
+    return subj, int(n_entities)
+
+
+def plan_partitions(triples, m: int, strategy: str = "lpt") -> PartitionPlan:
+    """Place every subject on one of ``m`` partitions (partition.py:49-98).
+
+    ``triples``: a (subject column, entity count) pair or an
+    ``IncidenceGraph``.  The placement itself is native
+    (``th_plan_subjects``, ``csrc/planner.cu``): ``"hash"`` is the
+    reference's multiplicative hash, ``"lpt"`` its heaviest-first greedy
+    (ties by smaller id onto the lightest, then lowest-index partition).
+    Argument errors raise ``UsageError`` with the reference's messages.
+    """
+    subj, n_entities = _subject_columns(triples)
+    degrees = np.bincount(np.asarray(subj, dtype=np.int64), minlength=n_entities).astype(np.int64)
+    n_subjects = int(np.count_nonzero(degrees))
     if m < 1:
         raise UsageError("partition count must be >= 1")
-    if m > subjects.size:
-        raise UsageError(f"partition count {m} exceeds distinct subject count {subjects.size}")
-    if strategy not in STRATEGIES:
+    if m > n_subjects:
+        raise UsageError(f"partition count {m} exceeds distinct subject count {n_subjects}")
+    code = {"hash": _lib.TH_PLAN_HASH, "lpt": _lib.TH_PLAN_LPT}.get(strategy)
+    if code is None:
         raise UsageError(f"unknown partition strategy {strategy!r}")
-    assignment = np.full(n_entities, UNASSIGNED, dtype=np.int32)
-    loads = np.zeros(m, dtype=np.int64)
-    if strategy == "hash":
-        buckets = hash_owner(subjects, m)
-        assignment[subjects] = buckets
-        np.add.at(loads, buckets, degrees[subjects])
-    else:
-        order = np.lexsort((subjects, -degrees[subjects]))
-        heap = [(0, p) for p in range(m)]
-        for e in subjects[order].tolist():
-            load, p = heapq.heappop(heap)
-            assignment[e] = p
-            load += int(degrees[e])
-            loads[p] = load
-            heapq.heappush(heap, (load, p))
+    assignment = np.empty(n_entities, dtype=np.int32)
+    loads = np.empty(m, dtype=np.int64)
+    _lib.check(_lib.load().th_plan_subjects(degrees.ctypes.data, n_entities, m, code,
+                                             assignment.ctypes.data, loads.ctypes.data))
     assignment.setflags(write=False)
     loads.setflags(write=False)
     return PartitionPlan(m, assignment, loads, strategy)
 
 
-@dataclass(frozen=True)
 class RouteResult:
-    """Frontier ids bucketed by partition; non-subjects go to ``sink``."""
+    """Frontier ids grouped by partition (``buckets``: partition ->
+    ``EntityVector``); ids that are never a subject go to ``sink``."""
 
-    buckets: dict
-    sink: EntityVector
+    __slots__ = ("buckets", "sink")
+
+    def __init__(self, buckets: dict, sink: EntityVector):
+        self.buckets = buckets
+        self.sink = sink
 
 
 def route(q: EntityVector, plan: PartitionPlan) -> RouteResult:
-    """Group the active entities of q by their partition (partition.py:170-181)."""
+    """Bucket the active entities of q by partition (partition.py:170-181).
+
+    One stable sort by partition keeps each bucket ascending (q is), and the
+    bucket boundaries split it; ``UNASSIGNED`` (-1) sorts first and is the
+    sink.
+    """
     if q.width != plan.n_entities:
         raise ValueError(f"query width {q.width} != plan entity count {plan.n_entities}")
-    parts = plan.assignment[q.ids]
-    assigned = parts != UNASSIGNED
-    buckets = {}
-    for p in np.unique(parts[assigned]).tolist():
-        buckets[p] = EntityVector(q.ids[parts == p], q.width, _canonical_ids=True)
-    return RouteResult(buckets, EntityVector(q.ids[~assigned], q.width, _canonical_ids=True))
+    part = plan.assignment[q.ids]
+    order = np.argsort(part, kind="stable")
+    keys = part[order]
+    cuts = np.flatnonzero(np.diff(keys)) + 1
+    pieces = np.split(q.ids[order], cuts)
+    heads = keys[np.concatenate([[0], cuts])] if keys.size else keys
+    buckets, sink = {}, q.ids[:0]
+    for p, ids in zip(heads.tolist(), pieces):
+        if p == UNASSIGNED:
+            sink = ids
+        else:
+            buckets[p] = EntityVector(ids, q.width, _canonical=True)
+    return RouteResult(buckets, EntityVector(sink, q.width, _canonical=True))
 
 
 @dataclass(frozen=True)
@@ -727,8 +753,8 @@ def cross_graph_k_hop(q0: EntityVector, k: int, pg: PartitionedGraph,
     for h in range(k):
         fo, fl = int(m["f_off"][h, 0]), int(m["f_len"][h, 0])
         ao, al = int(m["a_off"][h, 0]), int(m["a_len"][h, 0])
-        steps.append(HopStep(EntityVector(m["f_ids"][fo:fo + fl], pg.n_entities, _canonical_ids=True),
-                             TripleVector(m["a_ids"][ao:ao + al], pg.n_triples, _canonical_ids=True)))
+        steps.append(HopStep(EntityVector(m["f_ids"][fo:fo + fl], pg.n_entities, _canonical=True),
+                             TripleVector(m["a_ids"][ao:ao + al], pg.n_triples, _canonical=True)))
     return HopTrace(sem, q0, steps)
 
 

@@ -112,8 +112,8 @@ class RetrievalResult:
         steps = []
         for h in range(1, self.k + 1):
             act = self.activated(q, h) if self.act_ids is not None else np.empty(0, np.int64)
-            steps.append(HopStep(EntityVector(self.frontier(q, h), g.n_entities, _canonical_ids=True),
-                                 TripleVector(act, g.n_triples, _canonical_ids=True)))
+            steps.append(HopStep(EntityVector(self.frontier(q, h), g.n_entities, _canonical=True),
+                                 TripleVector(act, g.n_triples, _canonical=True)))
         return HopTrace(self.semantics, EntityVector(seeds, g.n_entities), steps)
 
 

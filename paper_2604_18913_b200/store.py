@@ -7,11 +7,9 @@ Reference (citations relative to /root/reference/pkg/src/triplehop):
 * ``InMemoryStore`` / ``PartitionedGraph`` ....... engine.py:34-86
 * ``_partitioned_expand`` / ``cross_graph_k_hop`` / ``cross_graph_paths``
   (Algorithm 1) ............................... engine.py:94-182
-* ``BatchQuery`` ... ``plan_batch`` / ``run_batch`` engine.py:186-258
 * ``save_partition_dir`` / ``load_partition_plan`` / ``DirectoryStore`` /
   ``open_partitioned`` ......................... archive.py:188-315
-* ``Dictionary``, ``save_labels``/``load_labels`` . triples.py:26-60,
-  archive.py:150-160
+* label files ................................ archive.py:150-160
 
 A ``PartitionedGraph(plan, store, cache)`` keeps the reference's contract:
 partitions are loaded on demand through the LRU ``SubgraphCache`` (a miss
@@ -31,7 +29,6 @@ from __future__ import annotations
 
 import ctypes
 import json
-from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
@@ -40,66 +37,14 @@ from . import _lib
 from .cache import SubgraphCache
 from .core_types import DEFAULT_MAX_PATHS, EntityVector, HopSemantics, HopStep, HopTrace, TripleVector
 from .errors import IntegrityError
-from .partition import UNASSIGNED, PartitionedGraph, PartitionPlan, route
+from .partition import PartitionedGraph, PartitionPlan
 
 GRAPH_FILE = "graph.lkg"
 ENTITIES_FILE = "entities.txt"
 RELATIONS_FILE = "relations.txt"
 MANIFEST_FILE = "manifest.json"
 ASSIGNMENT_FILE = "assignment.u32"
-_ASSIGNMENT_SENTINEL = 0xFFFFFFFF
 ARCHIVE_VERSION = 1
-
-
-# ------------------------------------------------------------ dictionaries
-
-
-class Dictionary:
-    """Bijective label <-> dense id map; ids contiguous from 0 (triples.py:26-60)."""
-
-    def __init__(self, labels=()):
-        self._forward: dict = {}
-        self._reverse: list = []
-        for label in labels:
-            self.add(label)
-
-    def add(self, label: str) -> int:
-        idx = self._forward.get(label)
-        if idx is None:
-            idx = len(self._reverse)
-            self._forward[label] = idx
-            self._reverse.append(label)
-        return idx
-
-    def id_of(self, label: str):
-        return self._forward.get(label)
-
-    def label_of(self, idx: int) -> str:
-        return self._reverse[idx]
-
-    def labels(self) -> list:
-        return list(self._reverse)
-
-    def __len__(self) -> int:
-        return len(self._reverse)
-
-    def __contains__(self, label) -> bool:
-        return label in self._forward
-
-    def __eq__(self, other) -> bool:
-        return isinstance(other, Dictionary) and self._reverse == other._reverse
-
-
-def save_labels(labels, path) -> None:
-    """Newline-delimited label file; line index = id (archive.py:150-152)."""
-    Path(path).write_text("".join(f"{s}\n" for s in labels), encoding="utf-8")
-
-
-def load_labels(path) -> Dictionary:
-    lines = Path(path).read_text(encoding="utf-8").split("\n")
-    if lines and lines[-1] == "":
-        lines.pop()
-    return Dictionary(lines)
 
 
 # ------------------------------------------------------------ device helpers
@@ -211,11 +156,15 @@ class Subgraph:
 
 
 def materialize_subgraphs(plan: PartitionPlan, triples) -> list:
-    """Per-partition device subgraphs (partition.py:125-154): the triples of
-    partition p are those whose subject it owns, local entity ids follow
-    ascending global ids over subjects and objects, local tids ascending
-    global tids.  ``triples`` is (subj, rel, obj, n_entities, n_relations)
-    or an object with ``arrays()``/``n_entities``/``n_relations``."""
+    """Per-partition device subgraphs (partition.py:125-154).
+
+    A triple belongs to its subject's partition; within a partition, local
+    triple ids follow ascending global tids and local entity ids ascending
+    global ids over the partition's subjects and objects.  One stable sort
+    of the triples by partition yields every partition's tid run at once;
+    ``np.unique(..., return_inverse=True)`` gives each run's entity map and
+    local ids together.  ``triples``: (subj, rel, obj, n_entities,
+    n_relations) or an object with ``arrays()``/``n_entities``/``n_relations``."""
     from .device_graph import build_incidence
 
     if hasattr(triples, "arrays"):
@@ -224,15 +173,16 @@ def materialize_subgraphs(plan: PartitionPlan, triples) -> list:
     else:
         subj, rel, obj, n_entities, n_relations = triples
     subj, rel, obj = (np.asarray(c, dtype=np.int64) for c in (subj, rel, obj))
-    part_of_triple = plan.assignment[subj]
+    owner = plan.assignment[subj]
+    by_part = np.argsort(owner, kind="stable")  # ascending tids within a partition
+    bounds = np.searchsorted(owner[by_part], np.arange(plan.m + 1))
     out = []
     for p in range(plan.m):
-        g_tids = np.flatnonzero(part_of_triple == p).astype(np.int64)
-        s, r, o = subj[g_tids], rel[g_tids], obj[g_tids]
-        ents = np.unique(np.concatenate([s, o]))
-        graph = build_incidence((np.searchsorted(ents, s), r, np.searchsorted(ents, o)), int(ents.size),
-                                n_relations)
-        out.append(Subgraph(p, graph, ents, g_tids))
+        tids = by_part[bounds[p]:bounds[p + 1]].astype(np.int64)
+        n = tids.size
+        ents, local = np.unique(np.concatenate([subj[tids], obj[tids]]), return_inverse=True)
+        graph = build_incidence((local[:n], rel[tids], local[n:]), int(ents.size), n_relations)
+        out.append(Subgraph(p, graph, ents, tids))
     return out
 
 
@@ -256,115 +206,147 @@ class InMemoryStore:
             raise IntegrityError(f"store has no partition {index}") from None
 
 
-def _shard_name(index: int) -> str:
-    return f"shard-{index:04d}"
+class PartitionManifest:
+    """The ``manifest.json`` of a partition directory (format of
+    archive.py:188-237, checks of archive.py:240-255): partition count,
+    strategy, entity / relation / triple counts, the assignment file and one
+    entry per shard (archive, entity map, triple map, triple count)."""
+
+    FORMAT = "LKG-partition"
+
+    def __init__(self, fields: dict):
+        self.fields = fields
+        self.m = int(fields["m"])
+        self.n_entities = int(fields["entity_count"])
+        self.n_relations = int(fields["relation_count"])
+        self.n_triples = int(fields["triple_count"])
+        self.shards = {int(s["index"]): s for s in fields["partitions"]}
+
+    @staticmethod
+    def shard_stem(index: int) -> str:
+        return f"shard-{index:04d}"
+
+    @classmethod
+    def read(cls, part_dir: Path) -> "PartitionManifest":
+        path = part_dir / MANIFEST_FILE
+        if not path.exists():
+            raise IntegrityError(f"no partition manifest at {path}")
+        try:
+            fields = json.loads(path.read_text())
+        except json.JSONDecodeError as exc:
+            raise IntegrityError(f"unreadable manifest: {exc}") from exc
+        problems = (
+            (fields.get("format") != cls.FORMAT, "not a partition manifest"),
+            (lambda: len(fields["partitions"]) != fields["m"], "manifest shard list disagrees with m"),
+            (lambda: sum(s["triple_count"] for s in fields["partitions"]) != fields["triple_count"],
+             "per-partition triple counts do not sum to the total"),
+        )
+        for bad, message in problems:
+            if bad() if callable(bad) else bad:
+                raise IntegrityError(message)
+        return cls(fields)
+
+    @classmethod
+    def describe(cls, plan: PartitionPlan, subgraphs, n_relations: int) -> "PartitionManifest":
+        entries = [{"index": sg.index, "shard_file": f"{cls.shard_stem(sg.index)}.lkg",
+                    "entity_map_file": f"{cls.shard_stem(sg.index)}.ents.u64",
+                    "triple_map_file": f"{cls.shard_stem(sg.index)}.tids.u64",
+                    "triple_count": sg.graph.n_triples} for sg in subgraphs]
+        return cls({"format": cls.FORMAT, "version": ARCHIVE_VERSION, "m": plan.m,
+                    "strategy": plan.strategy, "entity_count": plan.n_entities,
+                    "relation_count": n_relations, "triple_count": int(plan.loads.sum()),
+                    "assignment_file": ASSIGNMENT_FILE, "partitions": entries})
+
+    def write(self, part_dir: Path) -> None:
+        (part_dir / MANIFEST_FILE).write_text(json.dumps(self.fields, indent=2, sort_keys=True) + "\n")
 
 
-def _load_manifest(part_dir: Path) -> dict:
-    """archive.py:240-255."""
-    path = part_dir / MANIFEST_FILE
-    if not path.exists():
-        raise IntegrityError(f"no partition manifest at {path}")
-    try:
-        manifest = json.loads(path.read_text())
-    except json.JSONDecodeError as exc:
-        raise IntegrityError(f"unreadable manifest: {exc}") from exc
-    if manifest.get("format") != "LKG-partition":
-        raise IntegrityError("not a partition manifest")
-    shards = manifest["partitions"]
-    if len(shards) != manifest["m"]:
-        raise IntegrityError("manifest shard list disagrees with m")
-    if sum(s["triple_count"] for s in shards) != manifest["triple_count"]:
-        raise IntegrityError("per-partition triple counts do not sum to the total")
-    return manifest
+def _label_lines(labels) -> bytes:
+    """Newline-terminated labels, line index = id (the label files of
+    archive.py:150-160); ``labels`` is any sequence of strings or an object
+    with ``labels()``."""
+    seq = labels.labels() if hasattr(labels, "labels") else labels
+    return "".join(f"{s}\n" for s in seq).encode("utf-8")
 
 
-def save_partition_dir(plan: PartitionPlan, subgraphs, entities: Dictionary, relations: Dictionary,
-                       n_relations: int, out_dir) -> Path:
-    """Write a partition directory the reference reads (archive.py:192-237)."""
+def _read_label_lines(path: Path) -> list:
+    text = path.read_text(encoding="utf-8")
+    return text.split("\n")[:-1] if text.endswith("\n") else text.split("\n") if text else []
+
+
+def save_partition_dir(plan: PartitionPlan, subgraphs, entities, relations, n_relations: int,
+                       out_dir) -> Path:
+    """Write a partition directory the reference reads (archive.py:192-237):
+    u32 assignment (UNASSIGNED as 0xFFFFFFFF), label files, and per shard an
+    LKG1 archive plus little-endian u64 entity / triple maps."""
     from .archive import save_graph
 
     out = Path(out_dir)
     out.mkdir(parents=True, exist_ok=True)
-    assignment = plan.assignment.astype(np.int64)
-    encoded = np.where(assignment == UNASSIGNED, _ASSIGNMENT_SENTINEL, assignment)
-    (out / ASSIGNMENT_FILE).write_bytes(encoded.astype("<u4").tobytes())
-    save_labels(entities.labels(), out / ENTITIES_FILE)
-    save_labels(relations.labels(), out / RELATIONS_FILE)
-    shards = []
-    for sg in subgraphs:
-        name = _shard_name(sg.index)
-        save_graph(sg.graph, out / f"{name}.lkg")
-        (out / f"{name}.ents.u64").write_bytes(sg.ent_to_global.astype("<u8").tobytes())
-        (out / f"{name}.tids.u64").write_bytes(sg.tid_to_global.astype("<u8").tobytes())
-        shards.append({"index": sg.index, "shard_file": f"{name}.lkg",
-                       "entity_map_file": f"{name}.ents.u64", "triple_map_file": f"{name}.tids.u64",
-                       "triple_count": sg.graph.n_triples})
-    manifest = {"format": "LKG-partition", "version": ARCHIVE_VERSION, "m": plan.m,
-                "strategy": plan.strategy, "entity_count": plan.n_entities,
-                "relation_count": n_relations, "triple_count": int(plan.loads.sum()),
-                "assignment_file": ASSIGNMENT_FILE, "partitions": shards}
-    (out / MANIFEST_FILE).write_text(json.dumps(manifest, indent=2, sort_keys=True) + "\n")
+    (out / ASSIGNMENT_FILE).write_bytes(plan.assignment.astype("<i4").view("<u4").tobytes())
+    (out / ENTITIES_FILE).write_bytes(_label_lines(entities))
+    (out / RELATIONS_FILE).write_bytes(_label_lines(relations))
+    man = PartitionManifest.describe(plan, subgraphs, n_relations)
+    for sg, entry in zip(subgraphs, man.fields["partitions"]):
+        save_graph(sg.graph, out / entry["shard_file"])
+        (out / entry["entity_map_file"]).write_bytes(sg.ent_to_global.astype("<u8").tobytes())
+        (out / entry["triple_map_file"]).write_bytes(sg.tid_to_global.astype("<u8").tobytes())
+    man.write(out)
     return out
 
 
 def load_partition_plan(part_dir) -> PartitionPlan:
-    """archive.py:258-272."""
+    """The plan a partition directory was written with (archive.py:258-272)."""
     d = Path(part_dir)
-    manifest = _load_manifest(d)
-    raw = np.frombuffer((d / manifest["assignment_file"]).read_bytes(), "<u4")
-    if raw.size != manifest["entity_count"]:
+    man = PartitionManifest.read(d)
+    raw = np.fromfile(d / man.fields["assignment_file"], dtype="<u4")
+    if raw.size != man.n_entities:
         raise IntegrityError("assignment array length disagrees with entity count")
-    assignment = raw.astype(np.int64)
-    assignment[assignment == _ASSIGNMENT_SENTINEL] = UNASSIGNED
-    assignment = assignment.astype(np.int32)
-    loads = np.zeros(manifest["m"], dtype=np.int64)
-    for s in manifest["partitions"]:
-        loads[s["index"]] = s["triple_count"]
+    assignment = raw.view("<i4").astype(np.int32)  # 0xFFFFFFFF reads back as -1 = UNASSIGNED
+    loads = np.zeros(man.m, dtype=np.int64)
+    idx = np.fromiter(man.shards.keys(), dtype=np.int64, count=len(man.shards))
+    loads[idx] = [int(e["triple_count"]) for e in man.shards.values()]
     assignment.setflags(write=False)
     loads.setflags(write=False)
-    return PartitionPlan(manifest["m"], assignment, loads, manifest.get("strategy", "lpt"))
+    return PartitionPlan(man.m, assignment, loads, man.fields.get("strategy", "lpt"))
 
 
 class DirectoryStore:
-    """Loads shard archives on demand from a partition directory straight
-    onto the device (archive.py:275-301)."""
+    """Shard archives of a partition directory, loaded on demand straight
+    onto the device (the role of archive.py:275-301)."""
 
     def __init__(self, part_dir):
         self.dir = Path(part_dir)
-        self.manifest = _load_manifest(self.dir)
-        self.m = int(self.manifest["m"])
-        self.n_entities = int(self.manifest["entity_count"])
-        self.n_relations = int(self.manifest["relation_count"])
-        self.n_triples = int(self.manifest["triple_count"])
-        self._shards = {s["index"]: s for s in self.manifest["partitions"]}
+        self.manifest = PartitionManifest.read(self.dir)
+        self.m = self.manifest.m
+        self.n_entities = self.manifest.n_entities
+        self.n_relations = self.manifest.n_relations
+        self.n_triples = self.manifest.n_triples
 
     def load(self, index: int) -> Subgraph:
         from .archive import load_graph
 
-        entry = self._shards.get(index)
+        entry = self.manifest.shards.get(index)
         if entry is None:
             raise IntegrityError(f"manifest has no partition {index}")
-        shard_path = self.dir / entry["shard_file"]
-        if not shard_path.exists():
-            raise IntegrityError(f"partition {index}: missing shard file {shard_path.name}")
-        graph = load_graph(shard_path)
-        ents = np.frombuffer((self.dir / entry["entity_map_file"]).read_bytes(), "<u8").astype(np.int64)
-        tids = np.frombuffer((self.dir / entry["triple_map_file"]).read_bytes(), "<u8").astype(np.int64)
-        if ents.size != graph.n_entities or tids.size != graph.n_triples:
+        archive = self.dir / entry["shard_file"]
+        if not archive.exists():
+            raise IntegrityError(f"partition {index}: missing shard file {archive.name}")
+        graph = load_graph(archive)
+        ents, tids = (np.fromfile(self.dir / entry[key], dtype="<u8").astype(np.int64)
+                      for key in ("entity_map_file", "triple_map_file"))
+        if (ents.size, tids.size) != (graph.n_entities, graph.n_triples):
             raise IntegrityError(f"partition {index}: id map sizes disagree with shard")
         return Subgraph(index, graph, ents, tids)
 
 
 def open_partitioned(part_dir, cache_capacity: int, record_trace: bool = False):
-    """A partition directory as a queryable PartitionedGraph (archive.py:304-315)."""
+    """A partition directory as a queryable ``PartitionedGraph`` plus its
+    entity and relation labels (lists, line index = id; archive.py:304-315)."""
     d = Path(part_dir)
-    plan = load_partition_plan(d)
-    store = DirectoryStore(d)
-    cache = SubgraphCache(cache_capacity, record_trace=record_trace)
-    entities = load_labels(d / ENTITIES_FILE)
-    relations = load_labels(d / RELATIONS_FILE)
-    return PartitionedGraph(plan, store, cache), entities, relations
+    pg = PartitionedGraph(load_partition_plan(d), DirectoryStore(d),
+                          SubgraphCache(cache_capacity, record_trace=record_trace))
+    return pg, _read_label_lines(d / ENTITIES_FILE), _read_label_lines(d / RELATIONS_FILE)
 
 
 # ------------------------------------------------------------ the graph
@@ -483,8 +465,8 @@ def store_k_hop(q0: EntityVector, k: int, pg: StorePartitionedGraph,
             if cum is not None:
                 _lib.check(lib.th_bits_or(cum.data_ptr(), reached.data_ptr(), E, _stream_ptr(dev)))
                 out = _compact(cum, E, dev)
-        steps.append(HopStep(EntityVector(_host_ids(out), E, _canonical_ids=True),
-                             TripleVector(_host_ids(activated), T, _canonical_ids=True)))
+        steps.append(HopStep(EntityVector(_host_ids(out), E, _canonical=True),
+                             TripleVector(_host_ids(activated), T, _canonical=True)))
     return HopTrace(sem, q0, steps)
 
 
@@ -526,69 +508,3 @@ def store_paths(q0: EntityVector, k: int, pg: StorePartitionedGraph,
     sub = build_incidence(tuple(cols), pg.n_entities, pg.n_relations)
     res = reconstruct_paths(q0, k, sub, max_paths)
     return PathResult(res.paths, res.truncated)
-
-
-# ------------------------------------------------------------ batches
-
-
-@dataclass(frozen=True)
-class BatchQuery:
-    query_id: object
-    q0: EntityVector
-    k: int
-
-
-@dataclass(frozen=True)
-class QueryBatch:
-    """Queries plus the execution-order permutation and its inverse (engine.py:193-211)."""
-
-    queries: list
-    execution_order: list
-
-    @property
-    def restore_order(self) -> list:
-        inverse = [0] * len(self.execution_order)
-        for rank, pos in enumerate(self.execution_order):
-            inverse[pos] = rank
-        return inverse
-
-    @classmethod
-    def identity(cls, queries) -> "QueryBatch":
-        return cls(list(queries), list(range(len(queries))))
-
-
-def signature(q0: EntityVector, plan: PartitionPlan) -> tuple:
-    """Sorted partitions the seeds route to (engine.py:214-216)."""
-    return tuple(sorted(route(q0, plan).buckets))
-
-
-def plan_batch(queries, plan: PartitionPlan) -> QueryBatch:
-    """Group queries by hop-0 signature, groups in signature order, stable
-    within a group (engine.py:219-231)."""
-    groups: dict = {}
-    for pos, q in enumerate(queries):
-        groups.setdefault(signature(q.q0, plan), []).append(pos)
-    order = [pos for sig in sorted(groups) for pos in groups[sig]]
-    return QueryBatch(list(queries), order)
-
-
-@dataclass
-class BatchResult:
-    query_id: object
-    trace: HopTrace | None
-    error: str | None = None
-
-
-def run_batch(batch: QueryBatch, pg, semantics=HopSemantics.FRONTIER) -> list:
-    """Execute in planned order, report in input order; a failing query is
-    reported under its id without aborting the batch (engine.py:241-258)."""
-    from .partition import cross_graph_k_hop
-
-    results: list = [None] * len(batch.queries)
-    for pos in batch.execution_order:
-        q = batch.queries[pos]
-        try:
-            results[pos] = BatchResult(q.query_id, cross_graph_k_hop(q.q0, q.k, pg, semantics))
-        except Exception as exc:  # noqa: BLE001 - per-query isolation, as the reference
-            results[pos] = BatchResult(q.query_id, None, f"{type(exc).__name__}: {exc}")
-    return results

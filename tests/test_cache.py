@@ -4,7 +4,9 @@ checked against the independent list model; device units on the GPU."""
 import numpy as np
 import pytest
 
-from paper_2604_18913_b200.cache import SubgraphCache, simulate_lru
+from lru_model import simulate_lru
+
+from paper_2604_18913_b200.cache import SubgraphCache
 
 
 def test_lru_golden_sequence():

@@ -58,29 +58,22 @@ def test_manifest_errors(tmp_path):
         store.DirectoryStore(d)
 
 
-def test_labels_round_trip(tmp_path):
-    d = store.load_labels(GOLDEN / "partdir_hash" / "entities.txt")
-    assert len(d) == 400 and d.label_of(17) == "e17" and d.id_of("e399") == 399 and "e5" in d
-    store.save_labels(d.labels(), tmp_path / "x.txt")
-    assert (tmp_path / "x.txt").read_bytes() == (GOLDEN / "partdir_hash" / "entities.txt").read_bytes()
-    assert store.load_labels(tmp_path / "x.txt") == d
+def test_label_files_round_trip(tmp_path):
+    """Label files written by save_partition_dir are byte-identical to the
+    reference's; open_partitioned reads them back as lists (line = id)."""
+    ref = GOLDEN / "partdir_hash" / "entities.txt"
+    labels = store._read_label_lines(ref)
+    assert len(labels) == 400 and labels[17] == "e17" and labels[399] == "e399"
+    assert store._label_lines(labels) == ref.read_bytes()
+    (tmp_path / "x.txt").write_bytes(store._label_lines(labels))
+    assert store._read_label_lines(tmp_path / "x.txt") == labels
 
 
-@pytest.mark.parametrize("strategy", ["lpt", "hash"])
-def test_plan_batch_order_matches_reference(strategy):
-    g = _golden(strategy)
-    plan = store.load_partition_plan(GOLDEN / f"partdir_{strategy}")
-    seeds = ([0], [5, 17], [123], [399], [2, 3, 250], [])
-    qs = [store.BatchQuery(f"q{i}", th.EntityVector(np.asarray(sd, np.int64), 400), 2)
-          for i, sd in enumerate(seeds)]
-    qs.append(store.BatchQuery("bad", th.EntityVector(np.asarray([1], np.int64), 400), 0))
-    batch = store.plan_batch(qs, plan)
-    assert batch.execution_order == g["batch_order"]
-    inv = batch.restore_order
-    assert [batch.execution_order[inv[p]] for p in range(len(qs))] == list(range(len(qs)))
-    assert store.QueryBatch.identity(qs).execution_order == list(range(len(qs)))
-    assert store.signature(qs[4].q0, plan) == tuple(sorted({int(plan.assignment[v]) for v in (2, 3, 250)
-                                                             if plan.assignment[v] >= 0}))
+def test_manifest_describe_round_trips(tmp_path):
+    man = store.PartitionManifest.read(GOLDEN / "partdir_lpt")
+    assert man.m == 3 and man.n_entities == 400 and man.n_relations == 6
+    assert sorted(man.shards) == [0, 1, 2]
+    assert store.PartitionManifest.shard_stem(7) == "shard-0007"
 
 
 def test_store_constructor_dispatch_without_gpu():
