@@ -59,7 +59,9 @@ extern "C" {
 #define TH_WANT_ACTIVATED 0x2u /* per-query sorted activated triple ids/hop  */
 #define TH_WANT_PATHS 0x4u     /* capped lexicographic walk enumeration       */
 #define TH_SINGLETON_SEEDS 0x8u /* every query is one seed (retrieve(seeds)):
-                                   paths start from the seed's CSR row       */
+                                   query q = {d_seeds[q]}, d_seeds holds
+                                   n_queries ids and d_seed_offsets is NOT
+                                   read; paths start from the seed's CSR row */
 
 /* th_graph_create flags */
 #define TH_GRAPH_NO_REVERSE 0x1u /* skip the reverse (by-object) CSR: no pull hops */
@@ -167,6 +169,10 @@ int th_session_set_list_min_entities(th_session* s, int64_t min_entities);
 /* Overlap hop h's frontier materialisation (K4) with hop h+1's expansion
  * on an internal stream (frontier-only runs).  Default on. */
 int th_session_set_overlap(th_session* s, int on);
+/* Count pass of the list-driven K4 (graphs of at least list_min_entities
+ * entities): 1 = row-major (whole-row loads, carry-save bit counting;
+ * default), 0 = word-per-warp loads with bit-sliced counting. */
+int th_session_set_k4_mode(th_session* s, int mode);
 /* Pull hops whose frontier sources more than 1/divisor of all in-edges
  * (by the frontier's out-degree sum) gather every in-neighbour row instead
  * of testing frontier flags first (default 2; <= 0 never). */

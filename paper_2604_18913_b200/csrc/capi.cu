@@ -254,6 +254,15 @@ int th_session_set_overlap(th_session* s, int on) {
   return TH_OK;
 }
 
+int th_session_set_k4_mode(th_session* s, int mode) {
+  if (!s || mode < 0 || mode > 1) {
+    th::set_error(!s ? "NULL handle" : "k4 mode must be 0 or 1");
+    return TH_ERR_INVALID;
+  }
+  s->s.k4_rowmajor = mode == 1;
+  return TH_OK;
+}
+
 int64_t th_session_launch_count(const th_session* s) { return s ? s->s.launches : -1; }
 
 int th_session_set_profiling(th_session* s, int on) {

@@ -51,7 +51,6 @@ __device__ __forceinline__ uint32_t transpose32(uint32_t x) {
   return x;
 }
 
-// Warp-aggregated append of `item` from the lanes with `take` set.  Must be
 // position of the r-th (0-based) set bit of x (r < popc(x)): a five-step
 // popcount search, a fixed dozen instructions (__fns is a software loop)
 __device__ __forceinline__ int select_bit(uint32_t x, int r) {
@@ -68,6 +67,7 @@ __device__ __forceinline__ int select_bit(uint32_t x, int r) {
   return pos;
 }
 
+// Warp-aggregated append of `item` from the lanes with `take` set.  Must be
 // called by all 32 lanes in converged code (full-mask collectives only; no
 // __activemask-based aggregation, which can deadlock under independent
 // thread scheduling when lanes diverge inside the aggregated region).

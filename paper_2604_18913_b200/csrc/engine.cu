@@ -93,7 +93,8 @@ __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int q = gw; q < a.nq; q += nw) {
-    const int32_t lo = qoff[q0 + q], hi = qoff[q0 + q + 1];
+    // (qoff == nullptr: singleton queries, query q is {seeds[q0 + q]})
+    const int32_t lo = qoff ? qoff[q0 + q] : q0 + q, hi = qoff ? qoff[q0 + q + 1] : q0 + q + 1;
     const uint32_t qb = 1u << (q & 31);
     const int qw = q >> 5;
     unsigned long long dsum = 0ull;
@@ -568,6 +569,7 @@ __global__ void build_mask_kernel(const uint32_t* __restrict__ masks, int mask_w
 // ------------------------------------------------------ materialisation
 
 #include "k4_materialize.cuh"
+#include "k4_rowmajor.cuh"
 
 // one block per query: exclusive scan over its block counts; totals[q]
 __global__ void mat_scan_rows_kernel(int32_t* counts, int nblk, int64_t* totals) {
@@ -738,8 +740,6 @@ __global__ void __launch_bounds__(kCompactThreads) flag_write_kernel(const uint3
 
 // ---------------------------------------------------------------- host
 
-std::atomic<uint64_t> g_alloc_epoch{0};
-
 template <typename T>
 T* ensure(DBuf& b, int64_t n, cudaStream_t st) {
   const size_t need = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
@@ -748,9 +748,33 @@ T* ensure(DBuf& b, int64_t n, cudaStream_t st) {
     b.p = nullptr;
     TH_CUDA(cudaMallocAsync(&b.p, need, st));
     b.bytes = need;
-    g_alloc_epoch.fetch_add(1, std::memory_order_relaxed);
   }
   return static_cast<T*>(b.p);
+}
+
+// Every device buffer a session's captured graph can reference; a change of
+// any of their addresses or sizes invalidates that session's graph (and
+// only that session's: other sessions' growth does not touch it).
+template <class F>
+void for_each_session_buf(Session* s, F&& f) {
+  for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
+                  &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
+                  &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
+                  &s->p_scratch, &s->p_tmp, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta, &s->counts2,
+                  &s->totals2, &s->rowlist2, &s->rowscan2, &s->k4_S2, &s->k4_meta2,
+                  &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks})
+    f(d);
+}
+
+uint64_t session_alloc_sig(Session* s) {
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over (address, size) pairs
+  for_each_session_buf(s, [&](DBuf* d) {
+    for (uint64_t v : {(uint64_t)(uintptr_t)d->p, (uint64_t)d->bytes}) {
+      h ^= v;
+      h *= 1099511628211ull;
+    }
+  });
+  return h;
 }
 
 unsigned persistent_grid() { return kNumSMs * 8; }
@@ -859,13 +883,40 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
     }
   }
   constexpr size_t smem_c = mat_smem_bytes<W, false>();
-  if (es.out)
-    mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, counts,
-                                                                      nullptr, nullptr, 0, es);
-  else
-    mat_kernel<W, Src, false><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, counts, nullptr,
-                                                                nullptr, 0);
-  TH_LAUNCHED();
+  bool counted = false;
+  if constexpr (Src::kRing) {
+    if (s->k4_rowmajor) {
+      // list-driven layers: whole-row loads, carry-save counting (k4_rowmajor.cuh)
+      static std::atomic<uint64_t> attr_r{0};
+      if (!(attr_r.load(std::memory_order_relaxed) & bit)) {
+        TH_CUDA(cudaFuncSetAttribute(rs_count_kernel<W, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)rs_count_smem<true>()));
+        TH_CUDA(cudaFuncSetAttribute(rs_count_kernel<W, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)rs_count_smem<false>()));
+        attr_r.fetch_or(bit, std::memory_order_relaxed);
+      }
+      RowMajorSrc<W> rsrc{src.A, src.neg, src.rows, src.n_dev, src.nq};
+      if (es.out)
+        rs_count_kernel<W, true><<<nblk, 32 * kRsWarps, rs_count_smem<true>(), s->st>>>(rsrc, nblk,
+                                                                                       counts, es);
+      else
+        rs_count_kernel<W, false><<<nblk, 32 * kRsWarps, rs_count_smem<false>(), s->st>>>(
+            rsrc, nblk, counts, es);
+      TH_LAUNCHED();
+      counted = true;
+    }
+  }
+  if (!counted) {
+    if (es.out)
+      mat_kernel<W, Src, false, true><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, counts,
+                                                                        nullptr, nullptr, 0, es);
+    else
+      mat_kernel<W, Src, false><<<grid, 32 * NW, smem_c, s->st>>>(src, nblk, counts, nullptr,
+                                                                  nullptr, 0);
+    TH_LAUNCHED();
+  }
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(counts, nblk, totals);
   TH_LAUNCHED();
   mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(totals, nq, off, len, cursor);
@@ -876,11 +927,6 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   s->launches += 4;
 }
 
-// Rows of A (minus neg) whose flag is set.  Small graphs scan the flag
-// bitmap directly (the whole state matrix is L2-resident and most rows of a
-// layer are live); large graphs first compact the flags into an ascending
-// row list so the work follows the rows a layer reached (C4: 10x fewer
-// tiles at hop 2, 2x at hop 3).
 template <int W>
 void materialize_dense(Session* s, WaveBufs& b, const uint32_t* A, const uint32_t* neg,
                        const uint32_t* flags, int nq, int64_t* off, int64_t* len, int32_t* out,
@@ -1024,7 +1070,8 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
       TH_LAUNCHED();
       s->launches += 1;
     }
-    seed_init_kernel<W><<<grid_for((int64_t)nq * 32), kThreads, 0, st>>>(a, q->d_seed_offsets,
+    seed_init_kernel<W><<<grid_for((int64_t)nq * 32), kThreads, 0, st>>>(
+        a, (q->flags & TH_SINGLETON_SEEDS) ? nullptr : q->d_seed_offsets,
                                                                          q->d_seeds, q0,
         filter ? nullptr : static_cast<int64_t*>(s->edges.p) + q0);
     TH_LAUNCHED();
@@ -1257,8 +1304,8 @@ static int run_body(Session* s, const th_query* q);
 // seeds lives on the device in Ctl).  A query repeating the previous run's
 // key is captured once into a graph and replayed with one cudaGraphLaunch;
 // its inputs are first copied into session-owned staging buffers so the
-// graph's pointers stay valid.  Any buffer (re)allocation anywhere bumps
-// g_alloc_epoch and invalidates the graph.
+// graph's pointers stay valid.  Any (re)allocation of one of the session's
+// buffers changes session_alloc_sig and invalidates its graph.
 static bool graph_eligible(const Session* s, const th_query* q) {
   static const bool debug_sync = std::getenv("TH_DEBUG_SYNC") != nullptr;
   // profiling: event records are captured too, so a replay needs the
@@ -1268,7 +1315,7 @@ static bool graph_eligible(const Session* s, const th_query* q) {
          (!s->prof || (s->ev_used == 0 && s->pending_cat.empty()));
 }
 
-static GraphKey graph_key(const Session* s, const th_query* q) {
+static GraphKey graph_key(Session* s, const th_query* q) {
   GraphKey k{};
   k.B = q->n_queries;
   k.k = q->k;
@@ -1282,8 +1329,8 @@ static GraphKey graph_key(const Session* s, const th_query* q) {
   k.pull_divisor = s->pull_divisor;
   k.dense_pull = s->dense_pull;
   k.list_min = s->list_min_entities;
-  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0);
-  k.epoch = g_alloc_epoch.load(std::memory_order_relaxed);
+  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_rowmajor ? 8 : 0);
+  k.epoch = session_alloc_sig(s);
   return k;
 }
 
@@ -1371,7 +1418,7 @@ static int run_graphed(Session* s, const th_query* q) {
     if (s->g_failures >= 3) s->use_graphs = false;
     return run_body(s, &qs);
   }
-  const uint64_t epoch = g_alloc_epoch.load(std::memory_order_relaxed);
+  const uint64_t epoch = session_alloc_sig(s);
   cudaGraphExec_t exec = nullptr;
   const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -1573,16 +1620,11 @@ int session_finish(Session* s, th_result* out) {
 
 void session_free(Session* s) {
   drop_graph(s);
-  for (DBuf* d : {&s->X, &s->N, &s->V, &s->S, &s->Xf, &s->Nf, &s->Vf, &s->lists, &s->heavy,
-                  &s->M, &s->counts, &s->totals, &s->ctl, &s->f_off, &s->f_len, &s->f_ids, &s->a_off,
-                  &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
-                  &s->p_scratch, &s->p_tmp, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta, &s->counts2,
-                  &s->totals2, &s->rowlist2, &s->rowscan2, &s->k4_S2, &s->k4_meta2,
-                  &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks}) {
+  for_each_session_buf(s, [&](DBuf* d) {
     if (d->p) cudaFreeAsync(d->p, s->st);
     d->p = nullptr;
     d->bytes = 0;
-  }
+  });
   cudaStreamSynchronize(s->st);
   for (cudaEvent_t e : s->ev_pool) cudaEventDestroy(e);
   s->ev_pool.clear();

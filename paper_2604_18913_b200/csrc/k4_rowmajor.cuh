@@ -1,0 +1,193 @@
+// Part of engine.cu (included inside namespace th::{anonymous}).
+//
+// Row-major count pass of the list-driven K4 (k4_materialize.cuh).
+//
+// A layer of a large graph (C4, C5) holds a few bits per 1,024-bit row --
+// C4's last layer averages ~36 set bits over 32 words.  The word-per-warp
+// count pass read every row as 32 separate 4-byte loads (one per word-warp,
+// 32 sectors per load instruction: L1-bound at 86%, 1.75 ms for 1.64 GB on
+// C4 k=3).  Here a warp reads whole rows (one coalesced 128-byte load per
+// row, lane j = word j = queries 32j..32j+31) and counts bits column-wise
+// with a carry-save adder tree: per (query, block) totals for the write
+// pass, over the SAME row blocks the write pass uses (whole 1,024-row
+// chunks, blk_rows from the device-side row count, as in mat_unit).
+//
+// Measured and rejected (C4 k=3, 1,024 seeds): a row-major WRITE pass that
+// scatters every id to its query's cursor (one 4-byte store per id into ~1M
+// concurrently open per-query runs: partially written sectors thrash L2,
+// 14.2 -> 21.7 ms), and one that stages a block's ids query-major in shared
+// memory (per-query bookkeeping of 1,024 queries per ~7K-id block: ~4.5
+// warp instructions per id, 14.2 -> 23.5 ms).  The transposing write pass
+// keeps 32 queries per warp, so its per-query staging stays small.
+#pragma once
+
+constexpr int kRsWarps = 16;   // warps per CTA
+constexpr int kRsUnroll = 8;   // rows in flight per warp (the adder tree sums 8)
+
+template <int W>
+struct RowMajorSrc {
+  const uint32_t* A;
+  const uint32_t* neg;
+  const int32_t* rows;   // ascending row list
+  const int32_t* n_dev;  // its length (device)
+  int nq;
+};
+
+// kRsUnroll rows starting at list position i (< end): row numbers and this
+// lane's words (lane j = word j)
+template <int W>
+__device__ __forceinline__ void rs_load(const RowMajorSrc<W>& src, int64_t i, int64_t end,
+                                        int32_t (&v)[kRsUnroll], uint32_t (&x)[kRsUnroll],
+                                        uint32_t valid) {
+  const unsigned lane = lane_id();
+  const int32_t mine = (int64_t)lane < kRsUnroll && i + lane < end ? __ldg(src.rows + i + lane) : -1;
+#pragma unroll
+  for (int u = 0; u < kRsUnroll; ++u) v[u] = __shfl_sync(TH_FULL, mine, u);
+#pragma unroll
+  for (int u = 0; u < kRsUnroll; ++u) {
+    uint32_t w = 0u;
+    if (v[u] >= 0 && lane < (unsigned)W) {
+      const size_t at = (size_t)v[u] * W + lane;
+      w = __ldcg(src.A + at);
+      if (src.neg) w &= ~__ldcg(src.neg + at);
+    }
+    x[u] = w & valid;
+  }
+}
+
+// full adder on bit planes (two LOP3s)
+__device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& cy) {
+  s = a ^ b ^ c;
+  cy = (a & b) | (c & (a ^ b));
+}
+
+// adds plane k's bits into cnt[b * 32 + lane] with weight 2^k
+__device__ __forceinline__ void rs_flush_plane(uint32_t p, int k, uint32_t* cnt) {
+  const unsigned lane = lane_id();
+  while (p) {
+    const int b = __ffs(p) - 1;
+    p &= p - 1u;
+    cnt[b * 32 + lane] += 1u << k;
+  }
+}
+
+// Per-query bit counts of list rows [lo, hi) added to cnt[b*32 + lane]
+// (query 32 lane + b) without per-bit work: eight rows at a time are summed
+// column-wise by a carry-save adder tree into a 4-bit bit-sliced count,
+// added into six running planes (counts up to 63) that are flushed to the
+// shared counters every 56 rows.
+template <int W>
+__device__ __forceinline__ void rs_count_sliced(const RowMajorSrc<W>& src, int64_t lo, int64_t hi,
+                                                uint32_t* cnt, uint32_t valid) {
+  static_assert(kRsUnroll == 8, "the adder tree sums 8 rows");
+  uint32_t c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u, c4 = 0u, c5 = 0u;
+  int acc = 0;
+  for (int64_t i = lo; i < hi; i += kRsUnroll) {
+    int32_t v[kRsUnroll];
+    uint32_t x[kRsUnroll];
+    rs_load<W>(src, i, hi, v, x, valid);
+    uint32_t a1, b1, a2, b2, p0, b4, q1, k1;
+    fa(x[0], x[1], x[2], a1, b1);
+    fa(x[3], x[4], x[5], a2, b2);
+    const uint32_t a3 = x[6] ^ x[7], b3 = x[6] & x[7];
+    fa(a1, a2, a3, p0, b4);
+    fa(b1, b2, b3, q1, k1);
+    const uint32_t p1 = q1 ^ b4, k2 = q1 & b4;
+    const uint32_t p2 = k1 ^ k2, p3 = k1 & k2;
+    // running planes += (p3 p2 p1 p0)
+    uint32_t cy, t;
+    t = c0 ^ p0; cy = c0 & p0; c0 = t;
+    fa(c1, p1, cy, t, cy); c1 = t;
+    fa(c2, p2, cy, t, cy); c2 = t;
+    fa(c3, p3, cy, t, cy); c3 = t;
+    t = c4 ^ cy; cy = c4 & cy; c4 = t;
+    c5 ^= cy;
+    acc += kRsUnroll;
+    if (acc >= 56) {
+      rs_flush_plane(c0, 0, cnt); rs_flush_plane(c1, 1, cnt); rs_flush_plane(c2, 2, cnt);
+      rs_flush_plane(c3, 3, cnt); rs_flush_plane(c4, 4, cnt); rs_flush_plane(c5, 5, cnt);
+      c0 = c1 = c2 = c3 = c4 = c5 = 0u;
+      acc = 0;
+    }
+  }
+  rs_flush_plane(c0, 0, cnt); rs_flush_plane(c1, 1, cnt); rs_flush_plane(c2, 2, cnt);
+  rs_flush_plane(c3, 3, cnt); rs_flush_plane(c4, 4, cnt); rs_flush_plane(c5, 5, cnt);
+}
+
+// EDGES variant: per-bit counting plus each row's out-degree per query
+// (|T_{h+1}(q)|; the layers that need it are the small early ones)
+template <int W>
+__device__ __forceinline__ void rs_count_edges(const RowMajorSrc<W>& src, int64_t lo, int64_t hi,
+                                               uint32_t* cnt, uint32_t* esum, const EdgeSum& es,
+                                               uint32_t valid) {
+  const unsigned lane = lane_id();
+  for (int64_t i = lo; i < hi; i += kRsUnroll) {
+    int32_t v[kRsUnroll];
+    uint32_t x[kRsUnroll];
+    rs_load<W>(src, i, hi, v, x, valid);
+#pragma unroll
+    for (int u = 0; u < kRsUnroll; ++u) {
+      uint32_t m = x[u];
+      // (the degree of the layer's own row: es.indptr is that graph's)
+      const uint32_t d = m ? degree(es, v[u]) : 0u;
+      while (m) {
+        const int b = __ffs(m) - 1;
+        m &= m - 1u;
+        cnt[b * 32 + lane] += 1u;
+        esum[b * 32 + lane] += d;
+      }
+    }
+  }
+}
+
+template <bool EDGES>
+constexpr size_t rs_count_smem() {
+  return (size_t)(EDGES ? 2 : 1) * kRsWarps * 1024 * sizeof(uint32_t);
+}
+
+// counts[q * nblk + blk] = bits of query q in row block blk of the list
+// (the write pass's partition: whole kChunkRows chunks, blk_rows from the
+// device row count).  One CTA per block; its warps take contiguous slices.
+template <int W, bool EDGES>
+__global__ void __launch_bounds__(32 * kRsWarps) rs_count_kernel(RowMajorSrc<W> src, int nblk,
+                                                                 int32_t* counts, EdgeSum es) {
+  // dynamic: [kRsWarps][1024] counters (+ [kRsWarps][1024] degree sums; a
+  // warp's degree sum per query covers distinct rows: <= T < 2^32)
+  extern __shared__ uint32_t rs_smem[];
+  const int warp = threadIdx.x >> 5;
+  const unsigned lane = lane_id();
+  const int blk = blockIdx.x;
+  if (blk >= nblk) return;
+  uint32_t* cnt = rs_smem + warp * 1024;
+  uint32_t* esum = rs_smem + (kRsWarps + warp) * 1024;
+  const int64_t nrows = *src.n_dev;
+  int64_t blk_rows = (nrows + nblk - 1) / nblk;
+  blk_rows = blk_rows < kChunkRows ? kChunkRows : (blk_rows + kChunkRows - 1) / kChunkRows * kChunkRows;
+  const int64_t r0 = (int64_t)blk * blk_rows;
+  const int64_t r1 = nrows < r0 + blk_rows ? nrows : r0 + blk_rows;
+  const int64_t per = r1 > r0 ? ((r1 - r0 + kRsWarps - 1) / kRsWarps + kRsUnroll - 1) / kRsUnroll * kRsUnroll
+                              : 0;
+  const int64_t lo = r0 + warp * per < r1 ? r0 + warp * per : r1;
+  const int64_t hi = lo + per < r1 ? lo + per : r1;
+  const uint32_t valid = lane < (unsigned)W ? valid_word((int)lane, src.nq) : 0u;
+#pragma unroll 8
+  for (int b = 0; b < 32; ++b) {
+    cnt[b * 32 + lane] = 0u;
+    if (EDGES) esum[b * 32 + lane] = 0u;
+  }
+  if (EDGES) rs_count_edges<W>(src, lo, hi, cnt, esum, es, valid);
+  else rs_count_sliced<W>(src, lo, hi, cnt, valid);
+  __syncthreads();
+  for (int q = threadIdx.x; q < src.nq; q += blockDim.x) {
+    const int at = (q & 31) * 32 + (q >> 5);
+    uint32_t t = 0u;
+    unsigned long long e = 0ull;
+#pragma unroll
+    for (int w = 0; w < kRsWarps; ++w) {
+      t += rs_smem[w * 1024 + at];
+      if (EDGES) e += rs_smem[(kRsWarps + w) * 1024 + at];
+    }
+    counts[(size_t)q * nblk + blk] = (int32_t)t;
+    if (EDGES && e) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), e);
+  }
+}

@@ -120,9 +120,9 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
       lo0 = a.l0_off[q];
       hi0 = lo0 + a.l0_len[q];
     } else {
-      const int32_t slo = a.qoff[q], shi = a.qoff[q + 1];
-      if (shi > slo) {
-        const int32_t s = a.seeds[slo];
+      // singleton queries: query q is {seeds[q]} (offsets are not read)
+      {
+        const int32_t s = a.seeds[q];
         if (s >= 0 && s < a.E) {
           lo0 = a.indptr[s];
           hi0 = a.indptr[s + 1];

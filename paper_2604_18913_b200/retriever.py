@@ -195,6 +195,10 @@ class Retriever:
         """K4 strategy knob: list-driven materialisation for graphs with >= n entities."""
         _lib.check(_lib.load().th_session_set_list_min_entities(self._handle, int(n)))
 
+    def set_k4_mode(self, mode: int) -> None:
+        """K4 form for list-driven layers: 1 row-major (default), 0 transposes."""
+        _lib.check(_lib.load().th_session_set_k4_mode(self._handle, int(mode)))
+
     def set_overlap(self, on: bool) -> None:
         """Overlap hop h's K4 with hop h+1's expansion (frontier-only runs)."""
         _lib.check(_lib.load().th_session_set_overlap(self._handle, int(bool(on))))
@@ -329,6 +333,12 @@ class Retriever:
         g = self.graph
         dev = g.device
         if isinstance(seeds, torch.Tensor):
+            if seeds.dtype != torch.int32 and seeds.numel():
+                # a wider id would wrap in the int32 cast (possibly onto a
+                # valid id): range-check before narrowing
+                lo, hi = (int(x) for x in torch.aminmax(seeds.reshape(-1)))
+                if lo < 0 or hi >= g.n_entities:
+                    raise ValueError(f"id out of range for width {g.n_entities}")
             s = seeds.to(device=dev, dtype=torch.int32).reshape(-1)
         else:
             arr = np.asarray(seeds, dtype=np.int64).reshape(-1)

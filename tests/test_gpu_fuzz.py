@@ -22,6 +22,7 @@ def _cases():
             alpha=float(rng.choice([0.8, 1.1, 1.4])), B=int(rng.choice([1, 7, 32, 33, 200, 1024, 1100])),
             k=int(rng.integers(1, 5)), sem=str(rng.choice(["exact", "frontier", "cumulative"])),
             filt=bool(rng.random() < 0.35), list_mode=bool(rng.random() < 0.5),
+            k4_mode=int(rng.integers(0, 2)),
             divisor=float(rng.choice([0.0, -1.0, 8.0])),
             paths=bool(rng.random() < 0.3), max_paths=[0, 5, 100, None][int(rng.integers(0, 4))], seed=i))
     return out
@@ -38,6 +39,7 @@ def test_random_configuration(th_mod, c):
     ret = th.Retriever(g)
     ret.set_pull_divisor(c["divisor"])
     ret.set_list_min_entities(0 if c["list_mode"] else 1 << 40)
+    ret.set_k4_mode(c["k4_mode"])
     for rep in range(3):  # eager run, graph capture, replay (new seeds each time)
         seeds = rng.integers(0, E, c["B"])
         filt = None
@@ -65,7 +67,7 @@ def th_mod(cuda_device):
 
 
 @pytest.mark.parametrize("direction", [0.0, -1.0, 8.0], ids=["push", "pull", "auto"])
-@pytest.mark.parametrize("list_mode", [False, True], ids=["dense", "list"])
+@pytest.mark.parametrize("list_mode", [False, True, 2], ids=["dense", "list", "list_t"])
 def test_overlapped_layers_repeatedly(th_mod, direction, list_mode):
     """The overlapped K4s of consecutive layers (two streams) under many
     repeats: FRONTIER, frontiers only, k = 4, graphs replayed -- every
@@ -79,6 +81,7 @@ def test_overlapped_layers_repeatedly(th_mod, direction, list_mode):
     ret = th.Retriever(g)
     ret.set_pull_divisor(direction)
     ret.set_list_min_entities(0 if list_mode else 1 << 40)
+    ret.set_k4_mode(0 if list_mode == 2 else 1)
     rng = np.random.default_rng(5)
     refs = {}
     for rep in range(12):

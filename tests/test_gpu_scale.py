@@ -1,6 +1,9 @@
-"""Full-size parity on the BASELINE configs, through sampled oracle checks
-and size-independent properties: C2 (407K entities / 3.4M
-triples, 1,024 seeds, k=3) and C4 (54.4M / 86.5M, 1,024 seeds, k=2)."""
+"""Full-size parity on the BASELINE configs the bench reports, through
+sampled oracle checks and size-independent properties over every seed
+(SURVEY 8c): C2 (407K entities / 3.4M triples, 1,024 seeds, k=3), C3 (C2
+graph, 4,096 filtered seeds, paths <= 10,000), C4 (54.4M / 86.5M, a full
+1,024-seed wave at k=2 and k=3) and a C5-shaped R-MAT graph (E > 2^27,
+64-of-2,000 relation masks)."""
 
 import numpy as np
 import pytest
@@ -49,26 +52,79 @@ def test_c2_full_batch_properties_and_sampled_oracle(c2):
             assert np.array_equal(fr.frontier(i, h + 1), ref["frontiers"][h])
 
 
+def device_layer_checks(res, seeds, deg, n_entities: int, edges_hops=None):
+    """Size-independent properties of a FRONTIER result over ALL queries, on
+    the device: every per-query segment strictly ascending (canonical
+    EntityVector form, incidence.py:83-91); layers pairwise disjoint and
+    never containing the seed (FRONTIER, incidence.py:301-315); |T_{h+1}(q)|
+    = out-degree sum of layer h (no filter, incidence.py:214-221)."""
+    import torch
+
+    B, k = res.n_queries, res.k
+    dev = res.frontier_ids.device
+    keys = [torch.arange(B, device=dev, dtype=torch.int64) * n_entities + seeds.long()]
+    for h in range(k):
+        ln = res.frontier_len[h].long()
+        off = res.frontier_off[h].long()
+        q = torch.repeat_interleave(torch.arange(B, device=dev), ln)
+        start = torch.cumsum(ln, 0) - ln
+        pos = off[q] + (torch.arange(q.numel(), device=dev) - start[q])
+        v = res.frontier_ids[pos].long()
+        same = q[1:] == q[:-1]
+        assert bool(((v[1:] > v[:-1]) | ~same).all()), f"hop {h + 1}: a segment is not strictly ascending"
+        if h + 1 < k and (edges_hops is None or h + 1 in edges_hops):
+            sums = torch.zeros(B, dtype=torch.int64, device=dev).index_add_(0, q, deg[v])
+            assert torch.equal(sums, res.edges[h + 1].long()), f"hop {h + 2}: edge counts != degree sums"
+        keys.append(q * n_entities + v)
+        del pos, v, same, q
+    allk = torch.sort(torch.cat(keys)).values
+    assert not bool((allk[1:] == allk[:-1]).any()), "layers overlap or contain the seed"
+
+
+def test_c2_device_properties_every_seed(c2):
+    """The same properties, checked on the device for all 1,024 seeds."""
+    import torch
+
+    th, s, r, o, E, R, g, og = c2
+    seeds = workloads.seed_batches(E, 1024, 1, seed=101)[0]
+    fr = th.retrieve(g, seeds, 3, semantics="frontier", copy=False)
+    deg = torch.from_numpy(np.diff(og.indptr)).cuda()
+    device_layer_checks(fr, torch.from_numpy(seeds).cuda(), deg, E)
+    assert torch.equal(fr.edges[0].long(), deg[torch.from_numpy(seeds).cuda().long()])
+
+
 def test_c3_sampled_paths_and_filters(c2):
+    """Filtered k=2 with paths <= 10,000: 64 hub seeds and 32 uniform seeds
+    against the oracle (frontiers, edge counts, path lists, truncation)."""
     th, s, r, o, E, R, g, og = c2
     seeds, rel_ids = workloads.c3_queries(s, E, R)
     res = th.retrieve(g, seeds, 2, relation_filter=list(rel_ids), paths=True, max_paths=10_000)
-    for i in list(range(0, 2048, 211)) + list(range(2048, 4096, 211)):
+    picks = list(range(0, 2048, 64)) + list(range(2048, 4096, 32))
+    n_trunc = 0
+    for i in picks:
         ref = orc.retrieve_one(og, int(seeds[i]), 2, "frontier", rel_ids[i], paths=True, max_paths=10_000)
         for h in range(2):
             assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h])
             assert int(res.edges[h, i]) == ref["edges"][h]
         assert res.path_tid_tuples(i) == ref["paths"]
         assert res.truncated(i) == ref["truncated"]
+        n_trunc += ref["truncated"]
+    assert len(picks) >= 96 and n_trunc > 0  # the cap binds on hub seeds
 
 
-def test_c4_full_size_sampled_oracle(cuda_device):
+@pytest.fixture(scope="module")
+def c4(cuda_device):
     import paper_2604_18913_b200 as th
 
     s, r, o, E, R = workloads.c4_graph()
     g = th.build_incidence((s, r, o), E, R)
     og = orc.build_csr(s, r, o, E, R)
     del s, r, o
+    return th, E, g, og
+
+
+def test_c4_full_size_sampled_oracle(c4):
+    th, E, g, og = c4
     seeds = workloads.seed_batches(E, 1024, 1, seed=400)[0]
     res = th.retrieve(g, seeds, 2, semantics="frontier")
     deg = np.diff(og.indptr)
@@ -80,3 +136,73 @@ def test_c4_full_size_sampled_oracle(cuda_device):
             assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h])
             assert int(res.edges[h, i]) == ref["edges"][h]
         assert int(res.edges[1, i]) == int(deg[res.frontier(i, 1)].sum())
+
+
+def test_c4_k3_full_wave(c4):
+    """C4 k=3 on a full 1,024-seed wave (the bench's dense pull at 54M
+    scale, ~480M output ids): device properties for every seed, and the
+    oracle on 40 seeds -- every 32nd seed plus the 8 whose hop-2 layers
+    are largest (they reach the hub core)."""
+    import torch
+
+    th, E, g, og = c4
+    seeds = workloads.seed_batches(E, 1024, 1, seed=400)[0]
+    res = th.retrieve(g, seeds, 3, semantics="frontier", copy=False)
+    assert res.pull_hops >= 1  # the dense hop ran as a pull
+    deg = torch.from_numpy(np.diff(og.indptr)).cuda()
+    device_layer_checks(res, torch.from_numpy(seeds).cuda(), deg, E)
+    lens = res.frontier_len.cpu().numpy()
+    assert lens[2].sum() > 100_000_000
+    big = np.argsort(-lens[1], kind="stable")[:8].tolist()
+    for i in sorted(set(range(0, 1024, 32)) | set(big)):
+        ref = orc.retrieve_one(og, int(seeds[i]), 3, "frontier")
+        for h in range(3):
+            assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
+            assert int(res.edges[h, i]) == ref["edges"][h], (i, h)
+
+
+def test_c5_shaped_rmat_filtered(cuda_device):
+    """C5's shape at a size the oracle finishes: R-MAT(.57,.19,.19,.05) over
+    150M entities (> 2^27), 20M triples, 2,000 relations, 1,024 seeds with
+    per-seed 64-of-2,000 relation masks, k=2 -- oracle on 16 seeds."""
+    import torch
+    import paper_2604_18913_b200 as th
+
+    E, T, R = 150_000_000, 20_000_000, 2_000
+    s, r, o = workloads.rmat_graph_gpu(E, T, R, seed=55)
+    host = [t.cpu().numpy() for t in (s, r, o)]
+    g = th.build_incidence((s, r, o), E, R)
+    del s, r, o
+    torch.cuda.empty_cache()
+    seeds, rel = workloads.c5_queries(E, R, seed=66, n=1024)
+    res = th.retrieve(g, seeds, 2, relation_filter=list(rel), semantics="frontier")
+    og = orc.build_csr(*host, E, R)
+    del host
+    for i in range(0, 1024, 64):
+        ref = orc.retrieve_one(og, int(seeds[i]), 2, "frontier", rel[i])
+        for h in range(2):
+            assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
+            assert int(res.edges[h, i]) == ref["edges"][h], (i, h)
+    assert int(res.frontier_len.sum()) > 0
+
+
+def test_plan_owner_hash_matches_reference_formula(c2):
+    """th_plan_owner_hash (device) = ((e * 0x9E3779B1) mod 2^32) mod m for
+    subjects, -1 (UNASSIGNED) otherwise (partition.py:80-84, :23)."""
+    import ctypes
+
+    import torch
+    from paper_2604_18913_b200 import _lib
+
+    th, s, r, o, E, R, g, og = c2
+    deg = np.diff(og.indptr)
+    for m in (1, 2, 3, 8, 1000):
+        out = torch.empty(E, dtype=torch.int32, device="cuda")
+        _lib.check(_lib.load().th_plan_owner_hash(g._handle, m, out.data_ptr(),
+                                                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        e = np.arange(E, dtype=np.int64)
+        want = np.where(deg > 0, ((e * 0x9E3779B1) & 0xFFFFFFFF) % m, -1)
+        assert np.array_equal(out.cpu().numpy(), want), m
+        plan = th.plan_partitions((s, E), m, "hash") if m <= np.count_nonzero(deg) else None
+        if plan is not None:
+            assert np.array_equal(plan.assignment, want)
