@@ -173,6 +173,10 @@ int th_session_set_overlap(th_session* s, int on);
  * entities): 1 = row-major (whole-row loads, carry-save bit counting;
  * default), 0 = word-per-warp loads with bit-sliced counting. */
 int th_session_set_k4_mode(th_session* s, int mode);
+/* Pull hops screen their in-row items one per lane for a frontier in-edge
+ * before lane groups expand the survivors: -1 = when the graph's mean
+ * in-edges per pull item is below 4 (default), 0 = never, 1 = always. */
+int th_session_set_pull_screen(th_session* s, int mode);
 /* Pull hops whose frontier sources more than 1/divisor of all in-edges
  * (by the frontier's out-degree sum) gather every in-neighbour row instead
  * of testing frontier flags first (default 2; <= 0 never). */

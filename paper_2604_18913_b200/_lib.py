@@ -34,6 +34,7 @@ EXPORTS = (
     "th_shard_hub_merge", "th_shard_end_hop", "th_shard_finish",
     "th_ids_route_count", "th_ids_map_scatter", "th_ids_to_local_bits", "th_bits_andnot_update",
     "th_bits_or", "th_bits_compact", "th_plan_subjects", "th_session_set_k4_mode",
+    "th_session_set_pull_screen",
 )
 PROF_CATEGORIES = ("setup", "edges", "activated", "push", "pull", "frontier", "clear", "paths")
 
@@ -105,6 +106,7 @@ def load():
         "th_session_set_list_min_entities": (ctypes.c_int, [_vp, ctypes.c_int64]),
         "th_session_set_overlap": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_session_set_k4_mode": (ctypes.c_int, [_vp, ctypes.c_int]),
+        "th_session_set_pull_screen": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_session_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_session_set_dense_pull": (ctypes.c_int, [_vp, ctypes.c_double]),
         "th_session_launch_count": (ctypes.c_int64, [_vp]),

@@ -263,6 +263,15 @@ int th_session_set_k4_mode(th_session* s, int mode) {
   return TH_OK;
 }
 
+int th_session_set_pull_screen(th_session* s, int mode) {
+  if (!s || mode < -1 || mode > 1) {
+    th::set_error(!s ? "NULL handle" : "pull screen mode must be -1, 0 or 1");
+    return TH_ERR_INVALID;
+  }
+  s->s.pull_screen = mode;
+  return TH_OK;
+}
+
 int64_t th_session_launch_count(const th_session* s) { return s ? s->s.launches : -1; }
 
 int th_session_set_profiling(th_session* s, int on) {

@@ -266,7 +266,15 @@ struct PushOp {
       const uint32_t old = atomicOr(&a.N[r], w);
       return old == 0u && flag_next(a, v);
     }
-    if (!(w & ~__ldcg(&a.V[r]))) return false;
+    const uint32_t seen = __ldcg(&a.V[r]);
+    if (!(w & ~seen)) return false;
+    if (a.last_frontier) {
+      // FRONTIER's last hop: V is not read afterwards, so dedupe on N and
+      // leave V untouched (its rows of this layer then need no clearing)
+      const uint32_t nb = w & ~seen;
+      const uint32_t old = atomicOr(&a.N[r], nb);
+      return old == 0u && flag_next(a, v);
+    }
     const uint32_t old = atomicOr(&a.V[r], w);
     const uint32_t nb = w & ~old;
     if (!nb) return false;
@@ -885,7 +893,10 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   constexpr size_t smem_c = mat_smem_bytes<W, false>();
   bool counted = false;
   if constexpr (Src::kRing) {
-    if (s->k4_rowmajor) {
+    // (layers whose count pass also sums edge counts keep the word-per-warp
+    // form: its shared degree planes beat per-bit degree sums, C4 hop 2
+    // 0.47 vs 1.03 ms)
+    if (s->k4_rowmajor && !es.out) {
       // list-driven layers: whole-row loads, carry-save counting (k4_rowmajor.cuh)
       static std::atomic<uint64_t> attr_r{0};
       if (!(attr_r.load(std::memory_order_relaxed) & bit)) {
@@ -962,6 +973,12 @@ void materialize_triples(Session* s, WaveBufs& b, int nq, int64_t* off, int64_t*
   materialize<W>(s, b, src, nq, off, len, out, cap, cursor);
 }
 
+// pull hops screen items per lane first on graphs of low mean in-degree
+// per pull item (k3_pull.cuh; C4: ~2.3 in-edges per item, C2: ~10)
+bool pull_screens(const Graph* g, int knob = -1) {
+  return knob >= 0 ? knob == 1 : (g->n_items > 0 && g->T < 4 * g->n_items);
+}
+
 template <int W, int SEM, bool FILTER>
 void expand_hop(Session* s, const WaveArgs& a) {
   const unsigned pg = persistent_grid();
@@ -977,7 +994,8 @@ void expand_hop(Session* s, const WaveArgs& a) {
   }
   if (s->g->rindptr) {
     ProfScope ps(s, TH_PROF_PULL);
-    pull_kernel<W, SEM, FILTER><<<pg, kThreads, 0, s->st>>>(a);
+    if (pull_screens(s->g, s->pull_screen)) pull_kernel<W, SEM, FILTER, true><<<pg, kThreads, 0, s->st>>>(a);
+    else pull_kernel<W, SEM, FILTER, false><<<pg, kThreads, 0, s->st>>>(a);
     TH_LAUNCHED();
     s->launches += 1;
   }
@@ -1202,7 +1220,9 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   // frontier K4, so its clear overlaps the last layer's materialisation)
   if (sem != TH_EXACT) {
     ProfScope ps(s, TH_PROF_CLEAR);
-    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, (int)k, E);
+    // (FRONTIER's last hop never writes V: its layer's rows are clean)
+    clear_rows_kernel<W><<<grid_for(E * W), kThreads, 0, st>>>(
+        b.V, b.lists, b.ctl, 0, sem == TH_FRONTIER ? (int)k - 1 : (int)k, E);
     TH_LAUNCHED();
     s->launches += 1;
   }
@@ -1329,7 +1349,8 @@ static GraphKey graph_key(Session* s, const th_query* q) {
   k.pull_divisor = s->pull_divisor;
   k.dense_pull = s->dense_pull;
   k.list_min = s->list_min_entities;
-  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_rowmajor ? 8 : 0);
+  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_rowmajor ? 8 : 0) |
+            ((s->pull_screen + 1) << 4);
   k.epoch = session_alloc_sig(s);
   return k;
 }
@@ -1950,13 +1971,16 @@ void shard_absorb_w(Shard* sh, int h, const uint64_t* recs, int64_t n) {
     const bool filter = s->last.d_rel_masks != nullptr;
     {
       ProfScope ps(s, TH_PROF_PULL);
+      const bool scr = pull_screens(&sh->gin, s->pull_screen);
+#define TH_SHARD_PULL(SEM, F)                                                          \
+  if (scr) pull_kernel<W, SEM, F, true><<<pg, kThreads, 0, st>>>(pa);                  \
+  else pull_kernel<W, SEM, F, false><<<pg, kThreads, 0, st>>>(pa);
       if (s->last.semantics == TH_EXACT) {
-        if (filter) pull_kernel<W, TH_EXACT, true><<<pg, kThreads, 0, st>>>(pa);
-        else pull_kernel<W, TH_EXACT, false><<<pg, kThreads, 0, st>>>(pa);
+        if (filter) { TH_SHARD_PULL(TH_EXACT, true) } else { TH_SHARD_PULL(TH_EXACT, false) }
       } else {
-        if (filter) pull_kernel<W, TH_FRONTIER, true><<<pg, kThreads, 0, st>>>(pa);
-        else pull_kernel<W, TH_FRONTIER, false><<<pg, kThreads, 0, st>>>(pa);
+        if (filter) { TH_SHARD_PULL(TH_FRONTIER, true) } else { TH_SHARD_PULL(TH_FRONTIER, false) }
       }
+#undef TH_SHARD_PULL
       TH_LAUNCHED();
     }
     shard_clear_frontier_kernel<W><<<grid, kThreads, 0, st>>>(sa, h - 1, recs, n);

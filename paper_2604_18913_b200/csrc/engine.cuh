@@ -60,6 +60,7 @@ struct Session {
   // runs; the main stream joins before it recycles the layer's rows)
   bool overlap = true;
   bool k4_cache = true;
+  int pull_screen = -1;     // pull items screened per lane first: -1 by graph shape, 0 off, 1 on
   bool k4_rowmajor = true;  // list-driven layers count rows row-major (k4_rowmajor.cuh)
   bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr, side2 = nullptr;  // K4 streams (odd / even layers)

@@ -165,6 +165,11 @@ __global__ void __launch_bounds__(32 * kRsWarps) rs_count_kernel(RowMajorSrc<W> 
   blk_rows = blk_rows < kChunkRows ? kChunkRows : (blk_rows + kChunkRows - 1) / kChunkRows * kChunkRows;
   const int64_t r0 = (int64_t)blk * blk_rows;
   const int64_t r1 = nrows < r0 + blk_rows ? nrows : r0 + blk_rows;
+  if (r0 >= r1) {
+    // (blocks past the layer's rows: zero counts, no shared-memory work)
+    for (int q = threadIdx.x; q < src.nq; q += blockDim.x) counts[(size_t)q * nblk + blk] = 0;
+    return;
+  }
   const int64_t per = r1 > r0 ? ((r1 - r0 + kRsWarps - 1) / kRsWarps + kRsUnroll - 1) / kRsUnroll * kRsUnroll
                               : 0;
   const int64_t lo = r0 + warp * per < r1 ? r0 + warp * per : r1;

@@ -199,6 +199,10 @@ class Retriever:
         """K4 form for list-driven layers: 1 row-major (default), 0 transposes."""
         _lib.check(_lib.load().th_session_set_k4_mode(self._handle, int(mode)))
 
+    def set_pull_screen(self, mode: int) -> None:
+        """Per-lane item screening in pull hops: -1 by graph shape (default), 0 off, 1 on."""
+        _lib.check(_lib.load().th_session_set_pull_screen(self._handle, int(mode)))
+
     def set_overlap(self, on: bool) -> None:
         """Overlap hop h's K4 with hop h+1's expansion (frontier-only runs)."""
         _lib.check(_lib.load().th_session_set_overlap(self._handle, int(bool(on))))

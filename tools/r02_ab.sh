@@ -1,4 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-timeout 900 python -m pytest -q -x tests/test_gpu_parity.py tests/test_gpu_fuzz.py > gpurun_out/ab_tests.log 2>&1; echo tests=$?; tail -2 gpurun_out/ab_tests.log
-timeout 600 python tools/ab_c4.py "{'k4_mode': 0}" "{'k4_mode': 1}" > gpurun_out/ab.log 2>&1; echo ab=$?
+timeout 900 python -m pytest -q -x tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_graphs.py > gpurun_out/ab_tests.log 2>&1; echo tests=$?; tail -2 gpurun_out/ab_tests.log
+timeout 600 python tools/ab_c4.py ${AB:-"{}"} > gpurun_out/ab.log 2>&1; echo ab=$?
 tail -8 gpurun_out/ab.log
+timeout 600 python bench.py --no-cpu --no-c3 --no-c4 --steps 20 --warmup 5 > gpurun_out/ab_bench.log 2>&1; echo bench=$?
+grep '^{' gpurun_out/ab_bench.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d.get('kernel_ms_per_step'))"
