@@ -322,18 +322,18 @@ def run_c3_leg(th, g, s, E, R, stream, peaks):
                     "h2d_bytes_per_step": int(seeds.nbytes + words.nbytes), "d2h_bytes_per_step": d2h}}
 
 
-def run_c4_leg(th, stream, peaks, n_batches=8):
+def run_c4_leg(th, stream, peaks, n_batches=8, cols=None):
     """BASELINE configs[3] on one GPU: 54.4M entities / 86.5M triples, 8,192
     uniform seeds as 8 waves of 1,024, k=2 and k=3, FRONTIER, frontiers
     materialised per wave (the state and results of a wave are far above L2)."""
     import torch
 
     t0 = time.perf_counter()
-    s, r, o, E, R = workloads.c4_graph()
+    s, r, o, E, R = cols if cols is not None else workloads.c4_graph()
     gen_s = time.perf_counter() - t0
     stats = workloads.graph_stats(s, o, E)
     g = th.build_incidence((s, r, o), E, R)
-    del s, r, o
+    del s, r, o, cols
     ret = th.Retriever(g, stream)
     batches = torch.from_numpy(workloads.seed_batches(E, BATCH, n_batches, seed=400)).to(g.device)
     offs = torch.arange(BATCH + 1, dtype=torch.int32, device=g.device)
@@ -375,10 +375,87 @@ def run_c4_leg(th, stream, peaks, n_batches=8):
     return out
 
 
+def partitioned_leg(th, cols, E, R, world, rank, ks=(2, 3), n_batches=4, reps=4):
+    """BASELINE configs[3] partitioned over the job's ranks (hash owners +
+    edge-split top-0.01% hubs, Algorithm 1 per hop with the ranks writing
+    into each other's exchange regions): per k, one wave of 1,024 uniform
+    seeds per step; seeds/s and edges/s over ALL ranks (strong scaling: the
+    wave is the whole job's work), records written to other ranks per hop
+    (12 B each: the interconnect bytes), and an e2e through
+    ``PartitionedGraph.retrieve`` (host seeds in, merged sorted per-seed
+    frontiers back on the host)."""
+    import torch
+
+    xch = th.LoopbackExchange(1) if world == 1 else th.DistExchange()
+    t0 = time.perf_counter()
+    pg = th.PartitionedGraph(cols, E, R, xch)
+    build_s = time.perf_counter() - t0
+    dev = pg.shards[0].device
+    stream = torch.cuda.current_stream(dev)
+    batches = workloads.seed_batches(E, BATCH, n_batches, seed=400)
+    out = {"workload": f"C4 partitioned over {world} rank(s): hash owners, top-0.01% hubs edge-split "
+                       f"({pg.plan.n_hubs} hubs), one wave of {BATCH} uniform seeds per step, FRONTIER",
+           "build_s": build_s, "local_triples": [sh.local_triples for sh in pg.shards]}
+
+    def wave(i, k, stats=None):
+        q = th.partition.WaveQuery(np.arange(BATCH + 1, dtype=np.int32), batches[i % n_batches], k,
+                                   th.HopSemantics.FRONTIER)
+        return pg.run(q, stats)
+
+    for k in ks:
+        for i in range(n_batches):  # sizes every buffer; every timed wave repeats one of these
+            wave(i, k)
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        edges, sent = 0, [0] * k
+        a.record(stream)
+        for i in range(reps):
+            stats = {}
+            parts = wave(i, k, stats)
+            edges += int(sum(int(p.edges.sum()) for p in parts))
+            for per in stats["sent_records"]:
+                sent = [x + y for x, y in zip(sent, per)]
+        b.record(stream)
+        torch.cuda.synchronize()
+        t_ms = a.elapsed_time(b)
+        vals = torch.tensor([t_ms, float(edges)] + [float(x) for x in sent], dtype=torch.float64)
+        if world > 1:
+            vals = vals.to(dev)
+            tmax = vals.clone()
+            torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+            torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.SUM)
+            vals[0] = tmax[0]
+            vals = vals.cpu()
+        t_ms = float(vals[0])
+        per_hop_bytes = [12.0 * float(x) / reps for x in vals[2:].tolist()]
+        # e2e: host seeds -> merged per-seed sorted frontiers on the host
+        e2e = []
+        for i in range(2):
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            res = pg.retrieve(batches[i], k)
+            res.frontier_ids.numpy()
+            e2e.append(time.perf_counter() - w0)
+        out[f"k{k}"] = {
+            "seeds_per_s": BATCH * reps / (t_ms / 1e3), "edges_per_s": float(vals[1]) / (t_ms / 1e3),
+            "ms_per_wave": t_ms / reps,
+            "interconnect": {"bytes_per_hop": per_hop_bytes,
+                             "GBps": sum(per_hop_bytes) / (t_ms / reps / 1e3) / 1e9,
+                             "peak_per_direction_GBps": 900.0,
+                             "note": "records written into other ranks' exchange inboxes (12 B each)"},
+            "e2e": {"value": BATCH / min(e2e), "unit": "seeds/s", "h2d_bytes_per_step": BATCH * 4,
+                    "d2h_bytes_per_step": int(res.frontier_ids.numel() * 4 + res.frontier_len.numel() * 16
+                                              + res.edges.numel() * 8),
+                    "api": "PartitionedGraph.retrieve (merge of the owners' slices on the device)"}}
+    del pg
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_partitioned(args, world, rank, local):
-    """C4 on a graph partitioned over the N ranks (hash owners + edge-split
-    hubs, NCCL all-to-all of candidate records per hop); every rank takes
-    part in every wave, so total work is fixed: strong scaling."""
+    """`--partitioned`: only the partitioned C4 leg, as the headline line."""
     import torch
     import torch.distributed as dist
 
@@ -386,75 +463,27 @@ def run_partitioned(args, world, rank, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-    os.environ.setdefault("MASTER_PORT", "29533")
-    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     s, r, o, E, R = workloads.c4_graph()
-    xch = th.DistExchange()
-    pg = th.PartitionedGraph((s, r, o), E, R, xch)
-    del s, r, o
-    # the timed waves cycle over the warm-up batches, so every result buffer
-    # was sized before timing (a wave whose output outgrows it is re-run by
-    # every rank, which would time two waves as one)
-    nb = max(1, args.warmup)
-    batches = workloads.seed_batches(E, BATCH, nb, seed=400)
-    k = args.part_k
-    stream = torch.cuda.current_stream(dev)
-
-    def wave(i):
-        q = th.partition.WaveQuery(np.arange(BATCH + 1, dtype=np.int32), batches[i % nb], k,
-                                   th.HopSemantics.FRONTIER)
-        return pg.run(q)
-
-    for i in range(args.warmup):
-        wave(i)
     clocks = ClockSampler(local)
-    clocks.start()  # (before the barrier: see ClockSampler.start)
-    dist.barrier()
-    torch.cuda.synchronize()
-    # the first wave after the asynchronous warm-up stalls once (~19 ms
-    # measured at world=1, every later wave 2.5-2.8 ms): absorb it untimed
-    parts = wave(0)
-    int(parts[0].edges.sum())
-    dist.barrier()
-    torch.cuda.synchronize()
-    b0 = xch.bytes_sent
-    launches0 = sum(sh.launch_count() for sh in pg.shards)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    edges = 0
-    w0 = time.perf_counter()
-    for i in range(args.steps):
-        parts = wave(i)
-        edges += int(parts[0].edges.sum())
-    b.record(stream)
-    torch.cuda.synchronize()
-    wall_ms = (time.perf_counter() - w0) * 1e3
+    clocks.start()
+    leg = partitioned_leg(th, (s, r, o), E, R, world, rank, ks=(args.part_k,),
+                          reps=max(args.steps, 1))
     clk = clocks.stop()
-    t_ms = a.elapsed_time(b)
-    tt = torch.tensor([t_ms, float(edges), float(xch.bytes_sent - b0)], dtype=torch.float64, device=dev)
-    tmax = tt.clone()
-    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-    t_ms = float(tmax[0].item())
+    k = args.part_k
     if rank == 0:
-        value = BATCH * args.steps / (t_ms / 1e3)
+        d = leg[f"k{k}"]
         print(json.dumps({
-            "metric": f"partitioned C4 k-hop seeds/s at k={k}", "value": value, "unit": "seeds/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "metric": f"partitioned C4 k-hop seeds/s at k={k}", "value": d["seeds_per_s"], "unit": "seeds/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": d["ms_per_wave"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic",
-            "config": {"workload": "C4 partitioned (BASELINE configs[3]): hash owners, top-0.01% hubs "
-                                   f"edge-split; one wave of {BATCH} uniform seeds per step (cycling over "
-                                   f"the {nb} warm-up batches), k={k}, FRONTIER",
-                       "parallelism": f"graph-partitioned x{world}"},
-            "edges_per_s": float(tt[1].item()) / (t_ms / 1e3),
-            "nvlink": {"bytes_per_step": float(tt[2].item()) / args.steps,
-                       "GBps": float(tt[2].item()) / (t_ms / 1e3) / 1e9, "peak_per_direction": 900.0},
-            "gpu_launches": sum(sh.launch_count() for sh in pg.shards) - launches0,
-            "wall_ms_per_step": wall_ms / args.steps,
+            "data": "synthetic", "config": {"workload": leg["workload"], "parallelism": f"graph-partitioned x{world}"},
+            "edges_per_s": d["edges_per_s"], "interconnect": d["interconnect"], "e2e": d["e2e"],
             "clocks": clk}), flush=True)
-    dist.destroy_process_group()
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_ours(args, world, rank, local):
@@ -625,10 +654,18 @@ def run_ours(args, world, rank, local):
                          f"oracle hop_trace per seed, fork pool, {dt:.1f} s)",
                "edges_per_s": e / dt}
 
-    # the extra legs run at N=1 only (like the CPU baseline), so multi-rank
-    # runs stay symmetric and short
+    # the C3 / C4 single-GPU legs run at N=1 only (like the CPU baseline);
+    # the partitioned C4 leg runs at every N (all ranks take part)
     c3 = run_c3_leg(th, g, s, E, R, stream, peaks) if (world == 1 and not args.no_c3) else None
-    c4 = run_c4_leg(th, stream, peaks) if (world == 1 and not args.no_c4) else None
+    c4 = part = None
+    if not args.no_c4:
+        del ret, g
+        torch.cuda.empty_cache()
+        c4_cols = workloads.c4_graph()
+        if world == 1:
+            c4 = run_c4_leg(th, stream, peaks, cols=c4_cols)
+        if not args.no_part:
+            part = partitioned_leg(th, c4_cols[:3], c4_cols[3], c4_cols[4], world, rank)
 
     if rank == 0:
         line = {
@@ -665,6 +702,7 @@ def run_ours(args, world, rank, local):
             "cpu_baseline": cpu,
             "c3": c3,
             "c4": c4,
+            "partitioned": part,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -685,6 +723,7 @@ def main():
     ap.add_argument("--partitioned", action="store_true",
                     help="C4 on a graph partitioned over the ranks (NCCL exchange per hop)")
     ap.add_argument("--part-k", type=int, default=2)
+    ap.add_argument("--no-part", action="store_true", help="skip the partitioned C4 leg")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

@@ -16,6 +16,7 @@
  *   th_shard_*        <- materialize_subgraphs / route / _partitioned_expand /
  *                        cross_graph_k_hop          partition.py:101-181,
  *                                                   engine.py:94-154
+ *                        (ranks exchange through each other's device memory)
  *
  * Conventions
  *   - plain C types only; every pointer argument documented as device (d_)
@@ -244,52 +245,83 @@ int th_plan_subjects(const int64_t* h_degrees, int64_t n_entities, int32_t m, in
  *                       number its entities in ascending id order)
  *   d_hub_index[E]      -1 or hub number < n_hubs; d_hub_ids[n_hubs] inverse
  *   d_l2g[n_local]      this rank's owned entities, ascending
+ *   inbox_records       capacity of this rank's exchange inbox (records)
  * The shard copies what it keeps; inputs may be freed afterwards. */
 typedef struct th_shard th_shard;
 int th_shard_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* d_obj,
                     int64_t n_triples, int64_t n_entities, int64_t n_relations,
                     const int32_t* d_lidx, const int32_t* d_hub_index, const int32_t* d_hub_ids,
                     int64_t n_hubs, const int32_t* d_l2g, int64_t n_local, int32_t rank,
-                    int32_t world, void* stream, th_shard** out);
+                    int32_t world, int64_t inbox_records, void* stream, th_shard** out);
 int th_shard_destroy(th_shard* s);
 int64_t th_shard_local_triples(const th_shard* s);
 int64_t th_shard_launch_count(const th_shard* s);
-
-/* One wave of <= 1024 queries, hop h = 1..k in order; every rank makes the
- * same calls with the same query arrays:
- *   th_shard_begin(q)                     seeds (hub seeds on every rank)
- *   th_shard_plan(h, &cost)               optional: this rank's frontier
- *       out-edge total; the caller sums it over ranks to pick the direction
- *   th_shard_expand(h, mode, counts, &send)
- *       mode 0 (push): push over local rows + hub slices; send[] = records
- *       bucketed by owner rank, counts[world] records per owner (host).
- *       Record = ((row_at_owner * W + word) << 32) | bits, W = 32-bit words
- *       per row (queries rounded up to a power of two / 32).
- *       mode 1 (pull, th_shard_can_pull): send[] = this rank's owned
- *       frontier rows as ((global_id * W + word) << 32) | bits, the same for
- *       every rank (counts[d] = their number)
- *   -- caller: mode 0 all-to-all, mode 1 all-gather of the records --
- *   th_shard_absorb(h, recv, n)           mode 0: apply received records;
- *       mode 1: stage all ranks' frontier rows, pull over the owned in-edges
- *   th_shard_hub_rows(h, &rows, &words)   uint32 [n_hubs][W]: owned hubs'
- *       next-layer rows, zero elsewhere
- *   -- caller: sum `rows` over ranks in place (one owner per hub) --
- *   th_shard_hub_merge(h)                 install hub frontier rows
- *   th_shard_end_hop(h)                   materialise owned frontier ids
- *   th_shard_finish(&result)              after hop k; like th_finish, with
- *       frontier ids = owned entities (global ids, sorted), activated =
- *       local triples (global tids, sorted), edges = this rank's share
- *       (sum over ranks = |T_h|).  TH_ERR_OVERFLOW: capacities grew, every
- *       rank must run the wave again.  Paths are not available here. */
-int th_shard_begin(th_shard* s, const th_query* q);
-int th_shard_plan(th_shard* s, int32_t hop, int64_t* h_cost);
 int th_shard_can_pull(const th_shard* s);
-int th_shard_expand(th_shard* s, int32_t hop, int32_t mode, int64_t* h_send_counts,
-                    const uint64_t** d_send);
-int th_shard_absorb(th_shard* s, int32_t hop, const uint64_t* d_recv, int64_t n_recv);
-int th_shard_hub_rows(th_shard* s, int32_t hop, uint32_t** d_rows, int64_t* n_words);
-int th_shard_hub_merge(th_shard* s, int32_t hop);
-int th_shard_end_hop(th_shard* s, int32_t hop);
+/* Pull hops when the ranks' summed frontier out-edges exceed
+ * n_triples / pull_divisor (default 8; <= 0 = push only). */
+int th_shard_set_pull_divisor(th_shard* s, double pull_divisor);
+
+/* Exchange.  Every shard owns an exchange region in its device memory --
+ * control words (inbox cursor, overflow flag, every rank's published
+ * frontier cost), an inbox of (int64 key, uint32 bits) records and a hub-row
+ * board -- and its peers' KERNELS WRITE INTO IT DIRECTLY (remote atomics
+ * reserve inbox space; stores deliver records, costs and hub rows).  Before
+ * a wave every shard must be connected to every peer's region:
+ *   same process (one device, or peer access enabled between devices):
+ *       th_shard_region(peer, &base, ...); th_shard_connect(self, p, base)
+ *   other processes: th_shard_ipc_handle(peer) -> 64 bytes, shipped to the
+ *       others, th_shard_ipc_open(self, p, bytes) (CUDA IPC mapping)
+ * Nothing is read back to the host during a wave. */
+int th_shard_region(const th_shard* s, void** d_base, uint64_t* bytes, int64_t* inbox_records);
+int th_shard_ipc_handle(const th_shard* s, void* h_handle64);
+int th_shard_connect(th_shard* s, int32_t peer, void* d_peer_base);
+int th_shard_ipc_open(th_shard* s, int32_t peer, const void* h_handle64);
+/* After an inbox overflow (th_shard_finish -> TH_ERR_OVERFLOW with
+ * th_shard_inbox_overflowed() == 1 on some rank): every rank grows its inbox
+ * (the region is reallocated), all ranks reconnect, and the wave runs again. */
+int th_shard_grow_inbox(th_shard* s, int64_t inbox_records);
+int th_shard_inbox_overflowed(const th_shard* s);
+/* Records this rank wrote into OTHER ranks' inboxes at hops 1..n of the
+ * last wave (12 bytes each over the interconnect).  Synchronises. */
+int th_shard_sent(th_shard* s, int64_t* h_per_hop, int n);
+
+/* One wave of <= 1024 queries; every rank makes the same calls with the
+ * same query arrays, and all ranks pass a barrier between consecutive calls
+ * (the peers' writes of the previous step are then complete):
+ *   th_shard_begin(q)          seeds (hub seeds on every rank); publishes
+ *                              hop 1's frontier cost to every rank
+ *   for h = 1..k, phase 0..2:  th_shard_hop(h, phase)
+ *     phase 0 (send)    direction from the published costs, edge counts;
+ *                       push: local test-and-set + records for remote
+ *                       targets into their owners' inboxes; pull: the owned
+ *                       frontier rows into every rank's inbox
+ *     phase 1 (receive) apply the inbox (push) or stage the frontier and
+ *                       pull over the owned in-edges (pull); owners write
+ *                       their hubs' next-layer rows onto every hub board
+ *     phase 2 (end)     hub frontier rows from the board, K4 over the owned
+ *                       rows, publish the new layer's frontier cost
+ *   th_shard_finish(&result)   like th_finish, with frontier ids = owned
+ *       entities (global ids, sorted), activated = local triples (global
+ *       tids, sorted), edges = this rank's share (sum over ranks = |T_h|).
+ *       TH_ERR_OVERFLOW: result capacities or the inbox grew/must grow;
+ *       every rank runs the wave again.  Paths are not available here. */
+/* The shard's own triples (device arrays, local tid order = ascending
+ * global tid): subject as a LOCAL row (rows < n_local map through l2g,
+ * hub slice rows n_local + h through hub_ids), relation, object (global),
+ * and the global tid of each local triple. */
+typedef struct {
+  int64_t n_triples, n_local, n_hubs;
+  const int32_t* subj_row;
+  const uint16_t* rel;
+  const int32_t* obj;
+  const int32_t* tid_l2g;
+  const int32_t* l2g;
+  const int32_t* hub_ids;
+} th_shard_cols;
+int th_shard_columns(const th_shard* s, th_shard_cols* out);
+
+int th_shard_begin(th_shard* s, const th_query* q);
+int th_shard_hop(th_shard* s, int32_t hop, int32_t phase);
 int th_shard_finish(th_shard* s, th_result* out);
 
 /* ---- id sets: store-backed partitioned retrieval ------------------------

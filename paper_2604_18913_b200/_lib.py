@@ -29,9 +29,9 @@ EXPORTS = (
     "th_session_set_list_min_entities", "th_session_set_overlap", "th_session_set_graphs", "th_session_set_dense_pull",
     "th_session_set_profiling", "th_session_profile", "th_session_wave_lists",
     "th_shard_create", "th_shard_destroy", "th_shard_local_triples", "th_shard_launch_count",
-    "th_shard_begin", "th_shard_plan", "th_shard_can_pull", "th_shard_expand", "th_shard_absorb",
-    "th_shard_hub_rows",
-    "th_shard_hub_merge", "th_shard_end_hop", "th_shard_finish",
+    "th_shard_begin", "th_shard_can_pull", "th_shard_set_pull_divisor", "th_shard_region",
+    "th_shard_ipc_handle", "th_shard_connect", "th_shard_ipc_open", "th_shard_grow_inbox",
+    "th_shard_inbox_overflowed", "th_shard_hop", "th_shard_finish", "th_shard_sent", "th_shard_columns",
     "th_ids_route_count", "th_ids_map_scatter", "th_ids_to_local_bits", "th_bits_andnot_update",
     "th_bits_or", "th_bits_compact", "th_plan_subjects", "th_session_set_k4_mode",
     "th_session_set_pull_screen",
@@ -59,6 +59,13 @@ class Query(ctypes.Structure):
         ("k", ctypes.c_int32), ("semantics", ctypes.c_int32),
         ("d_rel_masks", _vp), ("mask_words", ctypes.c_int32),
         ("flags", ctypes.c_uint32), ("max_paths", ctypes.c_int64),
+    ]
+
+
+class ShardCols(ctypes.Structure):
+    _fields_ = [
+        ("n_triples", ctypes.c_int64), ("n_local", ctypes.c_int64), ("n_hubs", ctypes.c_int64),
+        ("subj_row", _vp), ("rel", _vp), ("obj", _vp), ("tid_l2g", _vp), ("l2g", _vp), ("hub_ids", _vp),
     ]
 
 
@@ -117,20 +124,24 @@ def load():
         "th_session_wave_lists": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
         "th_shard_create": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                            _vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
-                                           ctypes.c_int32, ctypes.c_int32, _vp, ctypes.POINTER(_vp)]),
+                                           ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _vp,
+                                           ctypes.POINTER(_vp)]),
         "th_shard_destroy": (ctypes.c_int, [_vp]),
         "th_shard_local_triples": (ctypes.c_int64, [_vp]),
         "th_shard_launch_count": (ctypes.c_int64, [_vp]),
         "th_shard_begin": (ctypes.c_int, [_vp, ctypes.POINTER(Query)]),
-        "th_shard_plan": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
         "th_shard_can_pull": (ctypes.c_int, [_vp]),
-        "th_shard_expand": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32,
-                                           ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_vp)]),
-        "th_shard_absorb": (ctypes.c_int, [_vp, ctypes.c_int32, _vp, ctypes.c_int64]),
-        "th_shard_hub_rows": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.POINTER(_vp),
-                                             ctypes.POINTER(ctypes.c_int64)]),
-        "th_shard_hub_merge": (ctypes.c_int, [_vp, ctypes.c_int32]),
-        "th_shard_end_hop": (ctypes.c_int, [_vp, ctypes.c_int32]),
+        "th_shard_set_pull_divisor": (ctypes.c_int, [_vp, ctypes.c_double]),
+        "th_shard_region": (ctypes.c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64),
+                                           ctypes.POINTER(ctypes.c_int64)]),
+        "th_shard_ipc_handle": (ctypes.c_int, [_vp, _vp]),
+        "th_shard_connect": (ctypes.c_int, [_vp, ctypes.c_int32, _vp]),
+        "th_shard_ipc_open": (ctypes.c_int, [_vp, ctypes.c_int32, _vp]),
+        "th_shard_grow_inbox": (ctypes.c_int, [_vp, ctypes.c_int64]),
+        "th_shard_inbox_overflowed": (ctypes.c_int, [_vp]),
+        "th_shard_sent": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
+        "th_shard_columns": (ctypes.c_int, [_vp, ctypes.POINTER(ShardCols)]),
+        "th_shard_hop": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32]),
         "th_shard_finish": (ctypes.c_int, [_vp, ctypes.POINTER(Result)]),
         "th_ids_route_count": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32,
                                               _vp, _vp]),

@@ -320,7 +320,7 @@ int th_shard_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* 
                     int64_t n_triples, int64_t n_entities, int64_t n_relations,
                     const int32_t* d_lidx, const int32_t* d_hub_index, const int32_t* d_hub_ids,
                     int64_t n_hubs, const int32_t* d_l2g, int64_t n_local, int32_t rank,
-                    int32_t world, void* stream, th_shard** out) {
+                    int32_t world, int64_t inbox_records, void* stream, th_shard** out) {
   return guarded([&]() -> int {
     if (!out) {
       th::set_error("out is NULL");
@@ -352,7 +352,7 @@ int th_shard_create(const int32_t* d_subj, const int32_t* d_rel, const int32_t* 
     try {
       rc = th::shard_create(&sh, d_subj, d_rel, d_obj, n_triples, n_entities, n_relations, d_lidx,
                             d_hub_index, d_hub_ids, n_hubs, d_l2g, n_local, rank, world,
-                            static_cast<cudaStream_t>(stream));
+                            inbox_records, static_cast<cudaStream_t>(stream));
     } catch (...) {
       if (sh) th::shard_free(sh);
       delete h;
@@ -397,64 +397,98 @@ int th_shard_begin(th_shard* s, const th_query* q) {
   });
 }
 
-int th_shard_plan(th_shard* s, int32_t hop, int64_t* h_cost) {
-  return guarded([&]() -> int {
-    TH_SHARD_GUARD(s);
-    if (!h_cost) {
-      th::set_error("NULL output");
-      return TH_ERR_INVALID;
-    }
-    return th::shard_plan(s->sh, hop, h_cost);
-  });
-}
-
 int th_shard_can_pull(const th_shard* s) { return (s && s->sh) ? th::shard_can_pull(s->sh) : 0; }
 
-int th_shard_expand(th_shard* s, int32_t hop, int32_t mode, int64_t* h_send_counts,
-                    const uint64_t** d_send) {
+int th_shard_region(const th_shard* s, void** d_base, uint64_t* bytes, int64_t* inbox_records) {
   return guarded([&]() -> int {
-    TH_SHARD_GUARD(s);
-    if (!h_send_counts || !d_send || (mode != 0 && mode != 1)) {
-      th::set_error("NULL output or bad mode");
+    if (!s || !s->sh || !d_base || !bytes) {
+      th::set_error("bad arguments");
       return TH_ERR_INVALID;
     }
-    return th::shard_expand(s->sh, hop, mode, h_send_counts, d_send);
+    return th::shard_region(s->sh, d_base, bytes, inbox_records);
   });
 }
 
-int th_shard_absorb(th_shard* s, int32_t hop, const uint64_t* d_recv, int64_t n_recv) {
+int th_shard_ipc_handle(const th_shard* s, void* h_handle64) {
   return guarded([&]() -> int {
-    TH_SHARD_GUARD(s);
-    if (n_recv < 0 || (n_recv > 0 && !d_recv)) {
-      th::set_error("bad receive buffer");
+    if (!s || !s->sh || !h_handle64) {
+      th::set_error("bad arguments");
       return TH_ERR_INVALID;
     }
-    return th::shard_absorb(s->sh, hop, d_recv, n_recv);
+    return th::shard_ipc_handle(s->sh, h_handle64);
   });
 }
 
-int th_shard_hub_rows(th_shard* s, int32_t hop, uint32_t** d_rows, int64_t* n_words) {
+int th_shard_connect(th_shard* s, int32_t peer, void* d_peer_base) {
   return guarded([&]() -> int {
-    TH_SHARD_GUARD(s);
-    if (!d_rows || !n_words) {
-      th::set_error("NULL output");
+    if (!s || !s->sh || !d_peer_base) {
+      th::set_error("bad arguments");
       return TH_ERR_INVALID;
     }
-    return th::shard_hub_rows(s->sh, hop, d_rows, n_words);
+    return th::shard_connect(s->sh, peer, d_peer_base, false);
   });
 }
 
-int th_shard_hub_merge(th_shard* s, int32_t hop) {
+int th_shard_ipc_open(th_shard* s, int32_t peer, const void* h_handle64) {
   return guarded([&]() -> int {
-    TH_SHARD_GUARD(s);
-    return th::shard_hub_merge(s->sh, hop);
+    if (!s || !s->sh || !h_handle64) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_ipc_open(s->sh, peer, h_handle64);
   });
 }
 
-int th_shard_end_hop(th_shard* s, int32_t hop) {
+int th_shard_grow_inbox(th_shard* s, int64_t inbox_records) {
   return guarded([&]() -> int {
-    TH_SHARD_GUARD(s);
-    return th::shard_end_hop(s->sh, hop);
+    if (!s || !s->sh || inbox_records < 1) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_grow_inbox(s->sh, inbox_records);
+  });
+}
+
+int th_shard_sent(th_shard* s, int64_t* h_per_hop, int n) {
+  return guarded([&]() -> int {
+    if (!s || !s->sh || !h_per_hop || n < 0) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_sent(s->sh, h_per_hop, n);
+  });
+}
+
+int th_shard_columns(const th_shard* s, th_shard_cols* out) {
+  return guarded([&]() -> int {
+    if (!s || !s->sh || !out) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_columns(s->sh, out);
+  });
+}
+
+int th_shard_inbox_overflowed(const th_shard* s) {
+  return (s && s->sh) ? th::shard_inbox_overflowed(s->sh) : -1;
+}
+
+int th_shard_set_pull_divisor(th_shard* s, double pull_divisor) {
+  if (!s || !s->sh) {
+    th::set_error("NULL handle");
+    return TH_ERR_INVALID;
+  }
+  th::shard_set_pull_divisor(s->sh, pull_divisor);
+  return TH_OK;
+}
+
+int th_shard_hop(th_shard* s, int32_t hop, int32_t phase) {
+  return guarded([&]() -> int {
+    if (!s || !s->sh || phase < 0 || phase > 2) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    return th::shard_hop(s->sh, hop, phase);
   });
 }
 

@@ -1686,10 +1686,11 @@ void plan_owner_hash(const Graph* g, int32_t m, int32_t* d_owner, cudaStream_t s
 
 
 // ============================================================ K6 shards
-// One rank's partitioned-graph session (see k6_shard.cuh).  The host drives
-// a wave hop by hop -- expand / (exchange) / absorb / hub rows / (all-reduce)
-// / hub merge / end hop -- so the collectives stay with the caller
-// (torch.distributed over NCCL, or an in-process loopback).
+// One rank's partitioned-graph session (see k6_shard.cuh).  The host issues
+// a wave hop by hop in three phases (send / receive / end) separated by a
+// barrier across ranks; all data movement between ranks is peers writing
+// into each other's exchange regions from the kernels, so the host never
+// waits on a count or a collective inside a wave.
 
 struct Shard {
   Graph g;                         // rows [0,n_local) owned, then hub slices
@@ -1698,17 +1699,24 @@ struct Shard {
   int32_t* hub_index = nullptr;    // [E]
   int32_t* hub_ids = nullptr;      // [H]
   int32_t* l2g = nullptr;          // [n_local] owned rows -> global ids (ascending)
-  int64_t E = 0, n_local = 0, H = 0;
+  int64_t E = 0, n_local = 0, H = 0, T_global = 0;
   int32_t rank = 0, world = 1;
   Session s;
-  DBuf O, Of, olist, send, pcnt, hubbuf;
+  DBuf O, Of, olist;               // remote staging (world > 1)
   Graph gin;                       // in-edges of owned objects (pull hops)
   bool can_pull = false;
-  int planned = 0;                 // hop whose bookkeeping th_shard_plan ran
-  int hop_mode[kMaxK + 2] = {};    // 0 push, 1 pull
+  double pull_divisor = 8.0;
+  // exchange region (peers write into it) and the peers' regions
+  uint8_t* xr = nullptr;
+  size_t xr_bytes = 0;
+  int64_t xcap = 0;                // inbox records
+  size_t off_keys = 0, off_bits = 0, off_hubs = 0;
+  std::vector<uint8_t*> peers;     // host copy of the peer bases ([world])
+  std::vector<bool> peer_ipc;      // opened through cudaIpcOpenMemHandle
+  uint8_t** d_peers = nullptr;     // device copy
   int W = 0;
   bool in_wave = false;
-  int next_hop = 0;
+  int next_hop = 0, next_phase = 0;
   int64_t rows() const { return n_local + H; }
 };
 
@@ -1720,6 +1728,50 @@ T* dcopy(const T* src, int64_t n, cudaStream_t st) {
   TH_CUDA(cudaMalloc(&p, sizeof(T) * std::max<int64_t>(n, 1)));
   if (n > 0) TH_CUDA(cudaMemcpyAsync(p, src, sizeof(T) * n, cudaMemcpyDeviceToDevice, st));
   return p;
+}
+
+// exchange region layout for an inbox of `cap` records and H hubs
+void shard_layout(Shard* sh, int64_t cap) {
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  sh->xcap = cap;
+  sh->off_keys = kXCtrlBytes;
+  sh->off_bits = up(sh->off_keys + sizeof(uint64_t) * (size_t)cap);
+  sh->off_hubs = up(sh->off_bits + sizeof(uint32_t) * (size_t)cap);
+  sh->xr_bytes = up(sh->off_hubs + sizeof(uint32_t) * (size_t)std::max<int64_t>(sh->H, 1) * 32);
+}
+
+void shard_alloc_region(Shard* sh, int64_t cap, cudaStream_t st) {
+  if (sh->xr) TH_CUDA(cudaFree(sh->xr));
+  sh->xr = nullptr;
+  shard_layout(sh, cap);
+  TH_CUDA(cudaMalloc(&sh->xr, sh->xr_bytes));
+  TH_CUDA(cudaMemsetAsync(sh->xr, 0, sh->xr_bytes, st));
+  TH_CUDA(cudaStreamSynchronize(st));  // (peers may map it right away)
+  sh->peers.assign(sh->world, nullptr);
+  sh->peer_ipc.assign(sh->world, false);
+  sh->peers[sh->rank] = sh->xr;
+}
+
+void shard_close_peers(Shard* sh) {
+  for (int d = 0; d < (int)sh->peers.size(); ++d)
+    if (sh->peer_ipc[d] && sh->peers[d]) cudaIpcCloseMemHandle(sh->peers[d]);
+  for (int d = 0; d < (int)sh->peers.size(); ++d) {
+    if (d != sh->rank) sh->peers[d] = nullptr;
+    sh->peer_ipc[d] = false;
+  }
+}
+
+bool shard_connected(const Shard* sh) {
+  for (uint8_t* p : sh->peers)
+    if (!p) return false;
+  return !sh->peers.empty();
+}
+
+// the kernels' copy of the peer table, once every peer is known
+void shard_publish_peers(Shard* sh) {
+  if (sh->d_peers && shard_connected(sh))
+    TH_CUDA(cudaMemcpy(sh->d_peers, sh->peers.data(), sizeof(uint8_t*) * sh->world,
+                       cudaMemcpyHostToDevice));
 }
 
 template <int W>
@@ -1760,6 +1812,11 @@ ShardArgs shard_args(Shard* sh) {
   sa.n_hubs = sh->H;
   sa.rank = sh->rank;
   sa.world = sh->world;
+  sa.px.base = sh->d_peers;
+  sa.px.cap = sh->xcap;
+  sa.px.off_keys = sh->off_keys;
+  sa.px.off_bits = sh->off_bits;
+  sa.px.off_hubs = sh->off_hubs;
   return sa;
 }
 
@@ -1809,23 +1866,27 @@ void shard_begin_w(Shard* sh, const th_query* q) {
   if (q->d_rel_masks) ensure<uint32_t>(s->M, std::max<int64_t>(sh->g.R, 1) * W, st);
   ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
   ensure<int64_t>(s->totals, kMaxWave, st);
-  const int64_t E = std::max<int64_t>(sh->E, 1);
-  if (sh->O.bytes < (size_t)E * W * 4) {
-    ensure<uint32_t>(sh->O, E * W, st);
-    TH_CUDA(cudaMemsetAsync(sh->O.p, 0, sh->O.bytes, st));
+  if (sh->world > 1) {
+    // remote staging, global-indexed (push pre-dedupe, pull frontier copy)
+    const int64_t E = std::max<int64_t>(sh->E, 1);
+    if (sh->O.bytes < (size_t)E * W * 4) {
+      ensure<uint32_t>(sh->O, E * W, st);
+      TH_CUDA(cudaMemsetAsync(sh->O.p, 0, sh->O.bytes, st));
+    }
+    if (sh->Of.bytes < (size_t)(ceil_div(E, 32) + 1) * 4) {
+      ensure<uint32_t>(sh->Of, ceil_div(E, 32) + 1, st);
+      TH_CUDA(cudaMemsetAsync(sh->Of.p, 0, sh->Of.bytes, st));
+    }
+    ensure<int32_t>(sh->olist, E, st);
   }
-  if (sh->Of.bytes < (size_t)(ceil_div(E, 32) + 1) * 4) {
-    ensure<uint32_t>(sh->Of, ceil_div(E, 32) + 1, st);
-    TH_CUDA(cudaMemsetAsync(sh->Of.p, 0, sh->Of.bytes, st));
-  }
-  ensure<int32_t>(sh->olist, E, st);
-  ensure<unsigned long long>(sh->pcnt, std::max(sh->world, 1), st);
-  ensure<uint32_t>(sh->hubbuf, std::max<int64_t>(sh->H, 1) * W, st);
   Ctl* ctl = static_cast<Ctl*>(s->ctl.p);
   TH_CUDA(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
   TH_CUDA(cudaMemsetAsync(s->Xf.p, 0, fwords * 4, st));
   TH_CUDA(cudaMemsetAsync(s->Nf.p, 0, fwords * 4, st));
   TH_CUDA(cudaMemsetAsync(s->Vf.p, 0, fwords * 4, st));
+  // own inbox empty, overflow flag down (peers send only after the barrier
+  // that follows this call)
+  TH_CUDA(cudaMemsetAsync(sh->xr, 0, 16, st));
   sh->next_hop = 0;
   ShardArgs sa = shard_args<W>(sh);
   if (q->d_rel_masks) {
@@ -1837,12 +1898,18 @@ void shard_begin_w(Shard* sh, const th_query* q) {
   shard_seed_kernel<W><<<grid_for((int64_t)q->n_queries * 32), kThreads, 0, st>>>(
       sa, q->d_seed_offsets, q->d_seeds);
   TH_LAUNCHED();
-  s->launches += 1;
+  shard_publish_cost_kernel<<<1, kMaxWorld, 0, st>>>(sa, 0);  // hop 1's frontier = the seeds
+  TH_LAUNCHED();
+  s->launches += 2;
   sh->next_hop = 1;
+  sh->next_phase = 0;
 }
 
+// phase 0: direction, edge counts, activated triples, then push (local
+// test-and-set + remote staging -> owners' inboxes) or pull (owned frontier
+// rows -> every inbox); the unchosen direction's kernels exit at once
 template <int W>
-void shard_expand_w(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_t** d_send) {
+void shard_send_w(Shard* sh, int h) {
   Session* s = &sh->s;
   cudaStream_t st = s->st;
   const th_query& q = s->last;
@@ -1852,12 +1919,12 @@ void shard_expand_w(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_
   ShardArgs sa = shard_args<W>(sh);
   sa.a.h = h;
   const unsigned pg = persistent_grid();
-  if (sh->planned != h) {
-    begin_hop_kernel<<<1, 1, 0, st>>>(b.ctl, h, sh->g.T, 0.0, 0);
+  {
+    ProfScope ps(s, TH_PROF_SETUP);
+    shard_begin_hop_kernel<<<1, 1, 0, st>>>(sa, h, sh->T_global, sh->pull_divisor, sh->can_pull ? 1 : 0);
     TH_LAUNCHED();
+    s->launches += 1;
   }
-  sh->hop_mode[h] = mode;
-  TH_CUDA(cudaMemsetAsync(&b.ctl->olen, 0, sizeof(int32_t), st));
   int64_t* e_out = static_cast<int64_t*>(s->edges.p) + (h - 1) * B;
   {
     ProfScope ps(s, TH_PROF_EDGES);
@@ -1881,26 +1948,6 @@ void shard_expand_w(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_
                            static_cast<int64_t*>(s->a_len.p) + (h - 1) * B,
                            static_cast<int32_t*>(s->a_ids.p), s->a_cap, &b.ctl->act_used);
   }
-  if (mode == 1) {
-    // pull hop: publish the owned frontier rows (same records for every rank)
-    const int32_t one = 1;
-    TH_CUDA(cudaMemcpyAsync(&b.ctl->mode[h], &one, sizeof(int32_t), cudaMemcpyHostToDevice, st));
-    unsigned long long* pc = static_cast<unsigned long long*>(sh->pcnt.p);
-    TH_CUDA(cudaMemsetAsync(pc, 0, sizeof(unsigned long long), st));
-    shard_frontier_pack_kernel<W, false><<<pg, kThreads, 0, st>>>(sa, h - 1, sh->l2g, pc, nullptr);
-    TH_LAUNCHED();
-    unsigned long long tot = 0;
-    TH_CUDA(cudaMemcpyAsync(&tot, pc, sizeof(tot), cudaMemcpyDeviceToHost, st));
-    TH_CUDA(cudaStreamSynchronize(st));
-    uint64_t* send = ensure<uint64_t>(sh->send, (int64_t)std::max<unsigned long long>(tot, 1), st);
-    TH_CUDA(cudaMemsetAsync(pc, 0, sizeof(unsigned long long), st));
-    shard_frontier_pack_kernel<W, true><<<pg, kThreads, 0, st>>>(sa, h - 1, sh->l2g, pc, send);
-    TH_LAUNCHED();
-    s->launches += 2;
-    for (int d = 0; d < sh->world; ++d) h_counts[d] = (int64_t)tot;
-    *d_send = send;
-    return;
-  }
   {
     ProfScope ps(s, TH_PROF_PUSH);
     const int sem = q.semantics == TH_EXACT ? TH_EXACT : TH_FRONTIER;
@@ -1919,122 +1966,98 @@ void shard_expand_w(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_
     }
 #undef TH_SHARD_PUSH
     s->launches += 3;  // light, heavy-chunk scan, heavy
+    if (sh->world > 1) {
+      shard_send_kernel<W><<<pg, kThreads, 0, st>>>(sa);
+      TH_LAUNCHED();
+      shard_frontier_send_kernel<W><<<pg, kThreads, 0, st>>>(sa, h - 1, sh->l2g);
+      TH_LAUNCHED();
+      s->launches += 2;
+    }
   }
-  // pack: per-owner totals -> host -> offsets -> records
-  const int G = sh->world;
-  unsigned long long* pc = static_cast<unsigned long long*>(sh->pcnt.p);
-  TH_CUDA(cudaMemsetAsync(pc, 0, sizeof(unsigned long long) * G, st));
-  shard_pack_kernel<W, false><<<pg, kThreads, 0, st>>>(sa, pc, nullptr);
-  TH_LAUNCHED();
-  std::vector<unsigned long long> cnt(G);
-  TH_CUDA(cudaMemcpyAsync(cnt.data(), pc, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost, st));
-  TH_CUDA(cudaStreamSynchronize(st));
-  std::vector<unsigned long long> off(G);
-  unsigned long long tot = 0;
-  for (int d = 0; d < G; ++d) {
-    off[d] = tot;
-    tot += cnt[d];
-    h_counts[d] = (int64_t)cnt[d];
-  }
-  uint64_t* send = ensure<uint64_t>(sh->send, (int64_t)std::max<unsigned long long>(tot, 1), st);
-  TH_CUDA(cudaMemcpyAsync(pc, off.data(), sizeof(unsigned long long) * G, cudaMemcpyHostToDevice, st));
-  shard_pack_kernel<W, true><<<pg, kThreads, 0, st>>>(sa, pc, send);
-  TH_LAUNCHED();
-  // (a pageable H2D copy is staged before cudaMemcpyAsync returns, so the
-  // host temporary `off` may go out of scope without a sync)
-  s->launches += 3;
-  *d_send = send;
 }
 
+// phase 1: apply what the peers sent (push: inbox records; pull: staged
+// frontier + pull over the owned in-edges), empty the inbox, publish the
+// owned hubs' next-layer rows
 template <int W>
-void shard_absorb_w(Shard* sh, int h, const uint64_t* recs, int64_t n) {
+void shard_receive_w(Shard* sh, int h) {
   Session* s = &sh->s;
+  cudaStream_t st = s->st;
   ShardArgs sa = shard_args<W>(sh);
   sa.a.h = h;
-  if (sh->hop_mode[h] == 1) {
-    // pull hop: all ranks' frontier rows (+ local hub rows) -> global staging,
-    // pull over the owned in-edges, then undo the staging
-    cudaStream_t st = s->st;
-    const unsigned grid = persistent_grid();
-    shard_gather_frontier_kernel<W><<<grid, kThreads, 0, st>>>(sa, h - 1, recs, n);
+  const unsigned pg = persistent_grid();
+  const bool filter = s->last.d_rel_masks != nullptr;
+  const int sem = s->last.semantics;
+  if (sh->world > 1) {
+    ProfScope ps(s, TH_PROF_PUSH);
+    if (sem == TH_EXACT) shard_absorb_kernel<W, TH_EXACT><<<pg, kThreads, 0, st>>>(sa);
+    else shard_absorb_kernel<W, TH_FRONTIER><<<pg, kThreads, 0, st>>>(sa);
     TH_LAUNCHED();
+    s->launches += 1;
+  }
+  if (sh->can_pull) {
+    ProfScope ps(s, TH_PROF_PULL);
     WaveArgs pa = sa.a;
-    pa.X = sa.O;
-    pa.Xf = sa.Of;
+    if (sh->world > 1) {
+      shard_gather_frontier_kernel<W><<<pg, kThreads, 0, st>>>(sa, h - 1);
+      TH_LAUNCHED();
+      pa.X = sa.O;
+      pa.Xf = sa.Of;
+      s->launches += 1;
+    }
+    // (one rank: the frontier is X itself, global rows = local rows)
     pa.rsrc = sh->gin.rsrc;
     pa.rrel = sh->gin.rrel;
     pa.item_v = sh->gin.item_v;
     pa.item_lo = sh->gin.item_lo;
     pa.item_hi = sh->gin.item_hi;
     pa.n_items = sh->gin.n_items;
-    const unsigned pg = persistent_grid();
-    const bool filter = s->last.d_rel_masks != nullptr;
-    {
-      ProfScope ps(s, TH_PROF_PULL);
-      const bool scr = pull_screens(&sh->gin, s->pull_screen);
+    const bool scr = pull_screens(&sh->gin, s->pull_screen);
 #define TH_SHARD_PULL(SEM, F)                                                          \
   if (scr) pull_kernel<W, SEM, F, true><<<pg, kThreads, 0, st>>>(pa);                  \
   else pull_kernel<W, SEM, F, false><<<pg, kThreads, 0, st>>>(pa);
-      if (s->last.semantics == TH_EXACT) {
-        if (filter) { TH_SHARD_PULL(TH_EXACT, true) } else { TH_SHARD_PULL(TH_EXACT, false) }
-      } else {
-        if (filter) { TH_SHARD_PULL(TH_FRONTIER, true) } else { TH_SHARD_PULL(TH_FRONTIER, false) }
-      }
-#undef TH_SHARD_PULL
-      TH_LAUNCHED();
+    if (sem == TH_EXACT) {
+      if (filter) { TH_SHARD_PULL(TH_EXACT, true) } else { TH_SHARD_PULL(TH_EXACT, false) }
+    } else {
+      if (filter) { TH_SHARD_PULL(TH_FRONTIER, true) } else { TH_SHARD_PULL(TH_FRONTIER, false) }
     }
-    shard_clear_frontier_kernel<W><<<grid, kThreads, 0, st>>>(sa, h - 1, recs, n);
+#undef TH_SHARD_PULL
     TH_LAUNCHED();
-    TH_CUDA(cudaMemsetAsync(sa.Of, 0, (size_t)(ceil_div(sh->E, 32) + 1) * 4, st));
-    s->launches += 3;
-    return;
+    s->launches += 1;
+    if (sh->world > 1) {
+      shard_clear_frontier_kernel<W><<<pg, kThreads, 0, st>>>(sa, h - 1);
+      TH_LAUNCHED();
+      s->launches += 1;
+    }
   }
-  if (n > 0) {
-    const int sem = s->last.semantics;
-    const unsigned grid = grid_for(n);
-    if (sem == TH_EXACT) shard_absorb_kernel<W, TH_EXACT><<<grid, kThreads, 0, s->st>>>(sa, recs, n);
-    else shard_absorb_kernel<W, TH_FRONTIER><<<grid, kThreads, 0, s->st>>>(sa, recs, n);
+  shard_inbox_reset_kernel<<<1, 32, 0, st>>>(sa);
+  TH_LAUNCHED();
+  s->launches += 1;
+  if (h < s->last.k && sh->H > 0) {  // the last layer is never expanded
+    shard_hub_out_kernel<W><<<grid_for(sh->H * W), kThreads, 0, st>>>(sa);
     TH_LAUNCHED();
     s->launches += 1;
   }
 }
 
+// phase 2: hub frontier rows from the board, K4 over the owned rows, retire
+// X, publish the new layer's cost
 template <int W>
-uint32_t* shard_hub_rows_w(Shard* sh, int h) {
-  Session* s = &sh->s;
-  ShardArgs sa = shard_args<W>(sh);
-  sa.a.h = h;
-  uint32_t* buf = static_cast<uint32_t*>(sh->hubbuf.p);
-  if (sh->H > 0) {
-    shard_hub_out_kernel<W><<<grid_for(sh->H * W), kThreads, 0, s->st>>>(sa, buf);
-    TH_LAUNCHED();
-    s->launches += 1;
-  }
-  return buf;
-}
-
-template <int W>
-void shard_hub_merge_w(Shard* sh, int h) {
-  Session* s = &sh->s;
-  ShardArgs sa = shard_args<W>(sh);
-  sa.a.h = h;
-  if (sh->H > 0) {
-    shard_hub_in_kernel<W><<<grid_for(sh->H), kThreads, 0, s->st>>>(
-        sa, static_cast<const uint32_t*>(sh->hubbuf.p));
-    TH_LAUNCHED();
-    s->launches += 1;
-  }
-}
-
-template <int W>
-void shard_end_hop_w(Shard* sh, int h) {
+void shard_end_w(Shard* sh, int h) {
   Session* s = &sh->s;
   cudaStream_t st = s->st;
   const th_query& q = s->last;
   const int64_t B = q.n_queries;
   WaveBufs b = shard_bufs<W>(sh);
+  ShardArgs sa = shard_args<W>(sh);
+  sa.a.h = h;
   const int64_t rows = std::max<int64_t>(sh->rows(), 1);
   const int64_t fwords = ceil_div(rows, 32) + 1;
+  if (h < q.k && sh->H > 0) {
+    shard_hub_in_kernel<W><<<grid_for(sh->H), kThreads, 0, st>>>(sa);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
   if (q.flags & TH_WANT_FRONTIERS) {
     ProfScope ps(s, TH_PROF_FRONTIER);
     int64_t* f_off = static_cast<int64_t*>(s->f_off.p) + (h - 1) * B;
@@ -2053,9 +2076,13 @@ void shard_end_hop_w(Shard* sh, int h) {
     TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
     s->launches += 1;
   }
+  if (h < q.k) {
+    shard_publish_cost_kernel<<<1, kMaxWorld, 0, st>>>(sa, h);
+    TH_LAUNCHED();
+    s->launches += 1;
+  }
   std::swap(s->X, s->N);
   std::swap(s->Xf, s->Nf);
-  sh->next_hop = h + 1;
 }
 
 template <int W>
@@ -2095,12 +2122,17 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
                  int64_t T, int64_t E, int64_t R, const int32_t* d_lidx,
                  const int32_t* d_hub_index, const int32_t* d_hub_ids, int64_t H,
                  const int32_t* d_l2g, int64_t n_local, int32_t rank, int32_t world,
-                 cudaStream_t st) {
+                 int64_t inbox_records, cudaStream_t st) {
+  if (world > kMaxWorld) {
+    set_error("world above " + std::to_string(kMaxWorld) + " ranks");
+    return TH_ERR_INVALID;
+  }
   auto* sh = new Shard();
   *out = sh;
   sh->E = E;
   sh->n_local = n_local;
   sh->H = H;
+  sh->T_global = T;
   sh->rank = rank;
   sh->world = world;
   sh->lidx = dcopy(d_lidx, E, st);
@@ -2146,9 +2178,9 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
     cudaFree(bsum);
     return rc;
   }
-  // in-edges of the owned objects (global sources) for pull hops: records
-  // key (gid * W + word) must fit 32 bits for W = 32
-  if (E * 32 < (int64_t(1) << 32) && T > 0) {
+  // in-edges of the owned objects (global sources) for pull hops; pull
+  // records carry 64-bit keys, so every graph size qualifies
+  if (T > 0) {
     shard_select_in_kernel<<<grid_for(T), kThreads, 0, st>>>(d_obj, T, sh->lidx, rank, world, key);
     TH_LAUNCHED();
     shard_count_kernel<<<nb, kCompactThreads, 0, st>>>(key, T, bsum);
@@ -2181,6 +2213,9 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
   }
   cudaFree(key);
   cudaFree(bsum);
+  TH_CUDA(cudaMalloc(&sh->d_peers, sizeof(uint8_t*) * world));
+  shard_alloc_region(sh, std::max<int64_t>(inbox_records, 1024), st);
+  shard_publish_peers(sh);  // (one rank: connected to itself already)
   Session* s = &sh->s;
   s->g = &sh->g;
   s->st = st;
@@ -2192,6 +2227,57 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
 }
 
 int64_t shard_local_triples(const Shard* sh) { return sh->g.T; }
+
+int shard_region(const Shard* sh, void** base, uint64_t* bytes, int64_t* records) {
+  *base = sh->xr;
+  *bytes = sh->xr_bytes;
+  if (records) *records = sh->xcap;
+  return TH_OK;
+}
+
+int shard_ipc_handle(const Shard* sh, void* out64) {
+  cudaIpcMemHandle_t h;
+  TH_CUDA(cudaIpcGetMemHandle(&h, sh->xr));
+  static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+  std::memcpy(out64, &h, sizeof(h));
+  return TH_OK;
+}
+
+int shard_connect(Shard* sh, int32_t peer, void* base, bool ipc) {
+  if (peer < 0 || peer >= sh->world) {
+    set_error("peer rank out of range");
+    return TH_ERR_INVALID;
+  }
+  if (peer == sh->rank) {
+    if (base != sh->xr) {
+      set_error("a shard's own region is its own");
+      return TH_ERR_INVALID;
+    }
+  } else {
+    if (sh->peer_ipc[peer] && sh->peers[peer]) cudaIpcCloseMemHandle(sh->peers[peer]);
+    sh->peers[peer] = static_cast<uint8_t*>(base);
+    sh->peer_ipc[peer] = ipc;
+  }
+  shard_publish_peers(sh);
+  return TH_OK;
+}
+
+int shard_ipc_open(Shard* sh, int32_t peer, const void* handle64) {
+  if (peer == sh->rank) return shard_connect(sh, peer, sh->xr, false);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof(h));
+  void* p = nullptr;
+  TH_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  return shard_connect(sh, peer, p, true);
+}
+
+int shard_grow_inbox(Shard* sh, int64_t records) {
+  if (records <= sh->xcap) return TH_OK;
+  shard_close_peers(sh);
+  shard_alloc_region(sh, records, sh->s.st);
+  shard_publish_peers(sh);
+  return TH_OK;
+}
 
 int shard_begin(Shard* sh, const th_query* q) {
   Session* s = &sh->s;
@@ -2216,6 +2302,10 @@ int shard_begin(Shard* sh, const th_query* q) {
     set_error("path reconstruction is not available on partitioned graphs");
     return TH_ERR_INVALID;
   }
+  if (!shard_connected(sh)) {
+    set_error("exchange regions of the peers are not connected (th_shard_connect / th_shard_ipc_open)");
+    return TH_ERR_STATE;
+  }
   cudaStream_t st = s->st;
   const int64_t B = q->n_queries, k = q->k;
   const int64_t kb = std::max<int64_t>(k * B, 1);
@@ -2231,79 +2321,31 @@ int shard_begin(Shard* sh, const th_query* q) {
   s->last = *q;
   s->has_run = true;
   sh->W = pick_words((int)std::max<int64_t>(B, 1));
-  if ((sh->rows() + 1) * (int64_t)sh->W >= (int64_t(1) << 32)) {
-    set_error("shard too large for 32-bit exchange keys (rows * W >= 2^32)");
-    return TH_ERR_INVALID;
-  }
   sh->in_wave = true;
   TH_W_DISPATCH(sh->W, shard_begin_w<WW>(sh, q));
   return TH_OK;
 }
 
-static int shard_check_hop(Shard* sh, int h) {
+int shard_hop(Shard* sh, int h, int phase) {
   if (!sh->in_wave) {
     set_error("no wave in progress (th_shard_begin first)");
     return TH_ERR_STATE;
   }
-  if (h != sh->next_hop || h > sh->s.last.k) {
-    set_error("hop out of sequence");
+  if (h != sh->next_hop || h > sh->s.last.k || phase != sh->next_phase) {
+    set_error("hop or phase out of sequence");
     return TH_ERR_STATE;
   }
-  return TH_OK;
-}
-
-int shard_plan(Shard* sh, int h, int64_t* h_cost) {
-  if (int rc = shard_check_hop(sh, h)) return rc;
-  Session* s = &sh->s;
-  Ctl* ctl = static_cast<Ctl*>(s->ctl.p);
-  begin_hop_kernel<<<1, 1, 0, s->st>>>(ctl, h, sh->g.T, 0.0, 0);
-  TH_LAUNCHED();
-  unsigned long long c = 0;
-  TH_CUDA(cudaMemcpyAsync(&c, &ctl->push_cost[h - 1], sizeof(c), cudaMemcpyDeviceToHost, s->st));
-  TH_CUDA(cudaStreamSynchronize(s->st));
-  *h_cost = (int64_t)c;
-  sh->planned = h;
-  return TH_OK;
-}
-
-int shard_expand(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_t** d_send) {
-  if (int rc = shard_check_hop(sh, h)) return rc;
-  if (mode == 1 && !sh->can_pull) {
-    set_error("this shard has no in-edge index for pull hops");
-    return TH_ERR_INVALID;
-  }
-  TH_W_DISPATCH(sh->W, shard_expand_w<WW>(sh, h, mode, h_counts, d_send));
+  if (phase == 0) TH_W_DISPATCH(sh->W, shard_send_w<WW>(sh, h))
+  else if (phase == 1) TH_W_DISPATCH(sh->W, shard_receive_w<WW>(sh, h))
+  else TH_W_DISPATCH(sh->W, shard_end_w<WW>(sh, h))
+  sh->next_phase = (phase + 1) % 3;
+  if (phase == 2) sh->next_hop = h + 1;
   return TH_OK;
 }
 
 int shard_can_pull(const Shard* sh) { return sh->can_pull ? 1 : 0; }
 
-int shard_absorb(Shard* sh, int h, const uint64_t* d_recv, int64_t n) {
-  if (int rc = shard_check_hop(sh, h)) return rc;
-  TH_W_DISPATCH(sh->W, shard_absorb_w<WW>(sh, h, d_recv, n));
-  return TH_OK;
-}
-
-int shard_hub_rows(Shard* sh, int h, uint32_t** d_rows, int64_t* words) {
-  if (int rc = shard_check_hop(sh, h)) return rc;
-  uint32_t* p = nullptr;
-  TH_W_DISPATCH(sh->W, p = shard_hub_rows_w<WW>(sh, h));
-  *d_rows = p;
-  *words = sh->H * sh->W;
-  return TH_OK;
-}
-
-int shard_hub_merge(Shard* sh, int h) {
-  if (int rc = shard_check_hop(sh, h)) return rc;
-  TH_W_DISPATCH(sh->W, shard_hub_merge_w<WW>(sh, h));
-  return TH_OK;
-}
-
-int shard_end_hop(Shard* sh, int h) {
-  if (int rc = shard_check_hop(sh, h)) return rc;
-  TH_W_DISPATCH(sh->W, shard_end_hop_w<WW>(sh, h));
-  return TH_OK;
-}
+void shard_set_pull_divisor(Shard* sh, double d) { sh->pull_divisor = d; }
 
 int shard_finish(Shard* sh, th_result* out) {
   if (!sh->in_wave || sh->next_hop != sh->s.last.k + 1) {
@@ -2312,19 +2354,56 @@ int shard_finish(Shard* sh, th_result* out) {
   }
   TH_W_DISPATCH(sh->W, shard_retire_w<WW>(sh));
   sh->in_wave = false;
-  return session_finish(&sh->s, out);
+  const int rc = session_finish(&sh->s, out);
+  XCtrl xc;
+  TH_CUDA(cudaMemcpy(&xc, sh->xr, sizeof(XCtrl), cudaMemcpyDeviceToHost));
+  if (xc.overflow) {
+    // the inbox must grow: every rank reallocates and reconnects, then the
+    // wave runs again (th_shard_grow_inbox)
+    set_error("exchange inbox overflowed; grow it and run the wave again");
+    return TH_ERR_OVERFLOW;
+  }
+  return rc;
+}
+
+int shard_columns(const Shard* sh, th_shard_cols* out) {
+  out->n_triples = sh->g.T;
+  out->n_local = sh->n_local;
+  out->n_hubs = sh->H;
+  out->subj_row = sh->g.subj;
+  out->rel = sh->g.rel;
+  out->obj = sh->g.obj;
+  out->tid_l2g = sh->tid_l2g;
+  out->l2g = sh->l2g;
+  out->hub_ids = sh->hub_ids;
+  return TH_OK;
+}
+
+int shard_sent(Shard* sh, int64_t* per_hop, int n) {
+  TH_CUDA(cudaStreamSynchronize(sh->s.st));
+  Ctl c;
+  TH_CUDA(cudaMemcpy(&c, sh->s.ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) per_hop[i] = i + 1 <= sh->s.last.k ? (int64_t)c.sent[i + 1] : 0;
+  return TH_OK;
+}
+
+int shard_inbox_overflowed(const Shard* sh) {
+  XCtrl xc;
+  if (cudaMemcpy(&xc, sh->xr, sizeof(XCtrl), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  return xc.overflow ? 1 : 0;
 }
 
 Session* shard_session(Shard* sh) { return &sh->s; }
 
 void shard_free(Shard* sh) {
   session_free(&sh->s);
-  for (DBuf* d : {&sh->O, &sh->Of, &sh->olist, &sh->send, &sh->pcnt, &sh->hubbuf}) {
+  shard_close_peers(sh);
+  for (DBuf* d : {&sh->O, &sh->Of, &sh->olist}) {
     if (d->p) cudaFree(d->p);
     d->p = nullptr;
   }
   for (void* p : {(void*)sh->tid_l2g, (void*)sh->lidx, (void*)sh->hub_index, (void*)sh->hub_ids,
-                  (void*)sh->l2g})
+                  (void*)sh->l2g, (void*)sh->xr, (void*)sh->d_peers})
     if (p) cudaFree(p);
   graph_free(&sh->g);
   graph_free(&sh->gin);

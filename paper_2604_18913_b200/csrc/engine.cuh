@@ -17,6 +17,7 @@ struct Ctl {
   int32_t list_len[kMaxK + 2];
   int64_t list_off[kMaxK + 2];
   unsigned long long push_cost[kMaxK + 2];
+  unsigned long long sent[kMaxK + 2];  // shards: records written to other ranks' inboxes per hop
   int32_t mode[kMaxK + 2];  // 0 = push, 1 = pull
   int32_t dense[kMaxK + 2]; // pull hop over a frontier that sources most in-edges
   int32_t heavy_len;
@@ -133,17 +134,21 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
                  int64_t T, int64_t E, int64_t R, const int32_t* d_lidx,
                  const int32_t* d_hub_index, const int32_t* d_hub_ids, int64_t H,
                  const int32_t* d_l2g, int64_t n_local, int32_t rank, int32_t world,
-                 cudaStream_t st);
+                 int64_t inbox_records, cudaStream_t st);
 int64_t shard_local_triples(const Shard* sh);
+int shard_region(const Shard* sh, void** base, uint64_t* bytes, int64_t* records);
+int shard_ipc_handle(const Shard* sh, void* out64);
+int shard_connect(Shard* sh, int32_t peer, void* base, bool ipc);
+int shard_ipc_open(Shard* sh, int32_t peer, const void* handle64);
+int shard_grow_inbox(Shard* sh, int64_t records);
+int shard_inbox_overflowed(const Shard* sh);
+void shard_set_pull_divisor(Shard* sh, double d);
 int shard_begin(Shard* sh, const th_query* q);
-int shard_plan(Shard* sh, int h, int64_t* h_cost);
-int shard_expand(Shard* sh, int h, int mode, int64_t* h_counts, const uint64_t** d_send);
+int shard_hop(Shard* sh, int h, int phase);
 int shard_can_pull(const Shard* sh);
-int shard_absorb(Shard* sh, int h, const uint64_t* d_recv, int64_t n);
-int shard_hub_rows(Shard* sh, int h, uint32_t** d_rows, int64_t* words);
-int shard_hub_merge(Shard* sh, int h);
-int shard_end_hop(Shard* sh, int h);
 int shard_finish(Shard* sh, th_result* out);
+int shard_sent(Shard* sh, int64_t* per_hop, int n);
+int shard_columns(const Shard* sh, th_shard_cols* out);
 Session* shard_session(Shard* sh);
 void shard_free(Shard* sh);
 

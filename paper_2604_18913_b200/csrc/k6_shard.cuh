@@ -9,21 +9,63 @@
 // out-degree entities) are the exception to subject cohesion: their rows
 // are edge-split over all ranks (triple t of a hub lives on rank
 // hash(t) mod world), and a hub in the frontier is expanded by every rank on
-// its slice.  Per hop, for one wave of <= 1024 queries:
-//   expand   push over the local frontier rows + the hub slices; targets
-//            owned here are test-and-set directly (as in K2); others are
-//            OR-ed into a staging matrix O (global rows) -- the local
-//            pre-dedupe, every (query, target) pair leaves a rank at most
-//            once per hop
-//   pack     staged rows -> (row-at-owner * W + word, bits) records bucketed
-//            by owner rank; the host exchanges them (NCCL all-to-all)
-//   absorb   received records are test-and-set like local targets
-//   hubs     owners publish their hubs' next-layer rows; the host sums the
-//            [hubs][W] buffer over ranks (one owner per hub, so the sum is
-//            the row) and every rank installs them as hub frontier rows
-//   end      K4 over the owned rows (ids mapped to global), retire X.
+// its slice.
+//
+// Exchange: every rank owns an exchange region in its HBM -- control words
+// (inbox cursor, overflow flag, the ranks' published frontier costs), an
+// inbox of (int64 key, uint32 bits) records and a hub-row board -- and its
+// peers WRITE INTO IT DIRECTLY: remote atomics reserve inbox space, plain
+// stores deliver records, costs and hub rows (NVLink P2P within a box; the
+// regions of other processes are CUDA-IPC mappings; on one device, plain
+// pointers).  Nothing is read back to the host during a wave.  A hop runs in
+// three phases separated by a barrier across ranks (the peers' writes of
+// the previous phase are complete):
+//   0 send     direction from the published costs (pull when the summed
+//              frontier out-edges exceed T / pull_divisor, as K2/K3);
+//              push: expand the local frontier rows + hub slices, owned
+//              targets test-and-set directly, remote ones OR-ed into the
+//              staging matrix O (each (query, target) leaves a rank at most
+//              once per hop), then staged rows -> records in the owners'
+//              inboxes; pull: the owned frontier rows -> records in EVERY
+//              rank's inbox (an all-gather)
+//   1 receive  push: test-and-set the inbox records; pull: stage the
+//              gathered frontier (global rows), pull over the owned
+//              in-edges; owners write their hubs' next-layer rows onto
+//              every rank's hub board
+//   2 end      install the hub frontier rows, K4 over the owned rows (ids
+//              mapped to global), retire X, publish the new layer's cost
 // Local row space: [0, n_local) owned entities in ascending id order, then
 // [n_local, n_local + n_hubs) hub slices.
+#pragma once
+
+constexpr int kMaxWorld = 64;
+
+// control words at the start of every exchange region
+struct XCtrl {
+  unsigned long long cursor;            // inbox records appended this hop
+  unsigned int overflow;                // an append did not fit the inbox (sticky per wave)
+  unsigned int pad;
+  unsigned long long cost[kMaxWorld];   // frontier out-edge totals published by each rank
+};
+constexpr size_t kXCtrlBytes = 1024;
+static_assert(sizeof(XCtrl) <= kXCtrlBytes, "control block");
+
+// the peers' exchange regions as this rank's kernels see them
+struct XPeers {
+  uint8_t* const* base;  // [world] device base addresses (own included)
+  int64_t cap;           // inbox records per region
+  size_t off_keys, off_bits, off_hubs;
+  __device__ __forceinline__ XCtrl* ctrl(int d) const { return reinterpret_cast<XCtrl*>(base[d]); }
+  __device__ __forceinline__ uint64_t* keys(int d) const {
+    return reinterpret_cast<uint64_t*>(base[d] + off_keys);
+  }
+  __device__ __forceinline__ uint32_t* bits(int d) const {
+    return reinterpret_cast<uint32_t*>(base[d] + off_bits);
+  }
+  __device__ __forceinline__ uint32_t* hubs(int d) const {
+    return reinterpret_cast<uint32_t*>(base[d] + off_hubs);
+  }
+};
 
 struct ShardArgs {
   WaveArgs a;              // local rows = n_local + n_hubs
@@ -36,6 +78,7 @@ struct ShardArgs {
   int32_t* olen;
   int64_t E_global, n_local, n_hubs;
   int32_t rank, world;
+  XPeers px;
 };
 
 __device__ __forceinline__ int32_t owner_of(int64_t v, int32_t world) {
@@ -166,6 +209,7 @@ __device__ __forceinline__ void shard_row_pairs(const ShardArgs& sa, int32_t u, 
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) shard_push_light_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
+  if (a.ctl->mode[a.h] != 0) return;
   __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
   WarpAppender app{abuf[threadIdx.x >> 5]};
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -188,6 +232,7 @@ __global__ void __launch_bounds__(kThreads) shard_push_light_kernel(ShardArgs sa
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
+  if (a.ctl->mode[a.h] != 0) return;
   __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
   WarpAppender app{abuf[threadIdx.x >> 5]};
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -225,14 +270,28 @@ __global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa
   app.finish(a);
 }
 
-// staged rows -> records bucketed by owner.  COUNT: per-owner record totals
-// into cnt[world]; WRITE: records at cursor[owner] (pre-set to the owner's
-// exclusive offset), staged rows and flags cleared.  Warp-aggregated: one
-// atomic per (warp, owner).
-template <int W, bool WRITE>
-__global__ void __launch_bounds__(kThreads) shard_pack_kernel(ShardArgs sa,
-                                                              unsigned long long* cnt_or_cursor,
-                                                              uint64_t* send) {
+// reserve n records in rank d's inbox; returns the first slot (records at or
+// beyond the capacity are dropped and flag the receiver's overflow)
+__device__ __forceinline__ unsigned long long inbox_reserve(const XPeers& px, int d, int n) {
+  return atomicAdd(&px.ctrl(d)->cursor, (unsigned long long)n);
+}
+
+__device__ __forceinline__ void inbox_put(const XPeers& px, int d, unsigned long long at, uint64_t key,
+                                          uint32_t bits) {
+  if ((int64_t)at < px.cap) {
+    px.keys(d)[at] = key;
+    px.bits(d)[at] = bits;
+  } else {
+    px.ctrl(d)->overflow = 1u;
+  }
+}
+
+// staged rows -> records ((row_at_owner * W + word), bits) written straight
+// into the owners' inboxes (warp-aggregated: one remote atomic per (warp,
+// owner)); staged rows and flags are cleared behind
+template <int W>
+__global__ void __launch_bounds__(kThreads) shard_send_kernel(ShardArgs sa) {
+  if (sa.a.ctl->mode[sa.a.h] != 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -251,10 +310,12 @@ __global__ void __launch_bounds__(kThreads) shard_pack_kernel(ShardArgs sa,
         nzc += words[j] != 0u;
       }
     }
-    for (int d = 0; d < sa.world; ++d) {
-      const bool mine = dest == d;
-      const unsigned m = __ballot_sync(TH_FULL, mine && nzc > 0);
-      if (!m) continue;
+    unsigned pending = __ballot_sync(TH_FULL, dest >= 0 && nzc > 0);
+    while (pending) {
+      // one owner per round: the lanes bound for it append together
+      const int d = __shfl_sync(TH_FULL, dest, __ffs(pending) - 1);
+      const bool mine = dest == d && nzc > 0;
+      pending &= ~__ballot_sync(TH_FULL, mine);
       int incl = mine ? nzc : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -263,17 +324,20 @@ __global__ void __launch_bounds__(kThreads) shard_pack_kernel(ShardArgs sa,
       }
       const int tot = __shfl_sync(TH_FULL, incl, 31);
       unsigned long long b0 = 0;
-      if (lane == 0) b0 = atomicAdd(&cnt_or_cursor[d], (unsigned long long)tot);
+      if (lane == 0) {
+        b0 = inbox_reserve(sa.px, d, tot);
+        if (d != sa.rank) atomicAdd(&sa.a.ctl->sent[sa.a.h], (unsigned long long)tot);
+      }
       b0 = __shfl_sync(TH_FULL, b0, 0);
-      if (WRITE && mine) {
-        uint64_t o = b0 + (uint64_t)(incl - nzc);
+      if (mine) {
+        unsigned long long o = b0 + (unsigned long long)(incl - nzc);
         const uint64_t key0 = (uint64_t)sa.lidx[v] * W;
 #pragma unroll
         for (int j = 0; j < W; ++j)
-          if (words[j]) send[o++] = ((key0 + j) << 32) | words[j];
+          if (words[j]) inbox_put(sa.px, d, o++, key0 + j, words[j]);
       }
     }
-    if (WRITE && v >= 0) {
+    if (v >= 0) {
 #pragma unroll
       for (int j = 0; j < W; ++j) sa.O[(size_t)v * W + j] = 0u;
       atomicAnd(&sa.Of[v >> 5], ~(1u << (v & 31)));
@@ -281,15 +345,18 @@ __global__ void __launch_bounds__(kThreads) shard_pack_kernel(ShardArgs sa,
   }
 }
 
-// received records -> local test-and-set, appended to the hop's list
+// this rank's inbox records -> local test-and-set, appended to the hop's list
 template <int W, int SEM>
-__global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa,
-                                                                const uint64_t* __restrict__ recs,
-                                                                int64_t n) {
+__global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
+  if (a.ctl->mode[a.h] != 0) return;
   const int lane = threadIdx.x & 31;
   __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
   WarpAppender app{abuf[threadIdx.x >> 5]};
+  const XCtrl* xc = sa.px.ctrl(sa.rank);
+  const int64_t n = (int64_t)min(xc->cursor, (unsigned long long)sa.px.cap);
+  const uint64_t* keys = sa.px.keys(sa.rank);
+  const uint32_t* bits = sa.px.bits(sa.rank);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t base = gw * 32; base < n; base += nw * 32) {
@@ -297,13 +364,13 @@ __global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa,
     bool fresh = false;
     int32_t row = 0;
     if (i < n) {
-      const uint64_t rec = recs[i];
-      const uint32_t key = (uint32_t)(rec >> 32);
+      const uint64_t key = keys[i];
       row = (int32_t)(key / W);
-      if (row >= sa.n_local) {
+      if (key / W >= (uint64_t)sa.n_local) {
         a.ctl->err = 2;  // malformed record: not an owned row
+        row = 0;
       } else {
-        fresh = local_set<W, SEM>(a, row, (int)(key % W), (uint32_t)rec);
+        fresh = local_set<W, SEM>(a, row, (int)(key % W), bits[i]);
       }
     }
     app.add(a, fresh, row);
@@ -311,24 +378,61 @@ __global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa,
   app.finish(a);
 }
 
-// owners publish their hubs' next-layer rows ([n_hubs][W], zero elsewhere)
+// hop h begins: the ranks' published frontier costs decide push or pull
+// (every rank sees the same costs, so all choose alike); list segment h
+__global__ void shard_begin_hop_kernel(ShardArgs sa, int h, int64_t T_global, double pull_divisor,
+                                       int can_pull) {
+  Ctl* ctl = sa.a.ctl;
+  const int32_t prev = ctl->list_len[h - 1];
+  ctl->list_off[h] = ctl->list_off[h - 1] + prev;
+  ctl->list_len[h] = 0;
+  ctl->push_cost[h] = 0;
+  ctl->heavy_len = 0;
+  ctl->olen = 0;
+  const XCtrl* xc = sa.px.ctrl(sa.rank);
+  unsigned long long cost = 0ull;
+  for (int d = 0; d < sa.world; ++d) cost += xc->cost[d];
+  const int pull = can_pull && pull_divisor > 0 && (double)cost * pull_divisor > (double)T_global;
+  ctl->mode[h] = pull;
+  ctl->dense[h] = pull && (double)cost * 2.0 > (double)T_global;
+  if (pull) ctl->pull_hops++;
+  else ctl->push_hops++;
+}
+
+// this rank's frontier cost of list segment `seg` onto every rank's board
+__global__ void shard_publish_cost_kernel(ShardArgs sa, int seg) {
+  const int d = threadIdx.x;
+  if (d < sa.world) sa.px.ctrl(d)->cost[sa.rank] = sa.a.ctl->push_cost[seg];
+}
+
+// the inbox is consumed: empty it for the peers' next sends
+__global__ void shard_inbox_reset_kernel(ShardArgs sa) {
+  if (threadIdx.x == 0) sa.px.ctrl(sa.rank)->cursor = 0ull;
+}
+
+// owners write their hubs' next-layer rows onto every rank's hub board
+// ([n_hubs][W]); each hub has exactly one owner, so every board ends up
+// holding every hub's row with no reduction
 template <int W>
-__global__ void shard_hub_out_kernel(ShardArgs sa, uint32_t* out) {
+__global__ void shard_hub_out_kernel(ShardArgs sa) {
   const int64_t n = sa.n_hubs * W;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t h = i / W;
     const int j = (int)(i % W);
     const int32_t v = sa.hub_ids[h];
-    out[i] = owner_of(v, sa.world) == sa.rank ? sa.a.N[(size_t)sa.lidx[v] * W + j] : 0u;
+    if (owner_of(v, sa.world) != sa.rank) continue;
+    const uint32_t w = sa.a.N[(size_t)sa.lidx[v] * W + j];
+    for (int d = 0; d < sa.world; ++d) sa.px.hubs(d)[i] = w;
   }
 }
 
-// install the summed hub rows as next-layer hub slice rows (frontier only:
+// install the board's hub rows as next-layer hub slice rows (frontier only:
 // a hub's visited bits stay with its owner)
 template <int W>
-__global__ void shard_hub_in_kernel(ShardArgs sa, const uint32_t* __restrict__ rows) {
+__global__ void shard_hub_in_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
+  const uint32_t* rows = sa.px.hubs(sa.rank);
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -412,12 +516,14 @@ __global__ void __launch_bounds__(kCompactThreads) shard_gather_kernel(
 
 // ---------------------------------------------------------------------------
 // Pull hops across partitions (dense frontiers).  Instead of pushing every
-// frontier edge's candidates to the target's owner, every rank publishes its
-// owned frontier rows -- records ((gid * W + word) << 32) | bits -- and all
-// ranks all-gather them into a global-indexed staging copy of the frontier
-// (the push staging matrix O, empty between hops); each rank then pulls for
-// the entities it owns over its in-edge CSR (global sources).  Hub frontier
-// rows are already replicated and are copied in locally.
+// frontier edge's candidates to the target's owner, every rank writes its
+// owned frontier rows -- records ((gid * W + word), bits) -- into every
+// rank's inbox (an all-gather over peer memory); each rank stages them into
+// a global-indexed copy of the frontier (the push staging matrix O, empty
+// between hops) and pulls for the entities it owns over its in-edge CSR
+// (global sources).  Hub frontier rows are already replicated and are
+// copied in locally.  On a single rank the frontier is its own X (global
+// rows = local rows) and nothing is staged.
 
 // in-edges of owned objects: key = object's local row, or -1
 __global__ void shard_select_in_kernel(const int32_t* __restrict__ obj, int64_t T,
@@ -430,13 +536,12 @@ __global__ void shard_select_in_kernel(const int32_t* __restrict__ obj, int64_t 
   }
 }
 
-// owned frontier rows of list segment `seg` -> records (COUNT: totals only)
-template <int W, bool WRITE>
-__global__ void __launch_bounds__(kThreads) shard_frontier_pack_kernel(ShardArgs sa, int seg,
-                                                                       const int32_t* __restrict__ l2g,
-                                                                       unsigned long long* cursor,
-                                                                       uint64_t* out) {
+// owned frontier rows of list segment `seg` -> records in every rank's inbox
+template <int W>
+__global__ void __launch_bounds__(kThreads) shard_frontier_send_kernel(ShardArgs sa, int seg,
+                                                                       const int32_t* __restrict__ l2g) {
   const WaveArgs& a = sa.a;
+  if (a.ctl->mode[a.h] != 1) return;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -466,30 +571,38 @@ __global__ void __launch_bounds__(kThreads) shard_frontier_pack_kernel(ShardArgs
       if (lane >= o) incl += y;
     }
     const int tot = __shfl_sync(TH_FULL, incl, 31);
-    unsigned long long b0 = 0;
-    if (lane == 0 && tot) b0 = atomicAdd(cursor, (unsigned long long)tot);
-    b0 = __shfl_sync(TH_FULL, b0, 0);
-    if (WRITE && row >= 0) {
-      uint64_t o = b0 + (uint64_t)(incl - nzc);
-      const uint64_t key0 = (uint64_t)l2g[row] * W;
+    if (!tot) continue;
+    const uint64_t key0 = row >= 0 ? (uint64_t)l2g[row] * W : 0ull;
+    for (int d = 0; d < sa.world; ++d) {
+      unsigned long long b0 = 0;
+      if (lane == 0) {
+        b0 = inbox_reserve(sa.px, d, tot);
+        if (d != sa.rank) atomicAdd(&a.ctl->sent[a.h], (unsigned long long)tot);
+      }
+      b0 = __shfl_sync(TH_FULL, b0, 0);
+      if (row >= 0) {
+        unsigned long long o = b0 + (unsigned long long)(incl - nzc);
 #pragma unroll
-      for (int j = 0; j < W; ++j)
-        if (words[j]) out[o++] = ((key0 + j) << 32) | words[j];
+        for (int j = 0; j < W; ++j)
+          if (words[j]) inbox_put(sa.px, d, o++, key0 + j, words[j]);
+      }
     }
   }
 }
 
-// gathered records (and the local hub frontier rows) -> global staging G, Gf
+// gathered records (and the local hub frontier rows) -> global staging O, Of
 template <int W>
-__global__ void shard_gather_frontier_kernel(ShardArgs sa, int seg, const uint64_t* __restrict__ recs,
-                                             int64_t n) {
+__global__ void shard_gather_frontier_kernel(ShardArgs sa, int seg) {
   const WaveArgs& a = sa.a;
+  if (a.ctl->mode[a.h] != 1) return;
+  const int64_t n = (int64_t)min(sa.px.ctrl(sa.rank)->cursor, (unsigned long long)sa.px.cap);
+  const uint64_t* keys = sa.px.keys(sa.rank);
+  const uint32_t* bits = sa.px.bits(sa.rank);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t rec = recs[i];
-    const uint32_t key = (uint32_t)(rec >> 32);
-    const int32_t g = (int32_t)(key / W);
-    sa.O[(size_t)key] = (uint32_t)rec;
+    const uint64_t key = keys[i];
+    const int64_t g = (int64_t)(key / W);
+    sa.O[key] = bits[i];
     atomicOr(&sa.Of[g >> 5], 1u << (g & 31));
   }
   // hub rows of the segment (rows >= n_local), one thread per (row, word)
@@ -509,20 +622,28 @@ __global__ void shard_gather_frontier_kernel(ShardArgs sa, int seg, const uint64
   }
 }
 
-// undo the staging: zero the gathered words and the hub rows' words
+// undo the staging: zero the gathered words, the hub rows' words and their
+// flag words (every staged entity is cleared here, so whole flag words can go)
 template <int W>
-__global__ void shard_clear_frontier_kernel(ShardArgs sa, int seg, const uint64_t* __restrict__ recs,
-                                            int64_t n) {
+__global__ void shard_clear_frontier_kernel(ShardArgs sa, int seg) {
   const WaveArgs& a = sa.a;
+  if (a.ctl->mode[a.h] != 1) return;
+  const int64_t n = (int64_t)min(sa.px.ctrl(sa.rank)->cursor, (unsigned long long)sa.px.cap);
+  const uint64_t* keys = sa.px.keys(sa.rank);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    sa.O[(size_t)(uint32_t)(recs[i] >> 32)] = 0u;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[i];
+    sa.O[key] = 0u;
+    sa.Of[(key / W) >> 5] = 0u;
+  }
   const int32_t nl = a.ctl->list_len[seg];
   const int32_t* list = a.lists + a.ctl->list_off[seg];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)nl * W;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t row = list[i / W];
     if (row < sa.n_local) continue;
-    sa.O[(size_t)sa.hub_ids[row - sa.n_local] * W + (i % W)] = 0u;
+    const int32_t g = sa.hub_ids[row - sa.n_local];
+    sa.O[(size_t)g * W + (i % W)] = 0u;
+    sa.Of[g >> 5] = 0u;
   }
 }

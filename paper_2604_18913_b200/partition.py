@@ -215,7 +215,8 @@ def plan_sharding(subj, n_entities: int, world: int, hub_fraction: float = DEFAU
         lidx[idx] = np.arange(idx.size, dtype=np.int32)
         n_local[p] = idx.size
     if n_hubs is None:
-        n_hubs = int(round(n_entities * hub_fraction))
+        # (hubs only spread a row's edges over ranks: one rank needs none)
+        n_hubs = int(round(n_entities * hub_fraction)) if world > 1 else 0
     hubs = select_hubs(subj, n_entities, n_hubs)
     hub_index = np.full(n_entities, -1, dtype=np.int32)
     hub_index[hubs] = np.arange(hubs.size, dtype=np.int32)
@@ -228,85 +229,69 @@ def plan_sharding(subj, n_entities: int, world: int, hub_fraction: float = DEFAU
 
 
 class Exchange:
-    """Collectives of the partitioned hop; hosts ``ranks`` of a ``world``."""
+    """What the partitioned wave needs from the transport between ranks.
+
+    The data path itself is not here: shards write into each other's
+    exchange regions from their kernels (k6_shard.cuh).  The exchange wires
+    the regions together (``connect``), separates the phases of a hop
+    (``barrier``: every peer's writes of the previous phase are complete),
+    agrees on a flag (``any``) and gathers the owners' result slices at the
+    end of a wave (``gather``).  It hosts ``ranks`` of a ``world``."""
 
     world: int
     ranks: list
 
-    def all_to_all(self, sends):  # [(int64 tensor, counts[world])] -> [int64 tensor]
+    def connect(self, shards) -> None:
         raise NotImplementedError
 
-    def sum_(self, tensors) -> None:  # in place, over ranks
-        raise NotImplementedError
-
-    def all_gather(self, sends):  # [(int64 tensor, counts)] -> [concat of all ranks' tensors]
-        raise NotImplementedError
-
-    def sum_int(self, values) -> int:  # sum of one int per hosted rank over all ranks
+    def barrier(self, shards) -> None:
         raise NotImplementedError
 
     def any(self, flags) -> bool:
         raise NotImplementedError
 
-    def gather(self, objs) -> list:  # one object per hosted rank -> all ranks', rank order
+    def gather(self, parts) -> list:  # one dict of tensors per hosted rank -> every rank's, rank order
+        raise NotImplementedError
+
+    def sum_int(self, values) -> int:  # one int per hosted rank -> the sum over all ranks
         raise NotImplementedError
 
 
 class LoopbackExchange(Exchange):
-    """Every rank of the world in this process (single-device testing)."""
+    """Every rank of the world in this process, on one device: the regions
+    are plain device pointers, and the ranks' kernels run one after another
+    on one stream, so stream order is the barrier."""
 
     def __init__(self, world: int):
         self.world = world
         self.ranks = list(range(world))
-        self.bytes_sent = 0
 
-    def all_to_all(self, sends):
-        import torch
+    def connect(self, shards) -> None:
+        bases = [sh.region_handle(local=True) for sh in shards]
+        for sh in shards:
+            for p, base in enumerate(bases):
+                sh.connect_peer(p, base, local=True)
 
-        G = self.world
-        offs = [np.concatenate([[0], np.cumsum(c)]).astype(np.int64) for _, c in sends]
-        out = []
-        for d in range(G):
-            parts = [t[int(o[d]): int(o[d + 1])] for (t, _), o in zip(sends, offs)]
-            out.append(torch.cat(parts) if parts else sends[0][0][:0])
-        self.bytes_sent += 8 * sum(int(sum(c)) for _, c in sends)
-        return out
+    def barrier(self, shards) -> None:
+        return None
 
-    def all_gather(self, sends):
-        import torch
-
-        parts = [t[: int(c[0])] if len(c) else t[:0] for t, c in sends]
-        full = torch.cat(parts) if parts else sends[0][0][:0]
-        self.bytes_sent += 8 * (self.world - 1) * sum(int(p.numel()) for p in parts)
-        return [full for _ in sends]
-
-    def sum_int(self, values):
-        return int(sum(int(v) for v in values))
-
-    def sum_(self, tensors):
-        if len(tensors) <= 1:
-            return
-        total = tensors[0].clone()
-        for t in tensors[1:]:
-            total += t
-        for t in tensors:
-            t.copy_(total)
-
-    def any(self, flags):
+    def any(self, flags) -> bool:
         return bool(any(flags))
 
-    def gather(self, objs):
-        return list(objs)
+    def gather(self, parts) -> list:
+        return list(parts)
+
+    def sum_int(self, values) -> int:
+        return int(sum(int(v) for v in values))
 
 
 class DistExchange(Exchange):
-    """One rank per process over torch.distributed.
-
-    NCCL moves device buffers directly (the B200 path).  With gloo (CPU
-    tests, or several ranks sharing one GPU in a functional test, where
-    NCCL refuses duplicate devices) device tensors are staged through host
-    memory, so no rank's kernels ever wait on another rank's.
-    """
+    """One rank per process over torch.distributed.  Peer regions are CUDA
+    IPC mappings (handles shipped once with all_gather_object); the phase
+    barrier is a stream synchronisation plus a process-group barrier, with
+    no data read back (on NCCL the barrier is a 1-element all-reduce).
+    ``gather`` moves the owners' result slices with all_gather (NCCL on
+    B200s; gloo with host tensors in the CPU tests)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -315,52 +300,30 @@ class DistExchange(Exchange):
         self.group = group
         self.world = dist.get_world_size(group)
         self.ranks = [dist.get_rank(group)]
-        self.bytes_sent = 0
         self.staged = dist.get_backend(group) != "nccl"
 
-    def _host(self, t):
-        return t.cpu() if (self.staged and t.is_cuda) else t
+    def connect(self, shards) -> None:
+        (sh,) = shards
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, sh.region_handle(local=False), group=self.group)
+        for p, h in enumerate(handles):
+            sh.connect_peer(p, h, local=False)
+        self.dist.barrier(group=self.group)
 
-    def all_to_all(self, sends):
+    def barrier(self, shards) -> None:
+        for sh in shards:
+            sh.synchronize()
+        self.dist.barrier(group=self.group)
+
+    def any(self, flags) -> bool:
         import torch
 
-        (send, counts), = sends
-        dev = send.device
-        cdev = "cpu" if self.staged else dev
-        cnt = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=cdev)
-        rcnt = torch.empty_like(cnt)
-        self.dist.all_to_all_single(rcnt, cnt, group=self.group)
-        rc = [int(x) for x in rcnt.tolist()]
-        n = int(sum(counts))
-        src = self._host(send[:n].contiguous())
-        recv = torch.empty(sum(rc), dtype=torch.int64, device=src.device)
-        self.dist.all_to_all_single(recv, src, output_split_sizes=rc,
-                                    input_split_sizes=[int(c) for c in counts], group=self.group)
-        self.bytes_sent += 8 * (n - int(counts[self.ranks[0]]))
-        return [recv.to(dev) if recv.device != dev else recv]
+        (f,) = flags
+        t = torch.tensor([1 if f else 0], dtype=torch.int32, device="cpu" if self.staged else "cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return bool(t.item())
 
-    def all_gather(self, sends):
-        import torch
-
-        (send, counts), = sends
-        dev = send.device
-        n = int(counts[0]) if len(counts) else 0
-        cdev = "cpu" if self.staged else dev
-        sizes = [torch.zeros(1, dtype=torch.int64, device=cdev) for _ in range(self.world)]
-        self.dist.all_gather(sizes, torch.tensor([n], dtype=torch.int64, device=cdev), group=self.group)
-        sizes = [int(x.item()) for x in sizes]
-        m = max(sizes) if sizes else 0
-        src = self._host(send[:n])
-        padded = torch.zeros(max(m, 1), dtype=torch.int64, device=src.device)
-        padded[:n] = src
-        out = torch.empty(self.world * max(m, 1), dtype=torch.int64, device=src.device)
-        self.dist.all_gather_into_tensor(out, padded, group=self.group)
-        parts = [out[r * max(m, 1): r * max(m, 1) + sizes[r]] for r in range(self.world)]
-        full = torch.cat(parts)
-        self.bytes_sent += 8 * n * (self.world - 1)
-        return [full.to(dev) if full.device != dev else full]
-
-    def sum_int(self, values):
+    def sum_int(self, values) -> int:
         import torch
 
         (v,) = values
@@ -368,37 +331,44 @@ class DistExchange(Exchange):
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return int(t.item())
 
-    def sum_(self, tensors):
-        (t,) = tensors
-        h = self._host(t)
-        self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
-        if h is not t:
-            t.copy_(h)
-
-    def any(self, flags):
+    def gather(self, parts) -> list:
+        """all_gather of every tensor of this rank's dict (sizes first, then
+        padded payloads): one entry per rank, on this rank's device."""
         import torch
 
-        (f,) = flags
-        dev = "cpu" if self.staged else "cuda"
-        t = torch.tensor([1 if f else 0], dtype=torch.int32, device=dev)
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
-        return bool(t.item())
-
-    def gather(self, objs):
-        (o,) = objs
-        out = [None] * self.world
-        self.dist.all_gather_object(out, o, group=self.group)
+        (mine,) = parts
+        names = sorted(k for k, v in mine.items() if v is not None)
+        out = [dict() for _ in range(self.world)]
+        for name in names:
+            t = mine[name]
+            dev = t.device
+            src = t.reshape(-1).cpu() if self.staged else t.reshape(-1)
+            n = torch.tensor([src.numel()], dtype=torch.int64, device=src.device)
+            sizes = [torch.zeros_like(n) for _ in range(self.world)]
+            self.dist.all_gather(sizes, n, group=self.group)
+            sizes = [int(x.item()) for x in sizes]
+            m = max(max(sizes), 1)
+            pad = torch.zeros(m, dtype=src.dtype, device=src.device)
+            pad[: src.numel()] = src
+            bufs = [torch.empty_like(pad) for _ in range(self.world)]
+            self.dist.all_gather(bufs, pad, group=self.group)
+            for r in range(self.world):
+                v = bufs[r][: sizes[r]].to(dev)
+                out[r][name] = v.reshape(-1, *t.shape[1:]) if t.dim() > 1 else v
         return out
 
 
 # --------------------------------------------------------------- device shard
 
+DEFAULT_INBOX = 1 << 22  # records per exchange inbox; grown after an overflow
+
 
 class GraphShard:
-    """One rank's device shard (th_shard): owned out-rows + hub slices."""
+    """One rank's device shard (th_shard): owned out-rows + hub slices, and
+    the exchange region its peers write into."""
 
     def __init__(self, cols, n_entities: int, n_relations: int, plan: ShardPlan, rank: int,
-                 stream=None):
+                 stream=None, inbox_records: int = DEFAULT_INBOX):
         import torch
 
         if not torch.cuda.is_available():
@@ -423,18 +393,51 @@ class GraphShard:
         _lib.check(lib.th_shard_create(
             s.data_ptr(), r.data_ptr(), o.data_ptr(), self.n_triples, self.n_entities, self.n_relations,
             lidx.data_ptr(), hidx.data_ptr(), hubs.data_ptr() if hubs.numel() else None, hubs.numel(),
-            l2g.data_ptr() if l2g.numel() else None, l2g.numel(), rank, plan.world,
+            l2g.data_ptr() if l2g.numel() else None, l2g.numel(), rank, plan.world, int(inbox_records),
             ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
         self._handle = h.value
         self._finalizer = weakref.finalize(self, lib.th_shard_destroy, self._handle)
         self.local_triples = int(lib.th_shard_local_triples(self._handle))
         self.can_pull = bool(lib.th_shard_can_pull(self._handle))
-        self._keep = None
+        self.inbox_records = int(inbox_records)
 
     def launch_count(self) -> int:
         return int(_lib.load().th_shard_launch_count(self._handle))
 
-    # -- the wave steps (ShardRunner protocol) ------------------------------
+    def set_pull_divisor(self, divisor: float) -> None:
+        _lib.check(_lib.load().th_shard_set_pull_divisor(self._handle, float(divisor)))
+
+    # -- exchange wiring -----------------------------------------------------
+    def region_handle(self, local: bool):
+        """This shard's exchange region: its device address (same process)
+        or its 64-byte CUDA IPC handle (other processes)."""
+        lib = _lib.load()
+        if local:
+            base, nbytes, rec = ctypes.c_void_p(), ctypes.c_uint64(), ctypes.c_int64()
+            _lib.check(lib.th_shard_region(self._handle, ctypes.byref(base), ctypes.byref(nbytes),
+                                           ctypes.byref(rec)))
+            return base.value
+        buf = ctypes.create_string_buffer(64)
+        _lib.check(lib.th_shard_ipc_handle(self._handle, buf))
+        return bytes(buf.raw)
+
+    def connect_peer(self, peer: int, handle, local: bool) -> None:
+        lib = _lib.load()
+        if local:
+            _lib.check(lib.th_shard_connect(self._handle, peer, ctypes.c_void_p(handle)))
+        elif peer == self.rank:
+            _lib.check(lib.th_shard_connect(self._handle, peer, ctypes.c_void_p(self.region_handle(True))))
+        else:
+            _lib.check(lib.th_shard_ipc_open(self._handle, peer, ctypes.create_string_buffer(handle, 64)))
+
+    def grow_inbox(self) -> None:
+        self.inbox_records *= 4
+        _lib.check(_lib.load().th_shard_grow_inbox(self._handle, self.inbox_records))
+
+    def synchronize(self) -> None:
+        self.stream.synchronize()
+
+    # -- the wave ---------------------------------------------------------------
     def begin(self, query: "WaveQuery") -> None:
         import torch
 
@@ -457,48 +460,25 @@ class GraphShard:
         self._q = q
         _lib.check(_lib.load().th_shard_begin(self._handle, ctypes.byref(q)))
 
-    def frontier_cost(self, hop: int) -> int:
-        """This rank's frontier out-edge total (direction choice)."""
-        c = ctypes.c_int64()
-        _lib.check(_lib.load().th_shard_plan(self._handle, hop, ctypes.byref(c)))
-        return int(c.value)
-
-    def expand(self, hop: int, mode: int = 0):
-        counts = (ctypes.c_int64 * self.plan.world)()
-        ptr = ctypes.c_void_p()
-        _lib.check(_lib.load().th_shard_expand(self._handle, hop, mode, counts, ctypes.byref(ptr)))
-        cnt = [int(c) for c in counts]
-        n = sum(cnt)
-        send = _lib.as_tensor(ptr.value, (n,), "<i8", owner=self)
-        return send, cnt
-
-    def absorb(self, hop: int, recv) -> None:
-        self._keep = recv  # must outlive the asynchronous kernel
-        _lib.check(_lib.load().th_shard_absorb(self._handle, hop, recv.data_ptr() if recv.numel() else None,
-                                               int(recv.numel())))
-
-    def hub_rows(self, hop: int):
-        ptr = ctypes.c_void_p()
-        words = ctypes.c_int64()
-        _lib.check(_lib.load().th_shard_hub_rows(self._handle, hop, ctypes.byref(ptr), ctypes.byref(words)))
-        return _lib.as_tensor(ptr.value, (int(words.value),), "<i4", owner=self)
-
-    def hub_merge(self, hop: int) -> None:
-        _lib.check(_lib.load().th_shard_hub_merge(self._handle, hop))
-
-    def end_hop(self, hop: int) -> None:
-        _lib.check(_lib.load().th_shard_end_hop(self._handle, hop))
+    def hop(self, hop: int, phase: int) -> None:
+        _lib.check(_lib.load().th_shard_hop(self._handle, hop, phase))
 
     def finish(self):
-        """-> ("ok", ShardResult) or ("overflow", None)."""
+        """-> ("ok", ShardResult), ("overflow", None) or ("inbox", None)."""
+        lib = _lib.load()
         res = _lib.Result()
-        rc = _lib.load().th_shard_finish(self._handle, ctypes.byref(res))
+        rc = lib.th_shard_finish(self._handle, ctypes.byref(res))
         if rc == _lib.TH_ERR_OVERFLOW:
-            return "overflow", None
+            return ("inbox" if lib.th_shard_inbox_overflowed(self._handle) == 1 else "overflow"), None
         _lib.check(rc)
-        return "ok", self._host_result(res)
+        return "ok", self._result(res)
 
-    def _host_result(self, res) -> "ShardResult":
+    def sent_records(self, k: int) -> list:
+        per = (ctypes.c_int64 * k)()
+        _lib.check(_lib.load().th_shard_sent(self._handle, per, k))
+        return [int(x) for x in per]
+
+    def _result(self, res) -> "ShardResult":
         """Device views of the shard's results (valid until its next wave)."""
         B, k = res.n_queries, res.k
         t = _lib.as_tensor
@@ -513,8 +493,24 @@ class GraphShard:
             out.a_ids = t(res.act_ids, (res.act_total,), "<i4", self)
         return out
 
-    def _to_host(self, r: "ShardResult") -> "ShardResult":
-        return r.to_host()
+    def triples_of(self, tids):
+        """(subject, relation, object) of this shard's triples with the given
+        (sorted, global) tids, all global ids -- device tensors."""
+        import torch
+
+        cols = _lib.ShardCols()
+        _lib.check(_lib.load().th_shard_columns(self._handle, ctypes.byref(cols)))
+        t = _lib.as_tensor
+        n = int(cols.n_triples)
+        tid_l2g = t(cols.tid_l2g, (n,), "<i4", self)
+        local = torch.searchsorted(tid_l2g, tids.to(torch.int32))
+        row = t(cols.subj_row, (n,), "<i4", self)[local].long()
+        rel = t(cols.rel, (n,), "<i2", self)[local].to(torch.int32) & 0xFFFF
+        obj = t(cols.obj, (n,), "<i4", self)[local]
+        # local rows: owned entities [0, n_local), then hub slices
+        row_gid = torch.cat([t(cols.l2g, (int(cols.n_local),), "<i4", self),
+                             t(cols.hub_ids, (int(cols.n_hubs),), "<i4", self)])
+        return row_gid[row].int(), rel.int(), obj.int()
 
 
 @dataclass
@@ -536,96 +532,87 @@ class WaveQuery:
 @dataclass
 class ShardResult:
     """One rank's share of a wave: owned frontier ids, local activated tids,
-    partial edge counts (CSR per (hop, query)); device tensors from a CUDA
-    shard until ``to_host``."""
+    partial edge counts (CSR per (hop, query)); tensors."""
 
     n_queries: int
     k: int
-    edges: np.ndarray = None
-    f_off: np.ndarray = None
-    f_len: np.ndarray = None
-    f_ids: np.ndarray = None
-    a_off: np.ndarray = None
-    a_len: np.ndarray = None
-    a_ids: np.ndarray = None
+    edges: object = None
+    f_off: object = None
+    f_len: object = None
+    f_ids: object = None
+    a_off: object = None
+    a_len: object = None
+    a_ids: object = None
 
-    def to_host(self) -> "ShardResult":
-        conv = lambda x: x if x is None or isinstance(x, np.ndarray) else x.cpu().numpy()  # noqa: E731
-        return ShardResult(self.n_queries, self.k, *(conv(getattr(self, f)) for f in
-                                                      ("edges", "f_off", "f_len", "f_ids", "a_off", "a_len",
-                                                       "a_ids")))
+    def tensors(self) -> dict:
+        return {n: getattr(self, n) for n in ("edges", "f_off", "f_len", "f_ids", "a_off", "a_len", "a_ids")}
 
 
 PULL_DIVISOR = 8.0  # pull when the frontier's out-edges exceed T / 8 (as K2/K3)
 
 
-def run_wave(shards, xch: Exchange, query: WaveQuery, stats: dict | None = None,
-             n_triples: int | None = None, pull_divisor: float = PULL_DIVISOR):
-    """Drive one wave through every hosted shard (Algorithm 1 per hop).
-
-    Per hop the ranks agree on a direction: push (candidate records to
-    their owners, all-to-all) or, for dense frontiers, pull (every rank's
-    owned frontier rows all-gathered, each owner pulls over its in-edges).
-    Returns the hosted shards' ShardResults.  An output overflow on any
-    rank makes every rank run the wave again with grown capacities.
-    """
-    can_pull = n_triples is not None and pull_divisor > 0 and all(
-        getattr(sh, "can_pull", False) for sh in shards)
-    for _attempt in range(4):
+def run_wave(shards, xch: Exchange, query: WaveQuery, stats: dict | None = None):
+    """Drive one wave through every hosted shard (Algorithm 1 per hop): three
+    phases per hop, each followed by the exchange's barrier; the data moves
+    between ranks inside the kernels.  Returns the hosted shards'
+    ShardResults.  An output (or inbox) overflow on any rank makes every rank
+    run the wave again with grown capacities."""
+    for _attempt in range(6):
         for sh in shards:
             sh.begin(query)
+        xch.barrier(shards)
         for h in range(1, query.k + 1):
-            mode = 0
-            if can_pull:
-                cost = xch.sum_int([sh.frontier_cost(h) for sh in shards])
-                mode = 1 if cost * pull_divisor > n_triples else 0
-            sends = [sh.expand(h, mode) if mode else sh.expand(h) for sh in shards]
-            if stats is not None:
-                stats.setdefault("records", []).append(sum(sum(c) for _, c in sends))
-                stats.setdefault("modes", []).append(mode)
-            recvs = xch.all_gather(sends) if mode else xch.all_to_all(sends)
-            for sh, rv in zip(shards, recvs):
-                sh.absorb(h, rv)
-            if h < query.k:  # the last layer is never expanded
-                rows = [sh.hub_rows(h) for sh in shards]
-                xch.sum_(rows)
+            for phase in (0, 1, 2):
                 for sh in shards:
-                    sh.hub_merge(h)
-            for sh in shards:
-                sh.end_hop(h)
+                    sh.hop(h, phase)
+                xch.barrier(shards)
         done = [sh.finish() for sh in shards]
-        if not xch.any([st == "overflow" for st, _ in done]):
+        inbox = xch.any([st == "inbox" for st, _ in done])
+        if not xch.any([st != "ok" for st, _ in done]):
+            if stats is not None:
+                stats["sent_records"] = [sh.sent_records(query.k) for sh in shards]
             return [r for _, r in done]
-    raise RuntimeError("partitioned wave kept overflowing its result buffers")
+        if inbox:
+            for sh in shards:
+                sh.grow_inbox()
+            xch.connect(shards)
+    raise RuntimeError("partitioned wave kept overflowing its buffers")
 
 
-def merge_results(parts, n_queries: int, k: int, activated: bool):
-    """Per (hop, query): concatenate the ranks' sorted slices and sort.
-    Owners are disjoint, so the union is duplicate-free."""
+def merge_results(parts, n_queries: int, k: int, activated: bool, width_f: int, width_a: int):
+    """The union of the owners' sorted slices per (hop, query), on the
+    device of the parts: owners are disjoint, so one sort of (segment, id)
+    keys gives every segment sorted and duplicate-free (the role of the
+    reference's sort/unique of a concatenation, engine.py:121-127)."""
+    import torch
 
-    def merge(name_off, name_len, name_ids):
-        keys, ids = [], []
+    def merge(name_off, name_len, name_ids, width):
+        keys = []
         for p in parts:
-            off, ln, data = getattr(p, name_off), getattr(p, name_len), getattr(p, name_ids)
-            flat_len = ln.reshape(-1)
-            key = np.repeat(np.arange(flat_len.size, dtype=np.int64), flat_len)
-            idx = np.concatenate([np.arange(o, o + n, dtype=np.int64)
-                                  for o, n in zip(off.reshape(-1), flat_len)]) if key.size else \
-                np.empty(0, np.int64)
-            keys.append(key)
-            ids.append(data[idx].astype(np.int64))
-        key = np.concatenate(keys) if keys else np.empty(0, np.int64)
-        val = np.concatenate(ids) if ids else np.empty(0, np.int64)
-        order = np.lexsort((val, key))
-        val = val[order]
-        cnt = np.bincount(key, minlength=k * n_queries).reshape(k, n_queries)
-        off = np.concatenate([[0], np.cumsum(cnt.reshape(-1))[:-1]]).reshape(k, n_queries)
-        return off, cnt, val
+            off, ln, data = p[name_off], p[name_len], p[name_ids]
+            dev = data.device
+            flat_len = ln.reshape(-1).long()
+            seg = torch.repeat_interleave(torch.arange(flat_len.numel(), device=dev), flat_len)
+            start = torch.cumsum(flat_len, 0) - flat_len
+            pos = off.reshape(-1).long()[seg] + (torch.arange(seg.numel(), device=dev) - start[seg])
+            keys.append(seg * width + data[pos].long())
+        key = torch.sort(torch.cat(keys)).values if keys else torch.empty(0, dtype=torch.int64)
+        seg = key // width
+        cnt = torch.bincount(seg, minlength=k * n_queries).reshape(k, n_queries)
+        off = (torch.cumsum(cnt.reshape(-1), 0) - cnt.reshape(-1)).reshape(k, n_queries)
+        return off, cnt, (key % width).to(torch.int32)
 
-    out = {"edges": sum(p.edges for p in parts)}
-    out["f_off"], out["f_len"], out["f_ids"] = merge("f_off", "f_len", "f_ids")
+    if len(parts) == 1:
+        # one rank owns everything: its segments are the answer already
+        p = parts[0]
+        out = {n: p[n] for n in ("edges", "f_off", "f_len", "f_ids")}
+        if activated:
+            out.update({n: p[n] for n in ("a_off", "a_len", "a_ids")})
+        return out
+    out = {"edges": sum(p["edges"].long() for p in parts)}
+    out["f_off"], out["f_len"], out["f_ids"] = merge("f_off", "f_len", "f_ids", width_f)
     if activated:
-        out["a_off"], out["a_len"], out["a_ids"] = merge("a_off", "a_len", "a_ids")
+        out["a_off"], out["a_len"], out["a_ids"] = merge("a_off", "a_len", "a_ids", width_a)
     return out
 
 
@@ -669,18 +656,32 @@ class PartitionedGraph:
         self.n_entities = int(n_entities)
         self.n_relations = int(n_relations)
         self.n_triples = int(len(subj))
-        # host copy of the columns: cross_graph_paths gathers the (s, r, o)
-        # of a query's activated triples from it (the reference keeps its
-        # shards on disk and maps tids through tid_to_global the same way)
-        self._cols = tuple(np.asarray(c.cpu().numpy() if hasattr(c, "cpu") else c, dtype=np.int32)
-                           for c in cols)
-        self.pull_divisor = PULL_DIVISOR  # 0 = push only
         factory = shard_factory or GraphShard
         self.shards = [factory(cols, n_entities, n_relations, plan, r) for r in exchange.ranks]
+        exchange.connect(self.shards)
+        self.pull_divisor = PULL_DIVISOR
+
+    @property
+    def pull_divisor(self) -> float:
+        return self._pull_divisor
+
+    @pull_divisor.setter
+    def pull_divisor(self, d: float) -> None:
+        """Pull when the ranks' summed frontier out-edges exceed T / d (0 = push only)."""
+        self._pull_divisor = float(d)
+        for sh in self.shards:
+            sh.set_pull_divisor(self._pull_divisor)
 
     def run(self, query: WaveQuery, stats: dict | None = None):
         """One wave; the hosted ranks' partial results (kept sharded)."""
-        return run_wave(self.shards, self.exchange, query, stats, self.n_triples, self.pull_divisor)
+        return run_wave(self.shards, self.exchange, query, stats)
+
+    def merged(self, query: WaveQuery, stats: dict | None = None) -> dict:
+        """One wave merged over all ranks (every rank gets the union), as
+        device tensors: edges [k, B], f_off/f_len [k, B], f_ids, (+ a_*)."""
+        parts = self.exchange.gather([r.tensors() for r in self.run(query, stats)])
+        return merge_results(parts, query.n_queries, query.k, query.activated, self.n_entities,
+                             self.n_triples)
 
     def retrieve(self, seeds, k: int, relation_filter=None, semantics="frontier",
                  activated: bool = False):
@@ -707,21 +708,20 @@ class PartitionedGraph:
             nq = q1 - q0
             wq = WaveQuery(np.arange(nq + 1, dtype=np.int32), arr[q0:q1].astype(np.int32), k, sem,
                            None if words is None else words[q0:q1], activated)
-            parts = self.exchange.gather([r.to_host() for r in self.run(wq)])
-            m = merge_results(parts, nq, k, activated)
+            m = {n: (v.cpu() if v is not None else None) for n, v in self.merged(wq).items()}
             merged["edges"].append(m["edges"])
             merged["f_off"].append(m["f_off"] + fbase)
             merged["f_len"].append(m["f_len"])
             merged["f_ids"].append(m["f_ids"])
-            fbase += m["f_ids"].size
+            fbase += m["f_ids"].numel()
             if activated:
                 merged["a_off"].append(m["a_off"] + abase)
                 merged["a_len"].append(m["a_len"])
                 merged["a_ids"].append(m["a_ids"])
-                abase += m["a_ids"].size
+                abase += m["a_ids"].numel()
             if B == 0:
                 break
-        cat = lambda xs, axis=1: torch.from_numpy(np.concatenate(xs, axis=axis))  # noqa: E731
+        cat = lambda xs, dim=1: torch.cat(xs, dim)  # noqa: E731
         out = RetrievalResult(B, k, sem, _graph=self)
         out.edges = cat(merged["edges"])
         out.frontier_off, out.frontier_len = cat(merged["f_off"]), cat(merged["f_len"])
@@ -747,8 +747,7 @@ def cross_graph_k_hop(q0: EntityVector, k: int, pg: PartitionedGraph,
     sem = HopSemantics.parse(semantics)
     ids = q0.ids.astype(np.int32)
     wq = WaveQuery(np.array([0, ids.size], dtype=np.int32), ids, k, sem, None, True)
-    parts = pg.exchange.gather([r.to_host() for r in pg.run(wq)])
-    m = merge_results(parts, 1, k, True)
+    m = {n: (v.cpu().numpy() if v is not None else None) for n, v in pg.merged(wq).items()}
     steps = []
     for h in range(k):
         fo, fl = int(m["f_off"][h, 0]), int(m["f_len"][h, 0])
@@ -785,12 +784,30 @@ def cross_graph_paths(q0: EntityVector, k: int, pg: PartitionedGraph,
         raise ValueError("hop count must be >= 1")
     if max_paths is not None and max_paths < 0:
         raise ValueError("max_paths must be >= 0")
-    tr = cross_graph_k_hop(q0, k, pg, HopSemantics.EXACT_WALK)
-    act = [tr.activated(h).ids for h in range(1, k + 1)]
-    tids = np.unique(np.concatenate(act)) if act else np.empty(0, np.int64)
-    s, r, o = (c[tids] for c in pg._cols)
+    s, r, o = walk_subgraph(q0, k, pg)
     sub = build_incidence((s, r, o), pg.n_entities, pg.n_relations)
     res = reconstruct_paths(q0, k, sub, max_paths)
     # entity and relation ids are global in the subgraph, so its Triples are
     # the full graph's
     return PathResult(res.paths, res.truncated)
+
+
+def walk_subgraph(q0: EntityVector, k: int, pg: PartitionedGraph):
+    """(s, r, o) of every triple activated by q0's exact-walk trace, in
+    ascending global tid order.  Every rank resolves the columns of ITS
+    activated triples (it owns them) on its device and the owners' pieces
+    are gathered -- no rank holds the full triple columns."""
+    import torch
+
+    ids = q0.ids.astype(np.int32)
+    wq = WaveQuery(np.array([0, ids.size], dtype=np.int32), ids, k, HopSemantics.EXACT_WALK, None, True)
+    mine = []
+    for sh, r in zip(pg.shards, pg.run(wq)):
+        a = r.a_ids.long() if r.a_ids is not None else torch.empty(0, dtype=torch.int64)
+        tids = torch.unique(a)  # a triple may be activated at several hops
+        s_, r_, o_ = sh.triples_of(tids)
+        mine.append({"tid": tids.int(), "s": s_, "r": r_, "o": o_})
+    parts = pg.exchange.gather(mine)
+    tid = torch.cat([p["tid"].long().cpu() for p in parts])
+    order = torch.argsort(tid)  # owners are disjoint: ascending global tids
+    return tuple(torch.cat([p[c].cpu() for p in parts])[order].numpy() for c in ("s", "r", "o"))

@@ -96,6 +96,29 @@ def test_two_waves_and_overflow_rerun(th):
             assert np.array_equal(part.frontier(i, h), single.frontier(i, h))
 
 
+def test_inbox_overflow_grows_and_reconnects(th):
+    """An exchange inbox far too small for a wave: the receivers flag the
+    overflow, every rank grows its region, the ranks reconnect and the wave
+    runs again -- results identical to the single-graph engine."""
+    s, r, o = _hub_graph(2000, 40000, 8, seed=21)
+    E, R = 2000, 8
+    g = th.build_incidence((s, r, o), E, R)
+
+    def small(cols, n_e, n_r, plan, rank):
+        return th.partition.GraphShard(cols, n_e, n_r, plan, rank, inbox_records=1024)
+
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(3), n_hubs=4, shard_factory=small)
+    pg.pull_divisor = 0.0  # push only: every candidate becomes an inbox record
+    seeds = np.random.default_rng(2).integers(0, E, 300)
+    part = pg.retrieve(seeds, 3)
+    assert all(sh.inbox_records > 1024 for sh in pg.shards)
+    single = th.retrieve(g, seeds, 3)
+    for i in range(0, 300, 11):
+        for h in range(1, 4):
+            assert np.array_equal(part.frontier(i, h), single.frontier(i, h))
+            assert int(part.edges[h - 1, i]) == int(single.edges[h - 1, i])
+
+
 @pytest.mark.parametrize("name", ["tiny", "er30_s0", "er60_s12", "pl500_hubs", "selfloop", "objonly"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_cross_graph_k_hop_golden(th, name, world):
@@ -164,9 +187,11 @@ def test_cross_graph_paths_golden(th, name):
 
 
 def _gpu_dist_worker(rank, world, port, errfile):
-    """One rank with a REAL CUDA shard; gloo carries the exchange (host-staged)
-    because NCCL refuses two ranks on one device.  No kernel of one rank waits
-    on another rank."""
+    """One rank per process with a REAL CUDA shard on the same device: the
+    ranks' kernels write into each other's exchange regions through CUDA IPC
+    mappings; gloo carries the phase barriers and the result gather (NCCL
+    refuses two ranks on one device).  No kernel of one rank waits on
+    another rank (the barriers are host-side)."""
     import os
 
     import torch
@@ -193,7 +218,15 @@ def _gpu_dist_worker(rank, world, port, errfile):
                     assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h])
                     assert np.array_equal(res.activated(i, h + 1), ref["activated"][h])
                     assert int(res.edges[h, i]) == ref["edges"][h]
-        assert xch.bytes_sent > 0
+        stats = {}
+        q = th.partition.WaveQuery(np.arange(151, dtype=np.int32), seeds.astype(np.int32), 2,
+                                   th.HopSemantics.FRONTIER)
+        pg.run(q, stats)
+        assert sum(stats["sent_records"][0]) > 0  # records crossed processes
+        pr = th.cross_graph_paths(th.EntityVector([int(seeds[0])], E), 2, pg, max_paths=100)
+        ref_p, ref_t = orc.walk_paths(og, [int(seeds[0])], 2, 100)
+        assert [tuple(tuple(int(x) for x in t) for t in p) for p in pr.paths] == orc.paths_as_triples(og, ref_p)
+        assert pr.truncated == ref_t
     except BaseException as e:  # pragma: no cover - reported to the parent
         with open(errfile, "a") as f:
             f.write(f"rank {rank}: {type(e).__name__}: {e}\n")

@@ -2,9 +2,10 @@
 exchange protocol (world_size 2 over gloo, one process per rank).
 
 The per-rank arithmetic runs in tests/shard_ref.py (numpy stand-in with
-the CUDA shard's layout and record format); the collectives, routing and
-merging are the product code of paper_2604_18913_b200.partition.  The CUDA
-shards themselves are checked on the GPU (tests/test_gpu_partition.py)."""
+the CUDA shard's layout and record format, exchange regions in host shared
+memory); the wave protocol, region wiring, barriers, gathers and merging are
+the product code of paper_2604_18913_b200.partition.  The CUDA shards
+themselves are checked on the GPU (tests/test_gpu_partition.py)."""
 
 import os
 import socket
@@ -156,7 +157,18 @@ def _dist_worker(rank, world, port, errfile):
         for h in range(2):
             assert np.array_equal(tr.frontier(h + 1).ids, ref[h][0])
             assert np.array_equal(tr.activated(h + 1).ids, ref[h][1])
-        assert xch.bytes_sent > 0  # records really crossed ranks
+        stats = {}
+        q = th.partition.WaveQuery(np.arange(61, dtype=np.int32), seeds.astype(np.int32), 2,
+                                   th.HopSemantics.FRONTIER)
+        pg.run(q, stats)
+        assert sum(stats["sent_records"][0]) > 0  # records really crossed ranks
+        # cross_graph_paths' input: the walk subgraph gathered from the owners
+        # (the path enumeration itself needs the device, test_gpu_partition)
+        for seeds_p in ([3], [1, 7, 42]):
+            s_, r_, o_ = th.partition.walk_subgraph(th.EntityVector(seeds_p, 500), 2, pg)
+            act = np.unique(np.concatenate([a for _, a in orc.hop_trace(og, seeds_p, 2, orc.EXACT)]))
+            assert np.array_equal(s_, og.subj[act]) and np.array_equal(r_, og.rel[act])
+            assert np.array_equal(o_, og.obj[act])
     except BaseException as e:  # pragma: no cover - reported to the parent
         with open(errfile, "a") as f:
             f.write(f"rank {rank}: {type(e).__name__}: {e}\n")
