@@ -1837,10 +1837,17 @@ WaveBufs shard_bufs(Shard* sh) {
   b.heavy = static_cast<int32_t*>(s->heavy.p);
   b.counts = static_cast<int32_t*>(s->counts.p);
   b.totals = static_cast<int64_t*>(s->totals.p);
-  b.counts2 = b.counts;  // shards run K4 on one stream (slot 0 only)
-  b.totals2 = b.totals;
+  b.counts2 = static_cast<int32_t*>(s->counts2.p);  // second K4 slot (overlapped layers)
+  b.totals2 = static_cast<int64_t*>(s->totals2.p);
   b.ctl = static_cast<Ctl*>(s->ctl.p);
   return b;
+}
+
+// edge counts come from the seeds / the previous layer's K4 (unfiltered
+// FRONTIER/EXACT waves without hub slices, whose rows K4 does not cover)
+bool shard_fused_edges(const Shard* sh) {
+  const th_query& q = sh->s.last;
+  return sh->H == 0 && !q.d_rel_masks && q.semantics != TH_CUMULATIVE;
 }
 
 template <int W>
@@ -1866,6 +1873,8 @@ void shard_begin_w(Shard* sh, const th_query* q) {
   if (q->d_rel_masks) ensure<uint32_t>(s->M, std::max<int64_t>(sh->g.R, 1) * W, st);
   ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
   ensure<int64_t>(s->totals, kMaxWave, st);
+  ensure<int32_t>(s->counts2, (int64_t)kMaxWave * (kMatBlocks + 64), st);
+  ensure<int64_t>(s->totals2, kMaxWave, st);
   if (sh->world > 1) {
     // remote staging, global-indexed (push pre-dedupe, pull frontier copy)
     const int64_t E = std::max<int64_t>(sh->E, 1);
@@ -1896,13 +1905,23 @@ void shard_begin_w(Shard* sh, const th_query* q) {
     s->launches += 1;
   }
   shard_seed_kernel<W><<<grid_for((int64_t)q->n_queries * 32), kThreads, 0, st>>>(
-      sa, q->d_seed_offsets, q->d_seeds);
+      sa, q->d_seed_offsets, q->d_seeds,
+      shard_fused_edges(sh) ? static_cast<int64_t*>(s->edges.p) : nullptr);
   TH_LAUNCHED();
   shard_publish_cost_kernel<<<1, kMaxWorld, 0, st>>>(sa, 0);  // hop 1's frontier = the seeds
   TH_LAUNCHED();
   s->launches += 2;
   sh->next_hop = 1;
   sh->next_phase = 0;
+}
+
+// frontier-only waves overlap each layer's K4 with the next hop
+bool shard_overlaps(Shard* sh) {
+  const th_query& q = sh->s.last;
+  const bool on = sh->s.overlap && (q.flags & TH_WANT_FRONTIERS) && !(q.flags & TH_WANT_ACTIVATED) &&
+                  q.semantics != TH_CUMULATIVE;
+  if (on) ensure_side_stream(&sh->s);
+  return on;
 }
 
 // phase 0: direction, edge counts, activated triples, then push (local
@@ -1926,7 +1945,9 @@ void shard_send_w(Shard* sh, int h) {
     s->launches += 1;
   }
   int64_t* e_out = static_cast<int64_t*>(s->edges.p) + (h - 1) * B;
-  {
+  // (no hub slices and no filter: the previous layer's K4 (or the seeds)
+  // already summed the expanded rows' out-degrees)
+  if (!shard_fused_edges(sh)) {
     ProfScope ps(s, TH_PROF_EDGES);
     if (filter) {
       edge_count_filtered_kernel<W><<<pg, kThreads, 0, st>>>(sa.a, e_out, 0);
@@ -2058,18 +2079,54 @@ void shard_end_w(Shard* sh, int h) {
     TH_LAUNCHED();
     s->launches += 1;
   }
+  // as in run_wave: the layer's K4 runs on a side stream (consecutive
+  // layers alternate between two, with their own scratch) and overlaps the
+  // next hop's phases, which only read the layer
+  const bool overlap = shard_overlaps(sh);
   if (q.flags & TH_WANT_FRONTIERS) {
-    ProfScope ps(s, TH_PROF_FRONTIER);
-    int64_t* f_off = static_cast<int64_t*>(s->f_off.p) + (h - 1) * B;
-    int64_t* f_len = static_cast<int64_t*>(s->f_len.p) + (h - 1) * B;
-    int32_t* ids = static_cast<int32_t*>(s->f_ids.p);
-    if (q.semantics == TH_CUMULATIVE)
-      materialize_dense<W>(s, b, b.V, b.S, b.Vf, (int)B, f_off, f_len, ids, s->f_cap, &b.ctl->ids_used);
-    else
-      materialize_dense<W>(s, b, b.N, nullptr, b.Nf, (int)B, f_off, f_len, ids, s->f_cap,
-                           &b.ctl->ids_used);
+    const int slot = overlap ? (int)(h & 1) : 0;
+    cudaStream_t kst = slot ? s->side2 : s->side;
+    if (overlap) {
+      TH_CUDA(cudaEventRecord(s->ev_expand[h], st));
+      TH_CUDA(cudaStreamWaitEvent(kst, s->ev_expand[h], 0));
+    }
+    StreamScope scope(s, overlap ? kst : st);
+    s->k4_slot = slot;
+    s->mark_counted = overlap ? s->ev_cnt[h] : nullptr;
+    s->counted_recorded = false;
+    {
+      ProfScope ps(s, TH_PROF_FRONTIER);
+      int64_t* f_off = static_cast<int64_t*>(s->f_off.p) + (h - 1) * B;
+      int64_t* f_len = static_cast<int64_t*>(s->f_len.p) + (h - 1) * B;
+      int32_t* ids = static_cast<int32_t*>(s->f_ids.p);
+      if (q.semantics == TH_CUMULATIVE) {
+        materialize_dense<W>(s, b, b.V, b.S, b.Vf, (int)B, f_off, f_len, ids, s->f_cap, &b.ctl->ids_used);
+      } else {
+        // the layer is the next hop's frontier: its K4 count pass also
+        // yields |T_{h+1}(q)| (all of this rank's expanded rows when there
+        // are no hub slices)
+        EdgeSum es{};
+        if (h < q.k && shard_fused_edges(sh)) {
+          int nplanes = 0;
+          while (nplanes < 31 && (int64_t(1) << nplanes) <= sh->g.max_out) ++nplanes;
+          es.indptr = sh->g.indptr;
+          es.nplanes = nplanes;
+          es.out = static_cast<int64_t*>(s->edges.p) + h * B;
+        }
+        materialize_dense<W>(s, b, b.N, nullptr, b.Nf, (int)B, f_off, f_len, ids, s->f_cap,
+                             &b.ctl->ids_used, es);
+      }
+    }
+    if (overlap) {
+      TH_CUDA(cudaEventRecord(s->ev_mat[h], kst));
+      if (!s->counted_recorded) TH_CUDA(cudaEventRecord(s->ev_cnt[h], kst));
+    }
+    s->mark_counted = nullptr;
+    s->k4_slot = 0;
   }
   {
+    // retiring X (layer h-1) waits until that layer's K4 read it
+    if (overlap && h > 1) TH_CUDA(cudaStreamWaitEvent(st, s->ev_cnt[h - 1], 0));
     ProfScope ps(s, TH_PROF_CLEAR);
     clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, h - 1, h - 1, rows);
     TH_LAUNCHED();
@@ -2093,8 +2150,15 @@ void shard_retire_w(Shard* sh) {
   const int k = q.k;
   WaveBufs b = shard_bufs<W>(sh);
   const int64_t rows = std::max<int64_t>(sh->rows(), 1);
+  const bool overlap = shard_overlaps(sh);
+  if (overlap) TH_CUDA(cudaStreamWaitEvent(st, s->ev_cnt[k], 0));
   clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.X, b.lists, b.ctl, k, k, rows);
   TH_LAUNCHED();
+  if (overlap) {
+    // results of the last two layers' K4s are complete before th_finish
+    TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k], 0));
+    if (k > 1) TH_CUDA(cudaStreamWaitEvent(st, s->ev_mat[k - 1], 0));
+  }
   if (q.semantics != TH_EXACT) {
     clear_rows_kernel<W><<<grid_for(rows * W), kThreads, 0, st>>>(b.V, b.lists, b.ctl, 0, k, rows);
     TH_LAUNCHED();

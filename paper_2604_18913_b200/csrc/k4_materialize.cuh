@@ -61,6 +61,8 @@ struct DenseSrc {
   }
   __device__ __forceinline__ int64_t rows_dev() const { return nrows; }
   __device__ __forceinline__ int32_t id(int64_t r) const { return map ? map[r] : (int32_t)r; }
+  // the graph row of list position r (unmapped: out-degrees are the row's)
+  __device__ __forceinline__ int32_t row(int64_t r) const { return (int32_t)r; }
 };
 
 // rows = the ascending list of nonzero entity rows of a layer (compacted
@@ -95,6 +97,7 @@ struct ListSrc {
     const int32_t v = __ldg(rows + r);
     return map ? __ldg(map + v) : v;
   }
+  __device__ __forceinline__ int32_t row(int64_t r) const { return __ldg(rows + r); }
 };
 
 // rows = triples in tid order; word j of row t = X[subj[t]] & M[rel[t]]
@@ -129,6 +132,7 @@ struct TripleSrc {
   }
   __device__ __forceinline__ int64_t rows_dev() const { return nrows; }
   __device__ __forceinline__ int32_t id(int64_t r) const { return map ? map[r] : (int32_t)r; }
+  __device__ __forceinline__ int32_t row(int64_t r) const { return (int32_t)r; }
 };
 
 template <int W>
@@ -356,7 +360,7 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       __syncthreads();  // the previous chunk's readers are done
       for (int t = warp; t < 32; t += NW) {
         const uint32_t ft = __shfl_sync(TH_FULL, cflags, t);
-        const uint32_t d = ((ft >> lane) & 1u) ? degree(es, src.id(c0 + 32 * t + lane)) : 0u;
+        const uint32_t d = ((ft >> lane) & 1u) ? degree(es, src.row(c0 + 32 * t + lane)) : 0u;
         const uint32_t lo = d & 0xffu;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -420,7 +424,7 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
             while (bg) {
               const int i = __ffs(bg) - 1;
               bg &= bg - 1u;
-              esum += (unsigned long long)(degree(es, src.id(c0 + 32 * t + i)) >> 8) << 8;
+              esum += (unsigned long long)(degree(es, src.row(c0 + 32 * t + i)) >> 8) << 8;
             }
           }
           if (BUILD_S) {
@@ -432,7 +436,7 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
           if (BUILD_S) S[lane * kSStride + t] = 0u;
           if (anyx) {
             uint32_t d = 0u;
-            if (EDGES && xu) d = degree(es, src.id(r));
+            if (EDGES && xu) d = degree(es, src.row(r));
             if (BUILD_S) {
               __syncwarp();
               touched |= __reduce_or_sync(TH_FULL, xu);

@@ -114,9 +114,11 @@ __device__ __forceinline__ bool remote_stage(const ShardArgs& sa, int32_t v, int
 
 // seeds: owned seeds set local rows; hub seeds set their hub rows (every rank
 // sees every seed, so hub rows need no exchange at hop 0)
+// (e_out: |T_1(q)| = out-degree sum of q's distinct owned seeds, when the
+// edge counts are fused -- no hub slices)
 template <int W>
 __global__ void shard_seed_kernel(ShardArgs sa, const int32_t* __restrict__ qoff,
-                                  const int32_t* __restrict__ seeds) {
+                                  const int32_t* __restrict__ seeds, int64_t* e_out) {
   const WaveArgs& a = sa.a;
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -125,6 +127,7 @@ __global__ void shard_seed_kernel(ShardArgs sa, const int32_t* __restrict__ qoff
     const int32_t lo = qoff[q], hi = qoff[q + 1];
     const uint32_t qb = 1u << (q & 31);
     const int qw = q >> 5;
+    unsigned long long dsum = 0ull;
     for (int32_t i0 = lo; i0 < hi; i0 += 32) {
       const int32_t i = i0 + lane;
       int32_t row = -1, hrow = -1;
@@ -141,7 +144,8 @@ __global__ void shard_seed_kernel(ShardArgs sa, const int32_t* __restrict__ qoff
       bool fresh = false, hfresh = false;
       if (row >= 0) {
         const size_t r = (size_t)row * W + qw;
-        atomicOr(&a.X[r], qb);
+        const uint32_t was = atomicOr(&a.X[r], qb);
+        if (e_out && !(was & qb)) dsum += (unsigned long long)(a.indptr[row + 1] - a.indptr[row]);
         if (a.sem != TH_EXACT) atomicOr(&a.V[r], qb);
         if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
         const uint32_t fb = 1u << (row & 31);
@@ -157,6 +161,11 @@ __global__ void shard_seed_kernel(ShardArgs sa, const int32_t* __restrict__ qoff
       warp_append_all(fresh, row, d, a.lists, &a.ctl->list_len[0], a.E, &a.ctl->push_cost[0]);
       const uint32_t hd = hfresh ? (uint32_t)(a.indptr[hrow + 1] - a.indptr[hrow]) : 0u;
       warp_append_all(hfresh, hrow, hd, a.lists, &a.ctl->list_len[0], a.E, &a.ctl->push_cost[0]);
+    }
+    if (e_out) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) dsum += __shfl_xor_sync(TH_FULL, dsum, o);
+      if (lane == 0) e_out[q] = (int64_t)dsum;
     }
   }
 }

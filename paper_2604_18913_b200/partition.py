@@ -444,9 +444,9 @@ class GraphShard:
         q = _lib.Query()
         B = query.n_queries
         self._dev = {
-            "offs": torch.from_numpy(query.seed_offsets).to(self.device),
-            "seeds": torch.from_numpy(query.seeds).to(self.device),
-            "masks": None if query.masks is None else torch.from_numpy(query.masks.view(np.int32)).to(self.device),
+            "offs": self._upload("offs", query.seed_offsets),
+            "seeds": self._upload("seeds", query.seeds),
+            "masks": None if query.masks is None else self._upload("masks", query.masks.view(np.int32)),
         }
         q.n_queries = B
         q.d_seed_offsets = self._dev["offs"].data_ptr()
@@ -459,6 +459,29 @@ class GraphShard:
         q.max_paths = 0
         self._q = q
         _lib.check(_lib.load().th_shard_begin(self._handle, ctypes.byref(q)))
+
+    def _upload(self, name, arr):
+        """Asynchronous H2D copy through a reused pinned staging buffer,
+        ordered on the shard's stream before the wave's kernels (the buffer
+        is rewritten only once its previous copy has finished)."""
+        import torch
+
+        a = np.ascontiguousarray(arr).reshape(-1)
+        pins = self.__dict__.setdefault("_pins", {})
+        buf, done = pins.get(name, (None, None))
+        if buf is None or buf.numel() < a.size:
+            buf = torch.empty(max(a.size, 1) * 2, dtype=torch.from_numpy(a[:0]).dtype).pin_memory()
+            done = None
+        if done is not None:
+            done.synchronize()  # the previous copy out of this buffer has finished
+        buf[: a.size].copy_(torch.from_numpy(a))
+        dev = torch.empty(a.size, dtype=buf.dtype, device=self.device)
+        with torch.cuda.stream(self.stream):
+            dev.copy_(buf[: a.size], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.stream)
+        pins[name] = (buf, done)
+        return dev.reshape(arr.shape)
 
     def hop(self, hop: int, phase: int) -> None:
         _lib.check(_lib.load().th_shard_hop(self._handle, hop, phase))
