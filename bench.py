@@ -50,17 +50,43 @@ BATCH = 1024
 
 # ----------------------------------------------------------------- helpers
 
-def load_traffic(group: str) -> dict:
-    """DRAM bytes per step of a kernel group from the latest committed ncu
-    capture of one C2 k=3 step (profiles/r*_c2_traffic.json, written by
-    tools/ncu_traffic.py from `ncu --set full`)."""
-    files = sorted((ROOT / "profiles").glob("r*_c2_traffic.json"))
+def load_traffic(group: str, cfg: str = "c2") -> dict:
+    """DRAM bytes per step (C2: one k=3 batch; C4: one k=3 wave) of a kernel
+    group from the latest committed ncu capture (profiles/r*_<cfg>_traffic.json,
+    written by tools/ncu_traffic.py from `ncu --set full`)."""
+    files = sorted((ROOT / "profiles").glob(f"r*_{cfg}_traffic.json"))
     if not files:
         return {}
     d = json.loads(files[-1].read_text())
     if group not in d:
         return {}
-    return {"bytes": d[group]["bytes"], "source": f"{files[-1].name} (ncu --set full, one step)"}
+    return {"bytes": d[group]["bytes"], "ncu_us": d[group].get("us"),
+            "source": f"{files[-1].name} (ncu --set full, one {'step' if cfg == 'c2' else 'k=3 wave'})"}
+
+
+def pull_alg_bytes(n_items: int, n_in_edges: int, W: int, lists: list, modes: list, sem_frontier=True):
+    """Algorithmic bytes of the pull hops of a wave (SURVEY 8d restated for
+    the dense direction): per pull hop h, the static schedule (12 B per item),
+    every in-edge source (4 B), each frontier row once (4W B) and each newly
+    reached row's next-layer write (4W B; + its visited row, 4W B, except on
+    FRONTIER's last hop)."""
+    k = len(lists) - 1
+    b = 0
+    for h in range(1, k + 1):
+        if modes[h]:
+            rows_out = lists[h] * (1 if (sem_frontier and h == k) else 2)
+            b += 12 * n_items + 4 * n_in_edges + 4 * W * lists[h - 1] + 4 * W * rows_out
+    return b
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def load_peaks() -> dict:
@@ -227,6 +253,7 @@ def run_reference(args, world, rank):
                    "step_sample_seeds": per_step},
         "edges_per_s": total_edges / t,
         "cpu_baseline": {"value": value, "unit": "seeds/s", "cores": cores, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{per_step} seeds of the first C2 batch per step, "
                                    "oracle/khop_oracle.hop_trace per seed, persistent fork pool"},
         "e2e": {"value": value, "unit": "seeds/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -336,6 +363,7 @@ def run_c4_leg(th, stream, peaks, n_batches=8, cols=None):
     s, r, o, E, R = cols if cols is not None else workloads.c4_graph()
     gen_s = time.perf_counter() - t0
     stats = workloads.graph_stats(s, o, E)
+    n_items = int(((np.bincount(o, minlength=E) + 31) // 32).sum())  # static pull items
     g = th.build_incidence((s, r, o), E, R)
     del s, r, o, cols
     ret = th.Retriever(g, stream)
@@ -351,28 +379,44 @@ def run_c4_leg(th, stream, peaks, n_batches=8, cols=None):
                                  copy=False)
         step(0)  # sizes the result buffers
         step(1)  # graph capture of this shape
-        tot_ms, seeds, edges, ids, lists = 0.0, 0, 0, 0, 0
+        tot_ms, seeds, edges, ids, lists, pbytes = 0.0, 0, 0, 0, 0, 0
+        W = 32
         for i in range(n_batches):
             ms, res = _timed(stream, lambda: step(i))
             tot_ms += ms
             seeds += BATCH
             edges += int(res.edges.sum().item())
             ids += int(res.frontier_len.sum().item())
-            lists += sum(ret.wave_lists(k)[1:])
+            wl = ret.wave_lists(k)
+            lists += sum(wl[1:])
+            pbytes += pull_alg_bytes(n_items, stats["n_triples"], W, wl, ret.wave_modes(k))
         prof = _profiled(ret, [lambda i=i: step(i) for i in range(n_batches)])
         kms = {c: v[0] / n_batches for c, v in prof.items() if v[0]}
         dom = max(("frontier", "pull", "push"), key=lambda c: kms.get(c, 0.0))
         leg = {"seeds_per_s": seeds / (tot_ms / 1e3), "edges_per_s": edges / (tot_ms / 1e3),
                "ms_per_batch": tot_ms / n_batches, "frontier_ids_per_batch": ids / n_batches,
                "kernel_ms_per_batch": kms, "dominant": dom}
-        if dom == "frontier":
-            W = 32
-            kbytes = 4 * ids + 4 * W * lists + 16 * k * seeds
-            a = kbytes / (prof["frontier"][0] / 1e3) / 1e9
-            leg["roofline"] = {"bound": "hbm", "achieved": a, "peak": peaks_leg["hbm_gbs"], "unit": "GB/s",
-                               "frac": a / peaks_leg["hbm_gbs"], "kernel": "K4 frontier",
-                               "alg_bytes_per_batch": kbytes / n_batches,
-                               "note": "4 B per output id + 4W B per nonzero layer row + offsets"}
+        # K4 (frontier materialisation) and the pull hop (the north star's
+        # hop kernel), each against its own algorithmic bytes; kernel times
+        # are CUDA events on each kernel's own stream in a profiled pass over
+        # the same batches (K4 runs on side streams overlapping the next
+        # hop, so its event time includes that contention)
+        kbytes = 4 * ids + 4 * W * lists + 16 * k * seeds
+        for key, group, b, note in (
+                ("roofline", "frontier", kbytes, "K4: 4 B per output id + 4W B per nonzero layer row + offsets"),
+                ("roofline_pull", "pull", pbytes,
+                 "pull hops: 12 B per item + 4 B per in-edge + 4W B per frontier row + 4W B per "
+                 "new row (x2 with its visited row)")):
+            t = prof[group][0]
+            if t <= 0 or b <= 0:
+                continue
+            a = b / (t / 1e3) / 1e9
+            tr = load_traffic(group, "c4") if k == 3 else {}
+            leg[key] = {"bound": "hbm", "achieved": a, "peak": peaks_leg["hbm_gbs"], "unit": "GB/s",
+                        "frac": a / peaks_leg["hbm_gbs"], "kernel": group,
+                        "kernel_ms_per_batch": t / n_batches, "alg_bytes_per_batch": b / n_batches,
+                        "traffic": tr.get("bytes"), "traffic_source": tr.get("source"),
+                        "note": note}
         out[f"k{k}"] = leg
     del ret, g
     torch.cuda.empty_cache()
@@ -534,6 +578,8 @@ def run_ours(args, world, rank, local):
     edges = ids = 0
     alg_bytes = 0
     lists_sum = 0
+    pull_bytes = 0
+    n_items = int(((np.bincount(o, minlength=E) + 31) // 32).sum())  # static pull items
     t_wall0 = time.perf_counter()
     for i in range(args.steps):
         flush.zero_()
@@ -548,7 +594,9 @@ def run_ours(args, world, rank, local):
         # SURVEY 8d per-seed algorithmic bytes: 8|X_{h-1}| + 4|T_h| + 4|Out_h|
         xs = torch.cat([torch.ones(1, BATCH, dtype=torch.int64, device=dev), fl[:-1]]).sum().item()
         alg_bytes += 8 * xs + 4 * e + 4 * int(fl.sum().item())
-        lists_sum += sum(ret.wave_lists(K_HOPS)[1:])
+        wl = ret.wave_lists(K_HOPS)
+        lists_sum += sum(wl[1:])
+        pull_bytes += pull_alg_bytes(n_items, int(s.size), 32, wl, ret.wave_modes(K_HOPS))
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall0
     clk = clocks.stop()
@@ -616,6 +664,16 @@ def run_ours(args, world, rank, local):
     kms = prof[dominant][0]
     achieved = kbytes / (kms / 1e3) / 1e9 if kms > 0 else 0.0
     traffic = load_traffic(dominant)
+    # the pull hop (the north star's hop kernel) against its own bytes
+    pms = prof["pull"][0]
+    pull_ach = pull_bytes / (pms / 1e3) / 1e9 if pms > 0 else 0.0
+    ptraffic = load_traffic("pull")
+    roofline_pull = {"bound": "hbm", "achieved": pull_ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": pull_ach / peaks["hbm_gbs"], "kernel": "pull",
+                     "kernel_ms_per_step": pms / args.steps, "alg_bytes_per_step": pull_bytes / args.steps,
+                     "traffic": ptraffic.get("bytes"), "traffic_source": ptraffic.get("source"),
+                     "note": "pull hops: 12 B per item + 4 B per in-edge + 4W B per frontier row + 4W B "
+                             "per new row (x2 with its visited row); C2's 69 MB graph state is L2-resident"}
 
     # e2e through the public API: pinned host seeds in, host results out
     e2e_times, h2d, d2h = [], 0, 0
@@ -656,7 +714,7 @@ def run_ours(args, world, rank, local):
         pool = cpu_pool(cores)
         n, e, dt = cpu_run(pool, batches[0], K_HOPS, args.cpu_budget)
         pool.terminate()
-        cpu = {"value": n / dt, "unit": "seeds/s", "cores": cores, "kind": "port",
+        cpu = {"value": n / dt, "unit": "seeds/s", "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"first {n} seeds of the first timed C2 batch (k={K_HOPS} FRONTIER, "
                          f"oracle hop_trace per seed, fork pool, {dt:.1f} s)",
                "edges_per_s": e / dt}
@@ -698,6 +756,7 @@ def run_ours(args, world, rank, local):
                          "traffic_source": traffic.get("source"), "kernel": dominant,
                          "kernel_ms_per_step": kms / args.steps, "alg_bytes_per_step": kbytes / args.steps,
                          "peak_source": peaks["source"], "note": note},
+            "roofline_pull": roofline_pull,
             "kernel_ms_per_step": {c: v[0] / args.steps for c, v in prof.items()},
             "kernel_ms_source": "CUDA events around each kernel group, profiled pass over the same K batches",
             "kernel_launches_per_step": {c: v[1] / args.steps for c, v in prof.items()},

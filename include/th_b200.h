@@ -170,14 +170,20 @@ int th_session_set_list_min_entities(th_session* s, int64_t min_entities);
 /* Overlap hop h's frontier materialisation (K4) with hop h+1's expansion
  * on an internal stream (frontier-only runs).  Default on. */
 int th_session_set_overlap(th_session* s, int on);
-/* Count pass of the list-driven K4 (graphs of at least list_min_entities
- * entities): 1 = row-major (whole-row loads, carry-save bit counting;
- * default), 0 = word-per-warp loads with bit-sliced counting. */
+/* K4 count pass: 0 = word-per-warp loads with bit transposes everywhere;
+ * 1 = row-major (whole-row loads, carry-save bit counting) for list-driven
+ * layers without fused edge counts (default); 2 = row-major for every
+ * entity layer (no mask cache for small dense layers). */
 int th_session_set_k4_mode(th_session* s, int mode);
 /* Pull hops screen their in-row items one per lane for a frontier in-edge
  * before lane groups expand the survivors: -1 = when the graph's mean
  * in-edges per pull item is below 4 (default), 0 = never, 1 = always. */
 int th_session_set_pull_screen(th_session* s, int mode);
+/* Boolean strategy knobs by name (A/B and tests): "paths_k2" (k = 2
+ * singleton capped path queries on a CTA each; default 1), "k4_cache"
+ * (small dense layers cache their tile masks; 1), "list_first_hop" (the
+ * first layer's overlapped K4 follows its row list; 1). */
+int th_session_set_knob(th_session* s, const char* name, int64_t value);
 /* Pull hops whose frontier sources more than 1/divisor of all in-edges
  * (by the frontier's out-degree sum) gather every in-neighbour row instead
  * of testing frontier flags first (default 2; <= 0 never). */
@@ -211,6 +217,8 @@ int th_session_profile(th_session* s, double* ms, int64_t* launches, int n);
 /* Entity-list lengths of the last wave: [0] = distinct seed entities,
  * [h] = entities newly set at hop h (rows of the hop-h layer).  n >= k+1. */
 int th_session_wave_lists(const th_session* s, int64_t* lens, int n);
+/* Direction of each hop of the last wave: [h] = 1 pull, 0 push ([0] = 0). */
+int th_session_wave_modes(const th_session* s, int32_t* modes, int n);
 
 /* ---- partitioning (multi-GPU ownership) -------------------------------- */
 

@@ -34,7 +34,7 @@ EXPORTS = (
     "th_shard_inbox_overflowed", "th_shard_hop", "th_shard_finish", "th_shard_sent", "th_shard_columns",
     "th_ids_route_count", "th_ids_map_scatter", "th_ids_to_local_bits", "th_bits_andnot_update",
     "th_bits_or", "th_bits_compact", "th_plan_subjects", "th_session_set_k4_mode",
-    "th_session_set_pull_screen",
+    "th_session_set_pull_screen", "th_session_wave_modes", "th_session_set_knob",
 )
 PROF_CATEGORIES = ("setup", "edges", "activated", "push", "pull", "frontier", "clear", "paths")
 
@@ -114,6 +114,7 @@ def load():
         "th_session_set_overlap": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_session_set_k4_mode": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_session_set_pull_screen": (ctypes.c_int, [_vp, ctypes.c_int]),
+        "th_session_set_knob": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int64]),
         "th_session_set_graphs": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_session_set_dense_pull": (ctypes.c_int, [_vp, ctypes.c_double]),
         "th_session_launch_count": (ctypes.c_int64, [_vp]),
@@ -122,6 +123,7 @@ def load():
         "th_session_profile": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_double),
                                               ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
         "th_session_wave_lists": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int]),
+        "th_session_wave_modes": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int32), ctypes.c_int]),
         "th_shard_create": (ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
                                            _vp, _vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
                                            ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, _vp,

@@ -255,11 +255,11 @@ int th_session_set_overlap(th_session* s, int on) {
 }
 
 int th_session_set_k4_mode(th_session* s, int mode) {
-  if (!s || mode < 0 || mode > 1) {
-    th::set_error(!s ? "NULL handle" : "k4 mode must be 0 or 1");
+  if (!s || mode < 0 || mode > 2) {
+    th::set_error(!s ? "NULL handle" : "k4 mode must be 0, 1 or 2");
     return TH_ERR_INVALID;
   }
-  s->s.k4_rowmajor = mode == 1;
+  s->s.k4_mode = mode;
   return TH_OK;
 }
 
@@ -269,6 +269,25 @@ int th_session_set_pull_screen(th_session* s, int mode) {
     return TH_ERR_INVALID;
   }
   s->s.pull_screen = mode;
+  return TH_OK;
+}
+
+int th_session_set_knob(th_session* s, const char* name, int64_t value) {
+  if (!s || !name) {
+    th::set_error("NULL argument");
+    return TH_ERR_INVALID;
+  }
+  const std::string n(name);
+  if (n == "paths_k2") {
+    s->s.paths_k2 = value != 0;
+  } else if (n == "k4_cache") {
+    s->s.k4_cache = value != 0;
+  } else if (n == "list_first_hop") {
+    s->s.list_first_hop = value != 0;
+  } else {
+    th::set_error("unknown knob " + n);
+    return TH_ERR_INVALID;
+  }
   return TH_OK;
 }
 
@@ -290,6 +309,16 @@ int th_session_profile(th_session* s, double* ms, int64_t* launches, int n) {
       return TH_ERR_INVALID;
     }
     return th::session_profile(&s->s, ms, launches, n);
+  });
+}
+
+int th_session_wave_modes(const th_session* s, int32_t* modes, int n) {
+  return guarded([&]() -> int {
+    if (!s || !modes) {
+      th::set_error("NULL handle");
+      return TH_ERR_INVALID;
+    }
+    return th::session_wave_modes(const_cast<th::Session*>(&s->s), modes, n);
   });
 }
 

@@ -26,6 +26,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "engine.cuh"
 #include "paths.cuh"
@@ -33,6 +35,17 @@
 namespace th {
 
 namespace {
+
+// NVTX range over a host scope (a wave, a hop, a shard phase): profilers
+// (nsys, ncu --nvtx) attribute the kernels launched inside it
+struct NvtxRange {
+  explicit NvtxRange(const char* fmt, int a = 0, int b = 0) {
+    char name[64];
+    std::snprintf(name, sizeof(name), fmt, a, b);
+    nvtxRangePushA(name);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -847,7 +860,7 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   // streams a layer-sized buffer through HBM twice, C4 k=3 18.5 -> 20.9 ms)
   if constexpr (Src::kDense && !Src::kRing) {
     const int64_t nchunks = ceil_div(rows, kChunkRows);
-    if (s->k4_cache && nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
+    if (s->k4_cache && s->k4_mode < 2 && nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
       SCache sc;
       sc.S = ensure<uint32_t>(kS, nchunks * W * 1024, s->st);
       sc.meta = ensure<uint2>(kMeta, nchunks * W + 1, s->st);
@@ -892,11 +905,11 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   }
   constexpr size_t smem_c = mat_smem_bytes<W, false>();
   bool counted = false;
-  if constexpr (Src::kRing) {
-    // (layers whose count pass also sums edge counts keep the word-per-warp
-    // form: its shared degree planes beat per-bit degree sums, C4 hop 2
-    // 0.47 vs 1.03 ms)
-    if (s->k4_rowmajor && !es.out) {
+  if constexpr (Src::kDense) {
+    // (k4_mode 1: list-driven layers without edge counts -- those keep the
+    // word-per-warp form: its shared degree planes beat per-bit degree sums,
+    // C4 hop 2 0.47 vs 1.03 ms; k4_mode 2: every entity layer)
+    if ((s->k4_mode == 1 && Src::kRing && !es.out) || s->k4_mode == 2) {
       // list-driven layers: whole-row loads, carry-save counting (k4_rowmajor.cuh)
       static std::atomic<uint64_t> attr_r{0};
       if (!(attr_r.load(std::memory_order_relaxed) & bit)) {
@@ -908,7 +921,17 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
                                      (int)rs_count_smem<false>()));
         attr_r.fetch_or(bit, std::memory_order_relaxed);
       }
-      RowMajorSrc<W> rsrc{src.A, src.neg, src.rows, src.n_dev, src.nq};
+      RowMajorSrc<W> rsrc{};
+      rsrc.A = src.A;
+      rsrc.neg = src.neg;
+      rsrc.nq = src.nq;
+      if constexpr (Src::kRing) {
+        rsrc.rows = src.rows;
+        rsrc.n_dev = src.n_dev;
+      } else {
+        rsrc.flags = src.flags;
+        rsrc.n_host = src.nrows;
+      }
       if (es.out)
         rs_count_kernel<W, true><<<nblk, 32 * kRsWarps, rs_count_smem<true>(), s->st>>>(rsrc, nblk,
                                                                                        counts, es);
@@ -1113,6 +1136,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   while (nplanes < 31 && (int64_t(1) << nplanes) <= g->max_out) ++nplanes;
   bool next_edges_done = !filter;  // hop 1's counts come from seed_init
   for (int h = 1; h <= k; ++h) {
+    NvtxRange nvtx_hop("th hop %d (wave of %d)", h, nq);
     a.h = h;
     a.last_frontier = h == k && sem == TH_FRONTIER;
     const bool edges_done = next_edges_done;
@@ -1307,6 +1331,15 @@ int session_profile(Session* s, double* ms, int64_t* launches, int n) {
   return TH_OK;
 }
 
+int session_wave_modes(Session* s, int32_t* modes, int n) {
+  if (!s->ctl.p) return TH_ERR_STATE;
+  TH_CUDA(cudaStreamSynchronize(s->st));
+  Ctl c;
+  TH_CUDA(cudaMemcpy(&c, s->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < kMaxK + 2; ++i) modes[i] = i >= 1 && i <= s->last.k ? c.mode[i] : 0;
+  return TH_OK;
+}
+
 int session_wave_lists(Session* s, int64_t* lens, int n) {
   if (!s->ctl.p) return TH_ERR_STATE;
   TH_CUDA(cudaStreamSynchronize(s->st));
@@ -1349,8 +1382,8 @@ static GraphKey graph_key(Session* s, const th_query* q) {
   k.pull_divisor = s->pull_divisor;
   k.dense_pull = s->dense_pull;
   k.list_min = s->list_min_entities;
-  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_rowmajor ? 8 : 0) |
-            ((s->pull_screen + 1) << 4);
+  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_mode << 8) |
+            ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0);
   k.epoch = session_alloc_sig(s);
   return k;
 }
@@ -1574,7 +1607,9 @@ static int run_body(Session* s, const th_query* q) {
     // capped queries whose slots fit 2 GiB take the single-DFS form
     if (q->max_paths > 0 && (int64_t)B * q->max_paths * k * 4 <= (int64_t(2) << 30))
       pa.tmp = ensure<int32_t>(s->p_tmp, (int64_t)B * q->max_paths * k, st);
+    pa.k2_parallel = s->paths_k2;
     ProfScope ps(s, TH_PROF_PATHS);
+    NvtxRange nvtx_paths("th paths (k=%d)", (int)k);
     s->launches += launch_paths(pa, st);
   }
   return TH_OK;
@@ -2399,6 +2434,7 @@ int shard_hop(Shard* sh, int h, int phase) {
     set_error("hop or phase out of sequence");
     return TH_ERR_STATE;
   }
+  NvtxRange nvtx_phase("th shard hop %d phase %d", h, phase);
   if (phase == 0) TH_W_DISPATCH(sh->W, shard_send_w<WW>(sh, h))
   else if (phase == 1) TH_W_DISPATCH(sh->W, shard_receive_w<WW>(sh, h))
   else TH_W_DISPATCH(sh->W, shard_end_w<WW>(sh, h))

@@ -61,8 +61,9 @@ struct Session {
   // runs; the main stream joins before it recycles the layer's rows)
   bool overlap = true;
   bool k4_cache = true;
+  bool paths_k2 = true;     // k = 2 singleton capped path queries: a CTA per query (paths.cu)
   int pull_screen = -1;     // pull items screened per lane first: -1 by graph shape, 0 off, 1 on
-  bool k4_rowmajor = true;  // list-driven layers count rows row-major (k4_rowmajor.cuh)
+  int k4_mode = 1;  // count pass: 0 word-per-warp, 1 row-major for list-driven layers, 2 for all (k4_rowmajor.cuh)
   bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr, side2 = nullptr;  // K4 streams (odd / even layers)
   int k4_slot = 0;                                // which K4 scratch set is in use
@@ -122,6 +123,7 @@ struct ProfScope {
 
 int session_profile(Session* s, double* ms, int64_t* launches, int n);
 int session_wave_lists(Session* s, int64_t* lens, int n);
+int session_wave_modes(Session* s, int32_t* modes, int n);
 
 int session_run(Session* s, const th_query* q);
 int session_finish(Session* s, th_result* out);

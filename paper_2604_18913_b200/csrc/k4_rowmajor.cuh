@@ -28,9 +28,12 @@ template <int W>
 struct RowMajorSrc {
   const uint32_t* A;
   const uint32_t* neg;
-  const int32_t* rows;   // ascending row list
-  const int32_t* n_dev;  // its length (device)
+  const int32_t* rows;     // ascending row list (nullptr: every row, filtered by `flags`)
+  const int32_t* n_dev;    // its length (device; nullptr: n_host)
   int nq;
+  const uint32_t* flags = nullptr;  // dense sources: "row is nonzero" bits
+  int64_t n_host = 0;
+  __device__ __forceinline__ int64_t count() const { return n_dev ? (int64_t)*n_dev : n_host; }
 };
 
 // kRsUnroll rows starting at list position i (< end): row numbers and this
@@ -40,7 +43,15 @@ __device__ __forceinline__ void rs_load(const RowMajorSrc<W>& src, int64_t i, in
                                         int32_t (&v)[kRsUnroll], uint32_t (&x)[kRsUnroll],
                                         uint32_t valid) {
   const unsigned lane = lane_id();
-  const int32_t mine = (int64_t)lane < kRsUnroll && i + lane < end ? __ldg(src.rows + i + lane) : -1;
+  int32_t mine = -1;
+  if ((int64_t)lane < kRsUnroll && i + lane < end) {
+    if (src.rows) {
+      mine = __ldg(src.rows + i + lane);
+    } else {
+      const int64_t r = i + lane;
+      mine = (!src.flags || ((__ldg(src.flags + (r >> 5)) >> (r & 31)) & 1u)) ? (int32_t)r : -1;
+    }
+  }
 #pragma unroll
   for (int u = 0; u < kRsUnroll; ++u) v[u] = __shfl_sync(TH_FULL, mine, u);
 #pragma unroll
@@ -145,9 +156,10 @@ constexpr size_t rs_count_smem() {
   return (size_t)(EDGES ? 2 : 1) * kRsWarps * 1024 * sizeof(uint32_t);
 }
 
-// counts[q * nblk + blk] = bits of query q in row block blk of the list
-// (the write pass's partition: whole kChunkRows chunks, blk_rows from the
-// device row count).  One CTA per block; its warps take contiguous slices.
+// counts[q * nblk + blk] = bits of query q in row block blk of the list (or
+// of the entity range, dense sources) -- the write pass's partition: whole
+// kChunkRows chunks, blk_rows from the row count.  One CTA per block; its
+// warps take contiguous slices.
 template <int W, bool EDGES>
 __global__ void __launch_bounds__(32 * kRsWarps) rs_count_kernel(RowMajorSrc<W> src, int nblk,
                                                                  int32_t* counts, EdgeSum es) {
@@ -160,7 +172,7 @@ __global__ void __launch_bounds__(32 * kRsWarps) rs_count_kernel(RowMajorSrc<W> 
   if (blk >= nblk) return;
   uint32_t* cnt = rs_smem + warp * 1024;
   uint32_t* esum = rs_smem + (kRsWarps + warp) * 1024;
-  const int64_t nrows = *src.n_dev;
+  const int64_t nrows = src.count();
   int64_t blk_rows = (nrows + nblk - 1) / nblk;
   blk_rows = blk_rows < kChunkRows ? kChunkRows : (blk_rows + kChunkRows - 1) / kChunkRows * kChunkRows;
   const int64_t r0 = (int64_t)blk * blk_rows;

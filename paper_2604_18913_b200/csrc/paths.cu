@@ -245,6 +245,93 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
   }
 }
 
+// k = 2, singleton queries, capped (the C3 shape): the paths of a query are
+// its seed's passing out-edges t1 (tid order) each followed by the passing
+// out-edges t2 of obj(t1) (tid order), so the paths starting with t1 occupy
+// a contiguous run whose length is the filtered degree of obj(t1).  A CTA
+// takes a query; its warps take the seed's out-edges kPathK2Warps at a time:
+// each warp counts its candidate's run (row length without a filter, one
+// ballot per 32 candidates with one), a block scan places the runs, and the
+// warps write the (t1, t2) pairs of runs that start below max_paths into the
+// query's slot -- so a hub query's enumeration is spread over 8 warps
+// instead of one warp's DFS (C3: the longest hub queries bounded K5).
+// Stops once max_paths + 1 walks are known (truncation).
+constexpr int kPathK2Warps = 8;
+
+__global__ void __launch_bounds__(32 * kPathK2Warps) paths_k2_kernel(PathArgs a) {
+  __shared__ int64_t run_s[kPathK2Warps];
+  __shared__ int64_t total_s;
+  const int warp = threadIdx.x >> 5;
+  const unsigned lane = lane_id();
+  const int64_t limit = a.max_paths + 1;
+  for (int q = blockIdx.x; q < a.B; q += gridDim.x) {
+    int64_t lo0 = 0, hi0 = 0;
+    const int32_t s = a.seeds[q];
+    if (s >= 0 && s < a.E) {
+      lo0 = a.indptr[s];
+      hi0 = a.indptr[s + 1];
+    }
+    int32_t* slot = a.tmp + (int64_t)q * a.max_paths * 2;
+    int64_t total = 0;  // walks placed so far (identical in every thread)
+    for (int64_t c0 = lo0; c0 < hi0 && total < limit; c0 += kPathK2Warps) {
+      // this warp's level-0 candidate and the run it heads
+      const int64_t i = c0 + warp;
+      int32_t t1 = 0;
+      int64_t rlo = 0, rhi = 0, run = 0;
+      if (i < hi0) {
+        t1 = a.csr_tid[i];
+        if (rel_ok(a, q, a.csr_rel[i])) {
+          const int32_t o = a.csr_obj[i];
+          rlo = a.indptr[o];
+          rhi = a.indptr[o + 1];
+        }
+      }
+      if (!a.masks) {
+        run = rhi - rlo;
+      } else {
+        for (int64_t b = rlo; b < rhi && run < limit; b += 32) {
+          const int64_t j = b + lane;
+          const bool ok = j < rhi && rel_ok(a, q, a.csr_rel[j]);
+          run += __popc(__ballot_sync(TH_FULL, ok));
+        }
+      }
+      if (lane == 0) run_s[warp] = run;
+      __syncthreads();
+      int64_t before = total;  // walks ahead of this warp's run
+      for (int w = 0; w < warp; ++w) before += run_s[w];
+      if (threadIdx.x == 0) {
+        int64_t t = total;
+        for (int w = 0; w < kPathK2Warps; ++w) t += run_s[w];
+        total_s = t;
+      }
+      // write the part of the run that lands in the slot
+      if (before < a.max_paths && run > 0) {
+        int64_t n = 0;  // passing candidates of the run seen so far
+        for (int64_t b = rlo; b < rhi && before + n < a.max_paths; b += 32) {
+          const int64_t j = b + lane;
+          const bool ok = j < rhi && rel_ok(a, q, a.csr_rel[j]);
+          const unsigned bal = __ballot_sync(TH_FULL, ok);
+          if (ok) {
+            const int64_t p = before + n + __popc(bal & lanemask_lt());
+            if (p < a.max_paths) {
+              slot[2 * p] = t1;
+              slot[2 * p + 1] = a.csr_tid[j];
+            }
+          }
+          n += __popc(bal);
+        }
+      }
+      __syncthreads();
+      total = total_s;
+      __syncthreads();  // (run_s / total_s are rewritten by the next chunk)
+    }
+    if (threadIdx.x == 0) {
+      a.p_cnt[q] = total < a.max_paths ? total : a.max_paths;
+      a.p_trunc[q] = total > a.max_paths;
+    }
+  }
+}
+
 // pack each query's slot of the single-pass buffer at its scanned offset
 // (warp per query); nothing is written past the capacity (th_finish then
 // reports the overflow and the run is repeated with room)
@@ -277,9 +364,15 @@ int launch_paths(const PathArgs& a, cudaStream_t st) {
       (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div((int64_t)a.B * 32, kPathThreads),
                                                        kNumSMs * 16));
   if (a.tmp) {
-    // capped: one writing DFS into per-query slots, then pack
+    // capped: one writing DFS into per-query slots (k = 2 singleton queries:
+    // a CTA per query, see paths_k2_kernel), then pack
     if (a.B > 0) {
-      paths_kernel<true, true><<<grid, kPathThreads, 0, st>>>(a);
+      if (a.k == 2 && a.singleton && a.k2_parallel) {
+        const unsigned g2 = (unsigned)std::min<int64_t>(a.B, kNumSMs * 8);
+        paths_k2_kernel<<<g2, 32 * kPathK2Warps, 0, st>>>(a);
+      } else {
+        paths_kernel<true, true><<<grid, kPathThreads, 0, st>>>(a);
+      }
       TH_LAUNCHED();
       launches += 1 + scan_exclusive<int64_t>(a.p_cnt, a.p_off, a.B, a.scratch, st);
     }

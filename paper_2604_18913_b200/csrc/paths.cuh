@@ -35,6 +35,7 @@ struct PathArgs {
   // max_paths-sized slot of tmp ([B][max_paths][k]), a compaction packs
   // them (instead of a counting DFS + a writing DFS); null = two passes
   int32_t* tmp = nullptr;
+  bool k2_parallel = true;  // k = 2 singleton capped queries: a CTA per query
 };
 
 int64_t scan_scratch_elems_i64(int64_t n);

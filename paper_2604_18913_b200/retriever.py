@@ -203,6 +203,13 @@ class Retriever:
         """Per-lane item screening in pull hops: -1 by graph shape (default), 0 off, 1 on."""
         _lib.check(_lib.load().th_session_set_pull_screen(self._handle, int(mode)))
 
+    def set_knob(self, name: str, value: int) -> None:
+        """Boolean strategy knobs: "paths_k2", "k4_cache", "list_first_hop"."""
+        _lib.check(_lib.load().th_session_set_knob(self._handle, name.encode(), int(value)))
+
+    def set_paths_k2(self, on: bool) -> None:
+        self.set_knob("paths_k2", int(bool(on)))
+
     def set_overlap(self, on: bool) -> None:
         """Overlap hop h's K4 with hop h+1's expansion (frontier-only runs)."""
         _lib.check(_lib.load().th_session_set_overlap(self._handle, int(bool(on))))
@@ -233,6 +240,12 @@ class Retriever:
         """Entity-list lengths of the last wave: seeds, then rows set at each hop."""
         buf = (ctypes.c_int64 * (k + 1))()
         _lib.check(_lib.load().th_session_wave_lists(self._handle, buf, k + 1))
+        return [int(x) for x in buf]
+
+    def wave_modes(self, k: int) -> list[int]:
+        """Direction of each hop of the last wave (index h = 1..k): 1 pull, 0 push."""
+        buf = (ctypes.c_int32 * (k + 1))()
+        _lib.check(_lib.load().th_session_wave_modes(self._handle, buf, k + 1))
         return [int(x) for x in buf]
 
     # -- raw device call ---------------------------------------------------

@@ -20,6 +20,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--oracle", type=int, default=0)
     ap.add_argument("--waves", type=int, default=16)
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run through PartitionedGraph (one rank, the device-side exchange protocol)")
     args = ap.parse_args()
     t0 = time.time()
     s, r, o, E, R = workloads.c5_graph_gpu()
@@ -29,6 +31,8 @@ def main():
     host = None
     if args.oracle:
         host = (s.cpu().numpy(), r.cpu().numpy(), o.cpu().numpy())
+    if args.partitioned:
+        return partitioned(args, s, r, o, E, R, host)
     t0 = time.time()
     g = th.build_incidence((s, r, o), E, R)
     del s, r, o
@@ -77,6 +81,60 @@ def main():
                 assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
                 assert int(res.edges[h, i]) == ref["edges"][h]
         print(f"oracle parity ok on {args.oracle} seeds ({time.time() - t0:.1f}s)", flush=True)
+
+
+def partitioned(args, s, r, o, E, R, host):
+    """C5 through the partitioned path on one rank: 64-bit exchange keys make
+    200M entities x 32 words addressable (round 1's 32-bit keys refused C5)."""
+    from paper_2604_18913_b200.retriever import _relation_masks
+
+    t0 = time.time()
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(1))
+    del s, r, o
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    print(f"partitioned build {time.time() - t0:.1f}s local_triples={pg.shards[0].local_triples} "
+          f"mem={torch.cuda.max_memory_allocated() / 1e9:.1f}GB", flush=True)
+    seeds, rel = workloads.c5_queries(E, R)
+    words = _relation_masks(list(rel), seeds.size, R)
+    sem = th.HopSemantics.FRONTIER
+
+    def wave(w, stats=None):
+        sl = slice(1024 * w, 1024 * (w + 1))
+        q = th.partition.WaveQuery(np.arange(1025, dtype=np.int32), seeds[sl], 2, sem, words[sl])
+        return pg.run(q, stats)
+
+    wave(0)
+    wave(1)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for w in range(args.waves):
+        wave(w)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    edges = ids = 0
+    for w in range(args.waves):
+        (part,) = wave(w)
+        edges += int(part.edges.sum())
+        ids += int(part.f_len.sum())
+    n = 1024 * args.waves
+    print(f"C5 partitioned (1 rank) k=2 filtered: {n} seeds in {ms:.1f} ms -> {n / ms * 1e3:.0f} seeds/s, "
+          f"{edges / ms * 1e3 / 1e9:.2f} G edges/s, ids/wave={ids / args.waves:.0f} "
+          f"peak_mem={torch.cuda.max_memory_allocated() / 1e9:.1f}GB", flush=True)
+    if args.oracle:
+        from oracle import khop_oracle as orc
+
+        og = orc.build_csr(*host, E, R)
+        base = 1024 * (args.waves - 1)
+        res = pg.retrieve(seeds[base:base + 1024], 2, relation_filter=list(rel[base:base + 1024]))
+        for i in range(0, 1024, 1024 // args.oracle):
+            ref = orc.retrieve_one(og, int(seeds[base + i]), 2, "frontier", rel[base + i])
+            for h in range(2):
+                assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
+                assert int(res.edges[h, i]) == ref["edges"][h]
+        print(f"oracle parity ok on {args.oracle} seeds", flush=True)
 
 
 if __name__ == "__main__":

@@ -11,7 +11,7 @@ import re
 import subprocess
 import sys
 
-GROUPS = {"frontier": r"mat_kernel<.*(DenseSrc|ListSrc)|mat_scan|flag_", "pull": r"pull_kernel",
+GROUPS = {"frontier": r"mat_kernel<.*(DenseSrc|ListSrc)|mat_scan|flag_|rs_count", "pull": r"pull_kernel",
           "push": r"push_(light|heavy)", "clear": r"clear_rows"}
 
 
@@ -32,7 +32,8 @@ def main(rep, out):
                     b += float(d[i]) * scale[units[i]]
                 i = hdr.index("gpu__time_duration.sum")
                 res[g]["bytes"] += b
-                res[g]["us"] += float(d[i]) * (1e-3 if units[i] == "nsecond" else 1e3 if units[i] == "msecond" else 1)
+                res[g]["us"] += float(d[i]) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+                                               "msecond": 1e3, "ms": 1e3}.get(units[i], 1.0)
                 res[g]["launches"] += 1
     res["source"] = rep
     json.dump(res, open(out, "w"), indent=1)

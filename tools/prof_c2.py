@@ -35,9 +35,13 @@ def main():
     if args.filter:
         rng = np.random.default_rng(5)
         flt = [rng.choice(R, 32, replace=False) for _ in range(seeds.numel())]
-    for _ in range(args.batches):
+    for b in range(args.batches):
+        if b == args.batches - 1:  # ncu --profile-from-start off: only the last batch
+            torch.cuda.synchronize()
+            torch.cuda.profiler.start()
         res = ret.retrieve(seeds, args.k, relation_filter=flt, paths=args.paths, copy=False)
     torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     print("ids", int(res.frontier_len.sum()), "edges", int(res.edges.sum()))
 
 
