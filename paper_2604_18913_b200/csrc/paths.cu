@@ -247,23 +247,72 @@ __global__ void __launch_bounds__(kPathThreads) paths_kernel(PathArgs a) {
 
 // k = 2, singleton queries, capped (the C3 shape): the paths of a query are
 // its seed's passing out-edges t1 (tid order) each followed by the passing
-// out-edges t2 of obj(t1) (tid order), so the paths starting with t1 occupy
-// a contiguous run whose length is the filtered degree of obj(t1).  A CTA
-// takes a query; its warps take the seed's out-edges kPathK2Warps at a time:
-// each warp counts its candidate's run (row length without a filter, one
-// ballot per 32 candidates with one), a block scan places the runs, and the
-// warps write the (t1, t2) pairs of runs that start below max_paths into the
-// query's slot -- so a hub query's enumeration is spread over 8 warps
-// instead of one warp's DFS (C3: the longest hub queries bounded K5).
-// Stops once max_paths + 1 walks are known (truncation).
+// out-edges t2 of obj(t1) (tid order).  A CTA takes a query and walks the
+// level-0 candidates in order (compacted 256 at a time); each candidate's
+// row of level-1 candidates is swept by the WHOLE CTA, 2,048 slots per step
+// (8 per thread, loads issued together, one block-wide ordered compaction
+// of all of them), so the long rows of hub objects -- which bounded the
+// one-warp DFS on C3's hub seeds -- go 8 warps wide.  Stops once
+// max_paths + 1 walks are known (truncation).  (Sweeping the candidates'
+// rows laid end to end instead, with a per-slot binary search for the row,
+// measured slower: C3 paths 2.55 vs 1.85 ms.)
 constexpr int kPathK2Warps = 8;
+constexpr int kPathK2Threads = 32 * kPathK2Warps;
+constexpr int kPathK2Unroll = 8;
 
-__global__ void __launch_bounds__(32 * kPathK2Warps) paths_k2_kernel(PathArgs a) {
-  __shared__ int64_t run_s[kPathK2Warps];
-  __shared__ int64_t total_s;
+// block-wide ordered count of `ok`: this thread's exclusive rank and the
+// block total (two barriers)
+__device__ __forceinline__ int block_rank(bool ok, int* wcnt, int& total) {
   const int warp = threadIdx.x >> 5;
-  const unsigned lane = lane_id();
-  const int64_t limit = a.max_paths + 1;
+  const unsigned bal = __ballot_sync(TH_FULL, ok);
+  if (lane_id() == 0) wcnt[warp] = __popc(bal);
+  __syncthreads();
+  int before = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < kPathK2Warps; ++w) {
+    const int c = wcnt[w];
+    before += w < warp ? c : 0;
+    total += c;
+  }
+  __syncthreads();  // (wcnt is rewritten by the next call)
+  return before + __popc(bal & lanemask_lt());
+}
+
+// block_rank over kPathK2Unroll slot groups at once (one barrier pair):
+// group u's slots come after every slot of groups < u
+__device__ __forceinline__ void block_rank_groups(const bool (&ok)[kPathK2Unroll], int (*wcnt)[kPathK2Warps],
+                                                  int (&rank)[kPathK2Unroll], int& total) {
+  const int warp = threadIdx.x >> 5;
+  unsigned bal[kPathK2Unroll];
+#pragma unroll
+  for (int u = 0; u < kPathK2Unroll; ++u) {
+    bal[u] = __ballot_sync(TH_FULL, ok[u]);
+    if (lane_id() == 0) wcnt[u][warp] = __popc(bal[u]);
+  }
+  __syncthreads();
+  int base = 0;
+#pragma unroll
+  for (int u = 0; u < kPathK2Unroll; ++u) {
+    int before = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kPathK2Warps; ++w) {
+      const int c = wcnt[u][w];
+      before += w < warp ? c : 0;
+      tot += c;
+    }
+    rank[u] = base + before + __popc(bal[u] & lanemask_lt());
+    base += tot;
+  }
+  total = base;
+  __syncthreads();  // (wcnt is rewritten by the next call)
+}
+
+__global__ void __launch_bounds__(kPathK2Threads) paths_k2_kernel(PathArgs a) {
+  __shared__ int wcnt[kPathK2Warps];
+  __shared__ int wcnt4[kPathK2Unroll][kPathK2Warps];
+  __shared__ int32_t l0_tid[kPathK2Threads], l0_obj[kPathK2Threads];
+  const int tid = threadIdx.x;
   for (int q = blockIdx.x; q < a.B; q += gridDim.x) {
     int64_t lo0 = 0, hi0 = 0;
     const int32_t s = a.seeds[q];
@@ -272,60 +321,46 @@ __global__ void __launch_bounds__(32 * kPathK2Warps) paths_k2_kernel(PathArgs a)
       hi0 = a.indptr[s + 1];
     }
     int32_t* slot = a.tmp + (int64_t)q * a.max_paths * 2;
-    int64_t total = 0;  // walks placed so far (identical in every thread)
-    for (int64_t c0 = lo0; c0 < hi0 && total < limit; c0 += kPathK2Warps) {
-      // this warp's level-0 candidate and the run it heads
-      const int64_t i = c0 + warp;
-      int32_t t1 = 0;
-      int64_t rlo = 0, rhi = 0, run = 0;
-      if (i < hi0) {
-        t1 = a.csr_tid[i];
-        if (rel_ok(a, q, a.csr_rel[i])) {
-          const int32_t o = a.csr_obj[i];
-          rlo = a.indptr[o];
-          rhi = a.indptr[o + 1];
-        }
+    int64_t total = 0;  // walks found so far (uniform across the CTA)
+    for (int64_t c0 = lo0; c0 < hi0 && total <= a.max_paths; c0 += kPathK2Threads) {
+      // this block's passing level-0 candidates, compacted in order
+      const int64_t i = c0 + tid;
+      const bool ok0 = i < hi0 && rel_ok(a, q, a.csr_rel[i]);
+      int n0;
+      const int r0 = block_rank(ok0, wcnt, n0);
+      if (ok0) {
+        l0_tid[r0] = a.csr_tid[i];
+        l0_obj[r0] = a.csr_obj[i];
       }
-      if (!a.masks) {
-        run = rhi - rlo;
-      } else {
-        for (int64_t b = rlo; b < rhi && run < limit; b += 32) {
-          const int64_t j = b + lane;
-          const bool ok = j < rhi && rel_ok(a, q, a.csr_rel[j]);
-          run += __popc(__ballot_sync(TH_FULL, ok));
-        }
-      }
-      if (lane == 0) run_s[warp] = run;
       __syncthreads();
-      int64_t before = total;  // walks ahead of this warp's run
-      for (int w = 0; w < warp; ++w) before += run_s[w];
-      if (threadIdx.x == 0) {
-        int64_t t = total;
-        for (int w = 0; w < kPathK2Warps; ++w) t += run_s[w];
-        total_s = t;
-      }
-      // write the part of the run that lands in the slot
-      if (before < a.max_paths && run > 0) {
-        int64_t n = 0;  // passing candidates of the run seen so far
-        for (int64_t b = rlo; b < rhi && before + n < a.max_paths; b += 32) {
-          const int64_t j = b + lane;
-          const bool ok = j < rhi && rel_ok(a, q, a.csr_rel[j]);
-          const unsigned bal = __ballot_sync(TH_FULL, ok);
-          if (ok) {
-            const int64_t p = before + n + __popc(bal & lanemask_lt());
-            if (p < a.max_paths) {
+      for (int j = 0; j < n0 && total <= a.max_paths; ++j) {
+        const int32_t t1 = l0_tid[j], o = l0_obj[j];
+        const int64_t rlo = a.indptr[o], rhi = a.indptr[o + 1];
+        for (int64_t b = rlo; b < rhi && total <= a.max_paths; b += kPathK2Threads * kPathK2Unroll) {
+          bool ok[kPathK2Unroll];
+          int32_t t2[kPathK2Unroll];
+#pragma unroll
+          for (int u = 0; u < kPathK2Unroll; ++u) {
+            const int64_t e = b + (int64_t)u * kPathK2Threads + tid;
+            ok[u] = e < rhi && rel_ok(a, q, a.csr_rel[e]);
+            t2[u] = ok[u] ? a.csr_tid[e] : 0;
+          }
+          int rank[kPathK2Unroll], n;
+          block_rank_groups(ok, wcnt4, rank, n);
+#pragma unroll
+          for (int u = 0; u < kPathK2Unroll; ++u) {
+            const int64_t p = total + rank[u];
+            if (ok[u] && p < a.max_paths) {
               slot[2 * p] = t1;
-              slot[2 * p + 1] = a.csr_tid[j];
+              slot[2 * p + 1] = t2[u];
             }
           }
-          n += __popc(bal);
+          total += n;
         }
       }
-      __syncthreads();
-      total = total_s;
-      __syncthreads();  // (run_s / total_s are rewritten by the next chunk)
+      __syncthreads();  // (l0_* are rewritten by the next block)
     }
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
       a.p_cnt[q] = total < a.max_paths ? total : a.max_paths;
       a.p_trunc[q] = total > a.max_paths;
     }
@@ -369,7 +404,7 @@ int launch_paths(const PathArgs& a, cudaStream_t st) {
     if (a.B > 0) {
       if (a.k == 2 && a.singleton && a.k2_parallel) {
         const unsigned g2 = (unsigned)std::min<int64_t>(a.B, kNumSMs * 8);
-        paths_k2_kernel<<<g2, 32 * kPathK2Warps, 0, st>>>(a);
+        paths_k2_kernel<<<g2, kPathK2Threads, 0, st>>>(a);
       } else {
         paths_kernel<true, true><<<grid, kPathThreads, 0, st>>>(a);
       }

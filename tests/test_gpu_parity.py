@@ -160,6 +160,39 @@ def test_hub_graph_two_waves_vs_oracle(th, sem, divisor, k4):
             assert int(res.edges[h, i]) == ref["edges"][h]
 
 
+@pytest.mark.parametrize("max_paths", [1, 7, 300, 5000])
+@pytest.mark.parametrize("filtered", [False, True])
+def test_k2_paths_cta_kernel_vs_dfs_and_oracle(th, max_paths, filtered):
+    """k = 2 capped singleton path queries take the CTA-per-query kernel
+    (paths_k2_kernel); it must equal the one-warp DFS and the oracle --
+    paths in order, counts and truncation -- on hub seeds with rows longer
+    than a 2,048-slot sweep step, with and without relation filters."""
+    s, r, o = _hub_graph(3000, 120000, 40, seed=17)
+    E, R = 3000, 40
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    deg = np.diff(og.indptr)
+    rng = np.random.default_rng(4)
+    seeds = np.concatenate([np.argsort(-deg)[:24], rng.integers(0, E, 40)])
+    filt = [sorted(rng.choice(R, 5, replace=False).tolist()) for _ in seeds] if filtered else None
+    out = {}
+    for k2 in (1, 0):
+        ret = th.Retriever(g)
+        ret.set_paths_k2(bool(k2))
+        out[k2] = ret.retrieve(seeds, 2, relation_filter=filt, paths=True, max_paths=max_paths)
+    n_trunc = 0
+    for i, sd in enumerate(seeds.tolist()):
+        assert out[1].path_tid_tuples(i) == out[0].path_tid_tuples(i), (i, sd)
+        assert out[1].truncated(i) == out[0].truncated(i), (i, sd)
+        if i % 4 == 0:
+            ref = orc.retrieve_one(og, sd, 2, "frontier", None if filt is None else filt[i], paths=True,
+                                   max_paths=max_paths)
+            assert out[1].path_tid_tuples(i) == ref["paths"], (i, sd)
+            assert out[1].truncated(i) == ref["truncated"]
+        n_trunc += out[1].truncated(i)
+    assert n_trunc > 0
+
+
 def test_filtered_hub_graph_vs_oracle(th):
     s, r, o = _hub_graph(2000, 40000, 40, seed=5)
     E, R = 2000, 40
