@@ -88,6 +88,7 @@ def partitioned(args, s, r, o, E, R, host):
     200M entities x 32 words addressable (round 1's 32-bit keys refused C5)."""
     from paper_2604_18913_b200.retriever import _relation_masks
 
+    torch.cuda.empty_cache()  # (the generator's cached blocks: the shard allocates outside torch)
     t0 = time.time()
     pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(1))
     del s, r, o
