@@ -130,7 +130,7 @@ __global__ void seed_init_kernel(WaveArgs a, const int32_t* __restrict__ qoff,
         if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
         const uint32_t fb = 1u << (e & 31);
         fresh = !(atomicOr(&a.Xf[e >> 5], fb) & fb);
-        if (fresh && a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[e >> 5], fb);
+        if (fresh && a.sem != TH_EXACT) atomicOr(&a.Vf[e >> 5], fb);
       }
       const uint32_t d = fresh ? (uint32_t)(a.indptr[e + 1] - a.indptr[e]) : 0u;
       warp_append_all(fresh, e, d, a.lists, &a.ctl->list_len[0], a.E, &a.ctl->push_cost[0]);
@@ -171,7 +171,7 @@ __global__ void begin_hop_kernel(Ctl* ctl, int h, int64_t T, double pull_divisor
 __device__ __forceinline__ bool flag_next(const WaveArgs& a, int32_t v) {
   const uint32_t fb = 1u << (v & 31);
   const bool fresh = !(atomicOr(&a.Nf[v >> 5], fb) & fb);
-  if (fresh && a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[v >> 5], fb);
+  if (fresh && a.sem != TH_EXACT) atomicOr(&a.Vf[v >> 5], fb);
   return fresh;
 }
 

@@ -150,7 +150,7 @@ __global__ void shard_seed_kernel(ShardArgs sa, const int32_t* __restrict__ qoff
         if (a.sem == TH_CUMULATIVE) atomicOr(&a.S[r], qb);
         const uint32_t fb = 1u << (row & 31);
         fresh = !(atomicOr(&a.Xf[row >> 5], fb) & fb);
-        if (fresh && a.sem == TH_CUMULATIVE) atomicOr(&a.Vf[row >> 5], fb);
+        if (fresh && a.sem != TH_EXACT) atomicOr(&a.Vf[row >> 5], fb);
       }
       if (hrow >= 0) {
         atomicOr(&a.X[(size_t)hrow * W + qw], qb);
