@@ -80,6 +80,7 @@ struct WaveArgs {
   Ctl* ctl;
   int nq, sem, h;
   int last_frontier;  // FRONTIER's last hop: nothing reads V afterwards
+  int last_hop;       // no hop follows: the new layer's out-degree total (push cost) is unused
 };
 
 template <int W>
@@ -212,8 +213,10 @@ struct WarpAppender {
     if (!fm) return;
     if (fresh) {
       wbuf[fill + __popc(fm & lanemask_lt())] = v;
-      const uint32_t d = (uint32_t)(a.indptr[v + 1] - a.indptr[v]);
-      cost += d > (1u << 26) ? (1u << 26) : d;
+      if (!a.last_hop) {  // (the next hop's direction reads it; the last has none)
+        const uint32_t d = (uint32_t)(a.indptr[v + 1] - a.indptr[v]);
+        cost += d > (1u << 26) ? (1u << 26) : d;
+      }
     }
     fill += __popc(fm);
     if (fill >= kAppendRun) flush(a);
@@ -1139,6 +1142,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
     NvtxRange nvtx_hop("th hop %d (wave of %d)", h, nq);
     a.h = h;
     a.last_frontier = h == k && sem == TH_FRONTIER;
+    a.last_hop = h == k;
     const bool edges_done = next_edges_done;
     next_edges_done = false;
     {
