@@ -1,4 +1,5 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
+export CUDA_MODULE_LOADING=EAGER
 timeout 900 python -m pytest -q -x tests/test_gpu_parity.py tests/test_gpu_fuzz.py tests/test_gpu_partition.py > gpurun_out/ab_tests.log 2>&1; echo tests=$?; tail -1 gpurun_out/ab_tests.log
 for L in lib lib_prev lib lib_prev; do
   echo "== $L"
