@@ -289,6 +289,25 @@ int th_shard_ipc_open(th_shard* s, int32_t peer, const void* h_handle64);
  * (the region is reallocated), all ranks reconnect, and the wave runs again. */
 int th_shard_grow_inbox(th_shard* s, int64_t inbox_records);
 int th_shard_inbox_overflowed(const th_shard* s);
+
+/* K7 on-demand hub-adjacency cache (the reference's LRU,
+ * cache.py:38-89, reached per partition from engine.py:80-81).  The shard's
+ * hub-slice rows leave HBM for a pinned host store; their CSR range is
+ * re-mapped page by page (CUDA virtual memory) onto `capacity_pages`
+ * physical HBM pages.  Before each hop the pages of the frontier's hubs are
+ * made resident, the least recently used page evicted first; a hop whose
+ * hubs span more pages than the capacity fails with TH_ERR_INVALID.
+ * Counters keep the reference's algebra: hits + misses = accesses, loads =
+ * misses, one eviction per load at capacity.  Enable between waves, once. */
+int th_shard_hub_cache(th_shard* s, int64_t capacity_pages);
+/* h_out8: hits, misses, loads, evictions, resident pages, capacity, pages of
+ * the hub region, edges per page. */
+int th_shard_hub_cache_stats(th_shard* s, int64_t* h_out8);
+/* Access log (page numbers, oldest first): returns its length n and, when
+ * cap >= n, copies it to h_out and clears it; -1 without a cache. */
+int64_t th_shard_hub_cache_trace(th_shard* s, int64_t* h_out, int64_t cap);
+/* Resident pages, least recently used first (copied when cap >= n). */
+int64_t th_shard_hub_cache_resident(th_shard* s, int64_t* h_out, int64_t cap);
 /* Records this rank wrote into OTHER ranks' inboxes at hops 1..n of the
  * last wave (12 bytes each over the interconnect).  Synchronises. */
 int th_shard_sent(th_shard* s, int64_t* h_per_hop, int n);

@@ -32,6 +32,8 @@ EXPORTS = (
     "th_shard_begin", "th_shard_can_pull", "th_shard_set_pull_divisor", "th_shard_region",
     "th_shard_ipc_handle", "th_shard_connect", "th_shard_ipc_open", "th_shard_grow_inbox",
     "th_shard_inbox_overflowed", "th_shard_hop", "th_shard_finish", "th_shard_sent", "th_shard_columns",
+    "th_shard_hub_cache", "th_shard_hub_cache_stats", "th_shard_hub_cache_trace",
+    "th_shard_hub_cache_resident",
     "th_ids_route_count", "th_ids_map_scatter", "th_ids_to_local_bits", "th_bits_andnot_update",
     "th_bits_or", "th_bits_compact", "th_plan_subjects", "th_session_set_k4_mode",
     "th_session_set_pull_screen", "th_session_wave_modes", "th_session_set_knob",
@@ -145,6 +147,10 @@ def load():
         "th_shard_columns": (ctypes.c_int, [_vp, ctypes.POINTER(ShardCols)]),
         "th_shard_hop": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32]),
         "th_shard_finish": (ctypes.c_int, [_vp, ctypes.POINTER(Result)]),
+        "th_shard_hub_cache": (ctypes.c_int, [_vp, ctypes.c_int64]),
+        "th_shard_hub_cache_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64)]),
+        "th_shard_hub_cache_trace": (ctypes.c_int64, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]),
+        "th_shard_hub_cache_resident": (ctypes.c_int64, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]),
         "th_ids_route_count": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int32,
                                               _vp, _vp]),
         "th_ids_map_scatter": (ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp,

@@ -9,6 +9,7 @@
 #include "../../include/th_b200.h"
 #include "engine.cuh"
 #include "graph.cuh"
+#include "hubcache.cuh"
 #include "idset.cuh"
 
 struct th_graph {
@@ -530,6 +531,34 @@ int th_shard_finish(th_shard* s, th_result* out) {
     }
     return th::shard_finish(s->sh, out);
   });
+}
+
+int th_shard_hub_cache(th_shard* s, int64_t capacity_pages) {
+  return guarded([&]() -> int {
+    TH_SHARD_GUARD(s);
+    return th::shard_hub_cache(s->sh, capacity_pages);
+  });
+}
+
+int th_shard_hub_cache_stats(th_shard* s, int64_t* h_out8) {
+  TH_SHARD_GUARD(s);
+  th::HubCache* hc = th::shard_hub_cache_of(s->sh);
+  if (!hc || !h_out8) {
+    th::set_error(hc ? "NULL output" : "the shard has no hub cache (th_shard_hub_cache)");
+    return hc ? TH_ERR_INVALID : TH_ERR_STATE;
+  }
+  th::hubcache_stats(hc, h_out8);
+  return TH_OK;
+}
+
+int64_t th_shard_hub_cache_trace(th_shard* s, int64_t* h_out, int64_t cap) {
+  th::HubCache* hc = (s && s->sh) ? th::shard_hub_cache_of(s->sh) : nullptr;
+  return hc ? th::hubcache_trace(hc, h_out, cap) : -1;
+}
+
+int64_t th_shard_hub_cache_resident(th_shard* s, int64_t* h_out, int64_t cap) {
+  th::HubCache* hc = (s && s->sh) ? th::shard_hub_cache_of(s->sh) : nullptr;
+  return hc ? th::hubcache_resident(hc, h_out, cap) : -1;
 }
 
 // ---- id sets (store-backed partitioned retrieval) ----

@@ -30,6 +30,7 @@
 
 #include "common.cuh"
 #include "engine.cuh"
+#include "hubcache.cuh"
 #include "paths.cuh"
 
 namespace th {
@@ -1756,6 +1757,7 @@ struct Shard {
   int W = 0;
   bool in_wave = false;
   int next_hop = 0, next_phase = 0;
+  HubCache* hc = nullptr;          // K7: hub slices paged in on demand (hubcache.cuh)
   int64_t rows() const { return n_local + H; }
 };
 
@@ -2439,6 +2441,16 @@ int shard_hop(Shard* sh, int h, int phase) {
     return TH_ERR_STATE;
   }
   NvtxRange nvtx_phase("th shard hop %d phase %d", h, phase);
+  if (phase == 0 && sh->hc) {
+    // the frontier's hub pages resident before any kernel of the hop reads
+    // them (the host waits for the flags; the loads queue on the stream)
+    TH_CUDA(cudaStreamSynchronize(sh->s.st));
+    const int rc = hubcache_step(sh->hc, static_cast<const uint32_t*>(sh->s.Xf.p), sh->s.st);
+    if (rc != TH_OK) {
+      sh->in_wave = false;
+      return rc;
+    }
+  }
   if (phase == 0) TH_W_DISPATCH(sh->W, shard_send_w<WW>(sh, h))
   else if (phase == 1) TH_W_DISPATCH(sh->W, shard_receive_w<WW>(sh, h))
   else TH_W_DISPATCH(sh->W, shard_end_w<WW>(sh, h))
@@ -2499,8 +2511,24 @@ int shard_inbox_overflowed(const Shard* sh) {
 
 Session* shard_session(Shard* sh) { return &sh->s; }
 
+int shard_hub_cache(Shard* sh, int64_t capacity) {
+  if (sh->in_wave) {
+    set_error("the hub cache cannot be enabled during a wave");
+    return TH_ERR_STATE;
+  }
+  if (sh->hc) {
+    set_error("the shard's hub cache is enabled already");
+    return TH_ERR_STATE;
+  }
+  TH_CUDA(cudaStreamSynchronize(sh->s.st));
+  return hubcache_create(&sh->hc, &sh->g, sh->n_local, capacity, sh->s.st);
+}
+
+HubCache* shard_hub_cache_of(Shard* sh) { return sh->hc; }
+
 void shard_free(Shard* sh) {
   session_free(&sh->s);
+  if (sh->hc) hubcache_free(sh->hc, &sh->g);
   shard_close_peers(sh);
   for (DBuf* d : {&sh->O, &sh->Of, &sh->olist}) {
     if (d->p) cudaFree(d->p);

@@ -152,6 +152,9 @@ int shard_finish(Shard* sh, th_result* out);
 int shard_sent(Shard* sh, int64_t* per_hop, int n);
 int shard_columns(const Shard* sh, th_shard_cols* out);
 Session* shard_session(Shard* sh);
+struct HubCache;
+int shard_hub_cache(Shard* sh, int64_t capacity);
+HubCache* shard_hub_cache_of(Shard* sh);
 void shard_free(Shard* sh);
 
 }  // namespace th

@@ -437,6 +437,41 @@ class GraphShard:
     def synchronize(self) -> None:
         self.stream.synchronize()
 
+    # -- K7 hub-adjacency cache ------------------------------------------------
+    def enable_hub_cache(self, capacity_pages: int) -> None:
+        """Page this shard's hub slices in on demand from a pinned host store
+        into ``capacity_pages`` HBM pages, least recently used out first
+        (csrc/hubcache.cu; the reference's LRU, cache.py:38-89)."""
+        _lib.check(_lib.load().th_shard_hub_cache(self._handle, int(capacity_pages)))
+
+    def hub_cache_stats(self) -> dict:
+        """Counters (the reference's algebra) plus the cache geometry."""
+        from .cache import CacheCounters
+
+        out = (ctypes.c_int64 * 8)()
+        _lib.check(_lib.load().th_shard_hub_cache_stats(self._handle, out))
+        h, m, ld, ev, res, cap, pages, pe = (int(x) for x in out)
+        return {"counters": CacheCounters(h, m, ld, ev, h / (h + m) if h + m else 0.0),
+                "resident": res, "capacity": cap, "pages": pages, "page_edges": pe}
+
+    def _cache_list(self, fn) -> list:
+        lib = _lib.load()
+        n = int(getattr(lib, fn)(self._handle, None, 0))
+        if n < 0:
+            raise RuntimeError("the shard has no hub cache (enable_hub_cache)")
+        buf = (ctypes.c_int64 * max(n, 1))()
+        getattr(lib, fn)(self._handle, buf, n)
+        return [int(x) for x in buf[:n]]
+
+    def hub_cache_trace(self) -> list:
+        """Pages accessed since the last call, in access order (the log is
+        cleared)."""
+        return self._cache_list("th_shard_hub_cache_trace")
+
+    def hub_cache_resident(self) -> list:
+        """Resident pages, least recently used first."""
+        return self._cache_list("th_shard_hub_cache_resident")
+
     # -- the wave ---------------------------------------------------------------
     def begin(self, query: "WaveQuery") -> None:
         import torch
@@ -659,7 +694,7 @@ class PartitionedGraph:
 
     def __init__(self, triples, n_entities: int, n_relations: int, exchange: Exchange | None = None,
                  plan: ShardPlan | None = None, hub_fraction: float = DEFAULT_HUB_FRACTION,
-                 n_hubs: int | None = None, shard_factory=None):
+                 n_hubs: int | None = None, shard_factory=None, hub_cache_pages: int | None = None):
         if exchange is None:
             exchange = LoopbackExchange(1)
         cols = triples if isinstance(triples, tuple) else tuple(np.asarray(list(triples)).reshape(-1, 3).T)
@@ -681,6 +716,11 @@ class PartitionedGraph:
         self.n_triples = int(len(subj))
         factory = shard_factory or GraphShard
         self.shards = [factory(cols, n_entities, n_relations, plan, r) for r in exchange.ranks]
+        if hub_cache_pages is not None:
+            # hub adjacency on demand (config 5): every hosted rank pages its
+            # hub slices through its own HBM budget
+            for sh in self.shards:
+                sh.enable_hub_cache(hub_cache_pages)
         exchange.connect(self.shards)
         self.pull_divisor = PULL_DIVISOR
 
@@ -694,6 +734,10 @@ class PartitionedGraph:
         self._pull_divisor = float(d)
         for sh in self.shards:
             sh.set_pull_divisor(self._pull_divisor)
+
+    def hub_cache_stats(self) -> list:
+        """Per hosted rank: the hub cache's counters and geometry."""
+        return [sh.hub_cache_stats() for sh in self.shards]
 
     def run(self, query: WaveQuery, stats: dict | None = None):
         """One wave; the hosted ranks' partial results (kept sharded)."""
