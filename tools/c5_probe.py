@@ -22,6 +22,10 @@ def main():
     ap.add_argument("--waves", type=int, default=16)
     ap.add_argument("--partitioned", action="store_true",
                     help="run through PartitionedGraph (one rank, the device-side exchange protocol)")
+    ap.add_argument("--hubs", type=int, default=0,
+                    help="partitioned: hub rows (top out-degree; 0.01%% of E = 20000 for config 5)")
+    ap.add_argument("--hub-cache", type=int, default=0,
+                    help="partitioned: page the hub rows through this many HBM pages (K7)")
     args = ap.parse_args()
     t0 = time.time()
     s, r, o, E, R = workloads.c5_graph_gpu()
@@ -90,12 +94,17 @@ def partitioned(args, s, r, o, E, R, host):
 
     torch.cuda.empty_cache()  # (the generator's cached blocks: the shard allocates outside torch)
     t0 = time.time()
-    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(1))
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(1), n_hubs=args.hubs or None,
+                             hub_cache_pages=args.hub_cache or None)
     del s, r, o
     torch.cuda.empty_cache()
     torch.cuda.synchronize()
     print(f"partitioned build {time.time() - t0:.1f}s local_triples={pg.shards[0].local_triples} "
-          f"mem={torch.cuda.max_memory_allocated() / 1e9:.1f}GB", flush=True)
+          f"hubs={pg.plan.n_hubs} mem={torch.cuda.max_memory_allocated() / 1e9:.1f}GB", flush=True)
+    if args.hub_cache:
+        st = pg.hub_cache_stats()[0]
+        print(f"hub cache: {st['pages']} pages of {st['page_edges']} edges, capacity {st['capacity']}",
+              flush=True)
     seeds, rel = workloads.c5_queries(E, R)
     words = _relation_masks(list(rel), seeds.size, R)
     sem = th.HopSemantics.FRONTIER
@@ -121,9 +130,14 @@ def partitioned(args, s, r, o, E, R, host):
         edges += int(part.edges.sum())
         ids += int(part.f_len.sum())
     n = 1024 * args.waves
-    print(f"C5 partitioned (1 rank) k=2 filtered: {n} seeds in {ms:.1f} ms -> {n / ms * 1e3:.0f} seeds/s, "
+    print(f"C5 partitioned (1 rank, {pg.plan.n_hubs} hubs, hub cache {args.hub_cache or 'off'}) k=2 filtered: "
+          f"{n} seeds in {ms:.1f} ms -> {n / ms * 1e3:.0f} seeds/s, "
           f"{edges / ms * 1e3 / 1e9:.2f} G edges/s, ids/wave={ids / args.waves:.0f} "
           f"peak_mem={torch.cuda.max_memory_allocated() / 1e9:.1f}GB", flush=True)
+    if args.hub_cache:
+        st = pg.hub_cache_stats()[0]
+        print(f"hub cache after {2 * args.waves + 2} waves: {st['counters']._asdict()} resident={st['resident']}",
+              flush=True)
     if args.oracle:
         from oracle import khop_oracle as orc
 
