@@ -21,6 +21,7 @@ from .core_types import (
     TripleVector,
     jaccard,
 )
+from .batch import BatchQuery, BatchResult, QueryBatch, plan_batch, run_batch, signature
 from .archive import graph_from_bytes, graph_to_bytes, load_graph, save_graph
 from .cache import CacheCounters, SubgraphCache
 from .device_graph import IncidenceGraph, build_incidence
@@ -54,6 +55,12 @@ from .store import (
 from .targets import GpuTarget, PartitionedGpuTarget
 
 __all__ = [
+    "BatchQuery",
+    "BatchResult",
+    "QueryBatch",
+    "plan_batch",
+    "run_batch",
+    "signature",
     "DirectoryStore",
     "InMemoryStore",
     "PartitionManifest",

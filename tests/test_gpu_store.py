@@ -50,8 +50,20 @@ def test_directory_store_replays_reference(th, strategy):
     pg, ents, rels = th.open_partitioned(GOLDEN / f"partdir_{strategy}", 2, record_trace=True)
     assert len(ents) == 400 and len(rels) == 6
     _replay(th, pg, g)
-    # (the reference's trace continues with a batch run, out of scope here)
-    assert list(pg.cache.trace) == g["cache_trace"][: len(pg.cache.trace)]
+    # the reference's script ends with a planned batch (plan_batch ->
+    # run_batch): same order, same per-query isolation, and the cache sees the
+    # same access sequence as the reference's LRU did
+    E = pg.n_entities
+    qs = [th.BatchQuery(f"q{i}", th.EntityVector(np.asarray(sd, np.int64), E), 2)
+          for i, sd in enumerate(([0], [5, 17], [123], [399], [2, 3, 250], []))]
+    qs.append(th.BatchQuery("bad", th.EntityVector(np.asarray([1], np.int64), E), 0))
+    batch = th.plan_batch(qs, pg.plan)
+    assert batch.execution_order == g["batch_order"]
+    for br, want in zip(th.run_batch(batch, pg), g["batch"]):
+        assert br.query_id == want["id"] and br.error == want["error"]
+        if want["frontiers"] is not None:
+            assert [br.trace.frontier(h).ids.tolist() for h in (1, 2)] == want["frontiers"]
+    assert list(pg.cache.trace) == g["cache_trace"]
 
 
 @pytest.mark.parametrize("strategy,m", [("lpt", 3), ("hash", 4)])

@@ -85,3 +85,25 @@ def test_store_constructor_dispatch_without_gpu():
     bad = th.PartitionPlan(2, plan.assignment, plan.loads[:2], "lpt")
     with pytest.raises(th.IntegrityError):
         th.PartitionedGraph(bad, st, th.SubgraphCache(2))
+
+
+@pytest.mark.parametrize("strategy", ["lpt", "hash"])
+def test_plan_batch_order_matches_reference(strategy):
+    """plan_batch over the reference's own batch (make_golden_store.py)
+    gives its execution order; restore_order inverts it."""
+    import json
+
+    import paper_2604_18913_b200 as th
+
+    g = json.loads((GOLDEN / f"store_{strategy}.json").read_text())
+    plan = th.load_partition_plan(GOLDEN / f"partdir_{strategy}")
+    seeds = ([0], [5, 17], [123], [399], [2, 3, 250], [])
+    qs = [th.BatchQuery(f"q{i}", th.EntityVector(np.asarray(sd, np.int64), 400), 2) for i, sd in enumerate(seeds)]
+    qs.append(th.BatchQuery("bad", th.EntityVector(np.asarray([1], np.int64), 400), 0))
+    b = th.plan_batch(qs, plan)
+    assert b.execution_order == g["batch_order"]
+    inv = b.restore_order
+    assert [b.execution_order[inv[p]] for p in range(len(qs))] == list(range(len(qs)))
+    assert th.QueryBatch.identity(qs).execution_order == list(range(len(qs)))
+    sigs = [th.signature(qs[p].q0, plan) for p in b.execution_order]
+    assert sigs == sorted(sigs)
