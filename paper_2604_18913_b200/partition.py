@@ -829,18 +829,12 @@ def cross_graph_paths(q0: EntityVector, k: int, pg: PartitionedGraph,
     """All length-k walks from q0 across the partitions, lexicographic in the
     triple ids, capped (engine.py:157-182 -> assemble_paths).
 
-    Every step of a walk is a triple activated at its hop under exact-walk
-    semantics, so the walks of the full graph are exactly the walks of the
-    subgraph of activated triples.  The partitioned exact-walk trace
-    supplies those triples; their subgraph (local tids a monotone renumbering
-    of the global ones, the reference's tid_to_global idea,
-    partition.py:145-153) is enumerated by the device path kernel (K5) and
-    mapped back -- identical paths, order and truncation flag.
+    Rank-sharded graphs exchange walk counts and capped per-prefix offers
+    between the ranks (``walks.sharded_paths``); the activated triples stay
+    with their owners.  Store-backed graphs enumerate the walk subgraph of
+    their exact-walk trace with the device path kernel (``store_paths``).
+    Identical paths, order and truncation flag either way.
     """
-    from .core_types import PathResult
-    from .device_graph import build_incidence
-    from .retriever import reconstruct_paths
-
     if getattr(pg, "store", None) is not None:
         from .store import store_paths
 
@@ -851,17 +845,15 @@ def cross_graph_paths(q0: EntityVector, k: int, pg: PartitionedGraph,
         raise ValueError("hop count must be >= 1")
     if max_paths is not None and max_paths < 0:
         raise ValueError("max_paths must be >= 0")
-    s, r, o = walk_subgraph(q0, k, pg)
-    sub = build_incidence((s, r, o), pg.n_entities, pg.n_relations)
-    res = reconstruct_paths(q0, k, sub, max_paths)
-    # entity and relation ids are global in the subgraph, so its Triples are
-    # the full graph's
-    return PathResult(res.paths, res.truncated)
+    from .walks import sharded_paths
+
+    return sharded_paths(q0, k, pg, max_paths)
 
 
 def walk_subgraph(q0: EntityVector, k: int, pg: PartitionedGraph):
     """(s, r, o) of every triple activated by q0's exact-walk trace, in
-    ascending global tid order.  Every rank resolves the columns of ITS
+    ascending global tid order (the walk subgraph; every length-k walk is a
+    walk of it -- a cross-check for ``sharded_paths``).  Every rank resolves the columns of ITS
     activated triples (it owns them) on its device and the owners' pieces
     are gathered -- no rank holds the full triple columns."""
     import torch

@@ -277,3 +277,26 @@ def test_run_batch_on_sharded_graph(th):
             for h in range(1, q.k + 1):
                 assert np.array_equal(br.trace.frontier(h).ids, ref.frontier(h).ids), (q.query_id, h)
                 assert np.array_equal(br.trace.activated(h).ids, ref.activated(h).ids), (q.query_id, h)
+
+
+@pytest.mark.parametrize("world,n_hubs", [(1, 0), (2, 12), (4, 40)])
+def test_sharded_paths_equal_single_graph_k5(th, world, n_hubs):
+    """Sharded walk enumeration (counts + capped offers between ranks) ==
+    the single-graph K5 kernel on a hub-heavy graph: hub seeds whose walk
+    counts dwarf the cap, multi-seed sets, uncapped small cases."""
+    s, r, o = _hub_graph(20000, 400000, 32, seed=5)
+    E, R = 20000, 32
+    g = th.build_incidence((s, r, o), E, R)
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(world), n_hubs=n_hubs)
+    deg = np.bincount(s, minlength=E)
+    hubs = np.argsort(-deg)[:5]
+    rng = np.random.default_rng(world)
+    cases = [([int(hubs[0])], 3, 10_000), ([int(hubs[1]), int(hubs[2])], 2, 10_000), ([int(hubs[3])], 3, 7),
+             (sorted(set(rng.integers(0, E, 6).tolist())), 3, 2_500), ([int(rng.integers(0, E))], 2, None),
+             ([int(hubs[4])], 1, None), ([int(hubs[0])], 2, 0)]
+    for seeds, k, cap in cases:
+        q0 = th.EntityVector(seeds, E)
+        a = th.cross_graph_paths(q0, k, pg, cap)
+        b = th.reconstruct_paths(q0, k, g, cap)
+        assert a.paths == b.paths, (seeds, k, cap)
+        assert a.truncated == b.truncated

@@ -162,8 +162,15 @@ def _dist_worker(rank, world, port, errfile):
                                    th.HopSemantics.FRONTIER)
         pg.run(q, stats)
         assert sum(stats["sent_records"][0]) > 0  # records really crossed ranks
-        # cross_graph_paths' input: the walk subgraph gathered from the owners
-        # (the path enumeration itself needs the device, test_gpu_partition)
+        # paths across the two processes: walk counts and capped offers
+        # exchanged over gloo (walks.sharded_paths) == the oracle's walks
+        for seeds_p, k, cap in (([3], 2, 100), ([1, 7, 42], 3, 50), ([1, 7, 42], 2, None), ([9], 1, 0),
+                                ([2, 3], 3, 1)):
+            pr = th.cross_graph_paths(th.EntityVector(seeds_p, 500), k, pg, cap)
+            ref_p, ref_t = orc.walk_paths(og, seeds_p, k, cap)
+            assert [tuple(tuple(int(x) for x in t) for t in p) for p in pr.paths] == \
+                orc.paths_as_triples(og, ref_p), (seeds_p, k, cap)
+            assert pr.truncated == ref_t
         for seeds_p in ([3], [1, 7, 42]):
             s_, r_, o_ = th.partition.walk_subgraph(th.EntityVector(seeds_p, 500), 2, pg)
             act = np.unique(np.concatenate([a for _, a in orc.hop_trace(og, seeds_p, 2, orc.EXACT)]))
@@ -181,3 +188,24 @@ def test_two_ranks_over_gloo_match_oracle(tmp_path):
     errfile = str(tmp_path / "err.txt")
     torch.multiprocessing.spawn(_dist_worker, args=(2, _free_port(), errfile), nprocs=2, join=True)
     assert not os.path.exists(errfile), open(errfile).read()
+
+
+@pytest.mark.parametrize("world,n_hubs", [(1, 0), (2, 4), (3, 0), (4, 9)])
+def test_sharded_paths_match_oracle(world, n_hubs):
+    """Walk counts + capped offers exchanged between ranks (walks.py) give
+    the reference's walks, order and truncation flag -- with hub rows split
+    over the ranks, walks revisiting vertices, and every cap regime."""
+    s, r, o = _graph(300, 4000, 5, seed=world)
+    og = orc.build_csr(s, r, o, 300, 5)
+    pg = th.PartitionedGraph((s, r, o), 300, 5, th.LoopbackExchange(world), n_hubs=n_hubs,
+                             shard_factory=RefShard)
+    rng = np.random.default_rng(world)
+    for _ in range(12):
+        seeds = sorted(set(rng.integers(0, 300, int(rng.integers(1, 4))).tolist()))
+        k = int(rng.integers(1, 4))
+        for cap in (0, 1, 5, 37, 1000, None):
+            pr = th.cross_graph_paths(th.EntityVector(seeds, 300), k, pg, cap)
+            ref_p, ref_t = orc.walk_paths(og, seeds, k, cap)
+            got = [tuple(tuple(int(x) for x in t) for t in p) for p in pr.paths]
+            assert got == orc.paths_as_triples(og, ref_p), (seeds, k, cap)
+            assert pr.truncated == ref_t
