@@ -214,6 +214,10 @@ int th_session_set_profiling(th_session* s, int on);
 /* Accumulated milliseconds and launches per category since the last call
  * (arrays of n >= TH_PROF_CATEGORIES); resets the accumulators. Syncs. */
 int th_session_profile(th_session* s, double* ms, int64_t* launches, int n);
+/* Timeline of the last profiled run: n scopes of 4 doubles (category, stream
+ * 0 = main / 1, 2 = the K4 side streams, start ms, end ms relative to the
+ * run's first scope), copied when cap >= n; returns n (-1 on error). */
+int64_t th_session_profile_trace(th_session* s, double* h_out4, int64_t cap);
 /* Entity-list lengths of the last wave: [0] = distinct seed entities,
  * [h] = entities newly set at hop h (rows of the hop-h layer).  n >= k+1. */
 int th_session_wave_lists(const th_session* s, int64_t* lens, int n);

@@ -27,7 +27,7 @@ EXPORTS = (
     "th_graph_info_get", "th_session_create", "th_session_destroy", "th_run", "th_finish",
     "th_session_set_pull_divisor", "th_session_launch_count", "th_plan_owner_hash",
     "th_session_set_list_min_entities", "th_session_set_overlap", "th_session_set_graphs", "th_session_set_dense_pull",
-    "th_session_set_profiling", "th_session_profile", "th_session_wave_lists",
+    "th_session_set_profiling", "th_session_profile", "th_session_profile_trace", "th_session_wave_lists",
     "th_shard_create", "th_shard_destroy", "th_shard_local_triples", "th_shard_launch_count",
     "th_shard_begin", "th_shard_can_pull", "th_shard_set_pull_divisor", "th_shard_region",
     "th_shard_ipc_handle", "th_shard_connect", "th_shard_ipc_open", "th_shard_grow_inbox",
@@ -147,6 +147,7 @@ def load():
         "th_shard_columns": (ctypes.c_int, [_vp, ctypes.POINTER(ShardCols)]),
         "th_shard_hop": (ctypes.c_int, [_vp, ctypes.c_int32, ctypes.c_int32]),
         "th_shard_finish": (ctypes.c_int, [_vp, ctypes.POINTER(Result)]),
+        "th_session_profile_trace": (ctypes.c_int64, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int64]),
         "th_shard_hub_cache": (ctypes.c_int, [_vp, ctypes.c_int64]),
         "th_shard_hub_cache_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64)]),
         "th_shard_hub_cache_trace": (ctypes.c_int64, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]),

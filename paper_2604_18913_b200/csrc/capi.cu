@@ -285,6 +285,8 @@ int th_session_set_knob(th_session* s, const char* name, int64_t value) {
     s->s.k4_cache = value != 0;
   } else if (n == "list_first_hop") {
     s->s.list_first_hop = value != 0;
+  } else if (n == "priority") {
+    s->s.priority = value != 0;
   } else {
     th::set_error("unknown knob " + n);
     return TH_ERR_INVALID;
@@ -311,6 +313,16 @@ int th_session_profile(th_session* s, double* ms, int64_t* launches, int n) {
     }
     return th::session_profile(&s->s, ms, launches, n);
   });
+}
+
+int64_t th_session_profile_trace(th_session* s, double* h_out4, int64_t cap) {
+  if (!s) return -1;
+  int64_t n = -1;
+  const int rc = guarded([&]() -> int {
+    n = th::session_profile_trace(&s->s, h_out4, cap);
+    return TH_OK;
+  });
+  return rc == TH_OK ? n : -1;
 }
 
 int th_session_wave_modes(const th_session* s, int32_t* modes, int n) {

@@ -1038,8 +1038,10 @@ struct StreamScope {
 
 void ensure_side_stream(Session* s) {
   if (s->side) return;
-  TH_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
-  TH_CUDA(cudaStreamCreateWithFlags(&s->side2, cudaStreamNonBlocking));
+  int least = 0, greatest = 0;
+  TH_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  TH_CUDA(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, least));
+  TH_CUDA(cudaStreamCreateWithPriority(&s->side2, cudaStreamNonBlocking, least));
   for (int i = 0; i < kMaxK + 2; ++i) {
     TH_CUDA(cudaEventCreateWithFlags(&s->ev_expand[i], cudaEventDisableTiming));
     TH_CUDA(cudaEventCreateWithFlags(&s->ev_mat[i], cudaEventDisableTiming));
@@ -1282,6 +1284,7 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
 
 ProfScope::ProfScope(Session* s_, int c) : s(s_), cat(c), l0(s_->launches) {
   if (!s->prof) return;
+  tag = (s->side && s->st == s->side) ? 1 : (s->side2 && s->st == s->side2) ? 2 : 0;
   if (s->ev_used + 2 > s->ev_pool.size()) {
     for (int i = 0; i < 64; ++i) {
       cudaEvent_t e;
@@ -1309,17 +1312,25 @@ ProfScope::~ProfScope() noexcept(false) {
                                    s->capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
   s->ev_used += 2;
   s->pending_cat.push_back(cat);
+  s->pending_tag.push_back(tag);
   s->pending_launch.push_back(s->launches - l0);
 }
 
 static void drain_profile(Session* s) {
+  if (!s->pending_cat.empty()) s->prof_trace.clear();
   for (size_t i = 0; i < s->pending_cat.size(); ++i) {
-    float ms = 0.f;
+    float ms = 0.f, t0 = 0.f, t1 = 0.f;
     TH_CUDA(cudaEventElapsedTime(&ms, s->ev_pool[2 * i], s->ev_pool[2 * i + 1]));
     s->prof_ms[s->pending_cat[i]] += ms;
     s->prof_launches[s->pending_cat[i]] += s->pending_launch[i];
+    // timeline relative to the run's first scope
+    TH_CUDA(cudaEventElapsedTime(&t0, s->ev_pool[0], s->ev_pool[2 * i]));
+    TH_CUDA(cudaEventElapsedTime(&t1, s->ev_pool[0], s->ev_pool[2 * i + 1]));
+    const int tag = i < s->pending_tag.size() ? s->pending_tag[i] : 0;
+    s->prof_trace.insert(s->prof_trace.end(), {(double)s->pending_cat[i], (double)tag, (double)t0, (double)t1});
   }
   s->pending_cat.clear();
+  s->pending_tag.clear();
   s->pending_launch.clear();
   s->ev_used = 0;
 }
@@ -1334,6 +1345,14 @@ int session_profile(Session* s, double* ms, int64_t* launches, int n) {
     s->prof_launches[i] = 0;
   }
   return TH_OK;
+}
+
+int64_t session_profile_trace(Session* s, double* out4, int64_t cap) {
+  TH_CUDA(cudaStreamSynchronize(s->st));
+  drain_profile(s);
+  const int64_t n = (int64_t)s->prof_trace.size() / 4;
+  if (out4 && cap >= n) std::copy(s->prof_trace.begin(), s->prof_trace.end(), out4);
+  return n;
 }
 
 int session_wave_modes(Session* s, int32_t* modes, int n) {
@@ -1388,7 +1407,7 @@ static GraphKey graph_key(Session* s, const th_query* q) {
   k.dense_pull = s->dense_pull;
   k.list_min = s->list_min_entities;
   k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_mode << 8) |
-            ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0);
+            ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0) | (s->priority ? 128 : 0);
   k.epoch = session_alloc_sig(s);
   return k;
 }
@@ -1421,6 +1440,7 @@ static int run_graphed(Session* s, const th_query* q) {
     s->launches += s->g_launches;
     if (s->prof) {
       s->pending_cat = s->g_pend_cat;
+      s->pending_tag = s->g_pend_tag;
       s->pending_launch = s->g_pend_launch;
       s->ev_used = s->g_ev_used;
     }
@@ -1443,7 +1463,11 @@ static int run_graphed(Session* s, const th_query* q) {
   // capture on a session-owned stream (the caller's may be the legacy
   // default stream, which cannot capture); nothing runs during capture, and
   // the graph is launched on the caller's stream
-  if (!s->cap) TH_CUDA(cudaStreamCreateWithFlags(&s->cap, cudaStreamNonBlocking));
+  if (!s->cap) {
+    int least = 0, greatest = 0;
+    TH_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    TH_CUDA(cudaStreamCreateWithPriority(&s->cap, cudaStreamNonBlocking, greatest));
+  }
   TH_CUDA(cudaStreamBeginCapture(s->cap, cudaStreamCaptureModeThreadLocal));
   int rc = TH_OK;
   const char* fail = nullptr;
@@ -1479,12 +1503,15 @@ static int run_graphed(Session* s, const th_query* q) {
   }
   const uint64_t epoch = session_alloc_sig(s);
   cudaGraphExec_t exec = nullptr;
-  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  // (node priorities: captured kernels carry their stream's priority)
+  const cudaError_t ie =
+      cudaGraphInstantiate(&exec, graph, s->priority ? cudaGraphInstantiateFlagUseNodePriority : 0);
   cudaGraphDestroy(graph);
   TH_CUDA(ie);
   s->gexec = exec;
   s->g_launches = s->launches - l0;
   s->g_pend_cat = s->pending_cat;
+  s->g_pend_tag = s->pending_tag;
   s->g_pend_launch = s->pending_launch;
   s->g_ev_used = s->ev_used;
   s->launches = l0 + s->g_launches;

@@ -64,6 +64,10 @@ struct Session {
   bool paths_k2 = true;     // k = 2 singleton capped path queries: a CTA per query (paths.cu)
   int pull_screen = -1;     // pull items screened per lane first: -1 by graph shape, 0 off, 1 on
   int k4_mode = 1;  // count pass: 0 word-per-warp, 1 row-major for list-driven layers, 2 for all (k4_rowmajor.cuh)
+  // captured waves: the hop chain's kernels get the device's highest stream
+  // priority and K4's side streams the lowest, so the block scheduler feeds
+  // the critical path first and K4 fills the gaps
+  bool priority = true;
   bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr, side2 = nullptr;  // K4 streams (odd / even layers)
   int k4_slot = 0;                                // which K4 scratch set is in use
@@ -91,7 +95,9 @@ struct Session {
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<int> pending_cat;
+  std::vector<int> pending_tag;     // stream of each scope: 0 main, 1/2 the K4 side streams
   std::vector<int64_t> pending_launch;
+  std::vector<double> prof_trace;   // last drained run: (category, stream, start ms, end ms) per scope
   size_t ev_used = 0;
   double prof_ms[TH_PROF_CATEGORIES] = {};
   int64_t prof_launches[TH_PROF_CATEGORIES] = {};
@@ -107,6 +113,7 @@ struct Session {
   bool g_seen = false, g_valid = false;
   int64_t g_launches = 0;
   std::vector<int> g_pend_cat;     // profile scopes the graph records
+  std::vector<int> g_pend_tag;
   std::vector<int64_t> g_pend_launch;
   size_t g_ev_used = 0;
   int g_failures = 0;               // captures that fell back to eager runs
@@ -116,12 +123,14 @@ struct Session {
 struct ProfScope {
   Session* s;
   int cat;
+  int tag = 0;
   int64_t l0;
   ProfScope(Session* s_, int c);
   ~ProfScope() noexcept(false);
 };
 
 int session_profile(Session* s, double* ms, int64_t* launches, int n);
+int64_t session_profile_trace(Session* s, double* out4, int64_t cap);
 int session_wave_lists(Session* s, int64_t* lens, int n);
 int session_wave_modes(Session* s, int32_t* modes, int n);
 

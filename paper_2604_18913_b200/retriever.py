@@ -236,6 +236,18 @@ class Retriever:
         _lib.check(_lib.load().th_session_profile(self._handle, ms, ln, n))
         return {c: (ms[i], int(ln[i])) for i, c in enumerate(_lib.PROF_CATEGORIES)}
 
+    def profile_trace(self) -> list:
+        """Timeline of the last profiled run: (category, stream, start ms,
+        end ms) per kernel group; stream 0 = main, 1 / 2 = K4 side streams."""
+        lib = _lib.load()
+        n = int(lib.th_session_profile_trace(self._handle, None, 0))
+        if n < 0:
+            raise RuntimeError(lib.th_last_error().decode(errors="replace"))
+        buf = (ctypes.c_double * max(4 * n, 1))()
+        lib.th_session_profile_trace(self._handle, buf, n)
+        return [(_lib.PROF_CATEGORIES[int(buf[4 * i])], int(buf[4 * i + 1]), buf[4 * i + 2], buf[4 * i + 3])
+                for i in range(n)]
+
     def wave_lists(self, k: int) -> list[int]:
         """Entity-list lengths of the last wave: seeds, then rows set at each hop."""
         buf = (ctypes.c_int64 * (k + 1))()

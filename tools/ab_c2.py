@@ -28,7 +28,7 @@ def main():
         for cfg in configs:
             ret = th.Retriever(g)
             for name, v in cfg.items():
-                getattr(ret, "set_" + name)(v)
+                (getattr(ret, "set_" + name)(v) if hasattr(ret, "set_" + name) else ret.set_knob(name, v))
             for i in range(4):
                 ret.run(offs, seeds[i], 3, "frontier", None, singleton=True, copy=False)
             ts = []

@@ -34,7 +34,7 @@ def main():
             ret = th.Retriever(g)
             for name, v in cfg.items():
                 ret.set_knob(name, v) if name in ("paths_k2", "k4_cache", "list_first_hop") else \
-                    getattr(ret, "set_" + name)(v)
+                    (getattr(ret, "set_" + name)(v) if hasattr(ret, "set_" + name) else ret.set_knob(name, v))
             for _ in range(2):
                 ret.run(offs, d_seeds, 2, "frontier", d_masks, paths=True, max_paths=10_000, singleton=True,
                         copy=False)
