@@ -631,7 +631,7 @@ __global__ void mat_scan_rows_kernel(int32_t* counts, int nblk, int64_t* totals)
 
 // single block: per-query output offsets from the running cursor
 __global__ void mat_scan_queries_kernel(const int64_t* totals, int nq, int64_t* off, int64_t* len,
-                                        int64_t* cursor) {
+                                        int64_t* cursor, int64_t* layer_total = nullptr) {
   __shared__ int64_t ws[32];
   const int q = threadIdx.x;
   const int64_t v = q < nq ? totals[q] : 0;
@@ -655,9 +655,11 @@ __global__ void mat_scan_queries_kernel(const int64_t* totals, int nq, int64_t* 
   // reserve this layer's output range atomically: consecutive layers' K4s
   // run on two streams and take their ranges from the same cursor
   __shared__ int64_t base_s;
-  if (q == 0)
+  if (q == 0) {
     base_s = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(cursor),
                                 (unsigned long long)ws[(blockDim.x >> 5) - 1]);
+    if (layer_total) *layer_total = ws[(blockDim.x >> 5) - 1];
+  }
   __syncthreads();
   const int64_t base = base_s;
   const int64_t ex = (warp ? ws[warp - 1] : 0) + x - v;
@@ -787,7 +789,7 @@ void for_each_session_buf(Session* s, F&& f) {
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
                   &s->p_scratch, &s->p_tmp, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta, &s->counts2,
                   &s->totals2, &s->rowlist2, &s->rowscan2, &s->k4_S2, &s->k4_meta2,
-                  &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks})
+                  &s->k4_P, &s->k4_G, &s->k4_P2, &s->k4_G2, &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks})
     f(d);
 }
 
@@ -909,6 +911,8 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   }
   constexpr size_t smem_c = mat_smem_bytes<W, false>();
   bool counted = false;
+  uint32_t* gcount = nullptr;  // bucketed write pass: per-slice group counts
+  RowMajorSrc<W> rsrc{};
   if constexpr (Src::kDense) {
     // (k4_mode 1: list-driven layers without edge counts -- those keep the
     // word-per-warp form: its shared degree planes beat per-bit degree sums,
@@ -925,13 +929,15 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
                                      (int)rs_count_smem<false>()));
         attr_r.fetch_or(bit, std::memory_order_relaxed);
       }
-      RowMajorSrc<W> rsrc{};
       rsrc.A = src.A;
       rsrc.neg = src.neg;
       rsrc.nq = src.nq;
       if constexpr (Src::kRing) {
         rsrc.rows = src.rows;
         rsrc.n_dev = src.n_dev;
+        if (s->k4_bucket && !es.out)
+          gcount = ensure<uint32_t>(s->k4_slot ? s->k4_G2 : s->k4_G, ((int64_t)nblk * kRsWarps + 1) * 32,
+                                    s->st);
       } else {
         rsrc.flags = src.flags;
         rsrc.n_host = src.nrows;
@@ -941,7 +947,7 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
                                                                                        counts, es);
       else
         rs_count_kernel<W, false><<<nblk, 32 * kRsWarps, rs_count_smem<false>(), s->st>>>(
-            rsrc, nblk, counts, es);
+            rsrc, nblk, counts, es, gcount);
       TH_LAUNCHED();
       counted = true;
     }
@@ -957,8 +963,35 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   }
   mat_scan_rows_kernel<<<nq, 256, 0, s->st>>>(counts, nblk, totals);
   TH_LAUNCHED();
-  mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(totals, nq, off, len, cursor);
+  mat_scan_queries_kernel<<<1, kMaxWave, 0, s->st>>>(totals, nq, off, len, cursor,
+                                                    gcount ? totals + kMaxWave : nullptr);
   TH_LAUNCHED();
+  if constexpr (Src::kRing) {
+    if (gcount) {
+      // (the layer's id total picks the pass on the device: the bucketed
+      // passes below when their entry buffer stays L2-sized, else the
+      // transposing write pass; the other side's kernels exit at once)
+      const int64_t* ltot = totals + kMaxWave;
+      // bucketed write: (row, bit) entries scattered into 32-query groups,
+      // then gathered into each query's output (k4_rowmajor.cuh)
+      uint32_t* P = ensure<uint32_t>(s->k4_slot ? s->k4_P2 : s->k4_P, std::max<int64_t>(cap, 1), s->st);
+      bucket_scan_kernel<<<W, 1024, 0, s->st>>>(gcount, nblk * kRsWarps, ltot);
+      TH_LAUNCHED();
+      bucket_scatter_kernel<W><<<nblk, 32 * kRsWarps, 0, s->st>>>(rsrc, nblk, gcount, off, P, cap, ltot);
+      TH_LAUNCHED();
+      // (the layer is free only after the write pass below, which re-reads
+      // it when the bucketed passes stood aside)
+      const int64_t units = (int64_t)nblk * W;
+      bucket_gather_kernel<W><<<(unsigned)ceil_div(units, kThreads / 32), kThreads, 0, s->st>>>(
+          src.rows, src.map, src.n_dev, nq, nblk, gcount, counts, off, P, out, cap, ltot);
+      TH_LAUNCHED();
+      mat_kernel<W, Src, true><<<grid, 32 * NW, smem_w, s->st>>>(src, nblk, counts, off, out, cap,
+                                                                 EdgeSum{}, SCache{}, ltot);
+      TH_LAUNCHED();
+      s->launches += 7;
+      return;
+    }
+  }
   mat_kernel<W, Src, true><<<grid, 32 * NW, smem_w, s->st>>>(src, nblk, counts, off, out,
                                                              cap);
   TH_LAUNCHED();
@@ -1071,9 +1104,9 @@ void run_wave(Session* s, const th_query* q, int q0, int nq) {
   b.heavy = ensure<int32_t>(s->heavy, std::max<int64_t>(E, 1), st);
   b.M = filter ? ensure<uint32_t>(s->M, std::max<int64_t>(g->R, 1) * W, st) : nullptr;
   b.counts = ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
-  b.totals = ensure<int64_t>(s->totals, kMaxWave, st);
+  b.totals = ensure<int64_t>(s->totals, kMaxWave + 1, st);  // (+ the layer total)
   b.counts2 = ensure<int32_t>(s->counts2, (int64_t)kMaxWave * (kMatBlocks + 64), st);
-  b.totals2 = ensure<int64_t>(s->totals2, kMaxWave, st);
+  b.totals2 = ensure<int64_t>(s->totals2, kMaxWave + 1, st);
   b.ctl = static_cast<Ctl*>(s->ctl.p);
   TH_CUDA(cudaMemsetAsync(b.ctl, 0, offsetof(Ctl, err), st));
   TH_CUDA(cudaMemsetAsync(b.Xf, 0, fwords * 4, st));
@@ -1407,7 +1440,8 @@ static GraphKey graph_key(Session* s, const th_query* q) {
   k.dense_pull = s->dense_pull;
   k.list_min = s->list_min_entities;
   k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_mode << 8) |
-            ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0) | (s->priority ? 128 : 0);
+            ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0) | (s->priority ? 128 : 0) |
+            (s->k4_bucket ? 256 : 0);
   k.epoch = session_alloc_sig(s);
   return k;
 }
@@ -1940,9 +1974,9 @@ void shard_begin_w(Shard* sh, const th_query* q) {
   ensure<int64_t>(s->heavy_off, rows + 1, st);
   if (q->d_rel_masks) ensure<uint32_t>(s->M, std::max<int64_t>(sh->g.R, 1) * W, st);
   ensure<int32_t>(s->counts, (int64_t)kMaxWave * (kMatBlocks + 64), st);
-  ensure<int64_t>(s->totals, kMaxWave, st);
+  ensure<int64_t>(s->totals, kMaxWave + 1, st);
   ensure<int32_t>(s->counts2, (int64_t)kMaxWave * (kMatBlocks + 64), st);
-  ensure<int64_t>(s->totals2, kMaxWave, st);
+  ensure<int64_t>(s->totals2, kMaxWave + 1, st);
   if (sh->world > 1) {
     // remote staging, global-indexed (push pre-dedupe, pull frontier copy)
     const int64_t E = std::max<int64_t>(sh->E, 1);

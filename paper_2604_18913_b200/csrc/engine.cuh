@@ -68,6 +68,7 @@ struct Session {
   // priority and K4's side streams the lowest, so the block scheduler feeds
   // the critical path first and K4 fills the gaps
   bool priority = true;
+  bool k4_bucket = true;  // list-driven layers: scatter/gather write pass (k4_rowmajor.cuh)
   bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr, side2 = nullptr;  // K4 streams (odd / even layers)
   int k4_slot = 0;                                // which K4 scratch set is in use
@@ -83,6 +84,7 @@ struct Session {
   // wave state
   DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals, rowlist, rowscan, k4_S, k4_meta, heavy_off;
   DBuf counts2, totals2, rowlist2, rowscan2, k4_S2, k4_meta2;  // second K4 slot
+  DBuf k4_P, k4_G, k4_P2, k4_G2;  // bucketed write pass: entries, group counts (per slot)
   DBuf ctl;
   // outputs
   DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch, p_tmp;

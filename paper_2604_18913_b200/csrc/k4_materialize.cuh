@@ -22,6 +22,9 @@
 #pragma once
 
 constexpr int kMatWordsPerCta = 8;          // warps per CTA (one row word each)
+// list layers with at most this many ids take the bucketed write passes
+// (k4_rowmajor.cuh): their 4-byte entry buffer stays L2-sized
+constexpr int64_t kBucketMaxIds = int64_t(20) << 20;
 constexpr int kChunkRows = 1024;            // 32 tiles of 32 rows
 constexpr int kSStride = 33;                // S[b][t] row stride (bank-conflict free)
 
@@ -601,7 +604,10 @@ __global__ void __launch_bounds__(32 * kMatWordsPerCta) mat_kernel(Src src, int 
                                                                    int32_t* counts,
                                                                    const int64_t* base, int32_t* out,
                                                                    int64_t cap, EdgeSum es = {},
-                                                                   SCache sc = {}) {
+                                                                   SCache sc = {},
+                                                                   const int64_t* bucket_total = nullptr) {
+  // (a list layer small enough for the bucketed passes is written by them)
+  if (bucket_total && *bucket_total <= kBucketMaxIds) return;
   constexpr int NW = mat_warps<W>();
   constexpr int NG = W / NW;  // word groups
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

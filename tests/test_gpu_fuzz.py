@@ -23,6 +23,7 @@ def _cases():
             k=int(rng.integers(1, 5)), sem=str(rng.choice(["exact", "frontier", "cumulative"])),
             filt=bool(rng.random() < 0.35), list_mode=bool(rng.random() < 0.5),
             k4_mode=int(rng.integers(0, 3)), screen=int(rng.integers(-1, 2)),
+            bucket=bool(rng.random() < 0.7),
             divisor=float(rng.choice([0.0, -1.0, 8.0])),
             paths=bool(rng.random() < 0.3), max_paths=[0, 5, 100, None][int(rng.integers(0, 4))], seed=i))
     return out
@@ -41,6 +42,7 @@ def test_random_configuration(th_mod, c):
     ret.set_list_min_entities(0 if c["list_mode"] else 1 << 40)
     ret.set_k4_mode(c["k4_mode"])
     ret.set_pull_screen(c["screen"])
+    ret.set_knob("k4_bucket", int(c["bucket"]))
     for rep in range(3):  # eager run, graph capture, replay (new seeds each time)
         seeds = rng.integers(0, E, c["B"])
         filt = None
