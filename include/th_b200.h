@@ -293,6 +293,13 @@ int th_shard_ipc_open(th_shard* s, int32_t peer, const void* h_handle64);
  * (the region is reallocated), all ranks reconnect, and the wave runs again. */
 int th_shard_grow_inbox(th_shard* s, int64_t inbox_records);
 int th_shard_inbox_overflowed(const th_shard* s);
+/* Every hop and phase of a begun wave for n shards that share one stream
+ * and one process (in-process worlds: stream order is the barrier), in the
+ * order th_shard_hop would take them -- one call instead of 3 k n. */
+int th_shards_run_hops(th_shard* const* shards, int32_t n, int32_t k);
+/* Per-phase kernel-group timing of the shard's waves (as th_session_*). */
+int th_shard_set_profiling(th_shard* s, int on);
+int64_t th_shard_profile_trace(th_shard* s, double* h_out4, int64_t cap);
 
 /* K7 on-demand hub-adjacency cache (the reference's LRU,
  * cache.py:38-89, reached per partition from engine.py:80-81).  The shard's

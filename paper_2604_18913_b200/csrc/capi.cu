@@ -547,6 +547,39 @@ int th_shard_finish(th_shard* s, th_result* out) {
   });
 }
 
+int th_shards_run_hops(th_shard* const* shards, int32_t n, int32_t k) {
+  return guarded([&]() -> int {
+    if (!shards || n < 1) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    for (int32_t i = 0; i < n; ++i) TH_SHARD_GUARD(shards[i]);
+    for (int32_t h = 1; h <= k; ++h)
+      for (int32_t phase = 0; phase < 3; ++phase)
+        for (int32_t i = 0; i < n; ++i) {
+          const int rc = th::shard_hop(shards[i]->sh, h, phase);
+          if (rc != TH_OK) return rc;
+        }
+    return TH_OK;
+  });
+}
+
+int th_shard_set_profiling(th_shard* s, int on) {
+  TH_SHARD_GUARD(s);
+  th::shard_session(s->sh)->prof = on != 0;
+  return TH_OK;
+}
+
+int64_t th_shard_profile_trace(th_shard* s, double* h_out4, int64_t cap) {
+  if (!s || !s->sh) return -1;
+  int64_t n = -1;
+  const int rc = guarded([&]() -> int {
+    n = th::session_profile_trace(th::shard_session(s->sh), h_out4, cap);
+    return TH_OK;
+  });
+  return rc == TH_OK ? n : -1;
+}
+
 int th_shard_hub_cache(th_shard* s, int64_t capacity_pages) {
   return guarded([&]() -> int {
     TH_SHARD_GUARD(s);

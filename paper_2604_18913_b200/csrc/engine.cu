@@ -2387,8 +2387,10 @@ int shard_create(Shard** out, const int32_t* d_subj, const int32_t* d_rel, const
   s->st = st;
   s->pull_divisor = 0.0;
   s->mat_rows = n_local;
-  s->row_map = sh->l2g;
-  s->tid_map = sh->tid_l2g;
+  // (one rank owns every entity and triple in id order: both maps are the
+  // identity, and K4 skips the per-id lookups)
+  s->row_map = world > 1 ? sh->l2g : nullptr;
+  s->tid_map = world > 1 ? sh->tid_l2g : nullptr;
   return TH_OK;
 }
 

@@ -202,7 +202,10 @@ __device__ __forceinline__ void shard_row_pairs(const ShardArgs& sa, int32_t u, 
       if (FILTER) w &= a.M[(size_t)a.csr_rel[pos] * W + j];
       if (w) {
         v = a.csr_obj[pos];
-        if (owner_of(v, sa.world) == sa.rank) {
+        if (sa.world == 1) {  // (one rank: every row is owned, local row = id)
+          row = v;
+          fresh = local_set<W, SEM>(a, row, j, w);
+        } else if (owner_of(v, sa.world) == sa.rank) {
           row = sa.lidx[v];
           fresh = local_set<W, SEM>(a, row, j, w);
         } else {

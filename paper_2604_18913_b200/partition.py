@@ -437,6 +437,21 @@ class GraphShard:
     def synchronize(self) -> None:
         self.stream.synchronize()
 
+    def set_profiling(self, on: bool) -> None:
+        _lib.check(_lib.load().th_shard_set_profiling(self._handle, int(bool(on))))
+
+    def profile_trace(self) -> list:
+        """Timeline of the last profiled wave: (category, stream, start ms,
+        end ms) per kernel group (stream 0 main, 1 / 2 K4 side streams)."""
+        lib = _lib.load()
+        n = int(lib.th_shard_profile_trace(self._handle, None, 0))
+        if n < 0:
+            raise RuntimeError(lib.th_last_error().decode(errors="replace"))
+        buf = (ctypes.c_double * max(4 * n, 1))()
+        lib.th_shard_profile_trace(self._handle, buf, n)
+        return [(_lib.PROF_CATEGORIES[int(buf[4 * i])], int(buf[4 * i + 1]), buf[4 * i + 2], buf[4 * i + 3])
+                for i in range(n)]
+
     # -- K7 hub-adjacency cache ------------------------------------------------
     def enable_hub_cache(self, capacity_pages: int) -> None:
         """Page this shard's hub slices in on demand from a pinned host store
@@ -619,11 +634,16 @@ def run_wave(shards, xch: Exchange, query: WaveQuery, stats: dict | None = None)
         for sh in shards:
             sh.begin(query)
         xch.barrier(shards)
-        for h in range(1, query.k + 1):
-            for phase in (0, 1, 2):
-                for sh in shards:
-                    sh.hop(h, phase)
-                xch.barrier(shards)
+        if isinstance(xch, LoopbackExchange) and all(isinstance(sh, GraphShard) for sh in shards):
+            # one process, one stream: the same phase order in one native call
+            handles = (ctypes.c_void_p * len(shards))(*[sh._handle for sh in shards])
+            _lib.check(_lib.load().th_shards_run_hops(handles, len(shards), query.k))
+        else:
+            for h in range(1, query.k + 1):
+                for phase in (0, 1, 2):
+                    for sh in shards:
+                        sh.hop(h, phase)
+                    xch.barrier(shards)
         done = [sh.finish() for sh in shards]
         inbox = xch.any([st == "inbox" for st, _ in done])
         if not xch.any([st != "ok" for st, _ in done]):
