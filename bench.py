@@ -377,8 +377,10 @@ def run_c4_leg(th, stream, peaks, n_batches=8, cols=None):
     for k in (2, 3):
         step = lambda i: ret.run(offs, batches[i], k, "frontier", None, singleton=True,  # noqa: E731
                                  copy=False)
-        step(0)  # sizes the result buffers
-        step(1)  # graph capture of this shape
+        for i in range(n_batches):  # warm-up: every batch once sizes the result buffers
+            step(i)
+        step(0)  # (stable shape: recorded, then captured as a CUDA graph)
+        step(1)
         tot_ms, seeds, edges, ids, lists, pbytes = 0.0, 0, 0, 0, 0, 0
         W = 32
         for i in range(n_batches):

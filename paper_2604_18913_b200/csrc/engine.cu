@@ -974,10 +974,10 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
       const int64_t* ltot = totals + kMaxWave;
       // bucketed write: (row, bit) entries scattered into 32-query groups,
       // then gathered into each query's output (k4_rowmajor.cuh)
-      uint32_t* P = ensure<uint32_t>(s->k4_slot ? s->k4_P2 : s->k4_P, std::max<int64_t>(cap, 1), s->st);
+      uint32_t* P = ensure<uint32_t>(s->k4_slot ? s->k4_P2 : s->k4_P, kBucketMaxIds, s->st);
       bucket_scan_kernel<<<W, 1024, 0, s->st>>>(gcount, nblk * kRsWarps, ltot);
       TH_LAUNCHED();
-      bucket_scatter_kernel<W><<<nblk, 32 * kRsWarps, 0, s->st>>>(rsrc, nblk, gcount, off, P, cap, ltot);
+      bucket_scatter_kernel<W><<<nblk, 32 * kRsWarps, 0, s->st>>>(rsrc, nblk, gcount, off, P, ltot);
       TH_LAUNCHED();
       // (the layer is free only after the write pass below, which re-reads
       // it when the bucketed passes stood aside)

@@ -294,7 +294,7 @@ template <int W>
 __global__ void __launch_bounds__(32 * kRsWarps) bucket_scatter_kernel(RowMajorSrc<W> src, int nblk,
                                                                        const uint32_t* __restrict__ gpre,
                                                                        const int64_t* __restrict__ off,
-                                                                       uint32_t* P, int64_t cap,
+                                                                       uint32_t* P,
                                                                        const int64_t* layer_total) {
   if (*layer_total > kBucketMaxIds) return;
   const int warp = threadIdx.x >> 5;
@@ -308,8 +308,10 @@ __global__ void __launch_bounds__(32 * kRsWarps) bucket_scatter_kernel(RowMajorS
   const int64_t lo = r0 + warp * per < r1 ? r0 + warp * per : r1;
   const int64_t hi = lo + per < r1 ? lo + per : r1;
   const uint32_t valid = lane < (unsigned)W ? valid_word((int)lane, src.nq) : 0u;
+  // (entry positions relative to the layer's first output: the buffer holds
+  // kBucketMaxIds entries whatever the result capacity)
   int64_t pos = 0;
-  if (valid) pos = off[32 * lane] + gpre[(size_t)(blk * kRsWarps + warp) * 32 + lane];
+  if (valid) pos = off[32 * lane] - off[0] + gpre[(size_t)(blk * kRsWarps + warp) * 32 + lane];
   for (int64_t i = lo; i < hi; i += kRsUnroll) {
     int32_t v[kRsUnroll];
     uint32_t x[kRsUnroll];
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(32 * kRsWarps) bucket_scatter_kernel(RowMajorS
       while (m) {
         const int b = __ffs(m) - 1;
         m &= m - 1u;
-        if (pos < cap) P[pos] = rel | (uint32_t)b;
+        if (pos < kBucketMaxIds) P[pos] = rel | (uint32_t)b;
         ++pos;
       }
     }
@@ -348,7 +350,7 @@ __global__ void __launch_bounds__(kThreads) bucket_gather_kernel(
     if (32 * j >= nq) continue;
     int64_t r0, r1;
     rs_block(nrows, nblk, blk, r0, r1);
-    const int64_t g0 = off[32 * j];
+    const int64_t g0 = off[32 * j] - off[0];
     const int64_t start = g0 + gpre[(size_t)(blk * kRsWarps) * 32 + j];
     const int64_t end = g0 + gpre[(size_t)((blk + 1) * kRsWarps) * 32 + j];
     const int q = 32 * j + (int)lane;
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(kThreads) bucket_gather_kernel(
       uint32_t e = 0u;
       int32_t id = 0;
       if (ok) {
-        e = i < cap ? __ldcs(P + i) : 0u;
+        e = i < kBucketMaxIds ? __ldcs(P + i) : 0u;
         const int32_t v = __ldg(rows + r0 + (e >> 5));
         id = map ? __ldg(map + v) : v;
       }
