@@ -763,7 +763,10 @@ def run_ours(args, world, rank, local):
             "kernel_ms_source": "CUDA events around each kernel group, profiled pass over the same K batches",
             "kernel_launches_per_step": {c: v[1] / args.steps for c, v in prof.items()},
             "e2e": {"value": e2e_value, "unit": "seeds/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "api": "Retriever.retrieve + pinned D2H of all results"},
+                    "d2h_bytes_per_step": d2h, "api": "Retriever.retrieve + pinned D2H of all results",
+                    # the host link bounds it: result bytes per second of the whole step
+                    "link_GBps": (h2d + d2h) / e2e_t / 1e9,
+                    "note": "PCIe-bound: every step returns all per-seed frontiers (int32) to the host"},
             "gpu_launches": launches,
             "wall_s_timed": wall,
             "clocks": clk,
