@@ -23,7 +23,7 @@ from .core_types import (
 )
 from .batch import BatchQuery, BatchResult, QueryBatch, plan_batch, run_batch, signature
 from .archive import graph_from_bytes, graph_to_bytes, load_graph, save_graph
-from .cache import CacheCounters, SubgraphCache
+from .cache import CacheCounters, SubgraphCache, simulate_lru
 from .device_graph import IncidenceGraph, build_incidence
 from .errors import DataError, IntegrityError, TripleHopError, UsageError
 from .partition import (
@@ -52,9 +52,14 @@ from .store import (
     open_partitioned,
     save_partition_dir,
 )
+from .service import Labels as Dictionary, LookupResult, lookup_entities
 from .targets import GpuTarget, PartitionedGpuTarget
 
 __all__ = [
+    "Dictionary",
+    "LookupResult",
+    "lookup_entities",
+    "simulate_lru",
     "BatchQuery",
     "BatchResult",
     "QueryBatch",

@@ -20,7 +20,7 @@ from __future__ import annotations
 
 import threading
 from pathlib import Path
-from typing import Literal
+from typing import Literal, NamedTuple
 
 import numpy as np
 from pydantic import BaseModel, Field, model_validator
@@ -35,14 +35,29 @@ RELATIONS_FILE = "relations.txt"
 
 class Labels:
     """Label <-> dense id, ids in first-occurrence order of the label file
-    (the reference's dictionary files: line index = id)."""
+    (the reference's dictionary files: line index = id); exported as
+    ``Dictionary`` for the reference's name (triples.py:26-60)."""
 
-    def __init__(self, labels):
+    def __init__(self, labels=()):
         self._labels = list(dict.fromkeys(labels))
         self._ids = {lab: i for i, lab in enumerate(self._labels)}
 
+    def add(self, label: str) -> int:
+        """The id of ``label``, the next free id when it is new."""
+        i = self._ids.get(label)
+        if i is None:
+            i = self._ids[label] = len(self._labels)
+            self._labels.append(label)
+        return i
+
     def __len__(self) -> int:
         return len(self._labels)
+
+    def __contains__(self, label) -> bool:
+        return label in self._ids
+
+    def __eq__(self, other) -> bool:
+        return isinstance(other, Labels) and self._labels == other._labels
 
     def id_of(self, label: str):
         return self._ids.get(label)
@@ -122,8 +137,14 @@ class QueryRequest(BaseModel):
         return self
 
 
-def lookup_entities(labels, entities: Labels):
-    """(sorted distinct ids, unknown labels in request order)."""
+class LookupResult(NamedTuple):
+    ids: list
+    unknown: list
+
+
+def lookup_entities(labels, entities: Labels) -> LookupResult:
+    """(sorted distinct ids, unknown labels in request order); unknown
+    labels are reported, never fatal."""
     ids, unknown = set(), []
     for lab in labels:
         i = entities.id_of(lab)
@@ -131,7 +152,7 @@ def lookup_entities(labels, entities: Labels):
             unknown.append(lab)
         else:
             ids.add(i)
-    return sorted(ids), unknown
+    return LookupResult(sorted(ids), unknown)
 
 
 def answer(registry: DeviceGraphRegistry, req: QueryRequest) -> dict:

@@ -75,3 +75,15 @@ def test_device_units_load_and_evict(cuda_device):
     assert 0 not in c and 1 in c and g1 is not g0
     res = th.retrieve(g1, [0], 2)
     assert res.frontier(0, 1).tolist() == [1, 2]
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_public_simulate_lru_matches_independent_model(seed):
+    """th.simulate_lru (the reference's public entry point, cache.py:92-117)
+    against the test suite's independent list model."""
+    import paper_2604_18913_b200 as th
+
+    rng = np.random.default_rng(100 + seed)
+    cap = int(rng.integers(1, 7))
+    trace = rng.integers(0, 11, 300).tolist()
+    assert th.simulate_lru(trace, cap) == simulate_lru(trace, cap)

@@ -57,3 +57,12 @@ def test_graph_dir_label_mismatch_is_integrity_error(tmp_path):
     (d / "relations.txt").write_text("r0\n")
     with pytest.raises((IntegrityError, RuntimeError)):  # (RuntimeError: no device to build on)
         load_graph_dir(d)
+
+
+def test_dictionary_export():
+    import paper_2604_18913_b200 as th
+
+    d = th.Dictionary()
+    assert [d.add(x) for x in ("p", "q", "p")] == [0, 1, 0]
+    assert "q" in d and len(d) == 2 and d == th.Dictionary(["p", "q"])
+    assert th.lookup_entities(["q", "zz"], d) == th.LookupResult([1], ["zz"])
