@@ -227,6 +227,20 @@ def _gpu_dist_worker(rank, world, port, errfile):
         ref_p, ref_t = orc.walk_paths(og, [int(seeds[0])], 2, 100)
         assert [tuple(tuple(int(x) for x in t) for t in p) for p in pr.paths] == orc.paths_as_triples(og, ref_p)
         assert pr.truncated == ref_t
+        # the same world with each process paging its hub slices through a K7
+        # hub cache (one page holds every slice here: hits after the first wave)
+        del pg
+        pc = th.PartitionedGraph((s, r, o), E, R, xch, n_hubs=8, hub_cache_pages=2)
+        for sem in ("frontier", "exact"):
+            res = pc.retrieve(seeds, 2, semantics=sem, activated=True)
+            for i in range(0, 150, 11):
+                ref = orc.retrieve_one(og, int(seeds[i]), 2, sem)
+                for h in range(2):
+                    assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h])
+                    assert np.array_equal(res.activated(i, h + 1), ref["activated"][h])
+        (st,) = pc.hub_cache_stats()
+        c = st["counters"]
+        assert c.hits > 0 and c.loads == c.misses <= st["pages"] and c.evictions == 0
     except BaseException as e:  # pragma: no cover - reported to the parent
         with open(errfile, "a") as f:
             f.write(f"rank {rank}: {type(e).__name__}: {e}\n")
