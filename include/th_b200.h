@@ -297,6 +297,12 @@ int th_shard_inbox_overflowed(const th_shard* s);
  * and one process (in-process worlds: stream order is the barrier), in the
  * order th_shard_hop would take them -- one call instead of 3 k n. */
 int th_shards_run_hops(th_shard* const* shards, int32_t n, int32_t k);
+/* A whole wave (th_shard_begin of every shard with queries[i], then every
+ * hop and phase) for such a world, replayed as one CUDA graph once a shape
+ * repeats (inputs staged into session buffers; h_n_seeds[i] = length of
+ * queries[i].d_seeds).  Eager for shards with a hub cache or profiling. */
+int th_shards_run_wave(th_shard* const* shards, int32_t n, const th_query* queries,
+                       const int64_t* h_n_seeds);
 /* Per-phase kernel-group timing of the shard's waves (as th_session_*). */
 int th_shard_set_profiling(th_shard* s, int on);
 int64_t th_shard_profile_trace(th_shard* s, double* h_out4, int64_t cap);

@@ -34,7 +34,7 @@ EXPORTS = (
     "th_shard_inbox_overflowed", "th_shard_hop", "th_shard_finish", "th_shard_sent", "th_shard_columns",
     "th_shard_hub_cache", "th_shard_hub_cache_stats", "th_shard_hub_cache_trace",
     "th_shard_hub_cache_resident", "th_shard_set_profiling", "th_shard_profile_trace",
-    "th_shards_run_hops",
+    "th_shards_run_hops", "th_shards_run_wave",
     "th_ids_route_count", "th_ids_map_scatter", "th_ids_to_local_bits", "th_bits_andnot_update",
     "th_bits_or", "th_bits_compact", "th_plan_subjects", "th_session_set_k4_mode",
     "th_session_set_pull_screen", "th_session_wave_modes", "th_session_set_knob",
@@ -152,6 +152,8 @@ def load():
         "th_shard_hub_cache": (ctypes.c_int, [_vp, ctypes.c_int64]),
         "th_shard_set_profiling": (ctypes.c_int, [_vp, ctypes.c_int]),
         "th_shards_run_hops": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32]),
+        "th_shards_run_wave": (ctypes.c_int, [ctypes.POINTER(_vp), ctypes.c_int32, ctypes.POINTER(Query),
+                                              ctypes.POINTER(ctypes.c_int64)]),
         "th_shard_profile_trace": (ctypes.c_int64, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int64]),
         "th_shard_hub_cache_stats": (ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_int64)]),
         "th_shard_hub_cache_trace": (ctypes.c_int64, [_vp, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]),

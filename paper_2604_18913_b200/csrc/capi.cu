@@ -5,6 +5,7 @@
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/th_b200.h"
 #include "engine.cuh"
@@ -561,6 +562,22 @@ int th_shards_run_hops(th_shard* const* shards, int32_t n, int32_t k) {
           if (rc != TH_OK) return rc;
         }
     return TH_OK;
+  });
+}
+
+int th_shards_run_wave(th_shard* const* shards, int32_t n, const th_query* queries,
+                       const int64_t* h_n_seeds) {
+  return guarded([&]() -> int {
+    if (!shards || n < 1 || !queries || !h_n_seeds) {
+      th::set_error("bad arguments");
+      return TH_ERR_INVALID;
+    }
+    std::vector<th::Shard*> sh(n);
+    for (int32_t i = 0; i < n; ++i) {
+      TH_SHARD_GUARD(shards[i]);
+      sh[i] = shards[i]->sh;
+    }
+    return th::shards_run_wave(sh.data(), n, queries, h_n_seeds);
   });
 }
 

@@ -1819,7 +1819,24 @@ struct Shard {
   bool in_wave = false;
   int next_hop = 0, next_phase = 0;
   HubCache* hc = nullptr;          // K7: hub slices paged in on demand (hubcache.cuh)
+  struct WaveGraph* group = nullptr;  // in-process worlds: the wave's CUDA graph (when members[0])
+  bool retired = false;            // the wave's retire kernels are issued already (shards_run_wave)
   int64_t rows() const { return n_local + H; }
+};
+
+// A whole wave of an in-process world (every rank on one stream) as one
+// CUDA graph: begin + every hop's phases of every shard, captured once per
+// shape and replayed (inputs staged into session buffers first, as
+// run_graphed does for single graphs).
+struct WaveGraph {
+  std::vector<Shard*> members;
+  std::vector<GraphKey> keys;
+  std::vector<uint64_t> sigs;
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t cap = nullptr;
+  bool seen = false, valid = false;
+  int failures = 0;
+  int64_t launches = 0;
 };
 
 namespace {
@@ -2490,6 +2507,7 @@ int shard_begin(Shard* sh, const th_query* q) {
   s->has_run = true;
   sh->W = pick_words((int)std::max<int64_t>(B, 1));
   sh->in_wave = true;
+  sh->retired = false;
   TH_W_DISPATCH(sh->W, shard_begin_w<WW>(sh, q));
   return TH_OK;
 }
@@ -2531,7 +2549,7 @@ int shard_finish(Shard* sh, th_result* out) {
     set_error("th_shard_finish before the last hop ended");
     return TH_ERR_STATE;
   }
-  TH_W_DISPATCH(sh->W, shard_retire_w<WW>(sh));
+  if (!sh->retired) TH_W_DISPATCH(sh->W, shard_retire_w<WW>(sh));
   sh->in_wave = false;
   const int rc = session_finish(&sh->s, out);
   XCtrl xc;
@@ -2589,7 +2607,172 @@ int shard_hub_cache(Shard* sh, int64_t capacity) {
 
 HubCache* shard_hub_cache_of(Shard* sh) { return sh->hc; }
 
+namespace {
+
+// the shard-side buffers a captured wave bakes in (exchange region, staging)
+uint64_t shard_sig(const Shard* sh) {
+  uint64_t h = 1469598103934665603ull;
+  for (uint64_t v : {(uint64_t)(uintptr_t)sh->xr, (uint64_t)sh->xcap, (uint64_t)sh->off_keys,
+                     (uint64_t)sh->off_bits, (uint64_t)sh->off_hubs, (uint64_t)(uintptr_t)sh->O.p,
+                     (uint64_t)sh->O.bytes, (uint64_t)(uintptr_t)sh->Of.p, (uint64_t)(uintptr_t)sh->olist.p,
+                     (uint64_t)(uintptr_t)sh->d_peers, (uint64_t)(sh->pull_divisor * 1024.0)}) {
+    h ^= v;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+// host-side state a begin + all hops leave behind (a replayed graph ran them)
+void shard_mark_wave(Shard* sh, const th_query* q) {
+  Session* s = &sh->s;
+  s->f_cap = std::max<int64_t>({s->f_cap, s->last_f_need, 1 << 16});
+  s->a_cap = std::max<int64_t>({s->a_cap, s->last_a_need, 1 << 16});
+  s->last = *q;
+  s->has_run = true;
+  sh->W = pick_words((int)std::max<int64_t>(q->n_queries, 1));
+  sh->in_wave = true;
+  sh->next_hop = q->k + 1;
+  sh->next_phase = 0;
+  sh->retired = true;
+}
+
+int shards_issue(Shard* const* sh, int n, const th_query* q) {
+  for (int i = 0; i < n; ++i) {
+    const int rc = shard_begin(sh[i], &q[i]);
+    if (rc != TH_OK) return rc;
+  }
+  for (int h = 1; h <= q[0].k; ++h)
+    for (int phase = 0; phase < 3; ++phase)
+      for (int i = 0; i < n; ++i) {
+        const int rc = shard_hop(sh[i], h, phase);
+        if (rc != TH_OK) return rc;
+      }
+  // the retire kernels too (they join the K4 side streams back)
+  for (int i = 0; i < n; ++i) {
+    TH_W_DISPATCH(sh[i]->W, shard_retire_w<WW>(sh[i]));
+    sh[i]->retired = true;
+  }
+  return TH_OK;
+}
+
+void wave_keys(Shard* const* sh, int n, const th_query* q, std::vector<GraphKey>& keys,
+               std::vector<uint64_t>& sigs) {
+  keys.resize(n);
+  sigs.resize(n);
+  for (int i = 0; i < n; ++i) {
+    keys[i] = graph_key(&sh[i]->s, &q[i]);
+    sigs[i] = shard_sig(sh[i]);
+  }
+}
+
+}  // namespace
+
+int shards_run_wave(Shard* const* sh, int n, const th_query* q, const int64_t* n_seeds) {
+  cudaStream_t st = sh[0]->s.st;
+  bool graphable = n >= 1;
+  for (int i = 0; i < n && graphable; ++i)
+    graphable = !sh[i]->hc && !sh[i]->s.prof && sh[i]->s.st == st && q[i].n_queries > 0 &&
+                q[i].k == q[0].k && shard_connected(sh[i]);
+  if (!graphable) return shards_issue(sh, n, q);
+  // stage the inputs into session buffers (their addresses are baked in)
+  std::vector<th_query> qs(q, q + n);
+  for (int i = 0; i < n; ++i) {
+    Session* s = &sh[i]->s;
+    const int64_t B = q[i].n_queries;
+    qs[i].d_seed_offsets = stage(s->in_offs, q[i].d_seed_offsets, B + 1, st);
+    qs[i].d_seeds = stage(s->in_seeds, q[i].d_seeds, std::max<int64_t>(n_seeds[i], 1), st);
+    if (q[i].d_rel_masks)
+      qs[i].d_rel_masks = stage(s->in_masks, q[i].d_rel_masks, B * (int64_t)q[i].mask_words, st);
+  }
+  if (!sh[0]->group) sh[0]->group = new WaveGraph();
+  WaveGraph* G = sh[0]->group;
+  std::vector<GraphKey> keys;
+  std::vector<uint64_t> sigs;
+  wave_keys(sh, n, qs.data(), keys, sigs);
+  const bool same = G->members == std::vector<Shard*>(sh, sh + n) && G->keys == keys && G->sigs == sigs;
+  if (G->exec && G->valid && same) {
+    TH_CUDA(cudaGraphLaunch(G->exec, st));
+    for (int i = 0; i < n; ++i) shard_mark_wave(sh[i], &qs[i]);
+    sh[0]->s.launches += G->launches;
+    return TH_OK;
+  }
+  if (G->exec) cudaGraphExecDestroy(G->exec);
+  G->exec = nullptr;
+  G->valid = false;
+  static const bool dbg_w = std::getenv("TH_GRAPH_DEBUG") != nullptr;
+  if (dbg_w)
+    std::fprintf(stderr, "[th] wave: exec=%d valid=%d seen=%d same=%d failures=%d\n", (int)(G->exec != nullptr),
+                 (int)G->valid, (int)G->seen, (int)same, G->failures);
+  if (!(G->seen && same) || G->failures >= 3) {
+    // first wave of this shape: eager (sizes every buffer), remembered
+    const int rc = shards_issue(sh, n, qs.data());
+    G->members.assign(sh, sh + n);
+    wave_keys(sh, n, qs.data(), G->keys, G->sigs);
+    G->seen = rc == TH_OK;
+    return rc;
+  }
+  // second wave of the same shape: capture on a session-owned stream
+  if (!G->cap) {
+    int least = 0, greatest = 0;
+    TH_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    TH_CUDA(cudaStreamCreateWithPriority(&G->cap, cudaStreamNonBlocking, greatest));
+  }
+  // (the capture stream must see the staged inputs)
+  cudaEvent_t staged;
+  TH_CUDA(cudaEventCreateWithFlags(&staged, cudaEventDisableTiming));
+  TH_CUDA(cudaEventRecord(staged, st));
+  TH_CUDA(cudaStreamWaitEvent(G->cap, staged, 0));
+  cudaEventDestroy(staged);
+  std::vector<int64_t> l0(n);
+  for (int i = 0; i < n; ++i) {
+    l0[i] = sh[i]->s.launches;
+    sh[i]->s.st = G->cap;
+  }
+  TH_CUDA(cudaStreamBeginCapture(G->cap, cudaStreamCaptureModeThreadLocal));
+  int rc = TH_OK;
+  bool threw = false;
+  try {
+    rc = shards_issue(sh, n, qs.data());
+  } catch (const CudaError&) {
+    threw = true;
+  }
+  for (int i = 0; i < n; ++i) sh[i]->s.st = st;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(G->cap, &graph);
+  std::vector<GraphKey> after;
+  std::vector<uint64_t> after_sigs;
+  wave_keys(sh, n, qs.data(), after, after_sigs);
+  if (threw || rc != TH_OK || ce != cudaSuccess || after != keys || after_sigs != sigs) {
+    // capture is an optimisation: drop it and run this wave eagerly
+    static const bool dbg = std::getenv("TH_GRAPH_DEBUG") != nullptr;
+    if (dbg)
+      std::fprintf(stderr, "[th] wave capture dropped: threw=%d rc=%d end=%s keys=%d sigs=%d\n", (int)threw, rc,
+                   cudaGetErrorString(ce), (int)(after == keys), (int)(after_sigs == sigs));
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    G->failures += 1;
+    G->seen = false;
+    for (int i = 0; i < n; ++i) sh[i]->s.launches = l0[i];
+    return shards_issue(sh, n, qs.data());
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(graph);
+  TH_CUDA(ie);
+  G->exec = exec;
+  G->valid = true;
+  G->launches = 0;
+  for (int i = 0; i < n; ++i) G->launches += sh[i]->s.launches - l0[i];
+  TH_CUDA(cudaGraphLaunch(G->exec, st));
+  return TH_OK;
+}
+
 void shard_free(Shard* sh) {
+  if (sh->group) {
+    if (sh->group->exec) cudaGraphExecDestroy(sh->group->exec);
+    if (sh->group->cap) cudaStreamDestroy(sh->group->cap);
+    delete sh->group;
+  }
   session_free(&sh->s);
   if (sh->hc) hubcache_free(sh->hc, &sh->g);
   shard_close_peers(sh);

@@ -165,6 +165,8 @@ int shard_columns(const Shard* sh, th_shard_cols* out);
 Session* shard_session(Shard* sh);
 struct HubCache;
 int shard_hub_cache(Shard* sh, int64_t capacity);
+// an in-process world's whole wave (begin + every hop), graph-captured per shape
+int shards_run_wave(Shard* const* sh, int n, const th_query* q, const int64_t* n_seeds);
 HubCache* shard_hub_cache_of(Shard* sh);
 void shard_free(Shard* sh);
 

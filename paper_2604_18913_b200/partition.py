@@ -489,8 +489,10 @@ class GraphShard:
 
     # -- the wave ---------------------------------------------------------------
     def begin(self, query: "WaveQuery") -> None:
-        import torch
+        _lib.check(_lib.load().th_shard_begin(self._handle, ctypes.byref(self.prepare(query))))
 
+    def prepare(self, query: "WaveQuery"):
+        """Upload the wave's query arrays; the th_query describing them."""
         q = _lib.Query()
         B = query.n_queries
         self._dev = {
@@ -508,7 +510,8 @@ class GraphShard:
         q.flags = _lib.TH_WANT_FRONTIERS | (_lib.TH_WANT_ACTIVATED if query.activated else 0)
         q.max_paths = 0
         self._q = q
-        _lib.check(_lib.load().th_shard_begin(self._handle, ctypes.byref(q)))
+        self._n_seeds = int(np.asarray(query.seeds).size)
+        return q
 
     def _upload(self, name, arr):
         """Asynchronous H2D copy through a reused pinned staging buffer,
@@ -631,14 +634,17 @@ def run_wave(shards, xch: Exchange, query: WaveQuery, stats: dict | None = None)
     ShardResults.  An output (or inbox) overflow on any rank makes every rank
     run the wave again with grown capacities."""
     for _attempt in range(6):
-        for sh in shards:
-            sh.begin(query)
-        xch.barrier(shards)
         if isinstance(xch, LoopbackExchange) and all(isinstance(sh, GraphShard) for sh in shards):
-            # one process, one stream: the same phase order in one native call
+            # one process, one stream: begin and every phase in one native
+            # call, replayed as a CUDA graph once the wave's shape repeats
+            qs = (_lib.Query * len(shards))(*[sh.prepare(query) for sh in shards])
             handles = (ctypes.c_void_p * len(shards))(*[sh._handle for sh in shards])
-            _lib.check(_lib.load().th_shards_run_hops(handles, len(shards), query.k))
+            nseeds = (ctypes.c_int64 * len(shards))(*[sh._n_seeds for sh in shards])
+            _lib.check(_lib.load().th_shards_run_wave(handles, len(shards), qs, nseeds))
         else:
+            for sh in shards:
+                sh.begin(query)
+            xch.barrier(shards)
             for h in range(1, query.k + 1):
                 for phase in (0, 1, 2):
                     for sh in shards:
