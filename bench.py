@@ -165,7 +165,39 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if _one_device():
+        local = 0
     return world, rank, local
+
+
+def _one_device() -> bool:
+    """TH_BENCH_ONE_DEVICE=1: every rank on cuda:0 with gloo collectives -- a
+    check of the multi-rank code path on a one-GPU box, never a measurement
+    (NCCL refuses two ranks on one device)."""
+    return os.environ.get("TH_BENCH_ONE_DEVICE") == "1"
+
+
+def _init_dist(dev, rank=None, world=None):
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    kw = {} if rank is None else {"rank": rank, "world_size": world}
+    if _one_device():
+        dist.init_process_group("gloo", **kw)
+    else:
+        dist.init_process_group("nccl", device_id=dev, **kw)
+
+
+def _all_reduce(t, op):
+    """In-place all-reduce of a device tensor (through the host under gloo)."""
+    import torch.distributed as dist
+
+    if _one_device():
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
 
 
 # --------------------------------------------------------------- CPU side
@@ -477,8 +509,8 @@ def partitioned_leg(th, cols, E, R, world, rank, ks=(2, 3), n_batches=4, reps=4)
         if world > 1:
             vals = vals.to(dev)
             tmax = vals.clone()
-            torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
-            torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.SUM)
+            _all_reduce(tmax, torch.distributed.ReduceOp.MAX)
+            _all_reduce(vals, torch.distributed.ReduceOp.SUM)
             vals[0] = tmax[0]
             vals = vals.cpu()
         t_ms = float(vals[0])
@@ -517,8 +549,7 @@ def run_partitioned(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        _init_dist(dev, rank, world)
     s, r, o, E, R = workloads.c4_graph()
     clocks = ClockSampler(local)
     clocks.start()
@@ -545,9 +576,7 @@ def run_ours(args, world, rank, local):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dev)
     import paper_2604_18913_b200 as th
 
     s, r, o, E, R = workloads.c2_graph()
@@ -623,7 +652,7 @@ def run_ours(args, world, rank, local):
         import torch.distributed as dist
 
         tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        _all_reduce(tt, dist.ReduceOp.MAX)
         t_ms = float(tt.item())
     seeds_total = BATCH * args.steps * world
     value = seeds_total / (t_ms / 1e3)
@@ -704,7 +733,7 @@ def run_ours(args, world, rank, local):
         import torch.distributed as dist
 
         tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        _all_reduce(tt, dist.ReduceOp.MAX)
         e2e_t = float(tt.item())
     e2e_value = BATCH * world / e2e_t
 
