@@ -161,7 +161,7 @@ def test_hub_cache_two_ranks(th, graph):
     for w in range(4):
         seeds = np.concatenate([hubs[rng.choice(N_HUBS, 3, replace=False)],
                                 pointers[rng.choice(N_HUBS, 2, replace=False)], rng.integers(0, E, 40)])
-        for sem in ("frontier", "exact"):
+        for sem in ("frontier", "exact", "cumulative"):
             a = pg.retrieve(seeds, 2, semantics=sem, activated=True)
             b = plain.retrieve(seeds, 2, semantics=sem, activated=True)
             _same(a, b, seeds.size, 2)
