@@ -2615,7 +2615,13 @@ uint64_t shard_sig(const Shard* sh) {
   for (uint64_t v : {(uint64_t)(uintptr_t)sh->xr, (uint64_t)sh->xcap, (uint64_t)sh->off_keys,
                      (uint64_t)sh->off_bits, (uint64_t)sh->off_hubs, (uint64_t)(uintptr_t)sh->O.p,
                      (uint64_t)sh->O.bytes, (uint64_t)(uintptr_t)sh->Of.p, (uint64_t)(uintptr_t)sh->olist.p,
-                     (uint64_t)(uintptr_t)sh->d_peers, (uint64_t)(sh->pull_divisor * 1024.0)}) {
+                     (uint64_t)(uintptr_t)sh->d_peers, (uint64_t)(sh->pull_divisor * 1024.0),
+                     // (the graph arrays too: a shard built later at a freed shard's address)
+                     (uint64_t)(uintptr_t)sh->g.indptr, (uint64_t)(uintptr_t)sh->g.csr_obj,
+                     (uint64_t)(uintptr_t)sh->g.csr_rel, (uint64_t)(uintptr_t)sh->g.csr_tid,
+                     (uint64_t)(uintptr_t)sh->g.subj, (uint64_t)(uintptr_t)sh->gin.rsrc,
+                     (uint64_t)(uintptr_t)sh->gin.item_v, (uint64_t)(uintptr_t)sh->lidx,
+                     (uint64_t)(uintptr_t)sh->l2g, (uint64_t)(uintptr_t)sh->tid_l2g}) {
     h ^= v;
     h *= 1099511628211ull;
   }
