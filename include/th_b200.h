@@ -175,9 +175,11 @@ int th_session_set_overlap(th_session* s, int on);
  * layers without fused edge counts (default); 2 = row-major for every
  * entity layer (no mask cache for small dense layers). */
 int th_session_set_k4_mode(th_session* s, int mode);
-/* Pull hops screen their in-row items one per lane for a frontier in-edge
- * before lane groups expand the survivors: -1 = when the graph's mean
- * in-edges per pull item is below 4 (default), 0 = never, 1 = always. */
+/* Pull hops screen their in-row items for a frontier in-edge before lane
+ * groups expand the survivors: -1 = when the graph's mean in-edges per pull
+ * item is below 4 (default; as mode 2), 0 = never, 1 = one item per lane
+ * inside the pull kernel, 2 = a separate edge-parallel screen kernel that
+ * compacts the surviving items, then the pull over that list. */
 int th_session_set_pull_screen(th_session* s, int mode);
 /* Boolean strategy knobs by name (A/B and tests): "paths_k2" (k = 2
  * singleton capped path queries on a CTA each; default 1), "k4_cache"

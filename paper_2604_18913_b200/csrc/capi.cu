@@ -266,8 +266,8 @@ int th_session_set_k4_mode(th_session* s, int mode) {
 }
 
 int th_session_set_pull_screen(th_session* s, int mode) {
-  if (!s || mode < -1 || mode > 1) {
-    th::set_error(!s ? "NULL handle" : "pull screen mode must be -1, 0 or 1");
+  if (!s || mode < -1 || mode > 2) {
+    th::set_error(!s ? "NULL handle" : "pull screen mode must be -1, 0, 1 or 2");
     return TH_ERR_INVALID;
   }
   s->s.pull_screen = mode;

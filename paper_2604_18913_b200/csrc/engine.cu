@@ -72,6 +72,7 @@ struct WaveArgs {
   const int32_t* item_lo;
   const int32_t* item_hi;
   int64_t n_items;
+  const int32_t* n_items_dev;  // device item count (the two-phase pull's compacted items)
   int64_t E, T;
   uint32_t *X, *N, *V, *S, *Xf, *Nf, *Vf;
   const uint32_t* M;
@@ -1035,8 +1036,37 @@ void materialize_triples(Session* s, WaveBufs& b, int nq, int64_t* off, int64_t*
 
 // pull hops screen items per lane first on graphs of low mean in-degree
 // per pull item (k3_pull.cuh; C4: ~2.3 in-edges per item, C2: ~10)
-bool pull_screens(const Graph* g, int knob = -1) {
-  return knob >= 0 ? knob == 1 : (g->n_items > 0 && g->T < 4 * g->n_items);
+// (0 none, 1 per lane inside the pull kernel, 2 the two-phase screen +
+// compacted pull)
+int pull_screen_mode(const Graph* g, int knob = -1) {
+  return knob >= 0 ? knob : (g->n_items > 0 && g->T < 4 * g->n_items) ? 2 : 0;
+}
+
+// one pull hop over graph g's items (the session's graph, or a shard's
+// in-edge graph) with the session's screening mode
+template <int W, int SEM, bool FILTER>
+void launch_pull(Session* s, const Graph* g, const WaveArgs& a, cudaStream_t st) {
+  const unsigned pg = persistent_grid();
+  const int mode = pull_screen_mode(g, s->pull_screen);
+  if (mode == 2) {
+    const int64_t n = std::max<int64_t>(g->n_items, 1);
+    int32_t* c = ensure<int32_t>(s->pull_items, 3 * n, st);
+    pull_screen_kernel<<<pg, kThreads, 0, st>>>(a, c, c + n, c + 2 * n);
+    TH_LAUNCHED();
+    WaveArgs pa = a;
+    pa.item_v = c;
+    pa.item_lo = c + n;
+    pa.item_hi = c + 2 * n;
+    pa.n_items_dev = &a.ctl->pull_items[a.h];
+    pull_kernel<W, SEM, FILTER, false><<<pg, kThreads, 0, st>>>(pa);
+    TH_LAUNCHED();
+    s->launches += 2;
+    return;
+  }
+  if (mode == 1) pull_kernel<W, SEM, FILTER, true><<<pg, kThreads, 0, st>>>(a);
+  else pull_kernel<W, SEM, FILTER, false><<<pg, kThreads, 0, st>>>(a);
+  TH_LAUNCHED();
+  s->launches += 1;
 }
 
 template <int W, int SEM, bool FILTER>
@@ -1054,10 +1084,7 @@ void expand_hop(Session* s, const WaveArgs& a) {
   }
   if (s->g->rindptr) {
     ProfScope ps(s, TH_PROF_PULL);
-    if (pull_screens(s->g, s->pull_screen)) pull_kernel<W, SEM, FILTER, true><<<pg, kThreads, 0, s->st>>>(a);
-    else pull_kernel<W, SEM, FILTER, false><<<pg, kThreads, 0, s->st>>>(a);
-    TH_LAUNCHED();
-    s->launches += 1;
+    launch_pull<W, SEM, FILTER>(s, s->g, a, s->st);
   }
 }
 
@@ -2152,18 +2179,13 @@ void shard_receive_w(Shard* sh, int h) {
     pa.item_lo = sh->gin.item_lo;
     pa.item_hi = sh->gin.item_hi;
     pa.n_items = sh->gin.n_items;
-    const bool scr = pull_screens(&sh->gin, s->pull_screen);
-#define TH_SHARD_PULL(SEM, F)                                                          \
-  if (scr) pull_kernel<W, SEM, F, true><<<pg, kThreads, 0, st>>>(pa);                  \
-  else pull_kernel<W, SEM, F, false><<<pg, kThreads, 0, st>>>(pa);
     if (sem == TH_EXACT) {
-      if (filter) { TH_SHARD_PULL(TH_EXACT, true) } else { TH_SHARD_PULL(TH_EXACT, false) }
+      if (filter) launch_pull<W, TH_EXACT, true>(s, &sh->gin, pa, st);
+      else launch_pull<W, TH_EXACT, false>(s, &sh->gin, pa, st);
     } else {
-      if (filter) { TH_SHARD_PULL(TH_FRONTIER, true) } else { TH_SHARD_PULL(TH_FRONTIER, false) }
+      if (filter) launch_pull<W, TH_FRONTIER, true>(s, &sh->gin, pa, st);
+      else launch_pull<W, TH_FRONTIER, false>(s, &sh->gin, pa, st);
     }
-#undef TH_SHARD_PULL
-    TH_LAUNCHED();
-    s->launches += 1;
     if (sh->world > 1) {
       shard_clear_frontier_kernel<W><<<pg, kThreads, 0, st>>>(sa, h - 1);
       TH_LAUNCHED();

@@ -20,6 +20,7 @@ struct Ctl {
   unsigned long long sent[kMaxK + 2];  // shards: records written to other ranks' inboxes per hop
   int32_t mode[kMaxK + 2];  // 0 = push, 1 = pull
   int32_t dense[kMaxK + 2]; // pull hop over a frontier that sources most in-edges
+  int32_t pull_items[kMaxK + 2];  // two-phase pull: items the screen kept per hop
   int32_t heavy_len;
   int32_t err;
   int64_t ids_used;
@@ -62,7 +63,9 @@ struct Session {
   bool overlap = true;
   bool k4_cache = true;
   bool paths_k2 = true;     // k = 2 singleton capped path queries: a CTA per query (paths.cu)
-  int pull_screen = -1;     // pull items screened per lane first: -1 by graph shape, 0 off, 1 on
+  // pull items screened first: -1 by graph shape, 0 off, 1 per lane inside the
+  // pull kernel, 2 a separate edge-parallel screen kernel + a compacted pull
+  int pull_screen = -1;
   int k4_mode = 1;  // count pass: 0 word-per-warp, 1 row-major for list-driven layers, 2 for all (k4_rowmajor.cuh)
   // captured waves: the hop chain's kernels get the device's highest stream
   // priority and K4's side streams the lowest, so the block scheduler feeds
@@ -84,7 +87,8 @@ struct Session {
   // wave state
   DBuf X, N, V, S, Xf, Nf, Vf, lists, heavy, M, counts, totals, rowlist, rowscan, k4_S, k4_meta, heavy_off;
   DBuf counts2, totals2, rowlist2, rowscan2, k4_S2, k4_meta2;  // second K4 slot
-  DBuf k4_P, k4_G, k4_P2, k4_G2;  // bucketed write pass: entries, group counts (per slot)
+  DBuf k4_P, k4_G, k4_P2, k4_G2;
+  DBuf pull_items;  // two-phase pull: the screened items (v, lo, hi)  // bucketed write pass: entries, group counts (per slot)
   DBuf ctl;
   // outputs
   DBuf f_off, f_len, f_ids, a_off, a_len, a_ids, edges, p_off, p_cnt, p_trunc, p_tids, p_scratch, p_tmp;

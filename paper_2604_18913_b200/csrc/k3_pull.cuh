@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   uint32_t valid[VEC];
 #pragma unroll
   for (int c = 0; c < VEC; ++c) valid[c] = valid_word(part * VEC + c, a.nq);
-  const int64_t n = a.n_items;
+  const int64_t n = a.n_items_dev ? (int64_t)*a.n_items_dev : a.n_items;
   // SCREEN (graphs of low mean in-degree, chosen on the host): items are
   // first screened 32 at a time, one per lane -- an item takes part only if
   // one of its in-edges comes from the frontier (any edge when the hop is
@@ -315,3 +315,95 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   app.finish(a);
 }
 
+
+// Two-phase pull, phase 1 (pull_screen 2): keep the pull items with a frontier
+// in-neighbour (every item when the hop is dense) and compact their
+// (v, lo, hi) into cv/clo/chi; phase 2 is pull_kernel<.., SCREEN = false>
+// over that list (n_items_dev = ctl->pull_items[h]).
+//
+// The in-kernel screen (SCREEN = true) walks an item's in-edges on one lane,
+// two dependent loads (source, frontier flag) per step, and the lane groups
+// then wait on the busiest lane's chain.  Here a warp takes 32 consecutive
+// items, whose in-edges are one contiguous run of the reverse CSR (items
+// split rows in order, rows without in-edges have none), and tests that run
+// 32 edges per step: coalesced source loads, independent flag loads, the
+// owning item found by a 5-step search over the lanes' item starts, the
+// items' activity OR-reduced in one instruction.  Survivors go to a
+// per-warp shared run stored with one global atomic per >= 32 items.
+constexpr int kScreenRun = 32;
+
+__global__ void __launch_bounds__(kThreads) pull_screen_kernel(WaveArgs a, int32_t* cv, int32_t* clo,
+                                                               int32_t* chi) {
+  if (a.ctl->mode[a.h] != 1) return;
+  const bool dense = a.ctl->dense[a.h] != 0;
+  __shared__ int32_t sb[kThreads / 32][3][2 * kScreenRun];
+  const int wib = threadIdx.x >> 5;
+  int32_t* bv = sb[wib][0];
+  int32_t* bl = sb[wib][1];
+  int32_t* bh = sb[wib][2];
+  int fill = 0;
+  const unsigned lane = lane_id();
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n = a.n_items;
+  int32_t* count = &a.ctl->pull_items[a.h];
+  auto flush = [&]() {
+    __syncwarp();
+    int32_t at = 0;
+    if (lane == 0) at = atomicAdd(count, fill);
+    at = __shfl_sync(TH_FULL, at, 0);
+    for (int i = (int)lane; i < fill; i += 32) {
+      cv[at + i] = bv[i];
+      clo[at + i] = bl[i];
+      chi[at + i] = bh[i];
+    }
+    fill = 0;
+    __syncwarp();
+  };
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t it = base + lane;
+    int32_t vv = 0, lo = INT32_MAX, hi = INT32_MAX;
+    if (it < n) {
+      vv = __ldg(a.item_v + it);
+      lo = __ldg(a.item_lo + it);
+      hi = __ldg(a.item_hi + it);
+    }
+    bool act = it < n;
+    if (!dense) {
+      const int last = n - base >= 32 ? 31 : (int)(n - 1 - base);
+      const int32_t L = __shfl_sync(TH_FULL, lo, 0), H = __shfl_sync(TH_FULL, hi, last);
+      unsigned am = 0u;
+      for (int32_t e0 = L; e0 < H; e0 += 32) {
+        const int32_t e = e0 + (int32_t)lane;
+        bool ea = false;
+        if (e < H) {
+          const int32_t u = __ldg(a.rsrc + e);
+          ea = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
+        }
+        if (__any_sync(TH_FULL, ea)) {
+          // owning item: the last lane whose item starts at or before e
+          int own = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1) {
+            const int32_t l = __shfl_sync(TH_FULL, lo, own + st);
+            if (l <= e) own += st;
+          }
+          am |= __reduce_or_sync(TH_FULL, ea ? 1u << own : 0u);
+        }
+      }
+      act = (am >> lane) & 1u;
+    }
+    const unsigned fm = __ballot_sync(TH_FULL, act);
+    if (fm) {
+      if (act) {
+        const int p = fill + __popc(fm & lanemask_lt());
+        bv[p] = vv;
+        bl[p] = lo;
+        bh[p] = hi;
+      }
+      fill += __popc(fm);
+      if (fill >= kScreenRun) flush();
+    }
+  }
+  if (fill) flush();
+}

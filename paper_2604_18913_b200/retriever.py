@@ -200,7 +200,7 @@ class Retriever:
         _lib.check(_lib.load().th_session_set_k4_mode(self._handle, int(mode)))
 
     def set_pull_screen(self, mode: int) -> None:
-        """Per-lane item screening in pull hops: -1 by graph shape (default), 0 off, 1 on."""
+        """Pull item screening: -1 by graph shape (default), 0 off, 1 per lane in the pull kernel, 2 screen kernel + compacted pull."""
         _lib.check(_lib.load().th_session_set_pull_screen(self._handle, int(mode)))
 
     def set_knob(self, name: str, value: int) -> None:

@@ -22,7 +22,7 @@ def _cases():
             alpha=float(rng.choice([0.8, 1.1, 1.4])), B=int(rng.choice([1, 7, 32, 33, 200, 1024, 1100])),
             k=int(rng.integers(1, 5)), sem=str(rng.choice(["exact", "frontier", "cumulative"])),
             filt=bool(rng.random() < 0.35), list_mode=bool(rng.random() < 0.5),
-            k4_mode=int(rng.integers(0, 3)), screen=int(rng.integers(-1, 2)),
+            k4_mode=int(rng.integers(0, 3)), screen=int(rng.integers(-1, 3)),
             bucket=bool(rng.random() < 0.7),
             divisor=float(rng.choice([0.0, -1.0, 8.0])),
             paths=bool(rng.random() < 0.3), max_paths=[0, 5, 100, None][int(rng.integers(0, 4))], seed=i))

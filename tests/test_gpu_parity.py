@@ -127,7 +127,7 @@ def _hub_graph(E, T, R, seed, alpha=1.2):
     return key // E // R, (key // E) % R, key % E
 
 
-@pytest.mark.parametrize("k4", ["dense", "list", "list_nb", "list_t", "screen"])
+@pytest.mark.parametrize("k4", ["dense", "list", "list_nb", "list_t", "screen", "screen2"])
 @pytest.mark.parametrize("divisor", [0.0, -1.0, 8.0], ids=["push", "pull", "auto"])
 @pytest.mark.parametrize("sem", ["exact", "frontier", "cumulative"])
 def test_hub_graph_two_waves_vs_oracle(th, sem, divisor, k4):
@@ -146,7 +146,8 @@ def test_hub_graph_two_waves_vs_oracle(th, sem, divisor, k4):
     ret.set_list_min_entities(0 if k4 != "dense" else 1 << 40)
     ret.set_k4_mode(0 if k4 == "list_t" else 1)  # list_t: the transposing list-driven K4
     ret.set_knob("k4_bucket", 0 if k4 == "list_nb" else 1)  # list: bucketed write; list_nb: transposing
-    ret.set_pull_screen(1 if k4 == "screen" else 0)  # screen: per-lane item screening in pulls
+    # screen: per-lane item screening in pulls; screen2: screen kernel + compacted pull
+    ret.set_pull_screen({"screen": 1, "screen2": 2}.get(k4, 0))
     k = 3
     res = ret.retrieve(seeds, k, semantics=sem)
     if divisor == 0.0:
