@@ -1049,18 +1049,22 @@ void launch_pull(Session* s, const Graph* g, const WaveArgs& a, cudaStream_t st)
   const unsigned pg = persistent_grid();
   const int mode = pull_screen_mode(g, s->pull_screen);
   if (mode == 2) {
-    const int64_t n = std::max<int64_t>(g->n_items, 1);
-    int32_t* c = ensure<int32_t>(s->pull_items, 3 * n, st);
-    pull_screen_kernel<<<pg, kThreads, 0, st>>>(a, c, c + n, c + 2 * n);
+    // (entries: compacted items (dense hops) or frontier in-edges, <= T)
+    const int64_t n = std::max<int64_t>(g->T, 1);
+    int32_t* c = ensure<int32_t>(s->pull_items, (FILTER ? 3 : 2) * n + g->n_items + 1, st);
+    int32_t* c2 = c + 2 * n;  // rel (FILTER) / item ends (dense)
+    pull_screen_kernel<FILTER><<<pg, kThreads, 0, st>>>(a, c, c + n, c2);
     TH_LAUNCHED();
     WaveArgs pa = a;
     pa.item_v = c;
     pa.item_lo = c + n;
-    pa.item_hi = c + 2 * n;
+    pa.item_hi = c2;
     pa.n_items_dev = &a.ctl->pull_items[a.h];
-    pull_kernel<W, SEM, FILTER, false><<<pg, kThreads, 0, st>>>(pa);
+    pull_kernel<W, SEM, FILTER, false><<<pg, kThreads, 0, st>>>(pa);  // dense hops
     TH_LAUNCHED();
-    s->launches += 2;
+    pull_edges_kernel<W, SEM, FILTER><<<pg, kThreads, 0, st>>>(a, c, c + n, c2);
+    TH_LAUNCHED();
+    s->launches += 3;
     return;
   }
   if (mode == 1) pull_kernel<W, SEM, FILTER, true><<<pg, kThreads, 0, st>>>(a);

@@ -61,6 +61,8 @@ __device__ __forceinline__ void st_words(uint32_t* p, const uint32_t (&v)[VEC]) 
 template <int W, int SEM, bool FILTER, bool SCREEN>
 __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   if (a.ctl->mode[a.h] != 1) return;
+  // (over the two-phase screen's compacted items: dense hops only)
+  if (a.n_items_dev && a.ctl->dense[a.h] == 0) return;
   const bool dense = a.ctl->dense[a.h] != 0;
   using RS = RowShape<W>;
   constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
@@ -316,46 +318,57 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
 }
 
 
-// Two-phase pull, phase 1 (pull_screen 2): keep the pull items with a frontier
-// in-neighbour (every item when the hop is dense) and compact their
-// (v, lo, hi) into cv/clo/chi; phase 2 is pull_kernel<.., SCREEN = false>
-// over that list (n_items_dev = ctl->pull_items[h]).
+// Two-phase pull (pull_screen 2).  Phase 1, pull_screen_kernel, finds the
+// in-edges of the hop that come from the frontier; phase 2 gathers them.
 //
 // The in-kernel screen (SCREEN = true) walks an item's in-edges on one lane,
 // two dependent loads (source, frontier flag) per step, and the lane groups
-// then wait on the busiest lane's chain.  Here a warp takes 32 consecutive
-// items, whose in-edges are one contiguous run of the reverse CSR (items
-// split rows in order, rows without in-edges have none), and tests that run
-// 32 edges per step: coalesced source loads, independent flag loads, the
-// owning item found by a 5-step search over the lanes' item starts, the
-// items' activity OR-reduced in one instruction.  Survivors go to a
-// per-warp shared run stored with one global atomic per >= 32 items.
+// then redo the flag tests before their row loads: a 5-deep dependent chain
+// per item (item, visited flag, sources, flags, rows), with 4 items per warp
+// in flight (C4 hop 3: 13M surviving items, 2.3 ms, 44% issue, DRAM 16%).
+// Here a warp takes 32 consecutive items, whose in-edges are one contiguous
+// run of the reverse CSR (items split rows in order; rows without in-edges
+// have none), and tests that run 32 edges per step: coalesced source loads,
+// independent flag loads, the owning item found by a 5-step search over the
+// lanes' item starts.
+//   non-dense hops: the frontier in-edges themselves are compacted, as
+//     (vv, u[, rel]) in edge order -- an item's entries stay consecutive --
+//     and pull_edges_kernel gathers them: one dependent step (the entry) in
+//     front of the row loads instead of three.
+//   dense hops (every in-edge is taken): the items are compacted as
+//     (v, lo, hi) and pull_kernel<.., SCREEN = false> runs over that list.
+// Entries go through a per-warp shared run stored with one global atomic
+// per >= 32 entries (ctl->pull_items[h] counts them).
 constexpr int kScreenRun = 32;
+constexpr int kScreenBuf = 64;
 
-__global__ void __launch_bounds__(kThreads) pull_screen_kernel(WaveArgs a, int32_t* cv, int32_t* clo,
-                                                               int32_t* chi) {
+template <bool FILTER>
+__global__ void __launch_bounds__(kThreads) pull_screen_kernel(WaveArgs a, int32_t* c0, int32_t* c1,
+                                                               int32_t* c2) {
   if (a.ctl->mode[a.h] != 1) return;
   const bool dense = a.ctl->dense[a.h] != 0;
-  __shared__ int32_t sb[kThreads / 32][3][2 * kScreenRun];
+  __shared__ int32_t sb[kThreads / 32][3][kScreenBuf];
   const int wib = threadIdx.x >> 5;
-  int32_t* bv = sb[wib][0];
-  int32_t* bl = sb[wib][1];
-  int32_t* bh = sb[wib][2];
+  int32_t* b0 = sb[wib][0];
+  int32_t* b1 = sb[wib][1];
+  int32_t* b2 = sb[wib][2];
   int fill = 0;
   const unsigned lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t n = a.n_items;
   int32_t* count = &a.ctl->pull_items[a.h];
+  // (dense: items, three words each; else edges, two or three)
+  const bool third = dense || FILTER;
   auto flush = [&]() {
     __syncwarp();
     int32_t at = 0;
     if (lane == 0) at = atomicAdd(count, fill);
     at = __shfl_sync(TH_FULL, at, 0);
     for (int i = (int)lane; i < fill; i += 32) {
-      cv[at + i] = bv[i];
-      clo[at + i] = bl[i];
-      chi[at + i] = bh[i];
+      c0[at + i] = b0[i];
+      c1[at + i] = b1[i];
+      if (third) c2[at + i] = b2[i];
     }
     fill = 0;
     __syncwarp();
@@ -368,42 +381,215 @@ __global__ void __launch_bounds__(kThreads) pull_screen_kernel(WaveArgs a, int32
       lo = __ldg(a.item_lo + it);
       hi = __ldg(a.item_hi + it);
     }
-    bool act = it < n;
-    if (!dense) {
-      const int last = n - base >= 32 ? 31 : (int)(n - 1 - base);
-      const int32_t L = __shfl_sync(TH_FULL, lo, 0), H = __shfl_sync(TH_FULL, hi, last);
-      unsigned am = 0u;
-      for (int32_t e0 = L; e0 < H; e0 += 32) {
-        const int32_t e = e0 + (int32_t)lane;
-        bool ea = false;
-        if (e < H) {
-          const int32_t u = __ldg(a.rsrc + e);
-          ea = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
-        }
-        if (__any_sync(TH_FULL, ea)) {
-          // owning item: the last lane whose item starts at or before e
-          int own = 0;
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1) {
-            const int32_t l = __shfl_sync(TH_FULL, lo, own + st);
-            if (l <= e) own += st;
-          }
-          am |= __reduce_or_sync(TH_FULL, ea ? 1u << own : 0u);
-        }
-      }
-      act = (am >> lane) & 1u;
-    }
-    const unsigned fm = __ballot_sync(TH_FULL, act);
-    if (fm) {
+    if (dense) {
+      const bool act = it < n;
+      const unsigned fm = __ballot_sync(TH_FULL, act);
       if (act) {
         const int p = fill + __popc(fm & lanemask_lt());
-        bv[p] = vv;
-        bl[p] = lo;
-        bh[p] = hi;
+        b0[p] = vv;
+        b1[p] = lo;
+        b2[p] = hi;
       }
       fill += __popc(fm);
       if (fill >= kScreenRun) flush();
+      continue;
     }
+    const int last = n - base >= 32 ? 31 : (int)(n - 1 - base);
+    const int32_t L = __shfl_sync(TH_FULL, lo, 0), H = __shfl_sync(TH_FULL, hi, last);
+    int32_t forced = -1;  // an item cut by a flush: all its entries are marked split
+    for (int32_t e0 = L; e0 < H; e0 += 32) {
+      const int32_t e = e0 + (int32_t)lane;
+      bool ea = false;
+      int32_t u = 0;
+      if (e < H) {
+        u = __ldg(a.rsrc + e);
+        ea = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
+      }
+      const unsigned em = __ballot_sync(TH_FULL, ea);
+      if (!em) continue;
+      // owning item: the last lane whose item starts at or before e
+      int own = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int32_t l = __shfl_sync(TH_FULL, lo, own + st);
+        if (l <= e) own += st;
+      }
+      int32_t ev = __shfl_sync(TH_FULL, vv, own);
+      const int c = __popc(em);
+      if (fill + c > kScreenBuf) {
+        // the item open at e0 (started in an earlier step) is cut: its
+        // buffered entries (a suffix of the run) and the rest of its
+        // entries become a split row's, merged with atomics in phase 2
+        const int own0 = __shfl_sync(TH_FULL, own, 0);
+        const int32_t v0 = __shfl_sync(TH_FULL, vv, own0);
+        const int32_t lo0 = __shfl_sync(TH_FULL, lo, own0);
+        if (lo0 < e0 && v0 >= 0) {
+          for (int i = (int)lane; i < fill; i += 32)
+            if (b0[i] == v0) b0[i] = ~v0;
+          forced = v0;
+        }
+        flush();
+      }
+      if (ev >= 0 && ev == forced) ev = ~ev;
+      if (ea) {
+        const int p = fill + __popc(em & lanemask_lt());
+        b0[p] = ev;
+        b1[p] = u;
+        if (FILTER) b2[p] = (int32_t)__ldg(a.rrel + e);
+      }
+      fill += c;
+    }
+    if (fill >= kScreenRun) flush();
   }
   if (fill) flush();
+}
+
+// Two-phase pull, phase 2 over compacted frontier in-edges (vv, u[, rel])
+// of a non-dense hop.  A warp takes a window of 32 entries; runs of equal
+// vv are segments (one target row each), handed to the lane groups GPW at a
+// time.  A whole row's run (vv >= 0, at most kPullChunk entries) belongs to
+// the window it starts in, which reads up to 31 entries past its end; split
+// rows' runs are cut at window edges and merged with atomicOr.  Per segment:
+// the frontier rows of its sources are loaded 4 at a time with the visited
+// row, then N (and V) are written; a whole row is flagged with a
+// non-returning atomic (only its own segment can reach it this hop).
+template <int W, int SEM, bool FILTER>
+__global__ void __launch_bounds__(kThreads) pull_edges_kernel(WaveArgs a, const int32_t* __restrict__ cv,
+                                                              const int32_t* __restrict__ cu,
+                                                              const int32_t* __restrict__ cr) {
+  if (a.ctl->mode[a.h] != 1 || a.ctl->dense[a.h] != 0) return;
+  using RS = RowShape<W>;
+  constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
+  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t segs[kThreads / 32][33];
+  WarpAppender app{abuf[threadIdx.x >> 5]};
+  int32_t* seg = segs[threadIdx.x >> 5];
+  const unsigned lane = lane_id();
+  const int part = (int)lane % LPR, grp = (int)lane / LPR;
+  const unsigned gbits = (LPR == 32 ? TH_FULL : ((1u << LPR) - 1u)) << (grp * LPR);
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t valid[VEC];
+#pragma unroll
+  for (int c = 0; c < VEC; ++c) valid[c] = valid_word(part * VEC + c, a.nq);
+  const int64_t n = a.ctl->pull_items[a.h];
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    int32_t ev = INT32_MIN, eu = 0, er = 0;
+    if (i < n) {
+      ev = __ldg(cv + i);
+      eu = __ldg(cu + i);
+      if (FILTER) er = __ldg(cr + i);
+    }
+    int32_t prev = __shfl_up_sync(TH_FULL, ev, 1);
+    if (lane == 0) prev = base > 0 ? __ldg(cv + base - 1) : INT32_MIN;
+    // a run starts where vv changes; a split row's run also at the window
+    // start; a whole row's run continuing from the previous window is its
+    const bool start = i < n && (ev != prev || (lane == 0 && ev < 0));
+    const unsigned S = __ballot_sync(TH_FULL, start);
+    if (!S) continue;
+    const int nseg = __popc(S);
+    const int wend = n - base >= 32 ? 32 : (int)(n - base);
+    // the last run continues past the window when it is a whole row's
+    const int ls = 31 - __clz((int)S);
+    const int32_t lv = __shfl_sync(TH_FULL, ev, ls);
+    int cont = 0;
+    int32_t u2 = 0, r2 = 0;
+    if (lv >= 0 && base + 32 < n) {
+      const int64_t j = base + 32 + lane;
+      const int32_t v2 = j < n ? __ldg(cv + j) : INT32_MIN;
+      const unsigned ne = __ballot_sync(TH_FULL, v2 != lv);
+      cont = ne ? __ffs(ne) - 1 : 32;
+      if ((int)lane < cont) {
+        u2 = __ldg(cu + j);
+        if (FILTER) r2 = __ldg(cr + j);
+      }
+    }
+    if (start) seg[__popc(S & lanemask_lt())] = (int)lane;
+    if (lane == 0) seg[nseg] = wend + cont;
+    __syncwarp();
+    for (int r0 = 0; r0 < nseg; r0 += GPW) {
+      const int si = r0 + grp;
+      const bool live = si < nseg;
+      const int s = live ? seg[si] : 0;
+      const int len = live ? seg[si + 1] - s : 0;
+      const int32_t vv = __shfl_sync(TH_FULL, ev, s);
+      const bool split = vv < 0;
+      const int32_t v = split ? ~vv : vv;
+      const size_t row = (size_t)v * W + part * VEC;
+      uint32_t seen[VEC], acc[VEC];
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        seen[c] = 0u;
+        acc[c] = 0u;
+      }
+      if (SEM != TH_EXACT && live && ((__ldcg(a.Vf + (v >> 5)) >> (v & 31)) & 1u))
+        ld_words<VEC>(a.V + row, seen);
+      const int maxlen = (int)__reduce_max_sync(TH_FULL, (unsigned)len);
+      for (int t0 = 0; t0 < maxlen; t0 += 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int t = s + t0 + k;
+          const int32_t ua = __shfl_sync(TH_FULL, eu, t & 31);
+          const int32_t ub = __shfl_sync(TH_FULL, u2, t & 31);
+          int32_t ra = 0, rb = 0;
+          if (FILTER) {
+            ra = __shfl_sync(TH_FULL, er, t & 31);
+            rb = __shfl_sync(TH_FULL, r2, t & 31);
+          }
+          if (t0 + k < len) {
+            const int32_t u = t < 32 ? ua : ub;
+            uint32_t x[VEC];
+            ldg_words<VEC>(a.X + (size_t)u * W + part * VEC, x);
+            if (FILTER) {
+              uint32_t m[VEC];
+              ldg_words<VEC>(a.M + (size_t)(t < 32 ? ra : rb) * W + part * VEC, m);
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) x[c] &= m[c];
+            }
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
+          }
+        }
+      }
+      uint32_t nb[VEC];
+      bool any = false;
+#pragma unroll
+      for (int c = 0; c < VEC; ++c) {
+        nb[c] = acc[c] & ~seen[c] & valid[c];
+        any |= nb[c] != 0u;
+      }
+      any = (__ballot_sync(TH_FULL, any) & gbits) != 0u;
+      bool fresh = false;
+      if (live && any) {
+        if (!split) {
+          st_words<VEC>(a.N + row, nb);
+          if (SEM != TH_EXACT && !a.last_frontier) {
+            uint32_t nw[VEC];
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) nw[c] = seen[c] | nb[c];
+            st_words<VEC>(a.V + row, nw);
+          }
+          if (part == 0) {
+            const uint32_t fb = 1u << (v & 31);
+            atomicOr(&a.Nf[v >> 5], fb);
+            if (SEM != TH_EXACT) atomicOr(&a.Vf[v >> 5], fb);
+            fresh = true;
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < VEC; ++c) {
+            if (nb[c]) {
+              atomicOr(a.N + row + c, nb[c]);
+              if (SEM != TH_EXACT && !a.last_frontier) atomicOr(a.V + row + c, nb[c]);
+            }
+          }
+          if (part == 0) fresh = flag_next(a, v);
+        }
+      }
+      app.add(a, fresh, v);
+    }
+    __syncwarp();
+  }
+  app.finish(a);
 }
