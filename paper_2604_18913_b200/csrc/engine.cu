@@ -68,11 +68,13 @@ struct WaveArgs {
   const int32_t* rindptr;
   const int32_t* rsrc;
   const uint16_t* rrel;
+  const int32_t* rdst;  // target row of each in-edge (~v: split row)
   const int32_t* item_v;
   const int32_t* item_lo;
   const int32_t* item_hi;
   int64_t n_items;
-  const int32_t* n_items_dev;  // device item count (the two-phase pull's compacted items)
+  const int32_t* n_items_dev;  // device item count (nullptr: n_items)
+  int pull_only_dense;         // pull_kernel beside the two-phase pull: dense hops only
   int64_t E, T;
   uint32_t *X, *N, *V, *S, *Xf, *Nf, *Vf;
   const uint32_t* M;
@@ -1049,20 +1051,20 @@ void launch_pull(Session* s, const Graph* g, const WaveArgs& a, cudaStream_t st)
   const unsigned pg = persistent_grid();
   const int mode = pull_screen_mode(g, s->pull_screen);
   if (mode == 2) {
-    // (entries: compacted items (dense hops) or frontier in-edges, <= T)
+    // (frontier in-edges of a non-dense hop, <= T entries)
     const int64_t n = std::max<int64_t>(g->T, 1);
-    int32_t* c = ensure<int32_t>(s->pull_items, (FILTER ? 3 : 2) * n + g->n_items + 1, st);
-    int32_t* c2 = c + 2 * n;  // rel (FILTER) / item ends (dense)
-    pull_screen_kernel<FILTER><<<pg, kThreads, 0, st>>>(a, c, c + n, c2);
+    int32_t* c = ensure<int32_t>(s->pull_items, (FILTER ? 3 : 2) * n, st);
+    int32_t* cr = FILTER ? c + 2 * n : nullptr;
+    WaveArgs ea = a;
+    ea.rdst = g->rdst;
+    ea.T = g->T;  // (a shard's in-edge graph: its own edge count)
+    pull_screen_edges_kernel<FILTER><<<pg, kThreads, 0, st>>>(ea, c, c + n, cr);
+    TH_LAUNCHED();
+    pull_edges_kernel<W, SEM, FILTER><<<pg, kThreads, 0, st>>>(a, c, c + n, cr);
     TH_LAUNCHED();
     WaveArgs pa = a;
-    pa.item_v = c;
-    pa.item_lo = c + n;
-    pa.item_hi = c2;
-    pa.n_items_dev = &a.ctl->pull_items[a.h];
+    pa.pull_only_dense = 1;
     pull_kernel<W, SEM, FILTER, false><<<pg, kThreads, 0, st>>>(pa);  // dense hops
-    TH_LAUNCHED();
-    pull_edges_kernel<W, SEM, FILTER><<<pg, kThreads, 0, st>>>(a, c, c + n, c2);
     TH_LAUNCHED();
     s->launches += 3;
     return;

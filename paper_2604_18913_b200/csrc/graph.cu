@@ -102,6 +102,15 @@ __global__ void item_count_kernel(const int32_t* __restrict__ rptr, int64_t E, i
   }
 }
 
+__global__ void rdst_kernel(const int32_t* __restrict__ rperm, const int32_t* __restrict__ obj,
+                            const int32_t* __restrict__ rptr, int64_t T, int32_t* rdst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < T;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = obj[rperm[e]];
+    rdst[e] = rptr[v + 1] - rptr[v] > kPullChunk ? ~v : v;
+  }
+}
+
 __global__ void item_fill_kernel(const int32_t* __restrict__ rptr, const int32_t* __restrict__ off,
                                  int64_t E, int32_t* iv, int32_t* ilo, int32_t* ihi) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < E;
@@ -230,11 +239,14 @@ int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int
     int32_t* rperm = talloc<int32_t>(T);
     g->rsrc = dalloc<int32_t>(g, T);
     g->rrel = dalloc<uint16_t>(g, T);
+    g->rdst = dalloc<int32_t>(g, T);
     sorted_rows(g, g->obj, T, E, g->rindptr, rperm, st);
     if (T > 0) {
       gather_kernel<<<grid_for(T), 256, 0, st>>>(rperm, g->subj, g->rel, g->rsrc, g->rrel, T);
       TH_LAUNCHED();
-      g->launches += 1;
+      rdst_kernel<<<grid_for(T), 256, 0, st>>>(rperm, g->obj, g->rindptr, T, g->rdst);
+      TH_LAUNCHED();
+      g->launches += 2;
     }
     TH_CUDA(cudaStreamSynchronize(st));
     cudaFree(rperm);
@@ -282,7 +294,7 @@ int graph_build(Graph* g, const int32_t* d_subj, const int32_t* d_rel, const int
 void graph_free(Graph* g) {
   for (void* p : {(void*)g->indptr, (void*)g->csr_tid, (void*)g->csr_obj, (void*)g->csr_rel,
                   (void*)g->subj, (void*)g->obj, (void*)g->rel, (void*)g->rindptr, (void*)g->rsrc,
-                  (void*)g->rrel, (void*)g->item_v, (void*)g->item_lo, (void*)g->item_hi}) {
+                  (void*)g->rrel, (void*)g->rdst, (void*)g->item_v, (void*)g->item_lo, (void*)g->item_hi}) {
     if (p) cudaFree(p);
   }
   *g = Graph{};

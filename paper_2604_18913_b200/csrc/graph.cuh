@@ -25,6 +25,9 @@ struct Graph {
   int32_t* rindptr = nullptr;  // [E+1]
   int32_t* rsrc = nullptr;     // [T]
   uint16_t* rrel = nullptr;    // [T]
+  // target row of each in-edge (~v when the row is split over several
+  // items): lets the two-phase pull's screen stream the in-edges
+  int32_t* rdst = nullptr;     // [T]
   // static pull schedule: item i covers in-edges [item_lo[i], item_hi[i]) of
   // entity item_v[i] (stored as ~v when the in-row is split over several
   // items, which then merge with atomics); items ascend by entity

@@ -61,8 +61,8 @@ __device__ __forceinline__ void st_words(uint32_t* p, const uint32_t (&v)[VEC]) 
 template <int W, int SEM, bool FILTER, bool SCREEN>
 __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   if (a.ctl->mode[a.h] != 1) return;
-  // (over the two-phase screen's compacted items: dense hops only)
-  if (a.n_items_dev && a.ctl->dense[a.h] == 0) return;
+  // (beside the two-phase pull's kernels: dense hops only)
+  if (a.pull_only_dense && a.ctl->dense[a.h] == 0) return;
   const bool dense = a.ctl->dense[a.h] != 0;
   using RS = RowShape<W>;
   constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
@@ -326,122 +326,144 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
 // then redo the flag tests before their row loads: a 5-deep dependent chain
 // per item (item, visited flag, sources, flags, rows), with 4 items per warp
 // in flight (C4 hop 3: 13M surviving items, 2.3 ms, 44% issue, DRAM 16%).
-// Here a warp takes 32 consecutive items, whose in-edges are one contiguous
-// run of the reverse CSR (items split rows in order; rows without in-edges
-// have none), and tests that run 32 edges per step: coalesced source loads,
-// independent flag loads, the owning item found by a 5-step search over the
-// lanes' item starts.
-//   non-dense hops: the frontier in-edges themselves are compacted, as
-//     (vv, u[, rel]) in edge order -- an item's entries stay consecutive --
-//     and pull_edges_kernel gathers them: one dependent step (the entry) in
-//     front of the row loads instead of three.
-//   dense hops (every in-edge is taken): the items are compacted as
-//     (v, lo, hi) and pull_kernel<.., SCREEN = false> runs over that list.
-// Entries go through a per-warp shared run stored with one global atomic
-// per >= 32 entries (ctl->pull_items[h] counts them).
+//   non-dense hops: pull_screen_edges_kernel streams the in-edges (source
+//     and target row of each, rdst) and compacts the frontier ones as
+//     (vv, u[, rel]) -- a whole row's entries stay consecutive -- through a
+//     per-warp shared run stored with one global atomic per >= 32 entries;
+//     pull_edges_kernel gathers them: one dependent step (the entry) in
+//     front of the row loads instead of four.
+//   dense hops (every in-edge is taken): pull_kernel<.., SCREEN = false>
+//     over the static items.
+// ctl->pull_items[h] counts the entries.
 constexpr int kScreenRun = 32;
-constexpr int kScreenBuf = 64;
 
+// non-dense hops: the frontier in-edges as (vv, u[, rel]).  Each warp
+// streams a contiguous range of 32-edge chunks (source and target row of
+// each edge, coalesced; the frontier flag from the L2-resident bitmap),
+// software-pipelined two chunks deep: chunk c+2's edges and chunk c+1's
+// flag words are loaded while chunk c is compacted.  A whole row's in-edges
+// (vv >= 0, at most kPullChunk) stay consecutive in the output: a warp
+// skips the leading edges of a row that started before its range and takes
+// the rest of its own last row past the range end; a flush stores the run
+// up to the start of a row still open at the chunk boundary.  Split rows'
+// edges may fall anywhere (their rows merge with atomics).
 template <bool FILTER>
-__global__ void __launch_bounds__(kThreads) pull_screen_kernel(WaveArgs a, int32_t* c0, int32_t* c1,
-                                                               int32_t* c2) {
-  if (a.ctl->mode[a.h] != 1) return;
-  const bool dense = a.ctl->dense[a.h] != 0;
-  __shared__ int32_t sb[kThreads / 32][3][kScreenBuf];
+__global__ void __launch_bounds__(kThreads) pull_screen_edges_kernel(WaveArgs a, int32_t* cv,
+                                                                     int32_t* cu, int32_t* cr) {
+  if (a.ctl->mode[a.h] != 1 || a.ctl->dense[a.h] != 0) return;
+  constexpr int kBuf = 3 * 32;  // < 32 left + a chunk + a row's continuation
+  __shared__ int32_t sb[kThreads / 32][FILTER ? 3 : 2][kBuf];
   const int wib = threadIdx.x >> 5;
-  int32_t* b0 = sb[wib][0];
-  int32_t* b1 = sb[wib][1];
-  int32_t* b2 = sb[wib][2];
+  int32_t* bv = sb[wib][0];
+  int32_t* bu = sb[wib][1];
+  int32_t* br = sb[wib][FILTER ? 2 : 1];
   int fill = 0;
   const unsigned lane = lane_id();
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n = a.n_items;
+  const int64_t T = a.T;
+  const int64_t nch = (T + 31) / 32;
+  const int64_t per = (nch + nwarps - 1) / nwarps;
+  const int64_t c_begin = warp * per;
+  const int64_t c_end = c_begin + per < nch ? c_begin + per : nch;
+  if (c_begin >= c_end) return;
   int32_t* count = &a.ctl->pull_items[a.h];
-  // (dense: items, three words each; else edges, two or three)
-  const bool third = dense || FILTER;
-  auto flush = [&]() {
+  auto ld = [&](int64_t c, int32_t& d, int32_t& u) {
+    const int64_t e = c * 32 + lane;
+    d = INT32_MIN;
+    u = 0;
+    if (e < T) {
+      d = __ldg(a.rdst + e);
+      u = __ldg(a.rsrc + e);
+    }
+  };
+  auto append = [&](bool take, int32_t v, int32_t u, int32_t r) {
+    const unsigned m = __ballot_sync(TH_FULL, take);
+    if (take) {
+      const int p = fill + __popc(m & lanemask_lt());
+      bv[p] = v;
+      bu[p] = u;
+      if (FILTER) br[p] = r;
+    }
+    fill += __popc(m);
+  };
+  // stores run [0, n) and moves [n, fill) to the front
+  auto flush = [&](int n) {
     __syncwarp();
     int32_t at = 0;
-    if (lane == 0) at = atomicAdd(count, fill);
+    if (lane == 0) at = atomicAdd(count, n);
     at = __shfl_sync(TH_FULL, at, 0);
-    for (int i = (int)lane; i < fill; i += 32) {
-      c0[at + i] = b0[i];
-      c1[at + i] = b1[i];
-      if (third) c2[at + i] = b2[i];
+    for (int i = (int)lane; i < n; i += 32) {
+      cv[at + i] = bv[i];
+      cu[at + i] = bu[i];
+      if (FILTER) cr[at + i] = br[i];
     }
-    fill = 0;
+    __syncwarp();
+    const int rest = fill - n;
+    int32_t tv = 0, tu = 0, tr = 0;
+    if ((int)lane < rest) {
+      tv = bv[n + lane];
+      tu = bu[n + lane];
+      if (FILTER) tr = br[n + lane];
+    }
+    __syncwarp();
+    if ((int)lane < rest) {
+      bv[lane] = tv;
+      bu[lane] = tu;
+      if (FILTER) br[lane] = tr;
+    }
+    fill = rest;
     __syncwarp();
   };
-  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    const int64_t it = base + lane;
-    int32_t vv = 0, lo = INT32_MAX, hi = INT32_MAX;
-    if (it < n) {
-      vv = __ldg(a.item_v + it);
-      lo = __ldg(a.item_lo + it);
-      hi = __ldg(a.item_hi + it);
+  int32_t d0, u0, d1, u1, d2, u2;
+  ld(c_begin, d0, u0);
+  ld(c_begin + 1, d1, u1);
+  uint32_t x0 = d0 != INT32_MIN ? __ldg(a.Xf + (u0 >> 5)) : 0u, x1 = 0u;
+  int32_t last = c_begin > 0 ? __ldg(a.rdst + c_begin * 32 - 1) : INT32_MIN;
+  bool first = true;
+  for (int64_t c = c_begin; c < c_end; ++c) {
+    x1 = d1 != INT32_MIN ? __ldg(a.Xf + (u1 >> 5)) : 0u;
+    ld(c + 2, d2, u2);
+    int32_t pd = __shfl_up_sync(TH_FULL, d0, 1);
+    if (lane == 0) pd = last;
+    int lead = 0;
+    if (first) {
+      // a whole row that started before the range: the previous warp's
+      const unsigned chg = __ballot_sync(TH_FULL, d0 != pd);
+      if (__shfl_sync(TH_FULL, d0, 0) >= 0 && !(chg & 1u)) lead = chg ? __ffs(chg) - 1 : 32;
+      first = false;
     }
-    if (dense) {
-      const bool act = it < n;
-      const unsigned fm = __ballot_sync(TH_FULL, act);
-      if (act) {
-        const int p = fill + __popc(fm & lanemask_lt());
-        b0[p] = vv;
-        b1[p] = lo;
-        b2[p] = hi;
+    const bool take = (int)lane >= lead && d0 != INT32_MIN && ((x0 >> (u0 & 31)) & 1u);
+    int32_t r = 0;
+    if (FILTER && take) r = (int32_t)__ldg(a.rrel + c * 32 + lane);
+    append(take, d0, u0, r);
+    last = __shfl_sync(TH_FULL, d0, 31);
+    const bool open = last >= 0 && __shfl_sync(TH_FULL, d1, 0) == last;  // row runs into c+1
+    if (c + 1 == c_end && open) {
+      // the range's last whole row: its edges in the next chunk
+      const unsigned ne = __ballot_sync(TH_FULL, d1 != last);
+      const int cont = ne ? __ffs(ne) - 1 : 32;
+      const bool t2 = (int)lane < cont && ((x1 >> (u1 & 31)) & 1u);
+      int32_t r2 = 0;
+      if (FILTER && t2) r2 = (int32_t)__ldg(a.rrel + (c + 1) * 32 + lane);
+      append(t2, last, u1, r2);
+    } else if (fill >= kScreenRun) {
+      // keep a row still open at the boundary with its next entries
+      int tail = 0;
+      if (open) {
+        const bool ok = (int)lane < fill && bv[fill - 1 - (int)lane] == last;
+        const unsigned nm = __ballot_sync(TH_FULL, !ok);
+        tail = nm ? __ffs(nm) - 1 : 32;
       }
-      fill += __popc(fm);
-      if (fill >= kScreenRun) flush();
-      continue;
+      if (fill - tail > 0) flush(fill - tail);
     }
-    const int last = n - base >= 32 ? 31 : (int)(n - 1 - base);
-    const int32_t L = __shfl_sync(TH_FULL, lo, 0), H = __shfl_sync(TH_FULL, hi, last);
-    int32_t forced = -1;  // an item cut by a flush: all its entries are marked split
-    for (int32_t e0 = L; e0 < H; e0 += 32) {
-      const int32_t e = e0 + (int32_t)lane;
-      bool ea = false;
-      int32_t u = 0;
-      if (e < H) {
-        u = __ldg(a.rsrc + e);
-        ea = (__ldg(a.Xf + (u >> 5)) >> (u & 31)) & 1u;
-      }
-      const unsigned em = __ballot_sync(TH_FULL, ea);
-      if (!em) continue;
-      // owning item: the last lane whose item starts at or before e
-      int own = 0;
-#pragma unroll
-      for (int st = 16; st >= 1; st >>= 1) {
-        const int32_t l = __shfl_sync(TH_FULL, lo, own + st);
-        if (l <= e) own += st;
-      }
-      int32_t ev = __shfl_sync(TH_FULL, vv, own);
-      const int c = __popc(em);
-      if (fill + c > kScreenBuf) {
-        // the item open at e0 (started in an earlier step) is cut: its
-        // buffered entries (a suffix of the run) and the rest of its
-        // entries become a split row's, merged with atomics in phase 2
-        const int own0 = __shfl_sync(TH_FULL, own, 0);
-        const int32_t v0 = __shfl_sync(TH_FULL, vv, own0);
-        const int32_t lo0 = __shfl_sync(TH_FULL, lo, own0);
-        if (lo0 < e0 && v0 >= 0) {
-          for (int i = (int)lane; i < fill; i += 32)
-            if (b0[i] == v0) b0[i] = ~v0;
-          forced = v0;
-        }
-        flush();
-      }
-      if (ev >= 0 && ev == forced) ev = ~ev;
-      if (ea) {
-        const int p = fill + __popc(em & lanemask_lt());
-        b0[p] = ev;
-        b1[p] = u;
-        if (FILTER) b2[p] = (int32_t)__ldg(a.rrel + e);
-      }
-      fill += c;
-    }
-    if (fill >= kScreenRun) flush();
+    d0 = d1;
+    u0 = u1;
+    x0 = x1;
+    d1 = d2;
+    u1 = u2;
   }
-  if (fill) flush();
+  if (fill) flush(fill);
 }
 
 // Two-phase pull, phase 2 over compacted frontier in-edges (vv, u[, rel])
@@ -473,37 +495,52 @@ __global__ void __launch_bounds__(kThreads) pull_edges_kernel(WaveArgs a, const 
 #pragma unroll
   for (int c = 0; c < VEC; ++c) valid[c] = valid_word(part * VEC + c, a.nq);
   const int64_t n = a.ctl->pull_items[a.h];
-  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    int32_t ev = INT32_MIN, eu = 0, er = 0;
+  // a window's loads, issued one window ahead: its entries, the 32 after it
+  // (the continuation of its last run) and the entry before it
+  int32_t ev, eu, er, ev2, eu2, er2, pv;
+  auto ld = [&](int64_t b) {
+    const int64_t i = b + lane, j = i + 32;
+    ev = ev2 = pv = INT32_MIN;
+    eu = eu2 = er = er2 = 0;
     if (i < n) {
       ev = __ldg(cv + i);
       eu = __ldg(cu + i);
       if (FILTER) er = __ldg(cr + i);
     }
-    int32_t prev = __shfl_up_sync(TH_FULL, ev, 1);
-    if (lane == 0) prev = base > 0 ? __ldg(cv + base - 1) : INT32_MIN;
+    if (j < n) {
+      ev2 = __ldg(cv + j);
+      eu2 = __ldg(cu + j);
+      if (FILTER) er2 = __ldg(cr + j);
+    }
+    if (lane == 0 && b > 0 && b <= n) pv = __ldg(cv + b - 1);
+  };
+  ld(warp * 32);
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const int32_t cev = ev, ceu = eu, cer = er, cev2 = ev2, ceu2 = eu2, cer2 = er2, cpv = pv;
+    ld(base + nwarps * 32);
+    // each lane's entry row: its visited flag, fetched ahead of the rounds
+    uint32_t vis = 0u;
+    if (SEM != TH_EXACT && i < n) {
+      const int32_t vi = cev < 0 ? ~cev : cev;
+      vis = (__ldcg(a.Vf + (vi >> 5)) >> (vi & 31)) & 1u;
+    }
+    int32_t prev = __shfl_up_sync(TH_FULL, cev, 1);
+    if (lane == 0) prev = cpv;
     // a run starts where vv changes; a split row's run also at the window
     // start; a whole row's run continuing from the previous window is its
-    const bool start = i < n && (ev != prev || (lane == 0 && ev < 0));
+    const bool start = i < n && (cev != prev || (lane == 0 && cev < 0));
     const unsigned S = __ballot_sync(TH_FULL, start);
     if (!S) continue;
     const int nseg = __popc(S);
     const int wend = n - base >= 32 ? 32 : (int)(n - base);
     // the last run continues past the window when it is a whole row's
     const int ls = 31 - __clz((int)S);
-    const int32_t lv = __shfl_sync(TH_FULL, ev, ls);
+    const int32_t lv = __shfl_sync(TH_FULL, cev, ls);
     int cont = 0;
-    int32_t u2 = 0, r2 = 0;
-    if (lv >= 0 && base + 32 < n) {
-      const int64_t j = base + 32 + lane;
-      const int32_t v2 = j < n ? __ldg(cv + j) : INT32_MIN;
-      const unsigned ne = __ballot_sync(TH_FULL, v2 != lv);
+    if (lv >= 0) {
+      const unsigned ne = __ballot_sync(TH_FULL, cev2 != lv);
       cont = ne ? __ffs(ne) - 1 : 32;
-      if ((int)lane < cont) {
-        u2 = __ldg(cu + j);
-        if (FILTER) r2 = __ldg(cr + j);
-      }
     }
     if (start) seg[__popc(S & lanemask_lt())] = (int)lane;
     if (lane == 0) seg[nseg] = wend + cont;
@@ -513,7 +550,8 @@ __global__ void __launch_bounds__(kThreads) pull_edges_kernel(WaveArgs a, const 
       const bool live = si < nseg;
       const int s = live ? seg[si] : 0;
       const int len = live ? seg[si + 1] - s : 0;
-      const int32_t vv = __shfl_sync(TH_FULL, ev, s);
+      const int32_t vv = __shfl_sync(TH_FULL, cev, s);
+      const uint32_t vs = __shfl_sync(TH_FULL, vis, s);
       const bool split = vv < 0;
       const int32_t v = split ? ~vv : vv;
       const size_t row = (size_t)v * W + part * VEC;
@@ -523,19 +561,19 @@ __global__ void __launch_bounds__(kThreads) pull_edges_kernel(WaveArgs a, const 
         seen[c] = 0u;
         acc[c] = 0u;
       }
-      if (SEM != TH_EXACT && live && ((__ldcg(a.Vf + (v >> 5)) >> (v & 31)) & 1u))
-        ld_words<VEC>(a.V + row, seen);
+      if (SEM != TH_EXACT && live && vs) ld_words<VEC>(a.V + row, seen);
       const int maxlen = (int)__reduce_max_sync(TH_FULL, (unsigned)len);
       for (int t0 = 0; t0 < maxlen; t0 += 4) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+          if (t0 + k >= maxlen) break;  // (warp-uniform: most runs hold one or two edges)
           const int t = s + t0 + k;
-          const int32_t ua = __shfl_sync(TH_FULL, eu, t & 31);
-          const int32_t ub = __shfl_sync(TH_FULL, u2, t & 31);
+          const int32_t ua = __shfl_sync(TH_FULL, ceu, t & 31);
+          const int32_t ub = __shfl_sync(TH_FULL, ceu2, t & 31);
           int32_t ra = 0, rb = 0;
           if (FILTER) {
-            ra = __shfl_sync(TH_FULL, er, t & 31);
-            rb = __shfl_sync(TH_FULL, r2, t & 31);
+            ra = __shfl_sync(TH_FULL, cer, t & 31);
+            rb = __shfl_sync(TH_FULL, cer2, t & 31);
           }
           if (t0 + k < len) {
             const int32_t u = t < 32 ? ua : ub;
