@@ -1472,7 +1472,7 @@ static GraphKey graph_key(Session* s, const th_query* q) {
   k.pull_divisor = s->pull_divisor;
   k.dense_pull = s->dense_pull;
   k.list_min = s->list_min_entities;
-  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_mode << 8) |
+  k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_mode << 10) |
             ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0) | (s->priority ? 128 : 0) |
             (s->k4_bucket ? 256 : 0);
   k.epoch = session_alloc_sig(s);

@@ -146,54 +146,21 @@ constexpr int mat_warps() {
 constexpr unsigned kSparseBits = 5;       // tiles with <= this many bits per lane skip the transpose
 constexpr unsigned kCoopIdsPerQuery = 48;  // chunk ids per touched query for the cooperative write
 
-// sparse-chunk staging: a small linear buffer per query (lane).  After every
-// tile (at most 32 new ids per lane) the lanes holding >= kFlushAt ids store
-// them as one coalesced run (no scattered 4-byte stores, whose partially
-// written sectors cost DRAM fills), so a buffer never exceeds
-// kFlushAt - 1 + 32 ids and the whole per-warp staging stays small enough
-// for three 8-warp CTAs per SM.
-constexpr int kFlushAt = 8;
-constexpr int kBuf = kFlushAt + 32;
-constexpr int kRingStride = kBuf + 1;
-constexpr int kRingWords = 32 * kRingStride;
-
-// per-warp shared words: WRITE = S (32 x kSStride) + a region shared by the
-// dense-chunk staging run (kChunkRows ids) and the sparse-chunk buffers
-// (emptied before a dense chunk); COUNT = per-query counters + degree sums
+// per-warp shared words: WRITE = S (32 x kSStride) + the staging run (a
+// whole chunk's ids of one query); COUNT = per-query counters + degree sums.
+// (Round 3: list-driven layers dropped their per-lane rings for sparse
+// chunks -- every chunk is written query by query -- C4 k=3 9.28 -> 9.19 ms;
+// capping the run at 256 / 512 ids to fit five / four CTAs per SM, with
+// longer runs stored lane by lane, lost: 11.5 / 10.5 ms.)
 template <bool WRITE, bool RING = false>
 constexpr size_t mat_warp_words() {
-  // (RING: + 32 words holding the current tile's row ids)
-  return WRITE ? (size_t)(32 * kSStride + (RING && kRingWords > kChunkRows ? kRingWords : kChunkRows) +
-                          (RING ? 32 : 0))
-               : 64;
+  return WRITE ? (size_t)(32 * kSStride + kChunkRows) : 64;
 }
 
-// lanes whose buffer holds >= `at` ids store all of them (all 32 lanes, converged)
-__device__ __forceinline__ void buf_flush(const int32_t* buf, int& fill, int64_t& pos, int32_t* out,
-                                          int64_t cap, int at) {
-  const unsigned lane = lane_id();
-  unsigned need = __ballot_sync(TH_FULL, fill >= at && fill > 0);
-  while (need) {
-    const int b = __ffs(need) - 1;
-    need &= need - 1u;
-    const int nb = __shfl_sync(TH_FULL, fill, b);
-    const int64_t pb = __shfl_sync(TH_FULL, pos, b);
-    for (int o = 0; o < nb; o += 32) {
-      const int i = o + (int)lane;
-      if (i < nb && pb + i < cap) out[pb + i] = buf[b * kRingStride + i];
-    }
-    if ((int)lane == b) {
-      pos += nb;
-      fill = 0;
-    }
-  }
-  __syncwarp();
-}
-
-// per-warp words of a write pass that loads cached masks: staging run or rings
+// per-warp words of a write pass that loads cached masks: the staging run
 template <bool RING>
 constexpr size_t mat_load_words() {
-  return RING && kRingWords > kChunkRows ? kRingWords : kChunkRows;
+  return kChunkRows;
 }
 
 // CTA-shared words of an EDGES count pass (degree planes, see mat_unit)
@@ -254,8 +221,6 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
   const int q = 32 * j + lane;
   if (blk >= nblk) return;
   // WRITE: S[32][kSStride] + staging run; COUNT: per-query counters
-  // rings (sparse chunks of large, list-driven layers) need more staging
-  // space; small graphs write sparse chunks directly and keep 6 CTAs/SM
   constexpr bool RING = Src::kRing;
   // count pass that builds S: S + per-query counters only (no staging run)
   constexpr size_t kWarpWords = BUILD_S && !WRITE ? (size_t)(32 * kSStride + 64)
@@ -263,8 +228,6 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
   uint32_t* S = LOAD_S ? nullptr : mat_smem + (size_t)warp * kWarpWords;
   int32_t* stg = LOAD_S ? reinterpret_cast<int32_t*>(mat_smem + (size_t)warp * mat_load_words<RING>())
                         : reinterpret_cast<int32_t*>(S + 32 * kSStride);
-  int32_t* ring = stg;  // sparse chunks (empty whenever stg is in use)
-  int fill = 0;  // sparse-chunk buffer of this lane's query
   // COUNT: [32] ids + [32] degree sums per query (sparse tiles), after S
   // when the pass also builds S
   uint32_t* cnt = BUILD_S && !WRITE ? S + 32 * kSStride : S;  // (unused when LOAD_S)
@@ -470,11 +433,9 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       continue;
     }
     __syncwarp();
-    // ---- WRITE.  Dense chunks (many ids per query): query by query, lane
-    // t extracts tile t's rows into a staging run stored coalesced.  Sparse
-    // chunks (a few ids per query, e.g. the C4 layers): every lane walks its
-    // own query's 32 tile masks into its ring, and full rings are stored 32
-    // ids at a time by the whole warp.
+    // ---- WRITE.  Query by query, lane t extracts tile t's rows into a
+    // staging run stored coalesced.  Sparse chunks of small graphs (a few
+    // ids per query): every lane writes its own query's ids directly.
     const unsigned ids = __reduce_add_sync(TH_FULL, nbits);
     if (!RING && ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
       if (q < src.nq) {
@@ -491,30 +452,6 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       __syncwarp();
       continue;
     }
-    if (RING && ids < kCoopIdsPerQuery * (unsigned)__popc(touched)) {
-      // the tile's 32 output ids are looked up once (one coalesced load of
-      // the row list) and shared through shared memory, so each id costs a
-      // shared load instead of a dependent global one
-      int32_t* tile_ids = ring + (kRingWords > kChunkRows ? kRingWords : kChunkRows);
-      for (int t = 0; t < 32; ++t) {
-        uint32_t m = q >= src.nq ? 0u : LOAD_S ? sc.S[sbase + lane * 32 + t] : S[lane * kSStride + t];
-        const int64_t rb = c0 + 32 * t;
-        const unsigned any = __ballot_sync(TH_FULL, m != 0u);
-        if (!any) continue;
-        tile_ids[lane] = rb + lane < rend ? src.id(rb + lane) : 0;
-        __syncwarp();
-        while (m) {
-          ring[lane * kRingStride + fill] = tile_ids[__ffs(m) - 1];
-          ++fill;
-          m &= m - 1u;
-        }
-        __syncwarp();
-        buf_flush(ring, fill, pos, out, cap, kFlushAt);
-      }
-      __syncwarp();
-      continue;
-    }
-    if (RING) buf_flush(ring, fill, pos, out, cap, 1);  // keep order; frees stg
     // entity layers without a row map stage final ids (the copy-out is then
     // a plain move); otherwise chunk-relative positions resolved on the way out
     const bool direct = !Src::kRing && Src::kDense && src.map == nullptr;
@@ -583,7 +520,6 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       __syncwarp();
     }
   }
-  if (WRITE && RING) buf_flush(ring, fill, pos, out, cap, 1);
   if (!WRITE) {
     __syncwarp();
     total += (int32_t)cnt[lane];
