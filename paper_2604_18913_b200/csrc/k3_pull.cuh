@@ -300,6 +300,14 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
           for (int c = 0; c < VEC; ++c) nv[c] = seen[c] | nb[c];
           st_words<VEC>(a.V + row, nv);
         }
+        // (a whole row is reached by its one item only: set its flags
+        // without waiting for the old value)
+        if (part == 0) {
+          const uint32_t fb = 1u << (v & 31);
+          atomicOr(&a.Nf[v >> 5], fb);
+          if (SEM != TH_EXACT) atomicOr(&a.Vf[v >> 5], fb);
+          fresh = true;
+        }
       } else {
 #pragma unroll
         for (int c = 0; c < VEC; ++c) {
@@ -308,8 +316,8 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
             if (SEM != TH_EXACT && !a.last_frontier) atomicOr(a.V + row + c, nb[c]);
           }
         }
+        if (part == 0) fresh = flag_next(a, v);
       }
-      if (part == 0) fresh = flag_next(a, v);
     }
     app.add(a, fresh, v);
     }
