@@ -190,14 +190,17 @@ __device__ __forceinline__ void append_next(const WaveArgs& a, bool fresh, int32
 
 // Buffered form of append_next for the hop kernels: a warp collects its
 // newly reached entities in shared memory and stores them with one global
-// atomic per >= 32 entities; the push-cost sum stays in registers until the
-// kernel ends.  At low degree (C4: 1.6 edges per entity) nearly every warp
-// step reaches an entity, and two same-address atomics per step serialised
-// in L2.  All calls converged (all 32 lanes).
-constexpr int kAppendRun = 32;
+// atomic per >= kAppendRun entities; the push-cost sum stays in registers
+// until the kernel ends.  At low degree (C4: 1.6 edges per entity) nearly
+// every warp step reaches an entity, and two same-address atomics per step
+// serialised in L2; runs of 32 still left the two-phase pull waiting on the
+// list counter (13% of its stalls at C4 hop 3): runs of 128 took C4 k=2
+// 1.17 -> 1.10 ms, k=3 9.3 -> 9.05 ms (512: no further gain).  All calls
+// converged (all 32 lanes).
+constexpr int kAppendRun = 128;
 
 struct WarpAppender {
-  int32_t* wbuf;  // [2 * kAppendRun] shared, this warp's
+  int32_t* wbuf;  // [kAppendRun + 32] shared, this warp's
   int fill = 0;
   unsigned long long cost = 0ull;
 
@@ -474,7 +477,7 @@ __device__ void drive_heavy(const WaveArgs& a, Op& op) {
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) push_light_kernel(WaveArgs a) {
   if (a.ctl->mode[a.h] != 0) return;
-  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t abuf[kThreads / 32][kAppendRun + 32];
   PushOp<W, SEM> op{a, WarpAppender{abuf[threadIdx.x >> 5]}};
   // with a relation filter the edge-count pass already built the heavy list
   drive_light<W, FILTER>(a, a.h - 1, op, !FILTER);
@@ -484,7 +487,7 @@ __global__ void __launch_bounds__(kThreads) push_light_kernel(WaveArgs a) {
 template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) push_heavy_kernel(WaveArgs a) {
   if (a.ctl->mode[a.h] != 0) return;
-  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t abuf[kThreads / 32][kAppendRun + 32];
   PushOp<W, SEM> op{a, WarpAppender{abuf[threadIdx.x >> 5]}};
   drive_heavy<W, FILTER>(a, op);
   op.app.finish(a);

@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
   // positions of m's set bits, ascending, one per nibble (replaces __fns,
   // a software loop)
   __shared__ uint32_t nth_bit[LPR >= 4 ? (1 << LPR) : 1];
-  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t abuf[kThreads / 32][kAppendRun + 32];
   if constexpr (LPR >= 4) {
     for (int m = threadIdx.x; m < (1 << LPR); m += blockDim.x) {
       uint32_t e = 0u;
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(kThreads) pull_edges_kernel(WaveArgs a, const 
   if (a.ctl->mode[a.h] != 1 || a.ctl->dense[a.h] != 0) return;
   using RS = RowShape<W>;
   constexpr int VEC = RS::VEC, LPR = RS::LPR, GPW = RS::GPW;
-  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t abuf[kThreads / 32][kAppendRun + 32];
   __shared__ int32_t segs[kThreads / 32][33];
   WarpAppender app{abuf[threadIdx.x >> 5]};
   int32_t* seg = segs[threadIdx.x >> 5];

@@ -222,7 +222,7 @@ template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) shard_push_light_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
   if (a.ctl->mode[a.h] != 0) return;
-  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t abuf[kThreads / 32][kAppendRun + 32];
   WarpAppender app{abuf[threadIdx.x >> 5]};
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -245,7 +245,7 @@ template <int W, int SEM, bool FILTER>
 __global__ void __launch_bounds__(kThreads) shard_push_heavy_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
   if (a.ctl->mode[a.h] != 0) return;
-  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t abuf[kThreads / 32][kAppendRun + 32];
   WarpAppender app{abuf[threadIdx.x >> 5]};
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kThreads) shard_absorb_kernel(ShardArgs sa) {
   const WaveArgs& a = sa.a;
   if (a.ctl->mode[a.h] != 0) return;
   const int lane = threadIdx.x & 31;
-  __shared__ int32_t abuf[kThreads / 32][2 * kAppendRun];
+  __shared__ int32_t abuf[kThreads / 32][kAppendRun + 32];
   WarpAppender app{abuf[threadIdx.x >> 5]};
   const XCtrl* xc = sa.px.ctrl(sa.rank);
   const int64_t n = (int64_t)min(xc->cursor, (unsigned long long)sa.px.cap);
