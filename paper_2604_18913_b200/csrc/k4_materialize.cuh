@@ -148,7 +148,7 @@ constexpr unsigned kCoopIdsPerQuery = 48;  // chunk ids per touched query for th
 
 // per-warp shared words: WRITE = S (32 x kSStride) + the staging run (a
 // whole chunk's ids of one query); COUNT = per-query counters + degree sums.
-// (Round 3: list-driven layers dropped their per-lane rings for sparse
+// (Round 2: list-driven layers dropped their per-lane rings for sparse
 // chunks -- every chunk is written query by query -- C4 k=3 9.28 -> 9.19 ms;
 // capping the run at 256 / 512 ids to fit five / four CTAs per SM, with
 // longer runs stored lane by lane, lost: 11.5 / 10.5 ms.)

@@ -3,5 +3,5 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 export CUDA_MODULE_LOADING=EAGER
 timeout 1200 ncu --set full --clock-control none --import-source on --profile-from-start off \
-  -k regex:"${KREGEX:-pull|mat_kernel}" -f -o gpurun_out/r03_c2 python tools/prof_c2.py > gpurun_out/r03_ncu_c2.log 2>&1; echo ncu=$?
-python tools/ncu_summary.py gpurun_out/r03_c2.ncu-rep > gpurun_out/r03_c2.txt; echo sum=$?
+  -k regex:"${KREGEX:-pull|mat_kernel}" -f -o gpurun_out/r02b_c2 python tools/prof_c2.py > gpurun_out/r02b_ncu_c2.log 2>&1; echo ncu=$?
+python tools/ncu_summary.py gpurun_out/r02b_c2.ncu-rep > gpurun_out/r02b_c2.txt; echo sum=$?
