@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) pull_kernel(WaveArgs a) {
 //   non-dense hops: pull_screen_edges_kernel streams the in-edges (source
 //     and target row of each, rdst) and compacts the frontier ones as
 //     (vv, u[, rel]) -- a whole row's entries stay consecutive -- through a
-//     per-warp shared run stored with one global atomic per >= 32 entries;
+//     per-warp shared run stored with one global atomic per >= 128 entries;
 //     pull_edges_kernel gathers them: one dependent step (the entry) in
 //     front of the row loads instead of four.
 //   dense hops (every in-edge is taken): pull_kernel<.., SCREEN = false>
@@ -348,7 +348,7 @@ constexpr int kScreenRun = 32;
 // non-dense hops: the frontier in-edges as (vv, u[, rel]).  Each warp
 // streams a contiguous range of 32-edge chunks (source and target row of
 // each edge, coalesced; the frontier flag from the L2-resident bitmap),
-// software-pipelined two chunks deep: chunk c+2's edges and chunk c+1's
+// software-pipelined three chunks deep: chunk c+3's edges and chunk c+2's
 // flag words are loaded while chunk c is compacted.  A whole row's in-edges
 // (vv >= 0, at most kPullChunk) stay consecutive in the output: a warp
 // skips the leading edges of a row that started before its range and takes
@@ -359,7 +359,8 @@ template <bool FILTER>
 __global__ void __launch_bounds__(kThreads) pull_screen_edges_kernel(WaveArgs a, int32_t* cv,
                                                                      int32_t* cu, int32_t* cr) {
   if (a.ctl->mode[a.h] != 1 || a.ctl->dense[a.h] != 0) return;
-  constexpr int kBuf = 3 * 32;  // < 32 left + a chunk + a row's continuation
+  constexpr int kRun = 128;  // entries per counter atomic
+  constexpr int kBuf = kRun + 2 * 32;  // < kRun left + a chunk + a row's continuation
   __shared__ int32_t sb[kThreads / 32][FILTER ? 3 : 2][kBuf];
   const int wib = threadIdx.x >> 5;
   int32_t* bv = sb[wib][0];
@@ -423,15 +424,17 @@ __global__ void __launch_bounds__(kThreads) pull_screen_edges_kernel(WaveArgs a,
     fill = rest;
     __syncwarp();
   };
-  int32_t d0, u0, d1, u1, d2, u2;
+  auto xf = [&](int32_t d, int32_t u) { return d != INT32_MIN ? __ldg(a.Xf + (u >> 5)) : 0u; };
+  int32_t d0, u0, d1, u1, d2, u2, d3, u3;
   ld(c_begin, d0, u0);
   ld(c_begin + 1, d1, u1);
-  uint32_t x0 = d0 != INT32_MIN ? __ldg(a.Xf + (u0 >> 5)) : 0u, x1 = 0u;
+  ld(c_begin + 2, d2, u2);
+  uint32_t x0 = xf(d0, u0), x1 = xf(d1, u1), x2;
   int32_t last = c_begin > 0 ? __ldg(a.rdst + c_begin * 32 - 1) : INT32_MIN;
   bool first = true;
   for (int64_t c = c_begin; c < c_end; ++c) {
-    x1 = d1 != INT32_MIN ? __ldg(a.Xf + (u1 >> 5)) : 0u;
-    ld(c + 2, d2, u2);
+    x2 = xf(d2, u2);
+    ld(c + 3, d3, u3);
     int32_t pd = __shfl_up_sync(TH_FULL, d0, 1);
     if (lane == 0) pd = last;
     int lead = 0;
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(kThreads) pull_screen_edges_kernel(WaveArgs a,
       int32_t r2 = 0;
       if (FILTER && t2) r2 = (int32_t)__ldg(a.rrel + (c + 1) * 32 + lane);
       append(t2, last, u1, r2);
-    } else if (fill >= kScreenRun) {
+    } else if (fill >= kRun) {
       // keep a row still open at the boundary with its next entries
       int tail = 0;
       if (open) {
@@ -470,6 +473,9 @@ __global__ void __launch_bounds__(kThreads) pull_screen_edges_kernel(WaveArgs a,
     x0 = x1;
     d1 = d2;
     u1 = u2;
+    x1 = x2;
+    d2 = d3;
+    u2 = u3;
   }
   if (fill) flush(fill);
 }
