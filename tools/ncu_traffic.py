@@ -11,7 +11,7 @@ import re
 import subprocess
 import sys
 
-GROUPS = {"frontier": r"mat_kernel<.*(DenseSrc|ListSrc)|mat_scan|flag_|rs_count", "pull": r"pull_kernel",
+GROUPS = {"frontier": r"mat_kernel<.*(DenseSrc|ListSrc)|mat_scan|flag_|rs_count|bucket_", "pull": r"pull_(kernel|screen|edges)",
           "push": r"push_(light|heavy)", "clear": r"clear_rows"}
 
 
