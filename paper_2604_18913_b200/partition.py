@@ -777,11 +777,13 @@ class PartitionedGraph:
                              self.n_triples)
 
     def retrieve(self, seeds, k: int, relation_filter=None, semantics="frontier",
-                 activated: bool = False):
+                 activated: bool = False, copy: bool = True):
         """Per-seed retrieval (one query per seed), merged on every rank.
 
-        Returns a host ``RetrievalResult`` with the same accessors as the
-        single-GPU engine (frontier(i, h), activated(i, h), edges)."""
+        Returns a ``RetrievalResult`` with the same accessors as the
+        single-GPU engine (frontier(i, h), activated(i, h), edges): host
+        tensors, or -- ``copy=False`` -- device tensors (the caller copies
+        what it needs, e.g. into pinned buffers)."""
         import torch
 
         from .retriever import RetrievalResult, _relation_masks
@@ -801,7 +803,7 @@ class PartitionedGraph:
             nq = q1 - q0
             wq = WaveQuery(np.arange(nq + 1, dtype=np.int32), arr[q0:q1].astype(np.int32), k, sem,
                            None if words is None else words[q0:q1], activated)
-            m = {n: (v.cpu() if v is not None else None) for n, v in self.merged(wq).items()}
+            m = {n: (v.cpu() if copy and v is not None else v) for n, v in self.merged(wq).items()}
             merged["edges"].append(m["edges"])
             merged["f_off"].append(m["f_off"] + fbase)
             merged["f_len"].append(m["f_len"])
@@ -814,7 +816,7 @@ class PartitionedGraph:
                 abase += m["a_ids"].numel()
             if B == 0:
                 break
-        cat = lambda xs, dim=1: torch.cat(xs, dim)  # noqa: E731
+        cat = lambda xs, dim=1: xs[0] if len(xs) == 1 else torch.cat(xs, dim)  # noqa: E731
         out = RetrievalResult(B, k, sem, _graph=self)
         out.edges = cat(merged["edges"])
         out.frontier_off, out.frontier_len = cat(merged["f_off"]), cat(merged["f_len"])
