@@ -1063,7 +1063,8 @@ void launch_pull(Session* s, const Graph* g, const WaveArgs& a, cudaStream_t st)
     ea.T = g->T;  // (a shard's in-edge graph: its own edge count)
     pull_screen_edges_kernel<FILTER><<<pg, kThreads, 0, st>>>(ea, c, c + n, cr);
     TH_LAUNCHED();
-    pull_edges_kernel<W, SEM, FILTER><<<pg, kThreads, 0, st>>>(a, c, c + n, cr);
+    if (s->pull_pair) pull_edges_kernel<W, SEM, FILTER, 2><<<pg, kThreads, 0, st>>>(a, c, c + n, cr);
+    else pull_edges_kernel<W, SEM, FILTER, 1><<<pg, kThreads, 0, st>>>(a, c, c + n, cr);
     TH_LAUNCHED();
     WaveArgs pa = a;
     pa.pull_only_dense = 1;
@@ -1477,7 +1478,7 @@ static GraphKey graph_key(Session* s, const th_query* q) {
   k.list_min = s->list_min_entities;
   k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_mode << 10) |
             ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0) | (s->priority ? 128 : 0) |
-            (s->k4_bucket ? 256 : 0);
+            (s->k4_bucket ? 256 : 0) | (s->pull_pair ? 512 : 0);
   k.epoch = session_alloc_sig(s);
   return k;
 }

@@ -72,6 +72,7 @@ struct Session {
   // the critical path first and K4 fills the gaps
   bool priority = true;
   bool k4_bucket = true;  // list-driven layers: scatter/gather write pass (k4_rowmajor.cuh)
+  bool pull_pair = true;  // two-phase pull gather: two target rows per lane group in flight
   bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr, side2 = nullptr;  // K4 streams (odd / even layers)
   int k4_slot = 0;                                // which K4 scratch set is in use

@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kThreads) pull_screen_edges_kernel(WaveArgs a,
 // the frontier rows of its sources are loaded 4 at a time with the visited
 // row, then N (and V) are written; a whole row is flagged with a
 // non-returning atomic (only its own segment can reach it this hop).
-template <int W, int SEM, bool FILTER>
+template <int W, int SEM, bool FILTER, int SPG = 2>
 __global__ void __launch_bounds__(kThreads) pull_edges_kernel(WaveArgs a, const int32_t* __restrict__ cv,
                                                               const int32_t* __restrict__ cu,
                                                               const int32_t* __restrict__ cr) {
@@ -559,87 +559,103 @@ __global__ void __launch_bounds__(kThreads) pull_edges_kernel(WaveArgs a, const 
     if (start) seg[__popc(S & lanemask_lt())] = (int)lane;
     if (lane == 0) seg[nseg] = wend + cont;
     __syncwarp();
-    for (int r0 = 0; r0 < nseg; r0 += GPW) {
-      const int si = r0 + grp;
-      const bool live = si < nseg;
-      const int s = live ? seg[si] : 0;
-      const int len = live ? seg[si + 1] - s : 0;
-      const int32_t vv = __shfl_sync(TH_FULL, cev, s);
-      const uint32_t vs = __shfl_sync(TH_FULL, vis, s);
-      const bool split = vv < 0;
-      const int32_t v = split ? ~vv : vv;
-      const size_t row = (size_t)v * W + part * VEC;
-      uint32_t seen[VEC], acc[VEC];
+    // SPG runs per lane group per round, their row loads issued together
+    for (int r0 = 0; r0 < nseg; r0 += GPW * SPG) {
+      bool live[SPG], split[SPG];
+      int s[SPG], len[SPG];
+      int32_t v[SPG];
+      size_t row[SPG];
+      uint32_t seen[SPG][VEC], acc[SPG][VEC];
+      int maxlen = 0;
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) {
-        seen[c] = 0u;
-        acc[c] = 0u;
+      for (int g = 0; g < SPG; ++g) {
+        const int si = r0 + g * GPW + grp;
+        live[g] = si < nseg;
+        s[g] = live[g] ? seg[si] : 0;
+        len[g] = live[g] ? seg[si + 1] - s[g] : 0;
+        const int32_t vv = __shfl_sync(TH_FULL, cev, s[g]);
+        const uint32_t vs = __shfl_sync(TH_FULL, vis, s[g]);
+        split[g] = vv < 0;
+        v[g] = split[g] ? ~vv : vv;
+        row[g] = (size_t)v[g] * W + part * VEC;
+#pragma unroll
+        for (int c = 0; c < VEC; ++c) {
+          seen[g][c] = 0u;
+          acc[g][c] = 0u;
+        }
+        if (SEM != TH_EXACT && live[g] && vs) ld_words<VEC>(a.V + row[g], seen[g]);
+        maxlen = max(maxlen, len[g]);
       }
-      if (SEM != TH_EXACT && live && vs) ld_words<VEC>(a.V + row, seen);
-      const int maxlen = (int)__reduce_max_sync(TH_FULL, (unsigned)len);
+      maxlen = (int)__reduce_max_sync(TH_FULL, (unsigned)maxlen);
       for (int t0 = 0; t0 < maxlen; t0 += 4) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (t0 + k >= maxlen) break;  // (warp-uniform: most runs hold one or two edges)
-          const int t = s + t0 + k;
-          const int32_t ua = __shfl_sync(TH_FULL, ceu, t & 31);
-          const int32_t ub = __shfl_sync(TH_FULL, ceu2, t & 31);
-          int32_t ra = 0, rb = 0;
-          if (FILTER) {
-            ra = __shfl_sync(TH_FULL, cer, t & 31);
-            rb = __shfl_sync(TH_FULL, cer2, t & 31);
-          }
-          if (t0 + k < len) {
-            const int32_t u = t < 32 ? ua : ub;
-            uint32_t x[VEC];
-            ldg_words<VEC>(a.X + (size_t)u * W + part * VEC, x);
+#pragma unroll
+          for (int g = 0; g < SPG; ++g) {
+            const int t = s[g] + t0 + k;
+            const int32_t ua = __shfl_sync(TH_FULL, ceu, t & 31);
+            const int32_t ub = __shfl_sync(TH_FULL, ceu2, t & 31);
+            int32_t ra = 0, rb = 0;
             if (FILTER) {
-              uint32_t m[VEC];
-              ldg_words<VEC>(a.M + (size_t)(t < 32 ? ra : rb) * W + part * VEC, m);
-#pragma unroll
-              for (int c = 0; c < VEC; ++c) x[c] &= m[c];
+              ra = __shfl_sync(TH_FULL, cer, t & 31);
+              rb = __shfl_sync(TH_FULL, cer2, t & 31);
             }
+            if (t0 + k < len[g]) {
+              const int32_t u = t < 32 ? ua : ub;
+              uint32_t x[VEC];
+              ldg_words<VEC>(a.X + (size_t)u * W + part * VEC, x);
+              if (FILTER) {
+                uint32_t m[VEC];
+                ldg_words<VEC>(a.M + (size_t)(t < 32 ? ra : rb) * W + part * VEC, m);
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) acc[c] |= x[c];
+                for (int c = 0; c < VEC; ++c) x[c] &= m[c];
+              }
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) acc[g][c] |= x[c];
+            }
           }
         }
       }
-      uint32_t nb[VEC];
-      bool any = false;
 #pragma unroll
-      for (int c = 0; c < VEC; ++c) {
-        nb[c] = acc[c] & ~seen[c] & valid[c];
-        any |= nb[c] != 0u;
-      }
-      any = (__ballot_sync(TH_FULL, any) & gbits) != 0u;
-      bool fresh = false;
-      if (live && any) {
-        if (!split) {
-          st_words<VEC>(a.N + row, nb);
-          if (SEM != TH_EXACT && !a.last_frontier) {
-            uint32_t nw[VEC];
+      for (int g = 0; g < SPG; ++g) {
+        uint32_t nb[VEC];
+        bool any = false;
 #pragma unroll
-            for (int c = 0; c < VEC; ++c) nw[c] = seen[c] | nb[c];
-            st_words<VEC>(a.V + row, nw);
-          }
-          if (part == 0) {
-            const uint32_t fb = 1u << (v & 31);
-            atomicOr(&a.Nf[v >> 5], fb);
-            if (SEM != TH_EXACT) atomicOr(&a.Vf[v >> 5], fb);
-            fresh = true;
-          }
-        } else {
-#pragma unroll
-          for (int c = 0; c < VEC; ++c) {
-            if (nb[c]) {
-              atomicOr(a.N + row + c, nb[c]);
-              if (SEM != TH_EXACT && !a.last_frontier) atomicOr(a.V + row + c, nb[c]);
-            }
-          }
-          if (part == 0) fresh = flag_next(a, v);
+        for (int c = 0; c < VEC; ++c) {
+          nb[c] = acc[g][c] & ~seen[g][c] & valid[c];
+          any |= nb[c] != 0u;
         }
+        any = (__ballot_sync(TH_FULL, any) & gbits) != 0u;
+        bool fresh = false;
+        if (live[g] && any) {
+          if (!split[g]) {
+            st_words<VEC>(a.N + row[g], nb);
+            if (SEM != TH_EXACT && !a.last_frontier) {
+              uint32_t nw[VEC];
+#pragma unroll
+              for (int c = 0; c < VEC; ++c) nw[c] = seen[g][c] | nb[c];
+              st_words<VEC>(a.V + row[g], nw);
+            }
+            if (part == 0) {
+              const uint32_t fb = 1u << (v[g] & 31);
+              atomicOr(&a.Nf[v[g] >> 5], fb);
+              if (SEM != TH_EXACT) atomicOr(&a.Vf[v[g] >> 5], fb);
+              fresh = true;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < VEC; ++c) {
+              if (nb[c]) {
+                atomicOr(a.N + row[g] + c, nb[c]);
+                if (SEM != TH_EXACT && !a.last_frontier) atomicOr(a.V + row[g] + c, nb[c]);
+              }
+            }
+            if (part == 0) fresh = flag_next(a, v[g]);
+          }
+        }
+        app.add(a, fresh, v[g]);
       }
-      app.add(a, fresh, v);
     }
     __syncwarp();
   }
