@@ -147,20 +147,23 @@ constexpr unsigned kSparseBits = 5;       // tiles with <= this many bits per la
 constexpr unsigned kCoopIdsPerQuery = 48;  // chunk ids per touched query for the cooperative write
 
 // per-warp shared words: WRITE = S (32 x kSStride) + the staging run (a
-// whole chunk's ids of one query); COUNT = per-query counters + degree sums.
+// whole chunk's ids of one query: final int32 ids for entity layers of small
+// graphs, 16-bit chunk positions for list-driven layers, which resolve them
+// through the row list on the way out -- 6.1 KB per warp, four 8-warp CTAs
+// per SM instead of three); COUNT = per-query counters + degree sums.
 // (Round 2: list-driven layers dropped their per-lane rings for sparse
 // chunks -- every chunk is written query by query -- C4 k=3 9.28 -> 9.19 ms;
 // capping the run at 256 / 512 ids to fit five / four CTAs per SM, with
 // longer runs stored lane by lane, lost: 11.5 / 10.5 ms.)
 template <bool WRITE, bool RING = false>
 constexpr size_t mat_warp_words() {
-  return WRITE ? (size_t)(32 * kSStride + kChunkRows) : 64;
+  return WRITE ? (size_t)(32 * kSStride + (RING ? kChunkRows / 2 : kChunkRows)) : 64;
 }
 
 // per-warp words of a write pass that loads cached masks: the staging run
 template <bool RING>
 constexpr size_t mat_load_words() {
-  return kChunkRows;
+  return RING ? kChunkRows / 2 : kChunkRows;
 }
 
 // CTA-shared words of an EDGES count pass (degree planes, see mat_unit)
@@ -226,8 +229,9 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
   constexpr size_t kWarpWords = BUILD_S && !WRITE ? (size_t)(32 * kSStride + 64)
                                                   : mat_warp_words<WRITE, RING>();
   uint32_t* S = LOAD_S ? nullptr : mat_smem + (size_t)warp * kWarpWords;
-  int32_t* stg = LOAD_S ? reinterpret_cast<int32_t*>(mat_smem + (size_t)warp * mat_load_words<RING>())
-                        : reinterpret_cast<int32_t*>(S + 32 * kSStride);
+  using StgT = std::conditional_t<RING, uint16_t, int32_t>;
+  StgT* stg = LOAD_S ? reinterpret_cast<StgT*>(mat_smem + (size_t)warp * mat_load_words<RING>())
+                     : reinterpret_cast<StgT*>(S + 32 * kSStride);
   // COUNT: [32] ids + [32] degree sums per query (sparse tiles), after S
   // when the pass also builds S
   uint32_t* cnt = BUILD_S && !WRITE ? S + 32 * kSStride : S;  // (unused when LOAD_S)
@@ -474,17 +478,17 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       const int n = __shfl_sync(TH_FULL, incl, 31);
       // highest set bit first, filling the lane's run from its end (FLO
       // gives the top bit directly; no bit reversal per id)
-      int32_t* dst = stg + incl - 1;
+      StgT* dst = stg + incl - 1;
       while (m) {
         const int bit = 31 - __clz((int)m);
-        *dst-- = rbase + bit;
+        *dst-- = (StgT)(rbase + bit);
         m ^= 1u << bit;
       }
       __syncwarp();
       const int64_t pb = __shfl_sync(TH_FULL, pos, b);
       if (direct && pb + n <= cap) {
         int32_t* o = out + pb + lane;
-        const int32_t* sp = stg + lane;
+        const StgT* sp = stg + lane;
         int i = lane;
         for (; i + 96 < n; i += 128, o += 128, sp += 128) {
           const int32_t v0 = sp[0], v1 = sp[32], v2 = sp[64], v3 = sp[96];
@@ -501,7 +505,7 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
         // ids resolve through the row list / map: four independent
         // lookups in flight per lane before their stores
         int32_t* o = out + pb + lane;
-        const int32_t* sp = stg + lane;
+        const StgT* sp = stg + lane;
         int i = lane;
         for (; i + 96 < n; i += 128, o += 128, sp += 128) {
           const int32_t v0 = src.id(c0 + sp[0]), v1 = src.id(c0 + sp[32]);
