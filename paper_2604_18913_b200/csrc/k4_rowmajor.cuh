@@ -73,12 +73,13 @@ __device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t&
 }
 
 // adds plane k's bits into cnt[b * 32 + lane] with weight 2^k
-__device__ __forceinline__ void rs_flush_plane(uint32_t p, int k, uint32_t* cnt) {
+template <typename C>
+__device__ __forceinline__ void rs_flush_plane(uint32_t p, int k, C* cnt) {
   const unsigned lane = lane_id();
   while (p) {
     const int b = __ffs(p) - 1;
     p &= p - 1u;
-    cnt[b * 32 + lane] += 1u << k;
+    cnt[b * 32 + lane] += (C)(1u << k);
   }
 }
 
@@ -87,9 +88,9 @@ __device__ __forceinline__ void rs_flush_plane(uint32_t p, int k, uint32_t* cnt)
 // column-wise by a carry-save adder tree into a 4-bit bit-sliced count,
 // added into six running planes (counts up to 63) that are flushed to the
 // shared counters every 56 rows.
-template <int W>
+template <int W, typename C>
 __device__ __forceinline__ uint32_t rs_count_sliced(const RowMajorSrc<W>& src, int64_t lo, int64_t hi,
-                                                    uint32_t* cnt, uint32_t valid) {
+                                                    C* cnt, uint32_t valid) {
   static_assert(kRsUnroll == 8, "the adder tree sums 8 rows");
   uint32_t c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u, c4 = 0u, c5 = 0u;
   uint32_t word_bits = 0u;  // this lane's word over the slice (the bucket pass's group count)
@@ -155,9 +156,15 @@ __device__ __forceinline__ void rs_count_edges(const RowMajorSrc<W>& src, int64_
   }
 }
 
+// per-(warp, query) counters: 32-bit with degree sums, else 16-bit (a warp
+// slice holds < 2^16 rows for any layer below 2^31 rows), so the plain count
+// pass fits four 16-warp CTAs per SM
+template <bool EDGES>
+using RsCnt = std::conditional_t<EDGES, uint32_t, uint16_t>;
+
 template <bool EDGES>
 constexpr size_t rs_count_smem() {
-  return (size_t)(EDGES ? 2 : 1) * kRsWarps * 1024 * sizeof(uint32_t);
+  return (size_t)(EDGES ? 2 : 1) * kRsWarps * 1024 * sizeof(RsCnt<EDGES>);
 }
 
 // counts[q * nblk + blk] = bits of query q in row block blk of the list (or
@@ -167,18 +174,20 @@ constexpr size_t rs_count_smem() {
 // (gcount, when given: [nblk * kRsWarps + 1][32] bits of word j in each
 // warp's slice -- the bucket write pass's partition, see below)
 template <int W, bool EDGES>
-__global__ void __launch_bounds__(32 * kRsWarps) rs_count_kernel(RowMajorSrc<W> src, int nblk,
+__global__ void __launch_bounds__(32 * kRsWarps, 4) rs_count_kernel(RowMajorSrc<W> src, int nblk,
                                                                  int32_t* counts, EdgeSum es,
                                                                  uint32_t* gcount = nullptr) {
   // dynamic: [kRsWarps][1024] counters (+ [kRsWarps][1024] degree sums; a
   // warp's degree sum per query covers distinct rows: <= T < 2^32)
-  extern __shared__ uint32_t rs_smem[];
+  extern __shared__ uint32_t rs_smem_words[];
+  using C = RsCnt<EDGES>;
+  C* rs_smem = reinterpret_cast<C*>(rs_smem_words);
   const int warp = threadIdx.x >> 5;
   const unsigned lane = lane_id();
   const int blk = blockIdx.x;
   if (blk >= nblk) return;
-  uint32_t* cnt = rs_smem + warp * 1024;
-  uint32_t* esum = rs_smem + (kRsWarps + warp) * 1024;
+  C* cnt = rs_smem + warp * 1024;
+  uint32_t* esum = rs_smem_words + (kRsWarps + warp) * 1024;  // (EDGES: C is 32-bit)
   const int64_t nrows = src.count();
   int64_t blk_rows = (nrows + nblk - 1) / nblk;
   blk_rows = blk_rows < kChunkRows ? kChunkRows : (blk_rows + kChunkRows - 1) / kChunkRows * kChunkRows;
@@ -197,10 +206,10 @@ __global__ void __launch_bounds__(32 * kRsWarps) rs_count_kernel(RowMajorSrc<W> 
   const uint32_t valid = lane < (unsigned)W ? valid_word((int)lane, src.nq) : 0u;
 #pragma unroll 8
   for (int b = 0; b < 32; ++b) {
-    cnt[b * 32 + lane] = 0u;
+    cnt[b * 32 + lane] = 0;
     if (EDGES) esum[b * 32 + lane] = 0u;
   }
-  if (EDGES) {
+  if constexpr (EDGES) {
     rs_count_edges<W>(src, lo, hi, cnt, esum, es, valid);
   } else {
     const uint32_t wb = rs_count_sliced<W>(src, lo, hi, cnt, valid);
@@ -214,7 +223,7 @@ __global__ void __launch_bounds__(32 * kRsWarps) rs_count_kernel(RowMajorSrc<W> 
 #pragma unroll
     for (int w = 0; w < kRsWarps; ++w) {
       t += rs_smem[w * 1024 + at];
-      if (EDGES) e += rs_smem[(kRsWarps + w) * 1024 + at];
+      if (EDGES) e += rs_smem_words[(kRsWarps + w) * 1024 + at];
     }
     counts[(size_t)q * nblk + blk] = (int32_t)t;
     if (EDGES && e) atomicAdd(reinterpret_cast<unsigned long long*>(es.out + q), e);
