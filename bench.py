@@ -522,7 +522,7 @@ def partitioned_leg(th, cols, E, R, world, rank, ks=(2, 3), n_batches=4, reps=4)
         for i in range(3):
             torch.cuda.synchronize()
             w0 = time.perf_counter()
-            res = pg.retrieve(batches[i % n_batches], k, copy=False)
+            res = pg.retrieve(batches[0], k, copy=False)  # (same shapes: no pinned regrowth)
             d2h = 0
             for name in ("frontier_off", "frontier_len", "frontier_ids", "edges"):
                 t = getattr(res, name)
