@@ -184,7 +184,11 @@ int th_session_set_pull_screen(th_session* s, int mode);
 /* Boolean strategy knobs by name (A/B and tests): "paths_k2" (k = 2
  * singleton capped path queries on a CTA each; default 1), "k4_cache"
  * (small dense layers cache their tile masks; 1), "list_first_hop" (the
- * first layer's overlapped K4 follows its row list; 1). */
+ * first layer's overlapped K4 follows its row list; 1), "priority" (the
+ * hop chain at the highest stream priority; 1), "k4_bucket" (list-driven
+ * layers up to 20M ids take the bucketed write; 1), "pull_pair" (the
+ * two-phase pull's gather keeps two target rows per lane group in flight;
+ * 1). */
 int th_session_set_knob(th_session* s, const char* name, int64_t value);
 /* Pull hops whose frontier sources more than 1/divisor of all in-edges
  * (by the frontier's out-degree sum) gather every in-neighbour row instead

@@ -275,3 +275,37 @@ def test_dense_pull_matches_flag_tested_pull(th, filtered):
         ref = orc.retrieve_one(og, int(seeds[i]), 3, "frontier", None if filt is None else filt[i])
         for h in range(3):
             assert np.array_equal(b.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
+
+
+@pytest.mark.parametrize("pair", [0, 1])
+@pytest.mark.parametrize("filtered", [False, True])
+@pytest.mark.parametrize("sem", ["exact", "frontier", "cumulative"])
+def test_two_phase_pull_every_hop_vs_oracle(th, sem, filtered, pair):
+    """The two-phase pull (edge screen + gather over compacted frontier
+    in-edges) forced on every hop and never dense, on a hub graph whose
+    in-rows split over several pull items (merged with atomics) and whose
+    whole rows straddle the screen's chunk and warp-range boundaries;
+    with and without relation filters and two rows per lane group."""
+    s, r, o = _hub_graph(3000, 100000, 64, seed=23)
+    E, R = 3000, 64
+    g = th.build_incidence((s, r, o), E, R)
+    assert g.stats()["max_in_degree"] > 32  # split rows
+    og = orc.build_csr(s, r, o, E, R)
+    rng = np.random.default_rng(5)
+    seeds = rng.integers(0, E, 700)
+    filt = None
+    if filtered:
+        filt = [sorted(rng.choice(R, 20, replace=False).tolist()) for _ in seeds]
+    ret = th.Retriever(g)
+    ret.set_pull_divisor(-1.0)  # every hop pulls
+    ret.set_dense_pull(0.0)  # never the dense (unscreened) form
+    ret.set_pull_screen(2)
+    ret.set_knob("pull_pair", pair)
+    k = 3
+    res = ret.retrieve(seeds, k, relation_filter=filt, semantics=sem)
+    assert res.push_hops == 0
+    for i in list(range(0, 700, 29)) + [699]:
+        ref = orc.retrieve_one(og, int(seeds[i]), k, sem, None if filt is None else filt[i])
+        for h in range(k):
+            assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (i, h)
+            assert int(res.edges[h, i]) == ref["edges"][h], (i, h)
