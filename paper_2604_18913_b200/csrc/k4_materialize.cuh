@@ -476,18 +476,13 @@ __device__ __forceinline__ void mat_unit(const Src& src, int nblk, int32_t* coun
       const int c = __popc(m);
       const int incl = warp_incl_scan(c);
       const int n = __shfl_sync(TH_FULL, incl, 31);
-      // two ids per step: the highest set bit fills the lane's run from its
-      // end, the lowest from its start (half the divergent steps)
+      // highest set bit first, filling the lane's run from its end (FLO
+      // gives the top bit directly; no bit reversal per id)
       StgT* dst = stg + incl - 1;
-      StgT* dlo = stg + incl - c;
       while (m) {
         const int bit = 31 - __clz((int)m);
         *dst-- = (StgT)(rbase + bit);
         m ^= 1u << bit;
-        if (m) {
-          *dlo++ = (StgT)(rbase + __ffs(m) - 1);
-          m &= m - 1u;
-        }
       }
       __syncwarp();
       const int64_t pb = __shfl_sync(TH_FULL, pos, b);
