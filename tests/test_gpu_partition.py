@@ -61,6 +61,32 @@ def test_partitioned_equals_single_and_oracle(th, world, n_hubs, sem, direction)
             assert int(part.edges[h, i]) == ref["edges"][h]
 
 
+@pytest.mark.parametrize("world,n_hubs", [(1, 0), (2, 0), (3, 6)])
+@pytest.mark.parametrize("sem", ["exact", "frontier"])
+def test_partitioned_sparse_graph_two_phase_pull(th, world, n_hubs, sem):
+    """A C4-shaped sparse graph (1.6 in-edges per entity): the shards' pull
+    hops take the two-phase pull (edge screen + gather) by graph shape;
+    forced pulls, against the single graph and the oracle."""
+    E, R = 20000, 16
+    s, r, o = _hub_graph(E, 32000, R, seed=61, alpha=1.3)
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    pg = th.PartitionedGraph((s, r, o), E, R, th.LoopbackExchange(world), n_hubs=n_hubs)
+    pg.pull_divisor = 1e18  # every hop after the first pulls
+    rng = np.random.default_rng(9)
+    seeds = rng.integers(0, E, 400)
+    part = pg.retrieve(seeds, 3, semantics=sem)
+    single = th.retrieve(g, seeds, 3, semantics=sem)
+    for i in range(seeds.size):
+        for h in range(1, 4):
+            assert np.array_equal(part.frontier(i, h), single.frontier(i, h)), (i, h)
+    assert np.array_equal(part.edges.numpy(), single.edges.cpu().numpy())
+    for i in range(0, seeds.size, 37):
+        ref = orc.retrieve_one(og, int(seeds[i]), 3, sem)
+        for h in range(3):
+            assert np.array_equal(part.frontier(i, h + 1), ref["frontiers"][h])
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_partitioned_relation_filter(th, world):
     """Relation masks on push hops (world 2, auto) and on pull hops (world 4)."""
