@@ -796,7 +796,8 @@ void for_each_session_buf(Session* s, F&& f) {
                   &s->a_len, &s->a_ids, &s->edges, &s->p_off, &s->p_cnt, &s->p_trunc, &s->p_tids,
                   &s->p_scratch, &s->p_tmp, &s->rowlist, &s->rowscan, &s->k4_S, &s->k4_meta, &s->counts2,
                   &s->totals2, &s->rowlist2, &s->rowscan2, &s->k4_S2, &s->k4_meta2,
-                  &s->k4_P, &s->k4_G, &s->k4_P2, &s->k4_G2, &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks})
+                  &s->k4_P, &s->k4_G, &s->k4_P2, &s->k4_G2, &s->heavy_off, &s->in_offs, &s->in_seeds, &s->in_masks,
+                  &s->pull_items})
     f(d);
 }
 
