@@ -740,14 +740,32 @@ def run_ours(args, world, rank, local):
         h2d = host_seeds.numel() * 4 + (BATCH + 1) * 4
         d2h = sum(outs.values())
     e2e_t = statistics.median(e2e_times)
+    # streaming e2e (the serving loop): RetrievalPipeline runs batch i+1's
+    # hops while batch i's results cross PCIe; every step still moves its
+    # pinned seeds in and all of its results out
+    from paper_2604_18913_b200.pipeline import RetrievalPipeline
+
+    pipe = RetrievalPipeline(g, depth=2)
+    host_batches = [torch.from_numpy(b).pin_memory() for b in batches]
+    for _ in pipe.run(host_batches[:4], K_HOPS):  # sizes buffers, captures both sessions' graphs
+        pass
+    torch.cuda.synchronize()
+    n_pipe = len(host_batches)
+    t0 = time.perf_counter()
+    pipe_d2h = 0
+    for hb in pipe.run(host_batches, K_HOPS):
+        pipe_d2h += hb.nbytes()
+    pipe_t = (time.perf_counter() - t0) / n_pipe
+    del pipe
     if world > 1:
         # whole job: every rank's batch over the slowest rank's time
         import torch.distributed as dist
 
-        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        tt = torch.tensor([e2e_t, pipe_t], dtype=torch.float64, device=dev)
         _all_reduce(tt, dist.ReduceOp.MAX)
-        e2e_t = float(tt.item())
+        e2e_t, pipe_t = (float(x) for x in tt.tolist())
     e2e_value = BATCH * world / e2e_t
+    pipe_value = BATCH * world / pipe_t
 
     # CPU baseline: oracle on the host cores, rank 0 at N=1 only
     cpu = None
@@ -803,11 +821,17 @@ def run_ours(args, world, rank, local):
             "kernel_ms_per_step": {c: v[0] / args.steps for c, v in prof.items()},
             "kernel_ms_source": "CUDA events around each kernel group, profiled pass over the same K batches",
             "kernel_launches_per_step": {c: v[1] / args.steps for c, v in prof.items()},
-            "e2e": {"value": e2e_value, "unit": "seeds/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "api": "Retriever.retrieve + pinned D2H of all results",
+            "e2e": {"value": pipe_value, "unit": "seeds/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": pipe_d2h // n_pipe, "steps": n_pipe,
+                    "api": "RetrievalPipeline.run (pipeline.py): pinned seeds in, every batch's results "
+                           "to pinned host memory, batch i+1's hops overlapping batch i's copy-out",
                     # the host link bounds it: result bytes per second of the whole step
-                    "link_GBps": (h2d + d2h) / e2e_t / 1e9,
-                    "note": "PCIe-bound: every step returns all per-seed frontiers (int32) to the host"},
+                    "link_GBps": (h2d + pipe_d2h / n_pipe) / pipe_t / 1e9,
+                    "note": "PCIe-bound: every step returns all per-seed frontiers (int32) to the host",
+                    "blocking": {"value": e2e_value, "unit": "seeds/s", "h2d_bytes_per_step": h2d,
+                                 "d2h_bytes_per_step": d2h,
+                                 "api": "Retriever.retrieve + pinned D2H of all results, one batch at a time",
+                                 "link_GBps": (h2d + d2h) / e2e_t / 1e9}},
             "gpu_launches": launches,
             "wall_s_timed": wall,
             "clocks": clk,

@@ -41,6 +41,7 @@ from .partition import (
     route,
 )
 from .retriever import RetrievalResult, Retriever, k_hop, one_hop, reconstruct_paths, retrieve
+from .pipeline import HostBatch, RetrievalPipeline
 from .store import (
     DirectoryStore,
     InMemoryStore,
@@ -56,6 +57,8 @@ from .service import Labels as Dictionary, LookupResult, lookup_entities
 from .targets import GpuTarget, PartitionedGpuTarget
 
 __all__ = [
+    "HostBatch",
+    "RetrievalPipeline",
     "Dictionary",
     "LookupResult",
     "lookup_entities",
