@@ -188,7 +188,8 @@ int th_session_set_pull_screen(th_session* s, int mode);
  * hop chain at the highest stream priority; 1), "k4_bucket" (list-driven
  * layers up to 20M ids take the bucketed write; 1), "pull_pair" (the
  * two-phase pull's gather keeps two target rows per lane group in flight;
- * 1). */
+ * 1), "k4_cache_filtered" (relation-filtered waves' layers cache their
+ * masks too when "k4_cache" is on; 0). */
 int th_session_set_knob(th_session* s, const char* name, int64_t value);
 /* Pull hops whose frontier sources more than 1/divisor of all in-edges
  * (by the frontier's out-degree sum) gather every in-neighbour row instead

@@ -292,6 +292,8 @@ int th_session_set_knob(th_session* s, const char* name, int64_t value) {
     s->s.k4_bucket = value != 0;
   } else if (n == "pull_pair") {
     s->s.pull_pair = value != 0;
+  } else if (n == "k4_cache_filtered") {
+    s->s.k4_cache_filtered = value != 0;
   } else {
     th::set_error("unknown knob " + n);
     return TH_ERR_INVALID;

@@ -874,7 +874,8 @@ void materialize(Session* s, WaveBufs& b, const Src& src, int nq, int64_t* off, 
   // streams a layer-sized buffer through HBM twice, C4 k=3 18.5 -> 20.9 ms)
   if constexpr (Src::kDense && !Src::kRing) {
     const int64_t nchunks = ceil_div(rows, kChunkRows);
-    if (s->k4_cache && s->k4_mode < 2 && nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
+    if (s->k4_cache && (es.out || !s->last.d_rel_masks || s->k4_cache_filtered) && s->k4_mode < 2 &&
+        nchunks * W * 1024 * 4 <= (int64_t(256) << 20)) {
       SCache sc;
       sc.S = ensure<uint32_t>(kS, nchunks * W * 1024, s->st);
       sc.meta = ensure<uint2>(kMeta, nchunks * W + 1, s->st);
@@ -1480,7 +1481,8 @@ static GraphKey graph_key(Session* s, const th_query* q) {
   k.list_min = s->list_min_entities;
   k.knobs = (s->overlap ? 1 : 0) | (s->k4_cache ? 2 : 0) | (s->prof ? 4 : 0) | (s->k4_mode << 10) |
             ((s->pull_screen + 1) << 4) | (s->paths_k2 ? 64 : 0) | (s->priority ? 128 : 0) |
-            (s->k4_bucket ? 256 : 0) | (s->pull_pair ? 512 : 0);
+            (s->k4_bucket ? 256 : 0) | (s->pull_pair ? 512 : 0) |
+            (s->k4_cache_filtered ? 1 << 20 : 0);
   k.epoch = session_alloc_sig(s);
   return k;
 }

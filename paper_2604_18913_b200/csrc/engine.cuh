@@ -73,6 +73,10 @@ struct Session {
   bool priority = true;
   bool k4_bucket = true;  // list-driven layers: scatter/gather write pass (k4_rowmajor.cuh)
   bool pull_pair = true;  // two-phase pull gather: two target rows per lane group in flight
+  // filtered waves' layers (no fused edge sums) cache their masks too: off --
+  // their layers are sparse, and the bit-sliced count + transposing write
+  // beat storing and re-reading the masks (C3 3.84 -> ~3.6 ms)
+  bool k4_cache_filtered = false;
   bool list_first_hop = true;  // K4 of hop 1 follows the compacted row list  // small layers: count pass caches tile masks for the write pass
   cudaStream_t side = nullptr, side2 = nullptr;  // K4 streams (odd / even layers)
   int k4_slot = 0;                                // which K4 scratch set is in use

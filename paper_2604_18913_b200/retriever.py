@@ -205,7 +205,7 @@ class Retriever:
 
     def set_knob(self, name: str, value: int) -> None:
         """Boolean strategy knobs: "paths_k2", "k4_cache", "list_first_hop", "priority",
-        "k4_bucket", "pull_pair" (th_b200.h)."""
+        "k4_bucket", "pull_pair", "k4_cache_filtered" (th_b200.h)."""
         _lib.check(_lib.load().th_session_set_knob(self._handle, name.encode(), int(value)))
 
     def set_paths_k2(self, on: bool) -> None:
