@@ -111,3 +111,11 @@ def test_product_never_imports_the_oracle():
     pkg = ROOT / "paper_2604_18913_b200"
     for f in pkg.rglob("*.py"):
         assert "oracle" not in f.read_text().replace("oracle/", ""), f
+
+
+def test_pipeline_rejects_bad_depth():
+    """RetrievalPipeline validates its depth before touching the device."""
+    import paper_2604_18913_b200 as th
+
+    with pytest.raises(ValueError):
+        th.RetrievalPipeline(None, depth=0)

@@ -172,3 +172,27 @@ def test_duplicate_seeds_in_a_query(th_mod):
         assert bool((a.edges == b.edges).all()), sem
         for h in range(3):
             assert np.array_equal(a.frontier(0, h + 1), b.frontier(0, h + 1)), (sem, h)
+
+
+@pytest.mark.parametrize("cache_filtered", [0, 1])
+@pytest.mark.parametrize("k", [2, 3])
+def test_filtered_waves_with_and_without_mask_cache(th_mod, cache_filtered, k):
+    """Relation-filtered waves skip K4's tile-mask cache by default
+    (k4_cache_filtered = 0); both forms against the oracle."""
+    th = th_mod
+    E, T, R = 1400, 24000, 30
+    s, r, o = _hub_graph(E, T, R, seed=11 + k, alpha=1.1)
+    g = th.build_incidence((s, r, o), E, R)
+    og = orc.build_csr(s, r, o, E, R)
+    rng = np.random.default_rng(5 + k)
+    ret = th.Retriever(g)
+    ret.set_knob("k4_cache_filtered", cache_filtered)
+    for rep in range(3):  # eager, capture, replay
+        seeds = rng.integers(0, E, 1024)
+        filt = [sorted(rng.choice(R, 10, replace=False).tolist()) for _ in range(1024)]
+        res = ret.retrieve(seeds, k, relation_filter=filt)
+        for i in (0, 1, 511, 1023):
+            ref = orc.retrieve_one(og, int(seeds[i]), k, "frontier", filt[i])
+            for h in range(k):
+                assert np.array_equal(res.frontier(i, h + 1), ref["frontiers"][h]), (rep, i, h)
+                assert int(res.edges[h, i]) == ref["edges"][h]
