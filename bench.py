@@ -452,7 +452,27 @@ def run_c4_leg(th, stream, peaks, n_batches=8, cols=None):
                         "traffic": tr.get("bytes"), "traffic_source": tr.get("source"),
                         "note": note}
         out[f"k{k}"] = leg
-    del ret, g
+    del ret
+    torch.cuda.empty_cache()
+    # streamed e2e (RetrievalPipeline, as the headline's): pinned host seeds
+    # in, every wave's per-seed frontiers out to pinned host memory
+    from paper_2604_18913_b200.pipeline import RetrievalPipeline
+
+    host = [torch.from_numpy(b).pin_memory() for b in batches.cpu().numpy()]
+    pipe = RetrievalPipeline(g, depth=2)
+    for k in (2, 3):
+        for _ in pipe.run(host, k):  # sizes every buffer; each session records + captures its graph
+            pass
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for hb in pipe.run(host, k):
+            d2h += hb.nbytes()
+        dt = (time.perf_counter() - t0) / len(host)
+        out[f"k{k}"]["e2e"] = {"value": BATCH / dt, "unit": "seeds/s", "h2d_bytes_per_step": 4 * BATCH + 4 * (BATCH + 1),
+                               "d2h_bytes_per_step": d2h // len(host), "link_GBps": d2h / len(host) / dt / 1e9,
+                               "api": "RetrievalPipeline.run, one 1,024-seed wave per step"}
+    del pipe, g
     torch.cuda.empty_cache()
     return out
 
