@@ -477,6 +477,58 @@ def run_c4_leg(th, stream, peaks, n_batches=8, cols=None):
     return out
 
 
+def run_c5_leg(th, stream, n_waves=16):
+    """BASELINE configs[4]'s graph on ONE GPU: 200M entities, 1e9 R-MAT
+    triples (generated on the device), 2,000 relations; 16,384 seeds in waves
+    of 1,024, k=2 FRONTIER, per-seed 64-of-2,000 relation masks.  The config
+    names 8 GPUs; this is its single-GPU point (the graph fits one B200's HBM)."""
+    import torch
+
+    from paper_2604_18913_b200.retriever import _relation_masks
+
+    t0 = time.perf_counter()
+    s, r, o, E, R = workloads.c5_graph_gpu()
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    g = th.build_incidence((s, r, o), E, R)
+    del s, r, o
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    seeds, rel = workloads.c5_queries(E, R)
+    words = _relation_masks(list(rel), seeds.size, R)
+    d_seeds = torch.from_numpy(seeds).to(g.device)
+    d_masks = torch.from_numpy(words.view(np.int32)).to(g.device)
+    ret = th.Retriever(g, stream)
+    offs = torch.arange(BATCH + 1, dtype=torch.int32, device=g.device)
+
+    def wave(w):
+        sl = slice(BATCH * w, BATCH * (w + 1))
+        return ret.run(offs, d_seeds[sl], 2, "frontier", d_masks[sl], singleton=True, copy=False)
+
+    for w in range(3):  # sizes buffers, records and captures the wave's graph
+        wave(w)
+    tot_ms, edges, ids = 0.0, 0, 0
+    for w in range(n_waves):
+        ms, res = _timed(stream, lambda: wave(w))
+        tot_ms += ms
+        edges += int(res.edges.sum().item())
+        ids += int(res.frontier_len.sum().item())
+    st = g.stats()
+    out = {"workload": "C5 (BASELINE configs[4]) graph on 1 GPU: 200M entities, 1e9 R-MAT triples, 2,000 "
+                       f"relations; {n_waves * BATCH} seeds in waves of {BATCH}, k=2 FRONTIER, per-seed "
+                       "64-of-2,000 relation masks",
+           "gen_s": gen_s, "build_s": build_s, "device_graph_bytes": st.get("device_bytes"),
+           "max_out_degree": st.get("max_out_degree"),
+           "seeds_per_s": n_waves * BATCH / (tot_ms / 1e3), "edges_per_s": edges / (tot_ms / 1e3),
+           "ms_per_wave": tot_ms / n_waves, "frontier_ids_per_wave": ids / n_waves,
+           "peak_device_GB": torch.cuda.max_memory_allocated() / 1e9}
+    del ret, g, d_seeds, d_masks
+    torch.cuda.empty_cache()
+    return out
+
+
 def partitioned_leg(th, cols, E, R, world, rank, ks=(2, 3), n_batches=4, reps=4):
     """BASELINE configs[3] partitioned over the job's ranks (hash owners +
     edge-split top-0.01% hubs, Algorithm 1 per hop with the ranks writing
@@ -812,6 +864,18 @@ def run_ours(args, world, rank, local):
             c4 = run_c4_leg(th, stream, peaks, cols=c4_cols)
         if not args.no_part:
             part = partitioned_leg(th, c4_cols[:3], c4_cols[3], c4_cols[4], world, rank)
+        del c4_cols
+    c5 = None
+    if world == 1 and not args.no_c5:
+        import gc
+
+        gc.collect()  # (the partitioned leg's shards free their device regions on collection)
+        torch.cuda.empty_cache()
+        try:
+            c5 = run_c5_leg(th, stream)
+        except (RuntimeError, MemoryError) as e:  # (a leg that cannot run must not lose the line)
+            c5 = {"error": f"{type(e).__name__}: {e}"[:300]}
+            torch.cuda.empty_cache()
 
     if rank == 0:
         line = {
@@ -859,6 +923,7 @@ def run_ours(args, world, rank, local):
             "c3": c3,
             "c4": c4,
             "partitioned": part,
+            "c5": c5,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -876,6 +941,7 @@ def main():
     ap.add_argument("--ref-step-seeds", type=int, default=256)
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 (filter + paths) leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 (54.4M-entity) leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (1e9-triple, one GPU) leg")
     ap.add_argument("--partitioned", action="store_true",
                     help="C4 on a graph partitioned over the ranks (NCCL exchange per hop)")
     ap.add_argument("--part-k", type=int, default=2)
