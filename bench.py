@@ -838,6 +838,19 @@ def run_ours(args, world, rank, local):
         e2e_t, pipe_t = (float(x) for x in tt.tolist())
     e2e_value = BATCH * world / e2e_t
     pipe_value = BATCH * world / pipe_t
+    # the e2e's own roofline: one raw pinned D2H of a step's result bytes on
+    # this box (the host link, not the kernels, bounds the streamed e2e)
+    nb = int(pipe_d2h // n_pipe)
+    raw_src = torch.empty(nb // 4 + 1, dtype=torch.int32, device=dev)
+    raw_dst = torch.empty(nb // 4 + 1, dtype=torch.int32).pin_memory()
+    link_peak = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        raw_dst.copy_(raw_src, non_blocking=True)
+        torch.cuda.synchronize()
+        link_peak = max(link_peak, raw_dst.numel() * 4 / (time.perf_counter() - t0) / 1e9)
+    del raw_src, raw_dst
 
     # CPU baseline: oracle on the host cores, rank 0 at N=1 only
     cpu = None
@@ -911,6 +924,9 @@ def run_ours(args, world, rank, local):
                            "to pinned host memory, batch i+1's hops overlapping batch i's copy-out",
                     # the host link bounds it: result bytes per second of the whole step
                     "link_GBps": (h2d + pipe_d2h / n_pipe) / pipe_t / 1e9,
+                    "link_peak_GBps": link_peak,
+                    "link_frac": (h2d + pipe_d2h / n_pipe) / pipe_t / 1e9 / link_peak if link_peak else None,
+                    "link_peak_note": "one raw pinned D2H of a step's result bytes, best of 3, same box",
                     "note": "PCIe-bound: every step returns all per-seed frontiers (int32) to the host",
                     "blocking": {"value": e2e_value, "unit": "seeds/s", "h2d_bytes_per_step": h2d,
                                  "d2h_bytes_per_step": d2h,
